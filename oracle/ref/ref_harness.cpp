@@ -1,0 +1,192 @@
+// ref_harness — TEST INFRASTRUCTURE ONLY (never on the product path).
+//
+// Drives the UNMODIFIED reference library (`stencilgrad`, compiled from the
+// sources under /root/reference/proj/src by oracle/ref/Makefile into
+// oracle/_ref/) so that the repo's own oracle restatement (oracle/sg_oracle.c)
+// and the CUDA path can be pinned against the reference's own semantics:
+//
+//   info   <spec> <n>                         program structure as JSON
+//                                             (assemble_adjoint, adjoint.cpp:152-163)
+//   run    <spec> <n> <in_dir> <out_dir> S=v  run_nest / run_program /
+//                                             run_scatter_adjoint (interp.cpp:183-228)
+//                                             on raw fp64 grids read from in_dir
+//   verify <spec> <n> <seed> <trials>         verify_problem (interp.cpp:413-435)
+//   emit   <spec> <out_dir>                   emit_primal / emit_adjoint /
+//                                             emit_scatter_adjoint with restrict,
+//                                             exactly as cmd_bench does
+//                                             (tools/stencilgrad.cpp:285-301)
+//
+// <spec> is a path to a JSON spec, or "example:<name>" for a bundled example
+// (examples.cpp:79).  Grids are raw little-endian fp64, row-major, named
+// <array>.f64.  Nothing here is shipped or timed.
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+
+#include "stencilgrad/adjoint.hpp"
+#include "stencilgrad/codegen.hpp"
+#include "stencilgrad/examples.hpp"
+#include "stencilgrad/interp.hpp"
+#include "stencilgrad/specfile.hpp"
+
+namespace sg = stencilgrad;
+
+static std::string slurp(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw sg::Error("cannot read " + path);
+  std::ostringstream os;
+  os << in.rdbuf();
+  return os.str();
+}
+
+static sg::Problem load(const std::string& spec) {
+  if (spec.rfind("example:", 0) == 0) return sg::example_problem(spec.substr(8));
+  auto r = sg::parse_spec(slurp(spec));
+  if (!r.problem) throw sg::Error("spec rejected:\n" + r.report.str());
+  return *r.problem;
+}
+
+static std::vector<long long> shape_of(const sg::ArrayDecl& a,
+                                       const std::map<std::string, long long>& sizes) {
+  std::vector<long long> s;
+  for (const auto& e : a.shape) s.push_back(e.eval(sizes));
+  return s;
+}
+
+static void read_grid(const std::string& path, sg::DenseGrid& g) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) return;  // absent file: keep zeros
+  in.read(reinterpret_cast<char*>(g.data().data()),
+          static_cast<std::streamsize>(g.data().size() * sizeof(double)));
+  if (!in) throw sg::Error("short read " + path);
+}
+
+static void write_grid(const std::string& path, const sg::DenseGrid& g) {
+  std::ofstream out(path, std::ios::binary);
+  out.write(reinterpret_cast<const char*>(g.data().data()),
+            static_cast<std::streamsize>(g.data().size() * sizeof(double)));
+}
+
+static void print_range(std::ostream& os, const sg::Range& r, const std::map<std::string, long long>& sz) {
+  os << "[" << r.lo.eval(sz) << "," << r.hi.eval(sz) << "]";
+}
+
+static int cmd_info(const sg::Problem& p, long long n) {
+  std::map<std::string, long long> sz{{"n", n}};
+  auto prog = sg::assemble_adjoint(p);
+  std::ostringstream os;
+  os << "{\"name\":\"" << p.name << "\",\"terms\":[";
+  for (std::size_t t = 0; t < prog.terms.size(); t++) {
+    if (t) os << ",";
+    os << "{\"array\":\"" << prog.terms[t].input.array << "\",\"adjoint\":\""
+       << prog.terms[t].adjoint_array << "\",\"offset\":[";
+    for (std::size_t i = 0; i < prog.terms[t].input.offset.size(); i++)
+      os << (i ? "," : "") << prog.terms[t].input.offset[i];
+    os << "],\"partial\":\"" << sg::to_input_string(prog.terms[t].partial) << "\"}";
+  }
+  os << "],\"core_index\":" << prog.core_index << ",\"guards\":[";
+  for (std::size_t g = 0; g < prog.extent_guards.size(); g++)
+    os << (g ? "," : "") << "[" << prog.extent_guards[g].first.eval(sz) << ","
+       << prog.extent_guards[g].second << "]";
+  os << "],\"core_bounds\":[";
+  auto cb = sg::core_bounds(prog.terms, p.nest);
+  for (std::size_t i = 0; i < cb.size(); i++) {
+    if (i) os << ",";
+    print_range(os, cb[i], sz);
+  }
+  os << "],\"nests\":[";
+  for (std::size_t k = 0; k < prog.nests.size(); k++) {
+    if (k) os << ",";
+    os << "{\"bounds\":[";
+    for (std::size_t i = 0; i < prog.nests[k].nest.bounds.size(); i++) {
+      if (i) os << ",";
+      print_range(os, prog.nests[k].nest.bounds[i], sz);
+    }
+    os << "],\"terms\":[";
+    for (std::size_t i = 0; i < prog.nests[k].terms.size(); i++)
+      os << (i ? "," : "") << prog.nests[k].terms[i];
+    os << "],\"core\":" << (prog.nests[k].core ? "true" : "false") << "}";
+  }
+  os << "]}\n";
+  std::cout << os.str();
+  return 0;
+}
+
+static int cmd_run(const sg::Problem& p, long long n, const std::string& in_dir,
+                   const std::string& out_dir, int argc, char** argv) {
+  sg::Env env;
+  env.sizes["n"] = n;
+  for (const auto& s : p.scalars) env.scalars[s] = 0.0;
+  for (int a = 0; a < argc; a++) {
+    std::string kv = argv[a];
+    auto eq = kv.find('=');
+    env.scalars[kv.substr(0, eq)] = std::strtod(kv.c_str() + eq + 1, nullptr);
+  }
+  for (const auto& a : p.arrays) {
+    sg::DenseGrid g(shape_of(a, env.sizes));
+    read_grid(in_dir + "/" + a.name + ".f64", g);
+    env.grids[a.name] = g;
+    if (a.active) {
+      sg::DenseGrid gb(shape_of(a, env.sizes));
+      read_grid(in_dir + "/" + a.adjoint + ".f64", gb);
+      env.grids[a.adjoint] = gb;
+    }
+  }
+  const sg::ArrayDecl& out = sg::output_array(p);
+  sg::Env primal = sg::run_nest(p.nest, env);
+  write_grid(out_dir + "/primal_" + out.name + ".f64", primal.grids.at(out.name));
+  auto prog = sg::assemble_adjoint(p);
+  sg::Env gather = sg::run_program(prog, env);
+  sg::Env scatter = sg::run_scatter_adjoint(p, env);
+  for (const auto& a : p.arrays) {
+    if (!a.active || a.name == out.name) continue;
+    write_grid(out_dir + "/gather_" + a.adjoint + ".f64", gather.grids.at(a.adjoint));
+    write_grid(out_dir + "/scatter_" + a.adjoint + ".f64", scatter.grids.at(a.adjoint));
+  }
+  return 0;
+}
+
+static int cmd_verify(const sg::Problem& p, long long n, unsigned long long seed, int trials) {
+  auto rep = sg::verify_problem(p, {{"n", n}}, seed, trials, true);
+  std::cout << rep.json_text();
+  return rep.pass() ? 0 : 1;
+}
+
+static int cmd_emit(const sg::Problem& p, const std::string& out_dir) {
+  sg::EmitOptions opts;
+  opts.restrict_pointers = true;  // as cmd_bench (tools/stencilgrad.cpp:286)
+  auto prog = sg::assemble_adjoint(p);
+  std::ofstream(out_dir + "/" + p.name + "_primal.c") << sg::emit_primal(p, opts);
+  std::ofstream(out_dir + "/" + p.name + "_adjoint.c") << sg::emit_adjoint(p, prog, opts);
+  std::ofstream(out_dir + "/" + p.name + "_scatter.c") << sg::emit_scatter_adjoint(p, opts);
+  std::ofstream(out_dir + "/" + p.name + "_protos.h")
+      << sg::primal_prototype(p, opts) << sg::adjoint_prototype(p, prog, opts)
+      << sg::scatter_prototype(p, opts);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  try {
+    if (argc < 3) {
+      std::cerr << "usage: ref_harness info|run|verify|emit <spec> ...\n";
+      return 2;
+    }
+    std::string cmd = argv[1];
+    sg::Problem p = load(argv[2]);
+    if (cmd == "info" && argc >= 4) return cmd_info(p, std::atoll(argv[3]));
+    if (cmd == "run" && argc >= 6)
+      return cmd_run(p, std::atoll(argv[3]), argv[4], argv[5], argc - 6, argv + 6);
+    if (cmd == "verify" && argc >= 6)
+      return cmd_verify(p, std::atoll(argv[3]), std::strtoull(argv[4], nullptr, 10),
+                        std::atoi(argv[5]));
+    if (cmd == "emit" && argc >= 4) return cmd_emit(p, argv[3]);
+    std::cerr << "bad arguments\n";
+    return 2;
+  } catch (const std::exception& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return 1;
+  }
+}
