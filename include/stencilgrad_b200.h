@@ -1,0 +1,182 @@
+/* stencilgrad_b200.h — C ABI of the B200 (sm_100a) adjoint-stencil library.
+ *
+ * Drop-in for the functions the reference's C/OpenMP emitter generates
+ * (/root/reference/proj/src/codegen.cpp): same names, same parameter order
+ * (every size symbol, then each referenced scalar as double, then each
+ * referenced array in declaration order with each primal followed by its
+ * adjoint; codegen.cpp:198-230), with three B200 differences:
+ *   - a dtype suffix (_f32 / _f64): arrays are float* or double*;
+ *   - array pointers are DEVICE pointers (cudaMalloc / torch CUDA memory);
+ *   - a trailing stream (cudaStream_t passed as void*; NULL = legacy stream).
+ * Calls are stream-ordered and asynchronous; the caller synchronises.
+ *
+ * Semantics (codegen.cpp:332-434, interp.cpp:183-228):
+ *   <name>           primal: out (=|+=) body over the primal box
+ *                    (emit_primal, codegen.cpp:311-330; run_nest, interp.hpp:56)
+ *   <name>_b         gather adjoint: every adjoint array is ACCUMULATED (+=),
+ *                    core + boundary regions of assemble_adjoint
+ *                    (adjoint.cpp:152-163) fused into one launch; points that
+ *                    no term reaches are left untouched
+ *                    (emit_adjoint, codegen.cpp:332-382; run_program, interp.hpp:59)
+ *   <name>_scatter_b scatter adjoint with atomics (ablation only)
+ *                    (emit_scatter_adjoint, codegen.cpp:384-434;
+ *                    run_scatter_adjoint, interp.hpp:63)
+ * Return codes: 0 success; 1 minimum-extent guard violated (checked on the
+ * host before any launch, as the emitted `if ( n - 3 < 2 ) return 1;`,
+ * codegen.cpp:353-357); negative: -(cudaError_t) of a failed launch, or
+ * SGB_EINVAL for an argument outside the supported domain (never a CPU
+ * fallback).  sgb_last_error() describes the last failure on this thread.
+ */
+#ifndef STENCILGRAD_B200_H
+#define STENCILGRAD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* sgb_stream_t; /* cudaStream_t */
+
+#define SGB_OK 0
+#define SGB_GUARD 1
+#define SGB_EINVAL (-10000)
+
+const char* sgb_last_error(void);
+const char* sgb_version(void);
+/* number of kernel launches issued by this library since load (all threads) */
+unsigned long long sgb_launch_count(void);
+
+/* ---- cfg 1: wave1d (oracle/specs/wave1d.json) -------------------------------
+ * u_next[i] = 2u[i] - u_prev[i] + c[i]^2 D (u[i-1] - 2u[i] + u[i+1]), i in [1, n-2]
+ * Reference prototypes: wave1d(int n, double D, double *c, double *u,
+ * double *u_prev, double *u_next); wave1d_b(int n, double D, double *c,
+ * double *c_b, double *u, double *u_b, double *u_prev_b, double *u_next_b). */
+int wave1d_f64(int n, double D, double* c, double* u, double* u_prev, double* u_next,
+               sgb_stream_t stream);
+int wave1d_b_f64(int n, double D, double* c, double* c_b, double* u, double* u_b,
+                 double* u_prev_b, double* u_next_b, sgb_stream_t stream);
+int wave1d_scatter_b_f64(int n, double D, double* c, double* c_b, double* u, double* u_b,
+                         double* u_prev_b, double* u_next_b, sgb_stream_t stream);
+int wave1d_f32(int n, double D, float* c, float* u, float* u_prev, float* u_next,
+               sgb_stream_t stream);
+int wave1d_b_f32(int n, double D, float* c, float* c_b, float* u, float* u_b, float* u_prev_b,
+                 float* u_next_b, sgb_stream_t stream);
+int wave1d_scatter_b_f32(int n, double D, float* c, float* c_b, float* u, float* u_b,
+                         float* u_prev_b, float* u_next_b, sgb_stream_t stream);
+
+/* ---- cfg 2: wave3d_c, 7-point star, linear c (oracle/specs/wave3d_c.json) ---
+ * u[i][j][k] += 2u_1 - u_2 + c D Lap7(u_1), box [1, n-2]^3.
+ * Reference prototype: wave3d_c_b(int n, double D, double *c, double *c_b,
+ * double *u_1, double *u_1_b, double *u_2_b, double *u_b).
+ * wave3d_c2 is the c^2 variant (oracle/specs/wave3d_c2.json), same ABI. */
+int wave3d_c_f32(int n, double D, float* c, float* u_1, float* u_2, float* u,
+                 sgb_stream_t stream);
+int wave3d_c_b_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                   float* u_2_b, float* u_b, sgb_stream_t stream);
+int wave3d_c_scatter_b_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                           float* u_2_b, float* u_b, sgb_stream_t stream);
+int wave3d_c_f64(int n, double D, double* c, double* u_1, double* u_2, double* u,
+                 sgb_stream_t stream);
+int wave3d_c_b_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                   double* u_2_b, double* u_b, sgb_stream_t stream);
+int wave3d_c_scatter_b_f64(int n, double D, double* c, double* c_b, double* u_1,
+                           double* u_1_b, double* u_2_b, double* u_b, sgb_stream_t stream);
+int wave3d_c2_f32(int n, double D, float* c, float* u_1, float* u_2, float* u,
+                  sgb_stream_t stream);
+int wave3d_c2_b_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                    float* u_2_b, float* u_b, sgb_stream_t stream);
+int wave3d_c2_scatter_b_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                            float* u_2_b, float* u_b, sgb_stream_t stream);
+int wave3d_c2_f64(int n, double D, double* c, double* u_1, double* u_2, double* u,
+                  sgb_stream_t stream);
+int wave3d_c2_b_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                    double* u_2_b, double* u_b, sgb_stream_t stream);
+int wave3d_c2_scatter_b_f64(int n, double D, double* c, double* c_b, double* u_1,
+                            double* u_1_b, double* u_2_b, double* u_b, sgb_stream_t stream);
+
+/* ---- cfg 3: burgers2d (oracle/specs/burgers2d.json) --------------------------
+ * Reference prototype: burgers2d_b(int n, double C, double D, double *u_1,
+ * double *u_1_b, double *u_b). */
+int burgers2d_f64(int n, double C, double D, double* u_1, double* u, sgb_stream_t stream);
+int burgers2d_b_f64(int n, double C, double D, double* u_1, double* u_1_b, double* u_b,
+                    sgb_stream_t stream);
+int burgers2d_scatter_b_f64(int n, double C, double D, double* u_1, double* u_1_b,
+                            double* u_b, sgb_stream_t stream);
+int burgers2d_f32(int n, double C, double D, float* u_1, float* u, sgb_stream_t stream);
+int burgers2d_b_f32(int n, double C, double D, float* u_1, float* u_1_b, float* u_b,
+                    sgb_stream_t stream);
+int burgers2d_scatter_b_f32(int n, double C, double D, float* u_1, float* u_1_b, float* u_b,
+                            sgb_stream_t stream);
+
+/* ---- cfg 4/5: wave3d_r4, 8th-order 25-point star (oracle/specs/wave3d_r4.json)
+ * u = 2u_1 - u_2 + c^2 D Lap25(u_1), box [4, n-5]^3; u_2 passive.
+ * Reference prototypes: wave3d_r4(int n, double D, double *c, double *u_1,
+ * double *u_2, double *u); wave3d_r4_b(int n, double D, double *c,
+ * double *c_b, double *u_1, double *u_1_b, double *u_b). */
+int wave3d_r4_f32(int n, double D, float* c, float* u_1, float* u_2, float* u,
+                  sgb_stream_t stream);
+int wave3d_r4_b_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                    float* u_b, sgb_stream_t stream);
+int wave3d_r4_scatter_b_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                            float* u_b, sgb_stream_t stream);
+int wave3d_r4_f64(int n, double D, double* c, double* u_1, double* u_2, double* u,
+                  sgb_stream_t stream);
+int wave3d_r4_b_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                    double* u_b, sgb_stream_t stream);
+int wave3d_r4_scatter_b_f64(int n, double D, double* c, double* c_b, double* u_1,
+                            double* u_1_b, double* u_b, sgb_stream_t stream);
+
+/* ---- z-slab (outermost counter i) entry points for multi-GPU decomposition --
+ * Local arrays hold planes [i_base, i_base + nplanes) of the global n^3 grid
+ * (n*n contiguous elements per plane).  Computes the gather adjoint for the
+ * global output planes [out_i0, out_i1), which must lie within
+ * [i_base + R, i_base + nplanes - R) unless they touch the global grid ends
+ * (R = stencil radius).  Bounds masks use GLOBAL indices, so the union of
+ * the slabs' outputs equals the single-GPU result bit for bit. */
+int wave3d_r4_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                         float* u_b, int i_base, int nplanes, int out_i0, int out_i1,
+                         sgb_stream_t stream);
+int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                        float* u_2_b, float* u_b, int i_base, int nplanes, int out_i0,
+                        int out_i1, sgb_stream_t stream);
+
+/* ---- device input generation (synthetic BASELINE distributions) -------------
+ * Counter-based: value(index) depends only on (seed, stream, global index), so
+ * any slab of any decomposition sees identical inputs.  index = global flat
+ * index of dst[0] is index_base.  kind: 0 = N(mean, scale), 1 = U[mean, mean+scale)
+ * (i.e. lo = mean, width = scale). */
+int sgb_fill_random_f32(float* dst, long long count, long long index_base, uint64_t seed,
+                        uint64_t stream_id, int kind, double mean, double scale,
+                        sgb_stream_t stream);
+int sgb_fill_random_f64(double* dst, long long count, long long index_base, uint64_t seed,
+                        uint64_t stream_id, int kind, double mean, double scale,
+                        sgb_stream_t stream);
+/* zero the h-point shell of planes [i_base, i_base+nplanes) of an n^d grid
+ * (d = 1, 2 or 3; for d < 3 pass i_base = 0, nplanes = n) */
+int sgb_zero_halo_f32(float* a, int d, int n, int h, int i_base, int nplanes,
+                      sgb_stream_t stream);
+int sgb_zero_halo_f64(double* a, int d, int n, int h, int i_base, int nplanes,
+                      sgb_stream_t stream);
+/* c[i][j][k] = value of layer floor(i*layers/n), layer values ~ U[lo, hi) from seed */
+int sgb_fill_layered_f32(float* c, int n, int layers, double lo, double hi, uint64_t seed,
+                         int i_base, int nplanes, sgb_stream_t stream);
+/* one interior pass of the 5-point average u <- (u + 4 neighbours)/5 (2D) */
+int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream);
+
+/* ---- host-buffer entry (end-to-end path) ------------------------------------
+ * Same arguments as <name>_b but HOST pointers; copies inputs and accumulated
+ * adjoints host->device, runs the gather adjoint, copies the adjoints back.
+ * A plan owns the device workspace so the call itself does not allocate. */
+typedef struct sgb_plan sgb_plan;
+sgb_plan* sgb_plan_create(const char* family, int n, int dtype_bytes);
+void sgb_plan_destroy(sgb_plan* plan);
+/* arrays[] in the reference prototype order of <family>_b (host pointers) */
+int sgb_plan_run_adjoint_host(sgb_plan* plan, const double* scalars, void** arrays,
+                              sgb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

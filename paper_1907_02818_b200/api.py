@@ -1,0 +1,203 @@
+"""Host-side API over the C ABI (include/stencilgrad_b200.h).
+
+Two layers, mirroring the reference's two interfaces:
+
+* generated-function layer on DEVICE tensors -- ``primal`` / ``adjoint`` /
+  ``scatter_adjoint`` call ``<name>``, ``<name>_b``, ``<name>_scatter_b``
+  (codegen.cpp:311-434) with arguments gathered by parameter name from a dict
+  of torch CUDA tensors, on the current torch stream;
+* in-memory layer on HOST numpy grids -- ``run_nest`` / ``run_program`` /
+  ``run_scatter_adjoint`` take ``(family, n, scalars, grids, adjoints)`` and
+  return new arrays, leaving the inputs untouched, like the reference's
+  ``Env run_program(const AdjointProgram&, const Env&)`` (interp.hpp:56-63).
+  They upload, run the sm_100a kernels and download.
+
+Unsupported families, shapes or dtypes raise; there is no CPU fallback.
+torch is only the device-memory / stream plumbing here.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+FAMILIES = {"wave1d": 1, "wave3d_c": 3, "wave3d_c2": 3, "burgers2d": 2, "wave3d_r4": 3}
+SCALARS = {"wave1d": ["D"], "wave3d_c": ["D"], "wave3d_c2": ["D"], "burgers2d": ["C", "D"],
+           "wave3d_r4": ["D"]}
+_SUFFIX = {"primal": "", "adjoint": "_b", "scatter": "_scatter_b", "slab": "_b_slab"}
+
+
+def _sfx(dtype) -> str:
+    import torch
+    if dtype in (torch.float32, np.float32, "f32", "float32"):
+        return "f32"
+    if dtype in (torch.float64, np.float64, "f64", "float64"):
+        return "f64"
+    raise _lib.StencilError(f"unsupported dtype {dtype} (f32 or f64 only)")
+
+
+def function_name(family: str, kind: str, dtype) -> str:
+    if family not in FAMILIES:
+        raise _lib.StencilError(f"unsupported stencil family '{family}'")
+    return f"{family}{_SUFFIX[kind]}_{_sfx(dtype)}"
+
+
+def array_params(family: str, kind: str, dtype="f32"):
+    """Array parameter names of the C entry point, in prototype order."""
+    _, params = _lib.PROTOTYPES[function_name(family, kind, dtype)]
+    return [p for t, p in params if t.endswith("*") and t not in ("const char*",)]
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _call(family, kind, n, scalars, arrays, stream=None, extra=()):
+    import torch
+    names = array_params(family, kind)
+    dtype = None
+    ptrs = []
+    for nm in names:
+        t = arrays.get(nm)
+        if t is None:
+            raise _lib.StencilError(f"{family}{_SUFFIX[kind]}: missing array '{nm}'")
+        if not (t.is_cuda and t.is_contiguous()):
+            raise _lib.StencilError(f"array '{nm}' must be a contiguous CUDA tensor")
+        if dtype is None:
+            dtype = t.dtype
+        elif t.dtype != dtype:
+            raise _lib.StencilError("all arrays must share one dtype")
+        ptrs.append(ctypes.c_void_p(t.data_ptr()))
+    fname = function_name(family, kind, dtype)
+    fn = getattr(_lib.lib(), fname)
+    sc = [float(scalars[s]) for s in SCALARS[family]]
+    rc = fn(int(n), *sc, *ptrs, *extra, _stream_ptr(stream))
+    _lib.check(rc, fname)
+    del torch
+
+
+def primal(family, n, scalars, arrays, stream=None):
+    """<name>_{f32,f64}: primal stencil (run_nest semantics, interp.cpp:153-173)."""
+    _call(family, "primal", n, scalars, arrays, stream)
+
+
+def adjoint(family, n, scalars, arrays, stream=None):
+    """<name>_b_{f32,f64}: fused core+boundary gather adjoint, accumulating (+=)."""
+    _call(family, "adjoint", n, scalars, arrays, stream)
+
+
+def scatter_adjoint(family, n, scalars, arrays, stream=None):
+    """<name>_scatter_b_{f32,f64}: atomic scatter adjoint (ablation)."""
+    _call(family, "scatter", n, scalars, arrays, stream)
+
+
+def adjoint_slab(family, n, scalars, arrays, i_base, nplanes, out_i0, out_i1, stream=None):
+    """z-slab gather adjoint over global output planes [out_i0, out_i1)."""
+    _call(family, "slab", n, scalars, arrays, stream,
+          extra=(int(i_base), int(nplanes), int(out_i0), int(out_i1)))
+
+
+# ------------------------------------------------------------ device inputs
+def fill_random(t, index_base: int, seed: int, stream_id: int, kind: str, a: float, b: float,
+                stream=None):
+    """kind 'normal': N(a, b^2); 'uniform': U[a, a + b). Counter-based in the
+    GLOBAL flat index, so any slab regenerates the single-GPU values."""
+    import torch
+    k = {"normal": 0, "uniform": 1}[kind]
+    fn = _lib.lib().sgb_fill_random_f32 if t.dtype == torch.float32 else \
+        _lib.lib().sgb_fill_random_f64
+    _lib.check(fn(ctypes.c_void_p(t.data_ptr()), t.numel(), int(index_base), int(seed),
+                  int(stream_id), k, float(a), float(b), _stream_ptr(stream)), "fill_random")
+
+
+def zero_halo(t, d: int, n: int, h: int, i_base: int = 0, nplanes: int | None = None,
+              stream=None):
+    import torch
+    fn = _lib.lib().sgb_zero_halo_f32 if t.dtype == torch.float32 else _lib.lib().sgb_zero_halo_f64
+    _lib.check(fn(ctypes.c_void_p(t.data_ptr()), d, n, h, i_base,
+                  n if nplanes is None else nplanes, _stream_ptr(stream)), "zero_halo")
+
+
+def fill_layered(t, n: int, layers: int, lo: float, hi: float, seed: int, i_base: int = 0,
+                 nplanes: int | None = None, stream=None):
+    _lib.check(_lib.lib().sgb_fill_layered_f32(
+        ctypes.c_void_p(t.data_ptr()), n, layers, lo, hi, seed, i_base,
+        n if nplanes is None else nplanes, _stream_ptr(stream)), "fill_layered")
+
+
+def smooth5(src, dst, n: int, stream=None):
+    _lib.check(_lib.lib().sgb_smooth5_f64(ctypes.c_void_p(src.data_ptr()),
+                                          ctypes.c_void_p(dst.data_ptr()), n,
+                                          _stream_ptr(stream)), "smooth5")
+
+
+# ------------------------------------------------------------ host (Env-style) layer
+def _to_dev(a: np.ndarray, dtype):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+def _run_host(kind, family, n, scalars, grids, adjs, dtype):
+    import torch
+    td = torch.float32 if _sfx(dtype) == "f32" else torch.float64
+    arrays = {}
+    for k, v in {**grids, **adjs}.items():
+        arrays[k] = _to_dev(v, td)
+    _call(family, kind, n, scalars, arrays)
+    torch.cuda.synchronize()
+    return {k: arrays[k].to("cpu", torch.float64).numpy() for k in arrays}
+
+
+def run_nest(family, n, scalars, grids, dtype="f64"):
+    """Primal on the B200; returns a new dict of host grids (interp.hpp:56)."""
+    return _run_host("primal", family, n, scalars, grids, {}, dtype)
+
+
+def run_program(family, n, scalars, grids, adjs, dtype="f64"):
+    """Gather adjoint on the B200; returns new host arrays (interp.hpp:59)."""
+    out = _run_host("adjoint", family, n, scalars, grids, adjs, dtype)
+    return {k: out[k] for k in adjs}
+
+
+def run_scatter_adjoint(family, n, scalars, grids, adjs, dtype="f64"):
+    """Atomic scatter adjoint on the B200 (interp.hpp:63)."""
+    out = _run_host("scatter", family, n, scalars, grids, adjs, dtype)
+    return {k: out[k] for k in adjs}
+
+
+class Plan:
+    """Device workspace for the host-buffer entry point (sgb_plan_*)."""
+
+    def __init__(self, family: str, n: int, dtype="f32"):
+        self.family, self.n = family, n
+        self.dtype_bytes = 4 if _sfx(dtype) == "f32" else 8
+        self._p = _lib.lib().sgb_plan_create(family.encode(), n, self.dtype_bytes)
+        if not self._p:
+            raise _lib.StencilError(_lib.lib().sgb_last_error().decode())
+        self.names = array_params(family, "adjoint")
+
+    def run_adjoint_host(self, scalars: dict, host_arrays: dict, stream=None):
+        """host_arrays: name -> pinned CPU tensor or numpy array (dtype of the plan)."""
+        ptrs = (ctypes.c_void_p * len(self.names))()
+        for i, nm in enumerate(self.names):
+            a = host_arrays[nm]
+            ptrs[i] = a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+        sc = (ctypes.c_double * 2)(*[float(scalars[s]) for s in SCALARS[self.family]])
+        s = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
+        _lib.check(_lib.lib().sgb_plan_run_adjoint_host(ctypes.c_void_p(self._p), sc, ptrs, s),
+                   "sgb_plan_run_adjoint_host")
+
+    def close(self):
+        if self._p:
+            _lib.lib().sgb_plan_destroy(ctypes.c_void_p(self._p))
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,235 @@
+// extern "C" entry points (include/stencilgrad_b200.h): argument checks, the
+// reference's minimum-extent guards, and dispatch to the sm_100a kernels.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "generic_kernels.cuh"
+#include "star3d_tma.cuh"
+
+namespace sgb {
+
+std::atomic<unsigned long long> g_launches{0};
+static thread_local std::string t_error;
+void set_error(const std::string& msg) { t_error = msg; }
+
+static int einval(const std::string& msg) {
+  set_error(msg);
+  return SGB_EINVAL;
+}
+
+// Minimum-extent guard of split_regions (adjoint.cpp:134-143), as the emitted
+// code checks it (codegen.cpp:353-357): (hi - lo) >= max o - min o per dim.
+static bool guard_ok(int fam, long long n) {
+  switch (fam) {
+    case WAVE1D:
+    case WAVE3D_C:
+    case WAVE3D_C2:
+    case BURGERS2D:
+      return (n - 3) >= 2;  // [1, n-2], offsets -1..1
+    case WAVE3D_R4:
+      return (n - 9) >= 8;  // [4, n-5], offsets -4..4
+  }
+  return false;
+}
+
+// ------------------------------------------------------------------ 3D stars
+template <int MODE, typename T>
+static int star3_gather(const char* name, long long n, double D, const T* c, T* c_b,
+                        const T* u_1, T* u_1_b, T* u_2_b, const T* u_b, long long i_base,
+                        long long nplanes, long long out_i0, long long out_i1,
+                        cudaStream_t s) {
+  using S = Star3<MODE>;
+  constexpr int R = S::R;
+  const int fam = MODE == 0 ? WAVE3D_C : MODE == 1 ? WAVE3D_C2 : WAVE3D_R4;
+  if (n <= 0) return einval(std::string(name) + ": n must be positive");
+  if (!guard_ok(fam, n)) return SGB_GUARD;
+  if (!c || !c_b || !u_1 || !u_1_b || !u_b || (S::kU2 && !u_2_b))
+    return einval(std::string(name) + ": null array");
+  if (out_i0 < 0 || out_i1 > n || out_i0 > out_i1 || nplanes <= 0)
+    return einval(std::string(name) + ": bad output plane range");
+  const long long need_lo = out_i0 - R < 0 ? 0 : out_i0 - R;
+  const long long need_hi = out_i1 - 1 + R > n - 1 ? n - 1 : out_i1 - 1 + R;
+  if (out_i1 > out_i0 && (need_lo < i_base || need_hi >= i_base + nplanes))
+    return einval(std::string(name) + ": slab does not hold the radius-R halo of the outputs");
+  if (out_i1 == out_i0) return 0;
+  const long long lo = R, hi = n - 1 - R;
+  Slab3 g{n, i_base, nplanes};
+  if (star3_tma_supported<MODE, T>(n)) {
+    return star3_tma_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
+                                  (float*)c_b, (const float*)u_1, (float*)u_1_b,
+                                  (float*)u_2_b, (const float*)u_b, s, name);
+  }
+  dim3 b(32, 4), gr((unsigned)((n + 31) / 32), (unsigned)((n + 3) / 4),
+                    (unsigned)(out_i1 - out_i0));
+  star3_gather_kernel<MODE, T>
+      <<<gr, b, 0, s>>>(g, lo, hi, out_i0, out_i1, (T)D, c, c_b, u_1, u_1_b, u_2_b, u_b);
+  return launch_status(name);
+}
+
+template <int MODE, typename T>
+static int star3_primal(const char* name, long long n, double D, const T* c, const T* u_1,
+                        const T* u_2, T* u, cudaStream_t s) {
+  constexpr int R = Star3<MODE>::R;
+  if (n <= 0) return einval(std::string(name) + ": n must be positive");
+  if (!c || !u_1 || !u_2 || !u) return einval(std::string(name) + ": null array");
+  if (n < 2 * R + 1) return 0;  // empty primal box
+  const long long lo = R, hi = n - 1 - R;
+  dim3 b(32, 4), gr((unsigned)((n + 31) / 32), (unsigned)((n + 3) / 4), (unsigned)n);
+  star3_primal_kernel<MODE, T><<<gr, b, 0, s>>>(Slab3{n, 0, n}, lo, hi, 0, n, (T)D, c, u_1,
+                                                u_2, u);
+  return launch_status(name);
+}
+
+template <int MODE, typename T>
+static int star3_scatter(const char* name, long long n, double D, const T* c, T* c_b,
+                         const T* u_1, T* u_1_b, T* u_2_b, const T* u_b, cudaStream_t s) {
+  using S = Star3<MODE>;
+  constexpr int R = S::R;
+  if (n <= 0) return einval(std::string(name) + ": n must be positive");
+  if (!c || !c_b || !u_1 || !u_1_b || !u_b || (S::kU2 && !u_2_b))
+    return einval(std::string(name) + ": null array");
+  const long long lo = R, hi = n - 1 - R;
+  if (hi < lo) return 0;
+  const long long m = hi - lo + 1;
+  dim3 b(32, 4), gr((unsigned)((m + 31) / 32), (unsigned)((m + 3) / 4), (unsigned)m);
+  star3_scatter_kernel<MODE, T>
+      <<<gr, b, 0, s>>>(Slab3{n, 0, n}, lo, hi, (T)D, c, c_b, u_1, u_1_b, u_2_b, u_b);
+  return launch_status(name);
+}
+
+// ------------------------------------------------------------------ wave1d
+template <typename T>
+static int wave1d_gather(long long n, double D, const T* c, T* c_b, const T* u, T* u_b,
+                         T* u_prev_b, const T* u_next_b, cudaStream_t s) {
+  if (n <= 0) return einval("wave1d_b: n must be positive");
+  if (!guard_ok(WAVE1D, n)) return SGB_GUARD;
+  if (!c || !c_b || !u || !u_b || !u_prev_b || !u_next_b) return einval("wave1d_b: null array");
+  wave1d_gather_kernel<T>
+      <<<grid_1d(n, 256), 256, 0, s>>>(n, (T)D, c, c_b, u, u_b, u_prev_b, u_next_b);
+  return launch_status("wave1d_b");
+}
+
+// ------------------------------------------------------------------ burgers2d
+template <typename T>
+static int burgers2d_gather(long long n, double C, double D, const T* u_1, T* u_1_b,
+                            const T* u_b, cudaStream_t s) {
+  if (n <= 0) return einval("burgers2d_b: n must be positive");
+  if (!guard_ok(BURGERS2D, n)) return SGB_GUARD;
+  if (!u_1 || !u_1_b || !u_b) return einval("burgers2d_b: null array");
+  dim3 b(64, 4), g((unsigned)((n + 63) / 64), (unsigned)((n + 3) / 4));
+  burgers2d_gather_kernel<T><<<g, b, 0, s>>>(n, (T)C, (T)D, u_1, u_1_b, u_b);
+  return launch_status("burgers2d_b");
+}
+
+}  // namespace sgb
+
+using namespace sgb;
+
+extern "C" {
+
+const char* sgb_last_error(void) { return t_error.c_str(); }
+const char* sgb_version(void) { return "stencilgrad_b200 0.1 sm_100a"; }
+unsigned long long sgb_launch_count(void) { return g_launches.load(); }
+
+// ---- wave1d
+#define SGB_WAVE1D(T, SFX)                                                                     \
+  int wave1d_##SFX(int n, double D, T* c, T* u, T* u_prev, T* u_next, sgb_stream_t stream) {   \
+    if (n <= 0 || !c || !u || !u_prev || !u_next) return einval("wave1d: bad arguments");      \
+    wave1d_primal_kernel<T><<<grid_1d(n, 256), 256, 0, as_stream(stream)>>>(n, (T)D, c, u,     \
+                                                                             u_prev, u_next);  \
+    return launch_status("wave1d");                                                            \
+  }                                                                                            \
+  int wave1d_b_##SFX(int n, double D, T* c, T* c_b, T* u, T* u_b, T* u_prev_b, T* u_next_b,    \
+                     sgb_stream_t stream) {                                                    \
+    return wave1d_gather<T>(n, D, c, c_b, u, u_b, u_prev_b, u_next_b, as_stream(stream));      \
+  }                                                                                            \
+  int wave1d_scatter_b_##SFX(int n, double D, T* c, T* c_b, T* u, T* u_b, T* u_prev_b,         \
+                             T* u_next_b, sgb_stream_t stream) {                               \
+    if (n <= 0 || !c || !c_b || !u || !u_b || !u_prev_b || !u_next_b)                          \
+      return einval("wave1d_scatter_b: bad arguments");                                        \
+    if (n < 3) return 0;                                                                       \
+    wave1d_scatter_kernel<T><<<grid_1d(n - 2, 256), 256, 0, as_stream(stream)>>>(              \
+        n, (T)D, c, c_b, u, u_b, u_prev_b, u_next_b);                                          \
+    return launch_status("wave1d_scatter_b");                                                  \
+  }
+SGB_WAVE1D(double, f64)
+SGB_WAVE1D(float, f32)
+
+// ---- 3D stars
+#define SGB_STAR3(NAME, MODE, T, SFX)                                                          \
+  int NAME##_##SFX(int n, double D, T* c, T* u_1, T* u_2, T* u, sgb_stream_t stream) {         \
+    return star3_primal<MODE, T>(#NAME, n, D, c, u_1, u_2, u, as_stream(stream));              \
+  }                                                                                            \
+  int NAME##_b_##SFX(int n, double D, T* c, T* c_b, T* u_1, T* u_1_b, T* u_2_b, T* u_b,        \
+                     sgb_stream_t stream) {                                                    \
+    return star3_gather<MODE, T>(#NAME "_b", n, D, c, c_b, u_1, u_1_b, u_2_b, u_b, 0, n, 0, n, \
+                                 as_stream(stream));                                           \
+  }                                                                                            \
+  int NAME##_scatter_b_##SFX(int n, double D, T* c, T* c_b, T* u_1, T* u_1_b, T* u_2_b,        \
+                             T* u_b, sgb_stream_t stream) {                                    \
+    return star3_scatter<MODE, T>(#NAME "_scatter_b", n, D, c, c_b, u_1, u_1_b, u_2_b, u_b,    \
+                                  as_stream(stream));                                          \
+  }
+SGB_STAR3(wave3d_c, 0, float, f32)
+SGB_STAR3(wave3d_c, 0, double, f64)
+SGB_STAR3(wave3d_c2, 1, float, f32)
+SGB_STAR3(wave3d_c2, 1, double, f64)
+
+#define SGB_R4(T, SFX)                                                                         \
+  int wave3d_r4_##SFX(int n, double D, T* c, T* u_1, T* u_2, T* u, sgb_stream_t stream) {      \
+    return star3_primal<2, T>("wave3d_r4", n, D, c, u_1, u_2, u, as_stream(stream));           \
+  }                                                                                            \
+  int wave3d_r4_b_##SFX(int n, double D, T* c, T* c_b, T* u_1, T* u_1_b, T* u_b,               \
+                        sgb_stream_t stream) {                                                 \
+    return star3_gather<2, T>("wave3d_r4_b", n, D, c, c_b, u_1, u_1_b, nullptr, u_b, 0, n, 0,  \
+                              n, as_stream(stream));                                           \
+  }                                                                                            \
+  int wave3d_r4_scatter_b_##SFX(int n, double D, T* c, T* c_b, T* u_1, T* u_1_b, T* u_b,       \
+                                sgb_stream_t stream) {                                         \
+    return star3_scatter<2, T>("wave3d_r4_scatter_b", n, D, c, c_b, u_1, u_1_b, nullptr, u_b,  \
+                               as_stream(stream));                                             \
+  }
+SGB_R4(float, f32)
+SGB_R4(double, f64)
+
+int wave3d_r4_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                         float* u_b, int i_base, int nplanes, int out_i0, int out_i1,
+                         sgb_stream_t stream) {
+  return star3_gather<2, float>("wave3d_r4_b_slab", n, D, c, c_b, u_1, u_1_b, nullptr, u_b,
+                                i_base, nplanes, out_i0, out_i1, as_stream(stream));
+}
+
+int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                        float* u_2_b, float* u_b, int i_base, int nplanes, int out_i0,
+                        int out_i1, sgb_stream_t stream) {
+  return star3_gather<0, float>("wave3d_c_b_slab", n, D, c, c_b, u_1, u_1_b, u_2_b, u_b, i_base,
+                                nplanes, out_i0, out_i1, as_stream(stream));
+}
+
+// ---- burgers2d
+#define SGB_BURGERS(T, SFX)                                                                    \
+  int burgers2d_##SFX(int n, double C, double D, T* u_1, T* u, sgb_stream_t stream) {          \
+    if (n <= 0 || !u_1 || !u) return einval("burgers2d: bad arguments");                       \
+    dim3 b(64, 4), g((unsigned)((n + 63) / 64), (unsigned)((n + 3) / 4));                      \
+    burgers2d_primal_kernel<T><<<g, b, 0, as_stream(stream)>>>(n, (T)C, (T)D, u_1, u);         \
+    return launch_status("burgers2d");                                                         \
+  }                                                                                            \
+  int burgers2d_b_##SFX(int n, double C, double D, T* u_1, T* u_1_b, T* u_b,                   \
+                        sgb_stream_t stream) {                                                 \
+    return burgers2d_gather<T>(n, C, D, u_1, u_1_b, u_b, as_stream(stream));                   \
+  }                                                                                            \
+  int burgers2d_scatter_b_##SFX(int n, double C, double D, T* u_1, T* u_1_b, T* u_b,           \
+                                sgb_stream_t stream) {                                         \
+    if (n <= 0 || !u_1 || !u_1_b || !u_b) return einval("burgers2d_scatter_b: bad arguments"); \
+    if (n < 3) return 0;                                                                       \
+    dim3 b(64, 4), g((unsigned)((n - 2 + 63) / 64), (unsigned)((n - 2 + 3) / 4));              \
+    burgers2d_scatter_kernel<T><<<g, b, 0, as_stream(stream)>>>(n, (T)C, (T)D, u_1, u_1_b,     \
+                                                                u_b);                          \
+    return launch_status("burgers2d_scatter_b");                                               \
+  }
+SGB_BURGERS(double, f64)
+SGB_BURGERS(float, f32)
+
+}  // extern "C"

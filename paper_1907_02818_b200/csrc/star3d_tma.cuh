@@ -1,0 +1,462 @@
+// Streaming gather-adjoint kernel for the 3D star families (sm_100a).
+//
+// What it computes is exactly the reference's adjoint program for
+// wave3d_c / wave3d_c2 / wave3d_r4 (assemble_adjoint, adjoint.cpp:152-163):
+// the core nest plus all 52 / 1456 boundary nests, fused into one launch by
+// the per-point predicate of SURVEY Appendix C.  Per target point y:
+//
+//   u_1_b[y] += sum_{o != 0} w_|o| * q[y - o] + w_0 * q[y] + 2 * ubm[y]
+//   c_b[y]   += g[y] * Lap(u_1)[y]                            (y in B only)
+//   u_2_b[y] += -ubm[y]                                       (y in B; c-modes)
+//
+// with ubm = u_b * [x in B], q = D * c(^2) * ubm and g = D * ubm (linear c)
+// or 2 * D * c * ubm (c^2).  Masking q at its source point is what turns the
+// hierarchical boundary nests into one predicated pass: a term l reaches y
+// iff y - o_l is in B (raster_check, proj/tests/support/region.hpp:97-122).
+//
+// B200 mapping
+//   * one CTA = 64 (k) x 16 (j) output column tile, streaming over the
+//     outermost counter i (the z-slab axis) for a chunk of planes;
+//   * every plane of c, u_b, u_1 (with a 4-float k halo and R-row j halo) is
+//     fetched by ONE thread with three cp.async.bulk.tensor.3d (TMA) loads
+//     into an S-stage shared-memory ring, completion on an mbarrier;
+//     out-of-grid boxes (also the slab ends) are zero-filled by the TMA unit;
+//   * q is formed once per plane in shared memory (masked at the source);
+//   * k and j neighbours come from shared memory (128-bit loads), the i
+//     direction is carried in registers as 2R+1 rotating accumulators per
+//     field (the plane loop is unrolled by 2R+1 so the rotation is static);
+//   * the read-modify-write of the adjoint arrays is one 128-bit load and
+//     store per 4 points, issued at the top of the plane so its latency
+//     overlaps the stencil work.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "generic_kernels.cuh"
+
+namespace sgb {
+
+namespace tma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                        int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+}  // namespace tma
+
+template <int MODE>
+struct StarTile {
+  static constexpr int R = Star3<MODE>::R;
+  static constexpr int TK = 64, TJ = 16, HK = 4, HJ = R;
+  static constexpr int BW = TK + 2 * HK;  // 72 floats = 288 B rows (16 B multiple)
+  static constexpr int BJ = TJ + 2 * HJ;
+  static constexpr int RING = 2 * R + 1;
+  static constexpr int STAGES = MODE == 2 ? 3 : 4;
+  static constexpr int THREADS = 256;
+  static constexpr int MIN_BLOCKS = 2;
+  static constexpr int BOX_BYTES = BW * BJ * 4;
+  static constexpr int FIELD_FLOATS = ((BOX_BYTES + 127) / 128) * 128 / 4;
+  static constexpr int QUEUE = R + 1;  // g (and ubm) per-thread ring depth
+  static constexpr int NQ = Star3<MODE>::kU2 ? 2 : 1;
+  static constexpr size_t SMEM =
+      (size_t)(STAGES * 3 + 2) * FIELD_FLOATS * 4 + (size_t)NQ * QUEUE * THREADS * 16 +
+      STAGES * 8;
+};
+
+// One field's contribution from one plane: in-plane (k from a 12-float
+// register window, j from R rows above/below in smem) into the accumulator of
+// this plane, and the plane's centre value into the 2R neighbouring planes'
+// accumulators (i direction).  ph is a compile-time constant after unrolling.
+template <int R, int RING>
+__device__ __forceinline__ void star_field_plane(const float* F, int crow, int tx, float w0,
+                                                 const float (&wr)[R + 1], float4 (&acc)[RING],
+                                                 int ph) {
+  constexpr int HK = 4, BW = 72;
+  float win[12];
+  {
+    const float4 a = *reinterpret_cast<const float4*>(F + crow + 4 * tx);
+    const float4 b = *reinterpret_cast<const float4*>(F + crow + 4 * tx + 4);
+    const float4 c = *reinterpret_cast<const float4*>(F + crow + 4 * tx + 8);
+    win[0] = a.x; win[1] = a.y; win[2] = a.z; win[3] = a.w;
+    win[4] = b.x; win[5] = b.y; win[6] = b.z; win[7] = b.w;
+    win[8] = c.x; win[9] = c.y; win[10] = c.z; win[11] = c.w;
+  }
+  float inp[4];
+#pragma unroll
+  for (int m = 0; m < 4; m++) {
+    float sacc = w0 * win[4 + m];
+#pragma unroll
+    for (int r = 1; r <= R; r++) sacc += wr[r] * (win[4 + m - r] + win[4 + m + r]);
+    inp[m] = sacc;
+  }
+#pragma unroll
+  for (int r = 1; r <= R; r++) {
+    const float4 up = *reinterpret_cast<const float4*>(F + crow - r * BW + HK + 4 * tx);
+    const float4 dn = *reinterpret_cast<const float4*>(F + crow + r * BW + HK + 4 * tx);
+    inp[0] += wr[r] * (up.x + dn.x);
+    inp[1] += wr[r] * (up.y + dn.y);
+    inp[2] += wr[r] * (up.z + dn.z);
+    inp[3] += wr[r] * (up.w + dn.w);
+  }
+  acc[ph].x += inp[0];
+  acc[ph].y += inp[1];
+  acc[ph].z += inp[2];
+  acc[ph].w += inp[3];
+  // Output p+R receives its FIRST contribution here: initialise its slot
+  // (this also discards whatever earlier, non-emitted planes aliased into it).
+  {
+    float4& a1 = acc[(ph + R) % RING];
+    a1 = make_float4(wr[R] * win[4], wr[R] * win[5], wr[R] * win[6], wr[R] * win[7]);
+  }
+#pragma unroll
+  for (int r = 1; r <= R; r++) {
+    if (r < R) {
+      float4& a1 = acc[(ph + r) % RING];
+      a1.x += wr[r] * win[4]; a1.y += wr[r] * win[5];
+      a1.z += wr[r] * win[6]; a1.w += wr[r] * win[7];
+    }
+    float4& a2 = acc[(ph + RING - r) % RING];
+    a2.x += wr[r] * win[4]; a2.y += wr[r] * win[5];
+    a2.z += wr[r] * win[6]; a2.w += wr[r] * win[7];
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2)
+    star3_tma_kernel(const __grid_constant__ CUtensorMap tm_c,
+                     const __grid_constant__ CUtensorMap tm_ub,
+                     const __grid_constant__ CUtensorMap tm_u1, float* __restrict__ c_b,
+                     float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n, int i_base,
+                     int lo, int hi, int out_i0, int out_i1, int chunk, int tiles_k, float D) {
+  using Tl = StarTile<MODE>;
+  using S3 = Star3<MODE>;
+  constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, BJ = Tl::BJ;
+  constexpr int RING = Tl::RING, NS = Tl::STAGES, FW = Tl::FIELD_FLOATS, QD = Tl::QUEUE;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage = reinterpret_cast<float*>(smem_raw);
+  float* qbuf = stage + NS * 3 * FW;
+  float4* gq = reinterpret_cast<float4*>(qbuf + 2 * FW);
+  float4* uq = gq + QD * Tl::THREADS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gq + Tl::NQ * QD * Tl::THREADS);
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int tk = blockIdx.x % tiles_k, tj = blockIdx.x / tiles_k;
+  const int k0 = tk * Tl::TK, j0 = tj * Tl::TJ;
+  const int o_begin = out_i0 + blockIdx.y * chunk;
+  const int o_end = min(o_begin + chunk, out_i1);
+  if (o_begin >= o_end) return;
+  const int pstart = o_begin - R;
+  const int P = (o_end - o_begin) + 2 * R;
+
+  const float w0 = S3::template w<float>(0);
+  float wr[R + 1];
+#pragma unroll
+  for (int r = 1; r <= R; r++) wr[r] = S3::template w<float>(r);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int it) {  // one plane -> stage it % NS
+    const int s = it % NS;
+    float* dst = stage + s * 3 * FW;
+    const int pl = pstart + it - i_base;  // local plane; out of slab -> zero fill
+    tma::mbar_arrive_expect_tx(&bars[s], 3 * Tl::BOX_BYTES);
+    tma::load_3d(dst + 0 * FW, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + 1 * FW, &tm_ub, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + 2 * FW, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
+  };
+  if (tid == 0)
+    for (int it = 0; it < NS && it < P; it++) issue(it);
+
+  // this thread's 4 output points: j = j0 + ty, k = k0 + 4 tx .. + 3
+  const int jc = j0 + ty, kc = k0 + 4 * tx;
+  const bool col_ok = jc < n && kc < n;  // n % 4 == 0 => all 4 or none
+  const bool jin = jc >= lo && jc <= hi;
+  bool kin[4];
+  int kout[4];
+#pragma unroll
+  for (int m = 0; m < 4; m++) {
+    const int k = kc + m;
+    kin[m] = k >= lo && k <= hi;
+    kout[m] = k < lo ? lo - k : (k > hi ? k - hi : 0);
+  }
+  const int jout = jc < lo ? lo - jc : (jc > hi ? jc - hi : 0);
+  const long long plane = (long long)n * n;
+  const long long col_off = (long long)jc * n + kc;
+
+  float4 accL[RING], accQ[RING];
+#pragma unroll
+  for (int s = 0; s < RING; s++) {
+    accL[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+    accQ[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+
+  for (int base = 0; base < P; base += RING) {
+#pragma unroll
+    for (int ph = 0; ph < RING; ph++) {
+      const int it = base + ph;
+      if (it < P) {
+        const int s = it % NS;
+        const int p = pstart + it;
+        const float* Cs = stage + s * 3 * FW;
+        const float* UBs = Cs + FW;
+        const float* U1s = Cs + 2 * FW;
+        float* Q = qbuf + (it & 1) * FW;
+        const bool emit = it >= 2 * R;
+        const int o = p - R;
+
+        // ---- prefetch the adjoint values this plane's emit will update
+        float4 cb_old = make_float4(0.f, 0.f, 0.f, 0.f), u1b_old = cb_old, u2b_old = cb_old;
+        const long long gidx = (long long)(o - i_base) * plane + col_off;
+        if (emit && col_ok) {
+          u1b_old = *reinterpret_cast<const float4*>(u_1_b + gidx);
+          if (o >= lo && o <= hi && jin) {
+            cb_old = *reinterpret_cast<const float4*>(c_b + gidx);
+            if (S3::kU2) u2b_old = *reinterpret_cast<const float4*>(u_2_b + gidx);
+          }
+        }
+
+        tma::mbar_wait(&bars[s], (it / NS) & 1);
+
+        // ---- q = D c(^2) u_b [x in B] over the whole halo box
+        const bool pin = p >= lo && p <= hi;
+        for (int e = tid; e < (BW / 4) * BJ; e += Tl::THREADS) {
+          const int row = e / (BW / 4), c4 = e - row * (BW / 4);
+          const int jg = j0 - HJ + row, kg = k0 - HK + 4 * c4;
+          const float4 cv = *reinterpret_cast<const float4*>(Cs + row * BW + 4 * c4);
+          const float4 uv = *reinterpret_cast<const float4*>(UBs + row * BW + 4 * c4);
+          const bool rm = pin && jg >= lo && jg <= hi;
+          float4 qv;
+          qv.x = (rm && kg + 0 >= lo && kg + 0 <= hi) ? D * (S3::kC2 ? cv.x * cv.x : cv.x) * uv.x : 0.f;
+          qv.y = (rm && kg + 1 >= lo && kg + 1 <= hi) ? D * (S3::kC2 ? cv.y * cv.y : cv.y) * uv.y : 0.f;
+          qv.z = (rm && kg + 2 >= lo && kg + 2 <= hi) ? D * (S3::kC2 ? cv.z * cv.z : cv.z) * uv.z : 0.f;
+          qv.w = (rm && kg + 3 >= lo && kg + 3 <= hi) ? D * (S3::kC2 ? cv.w * cv.w : cv.w) * uv.w : 0.f;
+          *reinterpret_cast<float4*>(Q + row * BW + 4 * c4) = qv;
+        }
+        // ---- own centre: ubm and g for this plane (queued until emit)
+        float4 ubm;
+        {
+          const int off = (ty + HJ) * BW + HK + 4 * tx;
+          const float4 uv = *reinterpret_cast<const float4*>(UBs + off);
+          const float4 cv = *reinterpret_cast<const float4*>(Cs + off);
+          const bool cm = pin && jin;
+          ubm.x = (cm && kin[0]) ? uv.x : 0.f;
+          ubm.y = (cm && kin[1]) ? uv.y : 0.f;
+          ubm.z = (cm && kin[2]) ? uv.z : 0.f;
+          ubm.w = (cm && kin[3]) ? uv.w : 0.f;
+          float4 g;
+          if (S3::kC2) {
+            g = make_float4(2.f * D * cv.x * ubm.x, 2.f * D * cv.y * ubm.y, 2.f * D * cv.z * ubm.z,
+                            2.f * D * cv.w * ubm.w);
+          } else {
+            g = make_float4(D * ubm.x, D * ubm.y, D * ubm.z, D * ubm.w);
+          }
+          const int slot = (it % QD) * Tl::THREADS + tid;
+          gq[slot] = g;
+          if (S3::kU2) uq[slot] = ubm;
+        }
+        __syncthreads();
+        // the stage used by the previous plane is free now: refill it
+        if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
+
+        // ---- in-plane stencils (k window in registers, j rows from smem)
+        star_field_plane<R, RING>(U1s, (ty + HJ) * BW, tx, w0, wr, accL, ph);
+        star_field_plane<R, RING>(Q, (ty + HJ) * BW, tx, w0, wr, accQ, ph);
+        accQ[ph].x += 2.f * ubm.x;
+        accQ[ph].y += 2.f * ubm.y;
+        accQ[ph].z += 2.f * ubm.z;
+        accQ[ph].w += 2.f * ubm.w;
+
+        // ---- emit output plane o = p - R (all its contributions are in)
+        if (emit) {
+          const int es = (ph + R + 1) % RING;
+          if (col_ok) {
+            const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
+            const bool oin = o >= lo && o <= hi;
+            // u_1_b: reached iff at most one coordinate outside [lo,hi], by <= R
+            float4 nv = u1b_old;
+            const float4 a = accQ[es];
+            const float av[4] = {a.x, a.y, a.z, a.w};
+            float* nvp = reinterpret_cast<float*>(&nv);
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+              const int nout = (oout > 0) + (jout > 0) + (kout[m] > 0);
+              const bool reach =
+                  nout == 0 || (nout == 1 && oout <= R && jout <= R && kout[m] <= R);
+              if (reach) nvp[m] = nvp[m] + av[m];
+            }
+            *reinterpret_cast<float4*>(u_1_b + gidx) = nv;
+            if (oin && jin) {
+              const int qs = ((it - R) % QD) * Tl::THREADS + tid;
+              const float4 g = gq[qs];
+              const float4 L = accL[es];
+              float4 cb = cb_old;
+              if (kin[0]) cb.x = cb.x + g.x * L.x;
+              if (kin[1]) cb.y = cb.y + g.y * L.y;
+              if (kin[2]) cb.z = cb.z + g.z * L.z;
+              if (kin[3]) cb.w = cb.w + g.w * L.w;
+              *reinterpret_cast<float4*>(c_b + gidx) = cb;
+              if (S3::kU2) {
+                const float4 um = uq[qs];
+                float4 u2 = u2b_old;
+                if (kin[0]) u2.x = u2.x + -um.x;
+                if (kin[1]) u2.y = u2.y + -um.y;
+                if (kin[2]) u2.z = u2.z + -um.z;
+                if (kin[3]) u2.w = u2.w + -um.w;
+                *reinterpret_cast<float4*>(u_2_b + gidx) = u2;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+template <int MODE, typename T>
+inline bool star3_tma_supported(long long n) {
+  if (sizeof(T) != 4) return false;
+  if (n % 4 != 0 || n < 16 || n > (1 << 20)) return false;
+  static int disabled = -1;
+  if (disabled < 0) {
+    const char* e = std::getenv("SGB_DISABLE_TMA");
+    disabled = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !disabled;
+}
+
+inline PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// Number of i-chunks per column tile: balances whole waves of resident CTAs
+// against the 2R halo planes each chunk re-reads.  SGB_ICHUNKS overrides.
+inline int choose_chunks(long long tiles, long long nout, int R, int per_sm) {
+  if (const char* e = std::getenv("SGB_ICHUNKS")) {
+    int c = std::atoi(e);
+    if (c > 0) return c;
+  }
+  const long long slots = (long long)num_sms() * per_sm;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int c = 1; c <= 32; c++) {
+    if (c > nout) break;
+    const long long blocks = tiles * c;
+    const long long L = (nout + c - 1) / c;
+    const double waves = (double)((blocks + slots - 1) / slots);
+    const double cost = waves * (double)(L + 2 * R);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = c;
+    }
+  }
+  return best;
+}
+
+template <int MODE>
+inline int star3_tma_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
+                            long long out_i1, float D, const float* c, float* c_b,
+                            const float* u_1, float* u_1_b, float* u_2_b, const float* u_b,
+                            cudaStream_t s, const char* name) {
+  using Tl = StarTile<MODE>;
+  auto encode = get_encode();
+  if (!encode) {
+    set_error(std::string(name) + ": cuTensorMapEncodeTiled unavailable");
+    return SGB_EINVAL;
+  }
+  CUtensorMap maps[3];
+  const float* src[3] = {c, u_b, u_1};
+  for (int f = 0; f < 3; f++) {
+    cuuint64_t dims[3] = {(cuuint64_t)g.n, (cuuint64_t)g.n, (cuuint64_t)g.nplanes};
+    cuuint64_t strides[2] = {(cuuint64_t)g.n * 4, (cuuint64_t)g.n * g.n * 4};
+    cuuint32_t box[3] = {(cuuint32_t)Tl::BW, (cuuint32_t)Tl::BJ, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(&maps[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)src[f], dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error(std::string(name) + ": tensor map encode failed (" + std::to_string((int)r) +
+                ")");
+      return SGB_EINVAL;
+    }
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(star3_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Tl::SMEM);
+    attr_set = true;
+  }
+  const int tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
+  const int tiles_j = (int)((g.n + Tl::TJ - 1) / Tl::TJ);
+  const long long nout = out_i1 - out_i0;
+  const int chunks = choose_chunks((long long)tiles_k * tiles_j, nout, Tl::R, Tl::MIN_BLOCKS);
+  const int chunk = (int)((nout + chunks - 1) / chunks);
+  dim3 grid((unsigned)(tiles_k * tiles_j), (unsigned)((nout + chunk - 1) / chunk));
+  star3_tma_kernel<MODE><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
+      maps[0], maps[1], maps[2], c_b, u_1_b, u_2_b, (int)g.n, (int)g.i_base, (int)lo, (int)hi,
+      (int)out_i0, (int)out_i1, chunk, tiles_k, D);
+  return launch_status(name);
+}
+
+}  // namespace sgb

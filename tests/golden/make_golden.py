@@ -99,7 +99,18 @@ def main() -> None:
         verify[f"{name}_n{n}_s{seed}"] = {"exit": r.returncode, "report": json.loads(r.stdout)}
     with open(os.path.join(HERE, "ref_verify.json"), "w") as fh:
         json.dump(verify, fh, indent=1)
-    print("structure + verify written")
+    # the reference emitter's prototypes (emit_primal/_adjoint/_scatter_adjoint
+    # with restrict, as cmd_bench; codegen.cpp:213-230) -- the C-ABI parameter order
+    protos = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name in ("wave1d", "wave3d_c", "wave3d_c2", "burgers2d", "wave3d_r4"):
+            harness("emit", oracle.spec_path(name), td)
+            lines = open(os.path.join(td, name + "_protos.h")).read().splitlines()
+            protos[name] = {k: v.replace("restrict ", "") for k, v in
+                            zip(("primal", "adjoint", "scatter"), lines)}
+    with open(os.path.join(HERE, "ref_protos.json"), "w") as fh:
+        json.dump(protos, fh, indent=1)
+    print("structure + verify + protos written")
 
 
 if __name__ == "__main__":
