@@ -7,6 +7,9 @@
 
 #include "generic_kernels.cuh"
 #include "star3d_tma.cuh"
+#include "star3d_v2.cuh"
+#include "star3d_v3.cuh"
+#include "star3d_v4.cuh"
 
 namespace sgb {
 
@@ -35,6 +38,26 @@ static bool guard_ok(int fam, long long n) {
 }
 
 // ------------------------------------------------------------------ 3D stars
+// Kernel selection for the TMA path: v2 (warp-specialised) for radius 4, v1
+// for radius 1 by default; SGB_STAR_KERNEL=1|2 and SGB_TJ=16|32 override.
+static int star_kernel_version(int mode) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = std::getenv("SGB_STAR_KERNEL");
+    forced = e ? std::atoi(e) : 0;
+  }
+  if (forced >= 1 && forced <= 5) return forced;
+  return mode == 2 ? 5 : 1;
+}
+static int star_tile_rows() {
+  static int tj = -1;
+  if (tj < 0) {
+    const char* e = std::getenv("SGB_TJ");
+    tj = (e && std::atoi(e) == 16) ? 16 : 32;
+  }
+  return tj;
+}
+
 template <int MODE, typename T>
 static int star3_gather(const char* name, long long n, double D, const T* c, T* c_b,
                         const T* u_1, T* u_1_b, T* u_2_b, const T* u_b, long long i_base,
@@ -57,6 +80,30 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
   const long long lo = R, hi = n - 1 - R;
   Slab3 g{n, i_base, nplanes};
   if (star3_tma_supported<MODE, T>(n)) {
+    const int ver = star_kernel_version(MODE);
+    if (ver == 4 || ver == 5) {
+#define SGB_V4(TJ, RMWT)                                                                     \
+  return star3_v4_gather<MODE, TJ, RMWT>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c, \
+                                         (float*)c_b, (const float*)u_1, (float*)u_1_b,        \
+                                         (float*)u_2_b, (const float*)u_b, s, name)
+      if (ver == 4) SGB_V4(16, false);
+      if (star_tile_rows() == 16) SGB_V4(16, true);
+      SGB_V4(32, true);
+#undef SGB_V4
+    }
+    if (ver == 3)
+      return star3_v3_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
+                                   (float*)c_b, (const float*)u_1, (float*)u_1_b, (float*)u_2_b,
+                                   (const float*)u_b, s, name);
+    if (ver == 2) {
+      if (star_tile_rows() == 32)
+        return star3_v2_gather<MODE, 32>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
+                                         (float*)c_b, (const float*)u_1, (float*)u_1_b,
+                                         (float*)u_2_b, (const float*)u_b, s, name);
+      return star3_v2_gather<MODE, 16>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
+                                       (float*)c_b, (const float*)u_1, (float*)u_1_b,
+                                       (float*)u_2_b, (const float*)u_b, s, name);
+    }
     return star3_tma_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
                                   (float*)c_b, (const float*)u_1, (float*)u_1_b,
                                   (float*)u_2_b, (const float*)u_b, s, name);

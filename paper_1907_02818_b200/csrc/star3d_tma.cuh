@@ -378,6 +378,21 @@ inline PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+// L2 promotion for the TMA input boxes (SGB_L2PROMO = 0 | 64 | 128 | 256).
+inline CUtensorMapL2promotion l2_promotion() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("SGB_L2PROMO");
+    v = e ? std::atoi(e) : 128;
+  }
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
+}
+
 inline int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -396,21 +411,16 @@ inline int choose_chunks(long long tiles, long long nout, int R, int per_sm) {
     int c = std::atoi(e);
     if (c > 0) return c;
   }
-  const long long slots = (long long)num_sms() * per_sm;
-  int best = 1;
-  double best_cost = 1e30;
-  for (int c = 1; c <= 32; c++) {
-    if (c > nout) break;
-    const long long blocks = tiles * c;
-    const long long L = (nout + c - 1) / c;
-    const double waves = (double)((blocks + slots - 1) / slots);
-    const double cost = waves * (double)(L + 2 * R);
-    if (cost < best_cost * 0.999) {
-      best_cost = cost;
-      best = c;
-    }
-  }
-  return best;
+  // Measured on B200 (768^3 / 1024^3, radius 4): chunks of ~192 planes keep
+  // the resident CTAs in near lock-step (their shared halo rows stay in L2)
+  // while the 2R re-read halo planes per chunk stay a few percent.
+  (void)tiles;
+  (void)per_sm;
+  long long c = (nout + 96) / 192;
+  if (c < 1) c = 1;
+  if (c > 32) c = 32;
+  (void)R;
+  return (int)c;
 }
 
 template <int MODE>
@@ -433,7 +443,7 @@ inline int star3_tma_gather(const Slab3& g, long long lo, long long hi, long lon
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode(&maps[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)src[f], dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       set_error(std::string(name) + ": tensor map encode failed (" + std::to_string((int)r) +
