@@ -1,0 +1,512 @@
+#!/usr/bin/env python
+"""Benchmark of the gather-form adjoint stencil (arXiv 1907.02818 hot path) on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line on rank 0.  For N > 1 it runs under torchrun, one rank per GPU,
+z-slab decomposition with a per-step NCCL halo exchange.
+
+Workload (default ``--config 4``; BASELINE.json configs[3]): wave3d_r4,
+8th-order 25-point star, fp32, 768^3 with a 4-point zero halo, adjoint w.r.t.
+u_1 and c, seeded synthetic inputs (c layered in z, u_1 and the seed u_b
+N(0,1)), D = 0.01.  One STEP = one reverse time step = the full gather adjoint
+(core + all 1456 boundary regions, one fused launch per rank) over the whole
+grid, plus the radius-4 halo exchange of u_1 and u_b when N > 1.
+
+value  = grid-point updates / s over all ranks (GPts/s), device time with CUDA
+         events, max over ranks; inputs resident in HBM (12.7 GB touched per
+         step at 768^3 >> 126 MB L2, so no flush is needed).
+e2e    = the same metric through the host-buffer C-ABI entry
+         (sgb_plan_run_adjoint_host): pinned host arrays in, H2D + kernel +
+         D2H of the accumulated adjoints inside the timed region.
+roofline: algorithmic bytes per launch (28 B/pt: c, u_1, u_b read; c_b, u_1_b
+         read+write) / average launch time vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline: the reference's own emitted OpenMP adjoint (oracle/_ref, built
+         from /root/reference by oracle/ref/Makefile) on the host cores.
+
+``--impl reference`` times that reference CPU implementation alone (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # id: family, n, dtype, algorithmic bytes/pt, scalars, description
+    "4": ("wave3d_r4", 768, "f32", 28, {"D": 0.01},
+          "cfg4 wave3d_r4 8th-order 25-pt star 768^3 fp32, 4-pt zero halo, c layered in z"),
+    "5": ("wave3d_r4", 1024, "f32", 28, {"D": 0.01},
+          "cfg5 wave3d_r4 1024^3 fp32 (one of the 100 reverse steps)"),
+    "2": ("wave3d_c", 512, "f32", 36, {"D": 0.1},
+          "cfg2 wave3d 7-pt star 512^3 fp32 linear c (one of the 10 reverse steps)"),
+    "1": ("wave1d", 1 << 24, "f64", 72, {"D": 0.25}, "cfg1 wave1d n=2^24 fp64"),
+    "3": ("burgers2d", 8192, "f64", 32, {"C": 0.2, "D": 0.002}, "cfg3 burgers2d 8192^2 fp64"),
+}
+DIMS = {"wave3d_r4": 3, "wave3d_c": 3, "wave1d": 1, "burgers2d": 2}
+RADIUS = {"wave3d_r4": 4, "wave3d_c": 1, "wave1d": 1, "burgers2d": 1}
+SEED = {"wave3d_r4": "u_b", "wave3d_c": "u_b", "wave1d": "u_next_b", "burgers2d": "u_b"}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            log("clock sampling unavailable:", e)
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ helpers
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def committed_traffic(workload: str, n: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the committed ncu --set full capture (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        e = d.get(f"{workload}@{n}")
+        return (float(e["dram_bytes_per_launch"]), e.get("source")) if e else (None, None)
+    except Exception:
+        return None, None
+
+
+def gen_inputs(api, torch, family, n, slab=None):
+    """Seeded synthetic inputs on the device (counter-based in the global flat
+    index, so every decomposition holds the single-GPU values)."""
+    d = DIMS[family]
+    seed = 0
+    if d == 3:
+        base = slab.base if slab else 0
+        npl = slab.nplanes if slab else n
+        shape = (npl, n, n)
+        ib = base * n * n
+    else:
+        base, npl, shape, ib = 0, n, (n,) * d, 0
+    dt = torch.float32 if family in ("wave3d_r4", "wave3d_c") else torch.float64
+    arrays = {nm: torch.zeros(shape, dtype=dt, device="cuda")
+              for nm in api.array_params(family, "adjoint")}
+    h = RADIUS[family]
+    if family == "wave3d_r4":
+        api.fill_layered(arrays["c"], n, 8, 1.5, 4.5, seed, base, npl)
+        api.fill_random(arrays["u_1"], ib, seed, 1, "normal", 0.0, 1.0)
+        api.zero_halo(arrays["u_1"], 3, n, 4, base, npl)
+        api.fill_random(arrays["u_b"], ib, seed, 3, "normal", 0.0, 1.0)
+    elif family == "wave3d_c":
+        api.fill_random(arrays["c"], ib, seed, 0, "uniform", 1.5, 3.0)
+        api.fill_random(arrays["u_1"], ib, seed, 1, "normal", 0.0, 1.0)
+        api.zero_halo(arrays["u_1"], 3, n, 1, base, npl)
+        api.fill_random(arrays["u_b"], ib, seed, 3, "normal", 0.0, 1.0)
+    elif family == "wave1d":
+        api.fill_random(arrays["c"], 0, seed, 0, "uniform", 1.5, 3.0)
+        api.fill_random(arrays["u"], 0, seed, 1, "normal", 0.0, 1.0)
+        api.zero_halo(arrays["u"], 1, n, h)
+        api.fill_random(arrays["u_next_b"], 0, seed, 3, "normal", 0.0, 1.0)
+    elif family == "burgers2d":
+        u = arrays["u_1"]
+        api.fill_random(u, 0, seed, 1, "uniform", -1.0, 2.0)
+        tmp = torch.empty_like(u)
+        for _ in range(3):
+            api.smooth5(u, tmp, n)
+            u, tmp = tmp, u
+        arrays["u_1"] = u
+        api.fill_random(arrays["u_b"], 0, seed, 3, "normal", 0.0, 1.0)
+    return arrays
+
+
+# ------------------------------------------------------------------ CPU side
+def _omp_env():
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    os.environ.setdefault("OMP_NUM_THREADS", str(ncpu))
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    return int(os.environ["OMP_NUM_THREADS"])
+
+
+def cpu_reference_runner(family: str):
+    """Returns (kind, call(n, scalars, arrays), label).  kind 'reference' = the
+    reference's own emitted OpenMP adjoint (oracle/_ref), else 'port' = the
+    repo's C restatement (oracle/sg_oracle.c, OpenMP predicate form)."""
+    import numpy as np
+    lib_path = os.path.join(ROOT, "oracle", "_ref", f"libref_{family}.so")
+    if os.path.exists(lib_path):
+        L = ctypes.CDLL(lib_path)
+        fn = getattr(L, f"{family}_b")
+        fn.restype = ctypes.c_int
+        opt = "-O2"
+        optf = os.path.join(ROOT, "oracle", "_ref", f"libref_{family}.opt")
+        if os.path.exists(optf):
+            opt = open(optf).read().strip()
+        from paper_1907_02818_b200 import api
+        names = api.array_params(family, "adjoint")
+        scal = api.SCALARS[family]
+
+        def call(n, scalars, arrays):
+            args = [ctypes.c_int(n)] + [ctypes.c_double(scalars[s]) for s in scal] + \
+                   [arrays[nm].ctypes.data_as(ctypes.c_void_p) for nm in names]
+            rc = fn(*args)
+            if rc != 0:
+                raise RuntimeError(f"reference {family}_b returned {rc}")
+        return "reference", call, f"reference emitted {family}_b, gcc {opt} -fopenmp, fp64"
+    from oracle import oracle
+
+    def call(n, scalars, arrays):
+        f = oracle.family(family)
+        grids = {a: arrays[a] for a in f.arrays if a in arrays}
+        adjs = {a: arrays[a] for a in f.adjoints if a and a in arrays}
+        oracle.run_program_omp(family, n, scalars, grids, adjs)
+    return "port", call, f"oracle port (sg_run_program_omp) {family}, fp64"
+
+
+def cpu_arrays(family, n):
+    import numpy as np
+    from paper_1907_02818_b200 import api
+    rng = np.random.default_rng(0)
+    shape = (n,) * DIMS[family]
+    out = {}
+    for nm in api.array_params(family, "adjoint"):
+        if nm == "c":
+            out[nm] = rng.uniform(1.5, 4.5, shape)
+        else:
+            out[nm] = rng.standard_normal(shape)
+    return out
+
+
+def time_cpu(family, scalars, n_full, target_s=6.0, calls=3):
+    """Best-of-`calls` time of one reference adjoint call on a bounded cube
+    sample sized so each call takes about target_s / calls seconds."""
+    threads = _omp_env()
+    kind, call, label = cpu_reference_runner(family)
+    d = DIMS[family]
+    # calibrate on a small sample
+    n0 = {3: 96, 2: 1024, 1: 1 << 20}[d]
+    a = cpu_arrays(family, n0)
+    t0 = time.perf_counter()
+    call(n0, scalars, a)
+    dt = max(time.perf_counter() - t0, 1e-4)
+    rate = n0 ** d / dt
+    n = int(round((rate * target_s / calls) ** (1.0 / d)))
+    n = max(n0, min(n, n_full))
+    if d == 3:
+        n -= n % 4
+    a = cpu_arrays(family, n)
+    call(n, scalars, a)  # warm-up / first touch
+    best = float("inf")
+    for _ in range(calls):
+        t0 = time.perf_counter()
+        call(n, scalars, a)
+        best = min(best, time.perf_counter() - t0)
+    pts = n ** d
+    return {"value": pts / best / 1e9, "unit": "GPts/s", "cores": threads, "kind": kind,
+            "sample": f"{label}; one call over the full {n}^{d} grid (bounded sample of the "
+                      f"{n_full}^{d} workload), best of {calls}", "seconds_per_call": best,
+            "n": n}
+
+
+def run_reference_arm(args, cfg):
+    family, n_full, dtype, bpp, scalars, desc = cfg
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = _omp_env()
+    kind, call, label = cpu_reference_runner(family)
+    d = DIMS[family]
+    # size each step so that warmup + steps end within ~2 minutes
+    budget = float(os.environ.get("SGB_REF_BUDGET_S", "90"))
+    per_call = budget / max(1, args.steps + args.warmup)
+    n0 = {3: 96, 2: 1024, 1: 1 << 20}[d]
+    a = cpu_arrays(family, n0)
+    t0 = time.perf_counter()
+    call(n0, scalars, a)
+    rate = n0 ** d / max(time.perf_counter() - t0, 1e-4)
+    n = int((rate * per_call) ** (1.0 / d))
+    n = max(min(n, n_full), {3: 24, 2: 64, 1: 4096}[d])
+    if d == 3:
+        n -= n % 4
+    a = cpu_arrays(family, n)
+    for _ in range(args.warmup):
+        call(n, scalars, a)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call(n, scalars, a)
+    sec = time.perf_counter() - t0
+    pts = n ** d * args.steps
+    value = pts / sec / 1e9
+    line = {
+        "impl": "reference", "metric": "adjoint GPts/s", "value": value, "unit": "GPts/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "family": family, "n": n_full, "sample_n": n,
+                   "note": "reference CPU path on the host cores; each step is one call "
+                           f"over a {n}^{d} sample of the workload"},
+        "cpu_baseline": {"value": value, "unit": "GPts/s", "cores": threads, "kind": kind,
+                         "sample": f"{label}; {n}^{d} grid per step"},
+        "e2e": {"value": value, "unit": "GPts/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, cfg):
+    import torch
+    family, n_full, dtype, bpp, scalars, desc = cfg
+    n = args.n or n_full
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1907_02818_b200 import api, _lib, slab as slabmod
+    _lib.lib()
+    d = DIMS[family]
+    R = RADIUS[family]
+    sl = None
+    if world > 1:
+        if d != 3:
+            raise SystemExit(f"{family} does not shard (replicas only); run with --gpus 1")
+        sl = slabmod.decompose(n, R, world, rank)
+    arrays = gen_inputs(api, torch, family, n, sl)
+    if sl is not None:
+        # c is static: exchange its halo once at setup (it is regenerated from
+        # global indices anyway; the exchange keeps the data path honest)
+        slabmod.exchange_halos(sl, [arrays["c"]])
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+
+    def kernel():
+        if sl is None:
+            api.adjoint(family, n, scalars, arrays)
+        else:
+            api.adjoint_slab(family, n, scalars, arrays, sl.base, sl.nplanes, sl.own0, sl.own1)
+
+    kev = []
+
+    def step(record):
+        if sl is not None:
+            slabmod.exchange_halos(sl, [arrays["u_1"], arrays["u_b"]])
+        if record:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            kernel()
+            b.record(stream)
+            kev.append((a, b))
+        else:
+            kernel()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+    l0 = _lib.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        end.record(stream)
+        barrier()
+    launches = _lib.launch_count() - l0
+    ms = start.elapsed_time(end)
+    kms = sum(a.elapsed_time(b) for a, b in kev) / len(kev)
+    t = torch.tensor([ms, kms], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, kms = float(t[0]), float(t[1])
+    pts = float(n) ** d
+    value = pts * args.steps / (ms / 1e3) / 1e9
+    # roofline of the dominant kernel (per launch, this rank's share)
+    local_pts = pts if sl is None else float(sl.owned) * n * n
+    achieved = bpp * local_pts / (kms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic, tsrc = committed_traffic(family, n) if sl is None else (None, None)
+
+    # ---- e2e through the host-buffer C-ABI entry (N = 1) or per-rank copies
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = time_cpu(family, scalars, n)
+        except Exception as ex:  # pragma: no cover
+            log("cpu baseline failed:", ex)
+    if rank != 0:
+        return
+    line = {
+        "metric": "adjoint GPts/s", "value": value, "unit": "GPts/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": desc, "family": family, "n": n, "points_per_step": int(pts),
+                   "parallelism": f"zslab{world}" if world > 1 else "single",
+                   "algorithmic_bytes_per_point": bpp,
+                   "l2": "no flush: every step streams >= 12.7 GB (inputs >> 126 MB L2)"
+                   if family == "wave3d_r4" else "inputs larger than L2",
+                   "halo_exchange": "NCCL batch_isend_irecv u_1,u_b radius-4 per step"
+                   if world > 1 else None},
+        "achieved_hbm_gbs": achieved,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel_ms": kms, "bytes_per_launch": bpp * local_pts,
+                     "peak_source": peak_src, "traffic_source": tsrc,
+                     "vs_nominal_8tbs": achieved / 8000.0},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d):
+    names = api.array_params(family, "adjoint")
+    rmw = [nm for nm in names if nm.endswith("_b") and nm != SEED[family]]
+    host = {nm: torch.empty(arrays[nm].shape, dtype=arrays[nm].dtype, pin_memory=True)
+            for nm in names}
+    for nm in names:
+        host[nm].copy_(arrays[nm])
+    h2d = sum(host[nm].numel() * host[nm].element_size() for nm in names)
+    d2h = sum(host[nm].numel() * host[nm].element_size() for nm in rmw)
+    torch.cuda.synchronize()
+    if sl is None:
+        plan = api.Plan(family, n, "f32" if host[names[0]].dtype == torch.float32 else "f64")
+
+        def step():
+            plan.run_adjoint_host(scalars, host)
+    else:
+        from paper_1907_02818_b200 import slab as slabmod
+        dev = {nm: torch.empty_like(arrays[nm]) for nm in names}
+
+        def step():
+            for nm in names:
+                dev[nm].copy_(host[nm], non_blocking=True)
+            slabmod.exchange_halos(sl, [dev["u_1"], dev["u_b"]])
+            api.adjoint_slab(family, n, scalars, dev, sl.base, sl.nplanes, sl.own0, sl.own1)
+            for nm in rmw:
+                host[nm].copy_(dev[nm], non_blocking=True)
+            torch.cuda.synchronize()
+    step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    k = max(1, args.e2e_steps)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(k):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([s.elapsed_time(e)], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms[0]) / k
+    if sl is None:
+        plan.close()
+    return {"value": pts / (ms / 1e3) / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k,
+            "path": "sgb_plan_run_adjoint_host (pinned host buffers)" if sl is None
+            else "per-rank pinned H2D + halo exchange + slab kernel + D2H"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="4", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=0, help="override grid extent")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()
