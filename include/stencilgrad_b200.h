@@ -153,6 +153,11 @@ int sgb_fill_random_f32(float* dst, long long count, long long index_base, uint6
 int sgb_fill_random_f64(double* dst, long long count, long long index_base, uint64_t seed,
                         uint64_t stream_id, int kind, double mean, double scale,
                         sgb_stream_t stream);
+/* N(mean, scale^2) on planes [i_base, i_base+nplanes) of an n^3 grid with the
+ * h-point shell set to zero (one fused pass; same counter-based values as
+ * sgb_fill_random_f32 at the same global indices) */
+int sgb_fill_normal3d_f32(float* dst, int n, int i_base, int nplanes, int halo, uint64_t seed,
+                          uint64_t stream_id, double mean, double scale, sgb_stream_t stream);
 /* zero the h-point shell of planes [i_base, i_base+nplanes) of an n^d grid
  * (d = 1, 2 or 3; for d < 3 pass i_base = 0, nplanes = n) */
 int sgb_zero_halo_f32(float* a, int d, int n, int h, int i_base, int nplanes,

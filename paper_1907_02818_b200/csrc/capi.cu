@@ -46,7 +46,7 @@ static int star_kernel_version(int mode) {
     const char* e = std::getenv("SGB_STAR_KERNEL");
     forced = e ? std::atoi(e) : 0;
   }
-  if (forced >= 1 && forced <= 5) return forced;
+  if (forced >= 1 && forced <= 6) return forced;
   return mode == 2 ? 5 : 1;
 }
 static int star_tile_rows() {
@@ -81,14 +81,16 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
   Slab3 g{n, i_base, nplanes};
   if (star3_tma_supported<MODE, T>(n)) {
     const int ver = star_kernel_version(MODE);
-    if (ver == 4 || ver == 5) {
-#define SGB_V4(TJ, RMWT)                                                                     \
-  return star3_v4_gather<MODE, TJ, RMWT>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c, \
-                                         (float*)c_b, (const float*)u_1, (float*)u_1_b,        \
-                                         (float*)u_2_b, (const float*)u_b, s, name)
-      if (ver == 4) SGB_V4(16, false);
-      if (star_tile_rows() == 16) SGB_V4(16, true);
-      SGB_V4(32, true);
+    if (ver >= 4 && ver <= 6) {
+#define SGB_V4(TJ, RMWT, ROLES)                                                              \
+  return star3_v4_gather<MODE, TJ, RMWT, ROLES>(g, lo, hi, out_i0, out_i1, (float)D,           \
+                                                (const float*)c, (float*)c_b, (const float*)u_1, \
+                                                (float*)u_1_b, (float*)u_2_b,                    \
+                                                (const float*)u_b, s, name)
+      if (ver == 4) SGB_V4(16, false, false);
+      if (ver == 6) SGB_V4(32, true, true);
+      if (star_tile_rows() == 16) SGB_V4(16, true, false);
+      SGB_V4(32, true, false);
 #undef SGB_V4
     }
     if (ver == 3)

@@ -21,13 +21,18 @@ __device__ __forceinline__ uint64_t hash3(uint64_t seed, uint64_t stream, uint64
   return mix64(seed * 0x9E3779B97F4A7C15ull + mix64(stream + 0xD1B54A32D192ED03ull) + ctr);
 }
 
-// kind 0: N(mean, scale^2) by Box-Muller in fp64; kind 1: U[mean, mean + scale)
+// kind 0: N(mean, scale^2); kind 1: U[mean, mean + scale).
+// Normals come in Box-Muller pairs: indices 2m and 2m+1 share the hash of m
+// (cos / sin branch), so value(index) is still a pure function of the index.
 __device__ __forceinline__ double draw(uint64_t seed, uint64_t stream, uint64_t idx, int kind) {
-  const uint64_t h1 = hash3(seed, stream, 2 * idx), h2 = hash3(seed, stream, 2 * idx + 1);
-  const double u2 = (double)(h2 >> 11) * 0x1.0p-53;
-  if (kind == 1) return u2;
-  const double u1 = (double)((h1 >> 11) + 1) * 0x1.0p-53;  // (0, 1]
-  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  if (kind == 1) return (double)(hash3(seed, stream, idx) >> 11) * 0x1.0p-53;
+  const uint64_t h = hash3(seed, stream, idx >> 1);
+  const float u1 = ((float)(uint32_t)(h >> 40) + 1.0f) * 0x1.0p-24f;  // (0, 1]
+  const float u2 = (float)(uint32_t)(h & 0xFFFFFFu) * 0x1.0p-24f;     // [0, 1)
+  const float rad = sqrtf(-2.0f * __logf(u1));
+  float sn, cs;
+  __sincosf(6.283185307179586f * u2, &sn, &cs);
+  return (double)((idx & 1) ? rad * sn : rad * cs);
 }
 
 template <typename T>
@@ -37,6 +42,34 @@ __global__ void fill_random_kernel(T* dst, long long count, long long base, uint
        t += (long long)gridDim.x * blockDim.x) {
     const double z = draw(seed, stream, (uint64_t)(base + t), kind);
     dst[t] = (T)(mean + scale * z);
+  }
+}
+
+// 3D fill with a fused zero halo: planes [i_base, i_base+nplanes) of an n^3
+// grid, h-point zero shell, N(mean, scale^2) elsewhere; 4 points per thread.
+__global__ void fill_normal3d_f32_kernel(float* dst, long long n, long long i_base,
+                                         long long nplanes, int h, uint64_t seed,
+                                         uint64_t stream, float mean, float scale) {
+  const long long k = 4 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+  const long long j = blockIdx.y;
+  if (k >= n) return;
+  for (long long li = blockIdx.z; li < nplanes; li += gridDim.z) {
+    const long long i = i_base + li;
+    const long long g = (i * n + j) * n + k;
+    float v[4];
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+      const long long kk = k + m;
+      const bool halo = i < h || i >= n - h || j < h || j >= n - h || kk < h || kk >= n - h;
+      v[m] = (halo || kk >= n) ? 0.f
+                               : mean + scale * (float)draw(seed, stream, (uint64_t)(g + m), 0);
+    }
+    float* p = dst + (li * n + j) * n + k;
+    if (n % 4 == 0) {
+      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      for (int m = 0; m < 4 && k + m < n; m++) p[m] = v[m];
+    }
   }
 }
 
@@ -133,6 +166,16 @@ int sgb_zero_halo_f64(double* a, int d, int n, int h, int i_base, int nplanes,
   zero_halo_kernel<double><<<fill_grid(per * nplanes), 256, 0, as_stream(stream)>>>(
       a, d, n, h, i_base, nplanes);
   return launch_status("sgb_zero_halo_f64");
+}
+
+int sgb_fill_normal3d_f32(float* dst, int n, int i_base, int nplanes, int halo, uint64_t seed,
+                          uint64_t stream_id, double mean, double scale, sgb_stream_t stream) {
+  if (!dst || n <= 0 || nplanes <= 0 || halo < 0) return SGB_EINVAL;
+  dim3 b(64), g((unsigned)((n / 4 + 63) / 64 + ((n % 4) ? 1 : 0)), (unsigned)n,
+                (unsigned)(nplanes < 64 ? nplanes : 64));
+  fill_normal3d_f32_kernel<<<g, b, 0, as_stream(stream)>>>(dst, n, i_base, nplanes, halo, seed,
+                                                           stream_id, (float)mean, (float)scale);
+  return launch_status("sgb_fill_normal3d_f32");
 }
 
 int sgb_fill_layered_f32(float* c, int n, int layers, double lo, double hi, uint64_t seed,

@@ -23,7 +23,7 @@
 
 namespace sgb {
 
-template <int MODE, int TJ_, bool RMW_TMA_>
+template <int MODE, int TJ_, bool RMW_TMA_, bool ROLES_ = false>
 struct StarTile4 {
   static constexpr int R = Star3<MODE>::R;
   static constexpr bool RMW_TMA = RMW_TMA_;  // old adjoint values staged by TMA
@@ -33,7 +33,9 @@ struct StarTile4 {
   static constexpr int RING = 2 * R + 1;  // 9 or 3: a multiple of NS
   static constexpr int NS = 3;
   static constexpr int NQB = 2;
-  static constexpr int THREADS = 16 * TJ;
+  static constexpr bool ROLES = ROLES_;  // field-specialised warp halves
+  static constexpr int HALF = 16 * TJ;   // threads covering the tile once
+  static constexpr int THREADS = ROLES ? 2 * HALF : HALF;
   static constexpr int MINB = THREADS <= 256 ? 2 : 1;
   static constexpr int BOX_BYTES = BW * BJ * 4;
   static constexpr int BF = ((BOX_BYTES + 127) / 128) * 128 / 4;
@@ -44,7 +46,7 @@ struct StarTile4 {
   static constexpr int QELEMS = (BW / 4) * BJ;
   static constexpr int EPT = (QELEMS + THREADS - 1) / THREADS;
   static constexpr size_t SMEM =
-      (size_t)(NS * SF + NQB * BF) * 4 + (size_t)QD * THREADS * 16 + NS * 8;
+      (size_t)(NS * SF + NQB * BF) * 4 + (size_t)QD * HALF * 16 + NS * 8;
   static_assert(RING % NS == 0, "static stage indexing");
 };
 
@@ -91,9 +93,9 @@ __device__ __forceinline__ void field1(const float* F, int crow, int col, float 
   }
 }
 
-template <int MODE, int TJ, bool RMWT>
-__global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT>::THREADS,
-                                  StarTile4<MODE, TJ, RMWT>::MINB)
+template <int MODE, int TJ, bool RMWT, bool ROLES>
+__global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT, ROLES>::THREADS,
+                                  StarTile4<MODE, TJ, RMWT, ROLES>::MINB)
     star3_v4_kernel(const __grid_constant__ CUtensorMap tm_c,
                     const __grid_constant__ CUtensorMap tm_ub,
                     const __grid_constant__ CUtensorMap tm_u1,
@@ -102,20 +104,26 @@ __global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT>::THREADS,
                     const __grid_constant__ CUtensorMap tm_u2b, float* __restrict__ c_b,
                     float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n, int i_base,
                     int lo, int hi, int out_i0, int out_i1, int chunk, int tiles_k, float D) {
-  using Tl = StarTile4<MODE, TJ, RMWT>;
+  using Tl = StarTile4<MODE, TJ, RMWT, ROLES>;
   using S3 = Star3<MODE>;
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
+  constexpr int HALF = Tl::HALF;
   constexpr int RING = Tl::RING, NS = Tl::NS, NQB = Tl::NQB, BF = Tl::BF, QD = Tl::QD;
   constexpr int SF = Tl::SF, TILE = Tl::TILE;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage = reinterpret_cast<float*>(smem_raw);  // [NS][c, ub, u1, (cb, u1b, u2b)]
   float* qbuf = stage + NS * SF;                       // [NQB]
-  float4* gq = reinterpret_cast<float4*>(qbuf + NQB * BF);  // [QD][256]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(gq + QD * Tl::THREADS);
+  float4* gq = reinterpret_cast<float4*>(qbuf + NQB * BF);  // [QD][HALF]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gq + QD * HALF);
 
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  // ROLES: threads [0, HALF) carry Lap(u_1) and emit c_b, [HALF, 2 HALF) carry
+  // the q stencil and emit u_1_b; otherwise every thread carries both fields.
+  const bool lap_part = !ROLES || tid < HALF;  // warp-uniform
+  const bool q_part = !ROLES || tid >= HALF;
+  const int rt = ROLES ? (tid % HALF) : tid;
+  const int tx = rt & 15, ty = rt >> 4;
   const int tk = blockIdx.x % tiles_k, tj = blockIdx.x / tiles_k;
   const int k0 = tk * Tl::TK, j0 = tj * Tl::TJ;
   const int o_begin = out_i0 + blockIdx.y * chunk;
@@ -179,6 +187,7 @@ __global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT>::THREADS,
   float4 accL[RING], accQ[RING];
 #pragma unroll
   for (int s = 0; s < RING; s++) accL[s] = accQ[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4(&AQ)[RING] = ROLES ? accL : accQ;  // the q role reuses the one array
 
   for (int base = 0; base < P; base += RING) {
     const int par0 = base / NS;
@@ -208,8 +217,8 @@ __global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT>::THREADS,
 
         tma::mbar_wait(&bars[s], (par0 + ph / NS) & 1);
         if (Tl::RMW_TMA && emit) {
-          cb_old = lds4(OLD);
-          u1b_old = lds4(OLD + TILE);
+          if (lap_part) cb_old = lds4(OLD);
+          if (q_part) u1b_old = lds4(OLD + TILE);
         }
 
         // ---- q = D c(^2) u_b [x in B] over the halo box
@@ -242,31 +251,38 @@ __global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT>::THREADS,
           if (pin) {
             float4 ubm = lds4(UBs + crow + col);
             if (!interior) ubm = mul4(ubm, kmask);
-            g = S3::kC2 ? mul4(muls4(gf, lds4(Cs + crow + col)), ubm) : muls4(gf, ubm);
-            accQ[ph] = fmas4(2.f, ubm, accQ[ph]);
-            if (S3::kU2 && col_ok && jin && p >= o_begin && p < o_end) {
-              float* ptr = u_2_b + (long long)(p - i_base) * plane + coff;
-              const float4 u2 = Tl::RMW_TMA ? lds4(OLD + 2 * TILE)
-                                            : __ldcs(reinterpret_cast<const float4*>(ptr));
-              __stcs(reinterpret_cast<float4*>(ptr),
-                     make_float4(kin[0] ? u2.x - ubm.x : u2.x, kin[1] ? u2.y - ubm.y : u2.y,
-                                 kin[2] ? u2.z - ubm.z : u2.z, kin[3] ? u2.w - ubm.w : u2.w));
+            if (lap_part)
+              g = S3::kC2 ? mul4(muls4(gf, lds4(Cs + crow + col)), ubm) : muls4(gf, ubm);
+            if (q_part) {
+              AQ[ph] = fmas4(2.f, ubm, AQ[ph]);
+              if (S3::kU2 && col_ok && jin && p >= o_begin && p < o_end) {
+                float* ptr = u_2_b + (long long)(p - i_base) * plane + coff;
+                const float4 u2 = Tl::RMW_TMA ? lds4(OLD + 2 * TILE)
+                                              : __ldcs(reinterpret_cast<const float4*>(ptr));
+                __stcs(reinterpret_cast<float4*>(ptr),
+                       make_float4(kin[0] ? u2.x - ubm.x : u2.x, kin[1] ? u2.y - ubm.y : u2.y,
+                                   kin[2] ? u2.z - ubm.z : u2.z, kin[3] ? u2.w - ubm.w : u2.w));
+              }
             }
           }
-          gq[(it % QD) * Tl::THREADS + tid] = g;
+          if (lap_part) gq[(it % QD) * HALF + rt] = g;
         }
         __syncthreads();
         // the stage read by the previous plane is free now: refill it
         if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
 
-        field1<R, RING>(U1s, crow, col, w0, wr, accL, ph);
-        field1<R, RING>(Q, crow, col, w0, wr, accQ, ph);
+        if (ROLES) {
+          field1<R, RING>(q_part ? Q : U1s, crow, col, w0, wr, accL, ph);
+        } else {
+          field1<R, RING>(U1s, crow, col, w0, wr, accL, ph);
+          field1<R, RING>(Q, crow, col, w0, wr, accQ, ph);
+        }
 
         // ---- emit output plane o = p - R (all of its contributions are in)
         if (emit && col_ok) {
           const int es = (ph + R + 1) % RING;
-          if (oin && jin) {
-            const float4 g = gq[((it - R) % QD) * Tl::THREADS + tid];
+          if (lap_part && oin && jin) {
+            const float4 g = gq[((it - R) % QD) * HALF + rt];
             float4 nv = fma4(g, accL[es], cb_old);
             if (!interior)
               nv = make_float4(kin[0] ? nv.x : cb_old.x, kin[1] ? nv.y : cb_old.y,
@@ -274,10 +290,11 @@ __global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT>::THREADS,
             __stcs(reinterpret_cast<float4*>(c_b + gidx), nv);
           }
           const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
-          if (interior) {
-            if (oout <= R) __stcs(reinterpret_cast<float4*>(u_1_b + gidx), add4(u1b_old, accQ[es]));
+          if (!q_part) {
+          } else if (interior) {
+            if (oout <= R) __stcs(reinterpret_cast<float4*>(u_1_b + gidx), add4(u1b_old, AQ[es]));
           } else {
-            const float4 a = accQ[es];
+            const float4 a = AQ[es];
             const float av[4] = {a.x, a.y, a.z, a.w};
             float4 nv = u1b_old;
             float* nvp = reinterpret_cast<float*>(&nv);
@@ -299,12 +316,12 @@ __global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT>::THREADS,
   }
 }
 
-template <int MODE, int TJ, bool RMWT>
+template <int MODE, int TJ, bool RMWT, bool ROLES = false>
 inline int star3_v4_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
                            long long out_i1, float D, const float* c, float* c_b,
                            const float* u_1, float* u_1_b, float* u_2_b, const float* u_b,
                            cudaStream_t s, const char* name) {
-  using Tl = StarTile4<MODE, TJ, RMWT>;
+  using Tl = StarTile4<MODE, TJ, RMWT, ROLES>;
   CUtensorMap maps[6];
   int rc = 0;
   rc |= encode_3d(&maps[0], c, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
@@ -317,7 +334,7 @@ inline int star3_v4_gather(const Slab3& g, long long lo, long long hi, long long
   if (rc) return SGB_EINVAL;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(star3_v4_kernel<MODE, TJ, RMWT>,
+    cudaFuncSetAttribute(star3_v4_kernel<MODE, TJ, RMWT, ROLES>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
     attr_set = true;
   }
@@ -327,7 +344,7 @@ inline int star3_v4_gather(const Slab3& g, long long lo, long long hi, long long
   const int chunks = choose_chunks((long long)tiles_k * tiles_j, nout, Tl::R, Tl::MINB);
   const int chunk = (int)((nout + chunks - 1) / chunks);
   dim3 grid((unsigned)(tiles_k * tiles_j), (unsigned)((nout + chunk - 1) / chunk));
-  star3_v4_kernel<MODE, TJ, RMWT><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
+  star3_v4_kernel<MODE, TJ, RMWT, ROLES><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
       maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
       (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D);
   return launch_status(name);

@@ -61,23 +61,28 @@ def decompose(n: int, radius: int, world: int, rank: int) -> Slab:
     return Slab(n, radius, rank, world, own0, own1, own0 - lo, own1 - own0 + lo + hi)
 
 
-def exchange_halos(slab: Slab, fields, group=None) -> None:
-    """Fill the halo planes of each local field (shape [nplanes, ...]) from the
-    neighbours' owned edge planes: one batched isend/irecv round."""
-    if slab.world == 1:
-        return
+def halo_ops(slab: Slab, fields, group=None):
+    """The point-to-point ops of one halo refresh: each rank sends its R owned
+    edge planes to each neighbour and receives that neighbour's into its halo.
+    Planes are contiguous, so every slice is a contiguous view (no packing)."""
     R = slab.radius
     ops = []
     below, above = slab.rank - 1, slab.rank + 1
     top = slab.halo_lo + slab.owned  # local index one past the owned planes
     for f in fields:
-        # planes are contiguous, so every slice below is a contiguous view:
-        # neighbours send straight from their owned edge into our halo
         if below >= 0:
             ops.append(dist.P2POp(dist.isend, f[slab.halo_lo:slab.halo_lo + R], below, group))
             ops.append(dist.P2POp(dist.irecv, f[0:slab.halo_lo], below, group))
         if above < slab.world:
             ops.append(dist.P2POp(dist.isend, f[top - R:top], above, group))
             ops.append(dist.P2POp(dist.irecv, f[top:top + R], above, group))
-    for req in dist.batch_isend_irecv(ops):
+    return ops
+
+
+def exchange_halos(slab: Slab, fields, group=None) -> None:
+    """Fill the halo planes of each local field (shape [nplanes, ...]) from the
+    neighbours' owned edge planes: one batched isend/irecv round."""
+    if slab.world == 1:
+        return
+    for req in dist.batch_isend_irecv(halo_ops(slab, fields, group)):
         req.wait()
