@@ -53,7 +53,8 @@ static int star_tile_rows() {
   static int tj = -1;
   if (tj < 0) {
     const char* e = std::getenv("SGB_TJ");
-    tj = (e && std::atoi(e) == 16) ? 16 : 32;
+    tj = e ? std::atoi(e) : 32;
+    if (tj != 16 && tj != 24) tj = 32;
   }
   return tj;
 }
@@ -90,6 +91,7 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
       if (ver == 4) SGB_V4(16, false, false);
       if (ver == 6) SGB_V4(32, true, true);
       if (star_tile_rows() == 16) SGB_V4(16, true, false);
+      if (star_tile_rows() == 24) SGB_V4(24, true, false);
       SGB_V4(32, true, false);
 #undef SGB_V4
     }

@@ -18,6 +18,10 @@ struct sgb_plan {
   size_t bytes = 0;
   std::vector<void*> dev;
   std::vector<bool> rmw;  // accumulated adjoint arrays (copied back)
+  // 3D families: copies and compute pipelined over i-chunks on three streams
+  cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  int chunks = 1;
 };
 
 namespace {
@@ -76,13 +80,86 @@ sgb_plan* sgb_plan_create(const char* family, int n, int dtype_bytes) {
     p->dev.push_back(d);
     p->rmw.push_back(fs->rmw[a]);
   }
+  if (fs->dims == 3 && p->dtype == 4) {
+    // pipelined host path: ~8 i-chunks (at least 2R planes each)
+    p->chunks = n >= 128 ? 8 : 1;
+    cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p->s_cmp, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
+    p->ev_in.resize(p->chunks);
+    p->ev_out.resize(p->chunks);
+    for (int c = 0; c < p->chunks; c++) {
+      cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&p->ev_out[c], cudaEventDisableTiming);
+    }
+  }
   return p;
 }
 
 void sgb_plan_destroy(sgb_plan* plan) {
   if (!plan) return;
   for (void* d : plan->dev) cudaFree(d);
+  for (auto e : plan->ev_in) cudaEventDestroy(e);
+  for (auto e : plan->ev_out) cudaEventDestroy(e);
+  if (plan->s_h2d) cudaStreamDestroy(plan->s_h2d);
+  if (plan->s_cmp) cudaStreamDestroy(plan->s_cmp);
+  if (plan->s_d2h) cudaStreamDestroy(plan->s_d2h);
   delete plan;
+}
+
+// 3D fp32 families: H2D of chunk c+1 (copy engine), the slab adjoint of
+// chunk c (SMs) and D2H of chunk c-1 (other copy engine) overlap.  Output
+// planes [o_c, o_{c+1}) need input planes up to o_{c+1} + R - 1, so chunk c's
+// kernel waits for the H2D of chunks c and c+1.
+static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
+  const int n = p->n, C = p->chunks;
+  const int R = p->family == "wave3d_r4" ? 4 : 1;
+  const size_t plane = (size_t)n * n * 4;
+  auto bound = [&](int c) { return (int)((long long)n * c / C); };
+  const size_t na = p->dev.size();
+  for (int c = 0; c < C; c++) {
+    const int a = bound(c), b = bound(c + 1);
+    for (size_t k = 0; k < na; k++) {
+      if (cudaMemcpyAsync((char*)p->dev[k] + a * plane, (const char*)arrays[k] + a * plane,
+                          (b - a) * plane, cudaMemcpyHostToDevice, p->s_h2d) != cudaSuccess) {
+        sgb::set_error("sgb_plan_run_adjoint_host: H2D copy failed");
+        return -1;
+      }
+    }
+    cudaEventRecord(p->ev_in[c], p->s_h2d);
+  }
+  for (int c = 0; c < C; c++) {
+    const int a = bound(c), b = bound(c + 1);
+    cudaStreamWaitEvent(p->s_cmp, p->ev_in[c], 0);
+    if (c + 1 < C) cudaStreamWaitEvent(p->s_cmp, p->ev_in[c + 1], 0);
+    (void)R;
+    float** d = reinterpret_cast<float**>(p->dev.data());
+    int rc;
+    if (p->family == "wave3d_r4")
+      rc = wave3d_r4_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], 0, n, a, b,
+                                p->s_cmp);
+    else if (p->family == "wave3d_c")
+      rc = wave3d_c_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], 0, n, a, b,
+                               p->s_cmp);
+    else
+      return SGB_EINVAL;
+    if (rc != 0) return rc;
+    cudaEventRecord(p->ev_out[c], p->s_cmp);
+    cudaStreamWaitEvent(p->s_d2h, p->ev_out[c], 0);
+    for (size_t k = 0; k < na; k++) {
+      if (!p->rmw[k]) continue;
+      if (cudaMemcpyAsync((char*)arrays[k] + a * plane, (const char*)p->dev[k] + a * plane,
+                          (b - a) * plane, cudaMemcpyDeviceToHost, p->s_d2h) != cudaSuccess) {
+        sgb::set_error("sgb_plan_run_adjoint_host: D2H copy failed");
+        return -1;
+      }
+    }
+  }
+  if (cudaStreamSynchronize(p->s_d2h) != cudaSuccess) {
+    sgb::set_error("sgb_plan_run_adjoint_host: stream synchronisation failed");
+    return -1;
+  }
+  return 0;
 }
 
 int sgb_plan_run_adjoint_host(sgb_plan* p, const double* scalars, void** arrays,
@@ -90,6 +167,20 @@ int sgb_plan_run_adjoint_host(sgb_plan* p, const double* scalars, void** arrays,
   if (!p || !arrays || !scalars) {
     sgb::set_error("sgb_plan_run_adjoint_host: null argument");
     return SGB_EINVAL;
+  }
+  if (p->chunks > 1 && (p->family == "wave3d_r4" || p->family == "wave3d_c")) {
+    for (size_t a = 0; a < p->dev.size(); a++)
+      if (!arrays[a]) {
+        sgb::set_error("sgb_plan_run_adjoint_host: null host array");
+        return SGB_EINVAL;
+      }
+    // order the pipeline after the caller's stream, then run on our streams
+    cudaEvent_t start;
+    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    cudaEventRecord(start, sgb::as_stream(stream));
+    cudaStreamWaitEvent(p->s_h2d, start, 0);
+    cudaEventDestroy(start);
+    return run_pipelined(p, scalars, arrays);
   }
   cudaStream_t s = sgb::as_stream(stream);
   const size_t na = p->dev.size();

@@ -21,6 +21,10 @@
 
 #include "star3d_v3.cuh"
 
+#ifndef SGB_TREE_SUM
+#define SGB_TREE_SUM 1
+#endif
+
 namespace sgb {
 
 template <int MODE, int TJ_, bool RMW_TMA_, bool ROLES_ = false>
@@ -30,13 +34,16 @@ struct StarTile4 {
   static constexpr int TK = 64, TJ = TJ_, HK = 4, HJ = R;
   static constexpr int BW = TK + 2 * HK;  // 72 floats = 288 B rows
   static constexpr int BJ = TJ + 2 * HJ;
-  static constexpr int RING = 2 * R + 1;  // 9 or 3: a multiple of NS
-  static constexpr int NS = 3;
+  static constexpr int RING = 2 * R + 1;  // 9 or 3
+  // 3 stages (RING % 3 == 0: static stage index); the 2-CTA/SM variant
+  // (TJ 16 with TMA-staged RMW) needs 2 stages to fit two CTAs' smem.
+  static constexpr int NS = (TJ_ == 16 && RMW_TMA_) ? 2 : 3;
   static constexpr int NQB = 2;
   static constexpr bool ROLES = ROLES_;  // field-specialised warp halves
   static constexpr int HALF = 16 * TJ;   // threads covering the tile once
   static constexpr int THREADS = ROLES ? 2 * HALF : HALF;
   static constexpr int MINB = THREADS <= 256 ? 2 : 1;
+  static constexpr bool STATIC_STAGE = RING % NS == 0;
   static constexpr int BOX_BYTES = BW * BJ * 4;
   static constexpr int BF = ((BOX_BYTES + 127) / 128) * 128 / 4;
   static constexpr int TILE = TK * TJ;  // floats of one adjoint tile
@@ -47,7 +54,6 @@ struct StarTile4 {
   static constexpr int EPT = (QELEMS + THREADS - 1) / THREADS;
   static constexpr size_t SMEM =
       (size_t)(NS * SF + NQB * BF) * 4 + (size_t)QD * HALF * 16 + NS * 8;
-  static_assert(RING % NS == 0, "static stage indexing");
 };
 
 // in-plane k-direction stencil for 4 points: window a|b|c = k0-4 .. k0+7
@@ -81,9 +87,22 @@ __device__ __forceinline__ void field1(const float* F, int crow, int col, float 
   constexpr int BW = 72;
   const float* cp = F + crow + col;
   const float4 a = lds4(cp - 4), b = lds4(cp), c = lds4(cp + 4);
+#if SGB_TREE_SUM
+  // j direction as a short tree (independent partial sums) to cut the
+  // dependent FFMA2 chain behind each shared-memory load
+  float4 jp[2];
+  jp[0] = muls4(wr[1], add4(lds4(cp - BW), lds4(cp + BW)));
+  jp[1] = R >= 2 ? muls4(wr[2], add4(lds4(cp - 2 * BW), lds4(cp + 2 * BW)))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int r = 3; r <= R; r++)
+    jp[r & 1] = fmas4(wr[r], add4(lds4(cp - r * BW), lds4(cp + r * BW)), jp[r & 1]);
+  const float4 in = add4(kstencil2<R>(a, b, c, w0, wr), R >= 2 ? add4(jp[0], jp[1]) : jp[0]);
+#else
   float4 in = kstencil2<R>(a, b, c, w0, wr);
 #pragma unroll
   for (int r = 1; r <= R; r++) in = fmas4(wr[r], add4(lds4(cp - r * BW), lds4(cp + r * BW)), in);
+#endif
   acc[ph] = add4(acc[ph], in);
   acc[(ph + R) % RING] = muls4(wr[R], b);
 #pragma unroll
@@ -190,12 +209,12 @@ __global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT, ROLES>::THREADS,
   float4(&AQ)[RING] = ROLES ? accL : accQ;  // the q role reuses the one array
 
   for (int base = 0; base < P; base += RING) {
-    const int par0 = base / NS;
+    const int par0 = base / NS;  // used when RING % NS == 0
 #pragma unroll
     for (int ph = 0; ph < RING; ph++) {
       const int it = base + ph;
       if (it < P) {
-        const int s = ph % NS;  // == it % NS
+        const int s = Tl::STATIC_STAGE ? ph % NS : it % NS;
         const int p = pstart + it;
         const float* Cs = stage + s * SF;
         const float* UBs = Cs + BF;
@@ -215,7 +234,7 @@ __global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT, ROLES>::THREADS,
           if (oin && jin) cb_old = __ldcs(reinterpret_cast<const float4*>(c_b + gidx));
         }
 
-        tma::mbar_wait(&bars[s], (par0 + ph / NS) & 1);
+        tma::mbar_wait(&bars[s], Tl::STATIC_STAGE ? ((par0 + ph / NS) & 1) : ((it / NS) & 1));
         if (Tl::RMW_TMA && emit) {
           if (lap_part) cb_old = lds4(OLD);
           if (q_part) u1b_old = lds4(OLD + TILE);

@@ -207,3 +207,24 @@ def test_dot_product_test_on_gpu(api):
         rhs = float(sum(np.sum(v[a] * res[f.adjoints[f.arrays.index(a)]]) for a in inputs))
         err = abs(lhs - rhs) / (1 + abs(rhs))
         assert err <= 1e-4, (name, err)
+
+
+@pytest.mark.parametrize("name,n,dtype", [("wave3d_r4", 136, "f32"), ("wave3d_c", 128, "f32"),
+                                          ("wave3d_r4", 40, "f64"), ("burgers2d", 64, "f64"),
+                                          ("wave1d", 300, "f64")])
+def test_host_buffer_plan_entry(api, name, n, dtype):
+    """sgb_plan_run_adjoint_host (host arrays in, accumulated adjoints out;
+    pipelined over i-chunks for 3D fp32) equals the device-pointer entry."""
+    import torch
+    scalars, grids, adjs = gen.family_inputs(name, n, seed=4, accumulate=True)
+    np_dt = np.float32 if dtype == "f32" else np.float64
+    host = {k: np.ascontiguousarray(v.astype(np_dt)) for k, v in {**grids, **adjs}.items()}
+    want = api.run_program(name, n, scalars, {k: host[k].astype(np.float64) for k in grids},
+                           {k: host[k].astype(np.float64) for k in adjs}, dtype=dtype)
+    plan = api.Plan(name, n, dtype)
+    plan.run_adjoint_host(scalars, host)
+    plan.close()
+    f = oracle.family(name)
+    for k in adjs:
+        got = host[k].astype(np.float64)
+        assert np.array_equal(got, want[k]), k
