@@ -13,7 +13,7 @@ import re
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 HEADER = os.path.join(ROOT, "include", "stencilgrad_b200.h")
-LIB_PATH = os.path.join(PKG, "libstencilgrad_b200.so")
+LIB_PATH = os.environ.get("SGB_LIB_PATH") or os.path.join(PKG, "libstencilgrad_b200.so")
 
 SGB_GUARD = 1
 SGB_EINVAL = -10000

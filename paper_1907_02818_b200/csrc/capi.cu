@@ -38,16 +38,17 @@ static bool guard_ok(int fam, long long n) {
 }
 
 // ------------------------------------------------------------------ 3D stars
-// Kernel selection for the TMA path: v2 (warp-specialised) for radius 4, v1
-// for radius 1 by default; SGB_STAR_KERNEL=1|2 and SGB_TJ=16|32 override.
+// Kernel selection for the TMA path ("Measured path"): v7 for
+// radius 4, v1 for radius 1 by default; SGB_STAR_KERNEL=1..7 and
+// SGB_TJ=16|24|32 select the earlier designs for A/B measurements.
 static int star_kernel_version(int mode) {
   static int forced = -1;
   if (forced < 0) {
     const char* e = std::getenv("SGB_STAR_KERNEL");
     forced = e ? std::atoi(e) : 0;
   }
-  if (forced >= 1 && forced <= 6) return forced;
-  return mode == 2 ? 5 : 1;
+  if (forced >= 1 && forced <= 7) return forced;
+  return mode == 2 ? 7 : 1;
 }
 static int star_tile_rows() {
   static int tj = -1;
@@ -82,6 +83,10 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
   Slab3 g{n, i_base, nplanes};
   if (star3_tma_supported<MODE, T>(n)) {
     const int ver = star_kernel_version(MODE);
+    if (ver == 7)
+      return star3_v7_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
+                                   (float*)c_b, (const float*)u_1, (float*)u_1_b, (float*)u_2_b,
+                                   (const float*)u_b, s, name);
     if (ver >= 4 && ver <= 6) {
 #define SGB_V4(TJ, RMWT, ROLES)                                                              \
   return star3_v4_gather<MODE, TJ, RMWT, ROLES>(g, lo, hi, out_i0, out_i1, (float)D,           \

@@ -370,3 +370,333 @@ inline int star3_v4_gather(const Slab3& g, long long lo, long long hi, long long
 }
 
 }  // namespace sgb
+
+namespace sgb {
+
+// ---------------------------------------------------------------------------
+// v7: shared-memory-traffic-lean variant of v5 (same TMA pipeline, 64x32
+// tile, TMA-staged adjoint tiles).  ncu on v5 shows the kernel bound by the
+// shared-memory crossbar (~160 B/pt incl. TMA fills).  v7 cuts it to ~115 B/pt:
+//   * warps [0,8) carry Lap(u_1) (emit c_b), warps [8,16) the q stencil
+//     (emit u_1_b); every thread owns 2 rows x 4 k-points of ONE field, so the
+//     j-direction reads (2R+2 rows per 8 points instead of 4R+2) are shared
+//     by the two rows in registers;
+//   * g = 2 D c u_b [y in B] is produced inside the q-pass (the thread that
+//     already holds c and u_b of that centre), so the centres are not re-read.
+template <int R, int RING>
+__device__ __forceinline__ void field2x4(const float* F, int r0, int col, float w0,
+                                         const float (&wr)[R + 1], float4 (&acc)[RING][2],
+                                         int ph) {
+  constexpr int BW = 72;
+  const float* row0 = F + r0 * BW + col;
+  const float4 b0 = lds4(row0), b1 = lds4(row0 + BW);
+  float4 in0 = kstencil2<R>(lds4(row0 - 4), b0, lds4(row0 + 4), w0, wr);
+  float4 in1 = kstencil2<R>(lds4(row0 + BW - 4), b1, lds4(row0 + BW + 4), w0, wr);
+  in0 = fmas4(wr[1], b1, in0);
+  in1 = fmas4(wr[1], b0, in1);
+#pragma unroll
+  for (int t = -R; t <= R + 1; t++) {
+    if (t == 0 || t == 1) continue;
+    const float4 v = lds4(row0 + t * BW);
+    const int d0 = t < 0 ? -t : t, d1 = t - 1 < 0 ? 1 - t : t - 1;
+    if (d0 <= R) in0 = fmas4(wr[d0], v, in0);
+    if (d1 <= R) in1 = fmas4(wr[d1], v, in1);
+  }
+  acc[ph][0] = add4(acc[ph][0], in0);
+  acc[ph][1] = add4(acc[ph][1], in1);
+  acc[(ph + R) % RING][0] = muls4(wr[R], b0);
+  acc[(ph + R) % RING][1] = muls4(wr[R], b1);
+#pragma unroll
+  for (int r = 1; r <= R; r++) {
+    if (r < R) {
+      acc[(ph + r) % RING][0] = fmas4(wr[r], b0, acc[(ph + r) % RING][0]);
+      acc[(ph + r) % RING][1] = fmas4(wr[r], b1, acc[(ph + r) % RING][1]);
+    }
+    acc[(ph + RING - r) % RING][0] = fmas4(wr[r], b0, acc[(ph + RING - r) % RING][0]);
+    acc[(ph + RING - r) % RING][1] = fmas4(wr[r], b1, acc[(ph + RING - r) % RING][1]);
+  }
+}
+
+template <int MODE>
+struct StarTile7 {
+  static constexpr int R = Star3<MODE>::R;
+  static constexpr int TK = 64, TJ = 32, HK = 4, HJ = R;
+  static constexpr int BW = TK + 2 * HK;
+  static constexpr int BJ = TJ + 2 * HJ;
+  static constexpr int RING = 2 * R + 1;
+#ifndef SGB_V7_NQB
+#define SGB_V7_NQB 2
+#endif
+#ifndef SGB_V7_QX
+#define SGB_V7_QX 2
+#endif
+  static constexpr int NS = 3, NQB = SGB_V7_NQB;
+  static constexpr int ROLE = 16 * (TJ / 2);  // 256 threads per field
+  static constexpr int THREADS = 2 * ROLE;
+  static constexpr int BOX_BYTES = BW * BJ * 4;
+  static constexpr int BF = ((BOX_BYTES + 127) / 128) * 128 / 4;
+  static constexpr int TILE = TK * TJ;
+  static constexpr int NT = Star3<MODE>::kU2 ? 3 : 2;
+  static constexpr int SF = 3 * BF + NT * TILE;
+  // g is written by q-pass threads and read by other (Lap) threads R planes
+  // later, after one more barrier; a fast thread may already run the next
+  // plane's q-pass, so the ring needs R + 2 slots (slot (it+1) != (it-R)).
+  static constexpr int QD = R + SGB_V7_QX;
+  static constexpr int QELEMS = (BW / 4) * BJ;
+  static constexpr int EPT = (QELEMS + THREADS - 1) / THREADS;
+  static constexpr size_t SMEM = (size_t)(NS * SF + NQB * BF + QD * TILE) * 4 + NS * 8;
+  static_assert(RING % NS == 0, "static stage index");
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
+    star3_v7_kernel(const __grid_constant__ CUtensorMap tm_c,
+                    const __grid_constant__ CUtensorMap tm_ub,
+                    const __grid_constant__ CUtensorMap tm_u1,
+                    const __grid_constant__ CUtensorMap tm_cb,
+                    const __grid_constant__ CUtensorMap tm_u1b,
+                    const __grid_constant__ CUtensorMap tm_u2b, float* __restrict__ c_b,
+                    float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n, int i_base,
+                    int lo, int hi, int out_i0, int out_i1, int chunk, int tiles_k, float D) {
+  using Tl = StarTile7<MODE>;
+  using S3 = Star3<MODE>;
+  constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
+  constexpr int RING = Tl::RING, NS = Tl::NS, NQB = Tl::NQB, BF = Tl::BF, QD = Tl::QD;
+  constexpr int SF = Tl::SF, TILE = Tl::TILE, ROLE = Tl::ROLE;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage = reinterpret_cast<float*>(smem_raw);  // [NS][c, ub, u1, cb, u1b, (u2b)]
+  float* qbuf = stage + NS * SF;                       // [NQB][box]
+  float* gq = qbuf + NQB * BF;                         // [QD][TJ][TK] (g of centres)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gq + QD * TILE);
+
+  const int tid = threadIdx.x;
+  const bool q_role = tid >= ROLE;  // warp-uniform
+  const int rt = q_role ? tid - ROLE : tid;
+  const int tx = rt & 15, ty = rt >> 4;  // 4 k-points x rows 2ty, 2ty+1
+  const int tk = blockIdx.x % tiles_k, tj = blockIdx.x / tiles_k;
+  const int k0 = tk * TK, j0 = tj * Tl::TJ;
+  const int o_begin = out_i0 + blockIdx.y * chunk;
+  const int o_end = min(o_begin + chunk, out_i1);
+  if (o_begin >= o_end) return;
+  const int pstart = o_begin - R;
+  const int P = (o_end - o_begin) + 2 * R;
+
+  const float w0 = S3::template w<float>(0);
+  float wr[R + 1];
+  wr[0] = w0;
+#pragma unroll
+  for (int r = 1; r <= R; r++) wr[r] = S3::template w<float>(r);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int it) {
+    const int s = it % NS;
+    float* dst = stage + s * SF;
+    const int p = pstart + it;
+    const int pl = p - i_base;
+    const bool emit = it >= 2 * R;
+    const bool u2 = S3::kU2 && p >= o_begin && p < o_end;
+    tma::mbar_arrive_expect_tx(&bars[s], 3 * Tl::BOX_BYTES +
+                                             ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE * 4);
+    tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + 2 * BF, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
+    if (emit) {
+      tma::load_3d(dst + 3 * BF, &tm_cb, &bars[s], k0, j0, pl - R);
+      tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
+    }
+    if (u2) tma::load_3d(dst + 3 * BF + 2 * TILE, &tm_u2b, &bars[s], k0, j0, pl);
+  };
+  if (tid == 0)
+    for (int it = 0; it < NS && it < P; it++) issue(it);
+
+  const int jr0 = j0 + 2 * ty, kc = k0 + 4 * tx;
+  const int r0 = 2 * ty + HJ, col = HK + 4 * tx;
+  const int trow = 2 * ty * TK + 4 * tx;  // offset of row 2ty in a 64x32 tile
+  const long long plane = (long long)n * n;
+  const long long coff = (long long)jr0 * n + kc;
+  const bool interior = j0 - HJ >= lo && j0 + Tl::TJ + HJ - 1 <= hi && k0 - HK >= lo &&
+                        k0 + TK + HK - 1 <= hi && j0 + Tl::TJ <= n && k0 + TK <= n;
+  bool kin[4];
+#pragma unroll
+  for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
+  const float gf = S3::kC2 ? 2.f * D : D;
+
+  float4 acc[RING][2];
+#pragma unroll
+  for (int s = 0; s < RING; s++) acc[s][0] = acc[s][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  for (int base = 0; base < P; base += RING) {
+    const int par0 = base / NS;
+#pragma unroll
+    for (int ph = 0; ph < RING; ph++) {
+      const int it = base + ph;
+      if (it < P) {
+        const int s = ph % NS;
+        const int p = pstart + it;
+        const float* Cs = stage + s * SF;
+        const float* UBs = Cs + BF;
+        const float* U1s = Cs + 2 * BF;
+        float* Q = qbuf + (it % NQB) * BF;
+        float* G = gq + (it % QD) * TILE;
+        const bool emit = it >= 2 * R;
+        const int o = p - R;
+        const bool pin = p >= lo && p <= hi;
+        const bool oin = o >= lo && o <= hi;
+
+        tma::mbar_wait(&bars[s], (par0 + ph / NS) & 1);
+        float4 old[2];
+        {
+          const float* OLD = Cs + 3 * BF + (q_role ? TILE : 0) + trow;
+          old[0] = lds4(OLD);
+          old[1] = lds4(OLD + TK);
+        }
+
+        // ---- q over the halo box; g for the centre elements
+#pragma unroll
+        for (int m = 0; m < Tl::EPT; m++) {
+          const int e = tid + m * Tl::THREADS;
+          if (e < Tl::QELEMS) {
+            const int row = e / (BW / 4), c4 = e - row * (BW / 4);
+            const int qo = row * BW + 4 * c4;
+            const bool centre = row >= HJ && row < HJ + Tl::TJ && c4 >= 1 && c4 <= TK / 4;
+            float4 qv = make_float4(0.f, 0.f, 0.f, 0.f), gv = qv;
+            if (pin) {
+              const float4 cv = lds4(Cs + qo);
+              float4 uv = lds4(UBs + qo);
+              if (!interior) {
+                const int jg = j0 - HJ + row, kg = k0 - HK + 4 * c4;
+                const bool rm = jg >= lo && jg <= hi;
+                if (!(rm && kg >= lo && kg <= hi)) uv.x = 0.f;
+                if (!(rm && kg + 1 >= lo && kg + 1 <= hi)) uv.y = 0.f;
+                if (!(rm && kg + 2 >= lo && kg + 2 <= hi)) uv.z = 0.f;
+                if (!(rm && kg + 3 >= lo && kg + 3 <= hi)) uv.w = 0.f;
+              }
+              const float4 du = muls4(D, uv);
+              qv = mul4(S3::kC2 ? mul4(cv, cv) : cv, du);
+              if (centre) gv = S3::kC2 ? mul4(muls4(2.f, cv), du) : du;
+            }
+            *reinterpret_cast<float4*>(Q + qo) = qv;
+            if (centre) *reinterpret_cast<float4*>(G + (row - HJ) * TK + 4 * (c4 - 1)) = gv;
+          }
+        }
+        // ---- q role: 2 u_b centre term (and u_2_b at plane p)
+        if (q_role && pin) {
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const bool jin = jr0 + h >= lo && jr0 + h <= hi;
+            float4 ubm = lds4(UBs + (r0 + h) * BW + col);
+            if (!interior)
+              ubm = make_float4(jin && kin[0] ? ubm.x : 0.f, jin && kin[1] ? ubm.y : 0.f,
+                                jin && kin[2] ? ubm.z : 0.f, jin && kin[3] ? ubm.w : 0.f);
+            acc[ph][h] = fmas4(2.f, ubm, acc[ph][h]);
+            if (S3::kU2 && jin && jr0 + h < n && kc < n && p >= o_begin && p < o_end) {
+              const float4 u2 = lds4(Cs + 3 * BF + 2 * TILE + trow + h * TK);
+              float* ptr = u_2_b + (long long)(p - i_base) * plane + coff + (long long)h * n;
+              __stcs(reinterpret_cast<float4*>(ptr),
+                     make_float4(kin[0] ? u2.x - ubm.x : u2.x, kin[1] ? u2.y - ubm.y : u2.y,
+                                 kin[2] ? u2.z - ubm.z : u2.z, kin[3] ? u2.w - ubm.w : u2.w));
+            }
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
+
+        field2x4<R, RING>(q_role ? Q : U1s, r0, col, w0, wr, acc, ph);
+
+        // ---- emit output plane o = p - R
+        if (emit) {
+          const int es = (ph + R + 1) % RING;
+          const long long obase = (long long)(o - i_base) * plane + coff;
+          if (!q_role) {
+            if (oin) {
+              const float* Go = gq + ((it - R) % QD) * TILE + trow;
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                const bool jin = jr0 + h >= lo && jr0 + h <= hi;
+                if (!jin || jr0 + h >= n || kc >= n) continue;
+                float4 nv = fma4(lds4(Go + h * TK), acc[es][h], old[h]);
+                if (!interior)
+                  nv = make_float4(kin[0] ? nv.x : old[h].x, kin[1] ? nv.y : old[h].y,
+                                   kin[2] ? nv.z : old[h].z, kin[3] ? nv.w : old[h].w);
+                __stcs(reinterpret_cast<float4*>(c_b + obase + (long long)h * n), nv);
+              }
+            }
+          } else {
+            const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int j = jr0 + h;
+              if (j >= n || kc >= n) continue;
+              float4 nv;
+              if (interior) {
+                if (oout > R) continue;
+                nv = add4(old[h], acc[es][h]);
+              } else {
+                const int jout = j < lo ? lo - j : (j > hi ? j - hi : 0);
+                const float4 a = acc[es][h];
+                const float av[4] = {a.x, a.y, a.z, a.w};
+                nv = old[h];
+                float* nvp = reinterpret_cast<float*>(&nv);
+                bool any = false;
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                  const int k = kc + m;
+                  const int kout = k < lo ? lo - k : (k > hi ? k - hi : 0);
+                  const int nout = (oout > 0) + (jout > 0) + (kout > 0);
+                  const bool reach =
+                      nout == 0 || (nout == 1 && oout <= R && jout <= R && kout <= R);
+                  if (reach) nvp[m] = nvp[m] + av[m];
+                  any |= reach;
+                }
+                if (!any) continue;
+              }
+              __stcs(reinterpret_cast<float4*>(u_1_b + obase + (long long)h * n), nv);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int MODE>
+inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
+                           long long out_i1, float D, const float* c, float* c_b,
+                           const float* u_1, float* u_1_b, float* u_2_b, const float* u_b,
+                           cudaStream_t s, const char* name) {
+  using Tl = StarTile7<MODE>;
+  CUtensorMap maps[6];
+  int rc = 0;
+  rc |= encode_3d(&maps[0], c, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
+  rc |= encode_3d(&maps[1], u_b, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
+  rc |= encode_3d(&maps[2], u_1, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
+  rc |= encode_3d(&maps[3], c_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
+  rc |= encode_3d(&maps[4], u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
+  rc |= encode_3d(&maps[5], Star3<MODE>::kU2 ? u_2_b : u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ,
+                  name);
+  if (rc) return SGB_EINVAL;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(star3_v7_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Tl::SMEM);
+    attr_set = true;
+  }
+  const int tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
+  const int tiles_j = (int)((g.n + Tl::TJ - 1) / Tl::TJ);
+  const long long nout = out_i1 - out_i0;
+  const int chunks = choose_chunks((long long)tiles_k * tiles_j, nout, Tl::R, 1);
+  const int chunk = (int)((nout + chunks - 1) / chunks);
+  dim3 grid((unsigned)(tiles_k * tiles_j), (unsigned)((nout + chunk - 1) / chunk));
+  star3_v7_kernel<MODE><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
+      maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+      (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D);
+  return launch_status(name);
+}
+
+}  // namespace sgb
