@@ -383,7 +383,7 @@ inline CUtensorMapL2promotion l2_promotion() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("SGB_L2PROMO");
-    v = e ? std::atoi(e) : 128;
+    v = e ? std::atoi(e) : 64;
   }
   switch (v) {
     case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
@@ -411,15 +411,17 @@ inline int choose_chunks(long long tiles, long long nout, int R, int per_sm) {
     int c = std::atoi(e);
     if (c > 0) return c;
   }
-  // Measured on B200 (768^3 / 1024^3, radius 4): chunks of ~192 planes keep
-  // the resident CTAs in near lock-step (their shared halo rows stay in L2)
-  // while the 2R re-read halo planes per chunk stay a few percent.
+  // Measured on B200 (768^3 / 1024^3, radius 4, profiles/): chunks of ~96
+  // planes keep the resident CTAs in near lock-step, so the halo rows a tile
+  // shares with its neighbours are still in L2 when the neighbour reads them,
+  // while the 2R re-read i-halo planes per chunk stay ~8% of a chunk.
   (void)tiles;
   (void)per_sm;
-  long long c = (nout + 96) / 192;
+  // radius 1 (v1 kernel, far less work per plane): ~192-plane chunks
+  const long long len = R >= 4 ? 96 : 192;
+  long long c = (nout + len / 2) / len;
   if (c < 1) c = 1;
-  if (c > 32) c = 32;
-  (void)R;
+  if (c > 64) c = 64;
   return (int)c;
 }
 

@@ -457,7 +457,8 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
                     const __grid_constant__ CUtensorMap tm_u1b,
                     const __grid_constant__ CUtensorMap tm_u2b, float* __restrict__ c_b,
                     float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n, int i_base,
-                    int lo, int hi, int out_i0, int out_i1, int chunk, int tiles_k, float D) {
+                    int lo, int hi, int out_i0, int out_i1, int chunk, int tiles_k, float D,
+                    int order) {
   using Tl = StarTile7<MODE>;
   using S3 = Star3<MODE>;
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
@@ -474,7 +475,11 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
   const bool q_role = tid >= ROLE;  // warp-uniform
   const int rt = q_role ? tid - ROLE : tid;
   const int tx = rt & 15, ty = rt >> 4;  // 4 k-points x rows 2ty, 2ty+1
-  const int tk = blockIdx.x % tiles_k, tj = blockIdx.x / tiles_k;
+  // tile order: order 0 = k fastest; order 1 = j fastest (the j neighbours,
+  // which share 2R halo rows, are consecutive CTAs and so run at the same time)
+  const int tiles_j = (n + Tl::TJ - 1) / Tl::TJ;
+  const int tk = order == 1 ? blockIdx.x / tiles_j : blockIdx.x % tiles_k;
+  const int tj = order == 1 ? blockIdx.x % tiles_j : blockIdx.x / tiles_k;
   const int k0 = tk * TK, j0 = tj * Tl::TJ;
   const int o_begin = out_i0 + blockIdx.y * chunk;
   const int o_end = min(o_begin + chunk, out_i1);
@@ -693,9 +698,14 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   const int chunks = choose_chunks((long long)tiles_k * tiles_j, nout, Tl::R, 1);
   const int chunk = (int)((nout + chunks - 1) / chunks);
   dim3 grid((unsigned)(tiles_k * tiles_j), (unsigned)((nout + chunk - 1) / chunk));
+  static int order = -1;
+  if (order < 0) {
+    const char* e = std::getenv("SGB_TILE_ORDER");
+    order = e ? std::atoi(e) : 0;
+  }
   star3_v7_kernel<MODE><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
       maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-      (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D);
+      (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D, order);
   return launch_status(name);
 }
 
