@@ -402,6 +402,18 @@ def run_ours(args, cfg):
     if not args.no_e2e:
         e2e = run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d)
 
+    ablation = None
+    if world == 1 and not args.no_ablation:
+        # GPU scatter-with-atomics adjoint on the same inputs (BASELINE cfg 5
+        # ablation; same algorithmic bytes as the gather form)
+        ms_sc = _time_launch(torch, lambda: api.scatter_adjoint(family, n, scalars, arrays),
+                             iters=5, warm=2)
+        ablation = {"scatter_atomic_ms": ms_sc, "scatter_GPts_s": pts / ms_sc / 1e6,
+                    "gather_kernel_ms": kms, "gather_speedup_vs_scatter": ms_sc / kms}
+    table = None
+    if world == 1 and not args.no_configs:
+        table = config_table(torch, api, peak, args.config)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -434,10 +446,46 @@ def run_ours(args, cfg):
                      "peak_source": peak_src, "traffic_source": tsrc,
                      "vs_nominal_8tbs": achieved / 8000.0},
         "cpu_baseline": cpu,
+        "ablation": ablation,
+        "other_configs": table,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def _time_launch(torch, fn, iters=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def config_table(torch, api, peak, skip):
+    """Single-GPU gather-adjoint kernel time for every BASELINE config (median
+    of 10 launches, inputs resident), so one bench line covers all five."""
+    out = {}
+    for cid, (family, n, dtype, bpp, scalars, desc) in sorted(CONFIGS.items()):
+        if cid == skip:
+            continue
+        arrays = gen_inputs(api, torch, family, n)
+        ms = _time_launch(torch, lambda: api.adjoint(family, n, scalars, arrays))
+        pts = float(n) ** DIMS[family]
+        gbs = bpp * pts / (ms / 1e3) / 1e9
+        out[f"cfg{cid}"] = {"workload": desc, "kernel_ms": ms, "GPts_s": pts / ms / 1e6,
+                            "alg_GB_s": gbs, "frac_measured_peak": gbs / peak,
+                            "frac_nominal_8TBs": gbs / 8000.0, "dtype": dtype}
+        del arrays
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d):
@@ -502,6 +550,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="exchange, then compute")
+    ap.add_argument("--no-ablation", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "generic_kernels.cuh"
+#include "lowdim.cuh"
 #include "star3d_tma.cuh"
 #include "star3d_v2.cuh"
 #include "star3d_v3.cuh"
@@ -16,6 +17,16 @@ namespace sgb {
 std::atomic<unsigned long long> g_launches{0};
 static thread_local std::string t_error;
 void set_error(const std::string& msg) { t_error = msg; }
+
+template <typename A, typename B, typename C, typename E>
+static bool aligned16(const A* a, const B* b, const C* c, const E* e) {
+  return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+           reinterpret_cast<uintptr_t>(c) | reinterpret_cast<uintptr_t>(e)) & 15) == 0;
+}
+template <typename A, typename B>
+static bool aligned16(const A* a, const B* b) {
+  return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
 
 static int einval(const std::string& msg) {
   set_error(msg);
@@ -162,6 +173,11 @@ static int wave1d_gather(long long n, double D, const T* c, T* c_b, const T* u, 
   if (n <= 0) return einval("wave1d_b: n must be positive");
   if (!guard_ok(WAVE1D, n)) return SGB_GUARD;
   if (!c || !c_b || !u || !u_b || !u_prev_b || !u_next_b) return einval("wave1d_b: null array");
+  if (n % 2 == 0 && aligned16(c, c_b, u, u_b) && aligned16(u_prev_b, u_next_b)) {
+    wave1d_stream_kernel<T>
+        <<<grid_1d(n / 2, 256), 256, 0, s>>>(n, (T)D, c, c_b, u, u_b, u_prev_b, u_next_b);
+    return launch_status("wave1d_b");
+  }
   wave1d_gather_kernel<T>
       <<<grid_1d(n, 256), 256, 0, s>>>(n, (T)D, c, c_b, u, u_b, u_prev_b, u_next_b);
   return launch_status("wave1d_b");
@@ -174,6 +190,17 @@ static int burgers2d_gather(long long n, double C, double D, const T* u_1, T* u_
   if (n <= 0) return einval("burgers2d_b: n must be positive");
   if (!guard_ok(BURGERS2D, n)) return SGB_GUARD;
   if (!u_1 || !u_1_b || !u_b) return einval("burgers2d_b: null array");
+  if (n % 2 == 0 && aligned16(u_1, u_1_b, u_b, u_b)) {
+    static int rb = -1;  // rows per block (SGB_BURGERS_RB), measured default
+    if (rb < 0) {
+      const char* e = std::getenv("SGB_BURGERS_RB");
+      rb = e ? std::atoi(e) : 32;
+      if (rb <= 0) rb = 32;
+    }
+    dim3 g((unsigned)((n / 2 + 127) / 128), (unsigned)((n + rb - 1) / rb));
+    burgers2d_stream_kernel<T><<<g, 128, 0, s>>>(n, (T)C, (T)D, u_1, u_1_b, u_b, rb);
+    return launch_status("burgers2d_b");
+  }
   dim3 b(64, 4), g((unsigned)((n + 63) / 64), (unsigned)((n + 3) / 4));
   burgers2d_gather_kernel<T><<<g, b, 0, s>>>(n, (T)C, (T)D, u_1, u_1_b, u_b);
   return launch_status("burgers2d_b");
