@@ -11,6 +11,10 @@
 //                                             run_scatter_adjoint (interp.cpp:183-228)
 //                                             on raw fp64 grids read from in_dir
 //   verify <spec> <n> <seed> <trials>         verify_problem (interp.cpp:413-435)
+//   b200   <spec> <n> <in_dir> S=v            run_program vs run_program_b200 (the
+//                                             INTEGRATION.md binding, b200_binding.cpp)
+//                                             on the same Env; prints the max
+//                                             compare_grids error as JSON
 //   emit   <spec> <out_dir>                   emit_primal / emit_adjoint /
 //                                             emit_scatter_adjoint with restrict,
 //                                             exactly as cmd_bench does
@@ -33,6 +37,10 @@
 #include "stencilgrad/specfile.hpp"
 
 namespace sg = stencilgrad;
+
+namespace stencilgrad {
+Env run_program_b200(const Problem& p, const Env& env);  // b200_binding.cpp
+}
 
 static std::string slurp(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
@@ -115,6 +123,51 @@ static int cmd_info(const sg::Problem& p, long long n) {
   return 0;
 }
 
+static sg::Env load_env(const sg::Problem& p, long long n, const std::string& in_dir, int argc,
+                        char** argv) {
+  sg::Env env;
+  env.sizes["n"] = n;
+  for (const auto& s : p.scalars) env.scalars[s] = 0.0;
+  for (int a = 0; a < argc; a++) {
+    std::string kv = argv[a];
+    auto eq = kv.find('=');
+    env.scalars[kv.substr(0, eq)] = std::strtod(kv.c_str() + eq + 1, nullptr);
+  }
+  for (const auto& a : p.arrays) {
+    sg::DenseGrid g(shape_of(a, env.sizes));
+    read_grid(in_dir + "/" + a.name + ".f64", g);
+    env.grids[a.name] = g;
+    if (a.active) {
+      sg::DenseGrid gb(shape_of(a, env.sizes));
+      read_grid(in_dir + "/" + a.adjoint + ".f64", gb);
+      env.grids[a.adjoint] = gb;
+    }
+  }
+  return env;
+}
+
+static int cmd_b200(const sg::Problem& p, long long n, const std::string& in_dir, int argc,
+                    char** argv) {
+  sg::Env env = load_env(p, n, in_dir, argc, argv);
+  sg::Env ref = sg::run_program(sg::assemble_adjoint(p), env);
+  sg::Env gpu = sg::run_program_b200(p, env);
+  const sg::ArrayDecl& out = sg::output_array(p);
+  double worst = 0.0;
+  std::ostringstream os;
+  os << "{\"name\":\"" << p.name << "\",\"n\":" << n << ",\"arrays\":{";
+  bool first = true;
+  for (const auto& a : p.arrays) {
+    if (!a.active || a.name == out.name) continue;
+    auto c = sg::compare_grids(gpu.grids.at(a.adjoint), ref.grids.at(a.adjoint), 1e-12);
+    worst = std::max(worst, c.max_rel_err);
+    os << (first ? "" : ",") << "\"" << a.adjoint << "\":" << c.max_rel_err;
+    first = false;
+  }
+  os << "},\"max_rel_err\":" << worst << "}\n";
+  std::cout << os.str();
+  return worst <= 1e-12 ? 0 : 1;
+}
+
 static int cmd_run(const sg::Problem& p, long long n, const std::string& in_dir,
                    const std::string& out_dir, int argc, char** argv) {
   sg::Env env;
@@ -183,6 +236,7 @@ int main(int argc, char** argv) {
       return cmd_verify(p, std::atoll(argv[3]), std::strtoull(argv[4], nullptr, 10),
                         std::atoi(argv[5]));
     if (cmd == "emit" && argc >= 4) return cmd_emit(p, argv[3]);
+    if (cmd == "b200" && argc >= 5) return cmd_b200(p, std::atoll(argv[3]), argv[4], argc - 5, argv + 5);
     std::cerr << "bad arguments\n";
     return 2;
   } catch (const std::exception& e) {
