@@ -177,6 +177,17 @@ def gen_inputs(api, torch, family, n, slab=None):
 
 
 # ------------------------------------------------------------------ CPU side
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def _omp_env():
     ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     os.environ.setdefault("OMP_NUM_THREADS", str(ncpu))
@@ -260,6 +271,7 @@ def time_cpu(family, scalars, n_full, target_s=6.0, calls=3):
         best = min(best, time.perf_counter() - t0)
     pts = n ** d
     return {"value": pts / best / 1e9, "unit": "GPts/s", "cores": threads, "kind": kind,
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
             "sample": f"{label}; one call over the full {n}^{d} grid (bounded sample of the "
                       f"{n_full}^{d} workload), best of {calls}", "seconds_per_call": best,
             "n": n}
@@ -303,6 +315,7 @@ def run_reference_arm(args, cfg):
                    "note": "reference CPU path on the host cores; each step is one call "
                            f"over a {n}^{d} sample of the workload"},
         "cpu_baseline": {"value": value, "unit": "GPts/s", "cores": threads, "kind": kind,
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                          "sample": f"{label}; {n}^{d} grid per step"},
         "e2e": {"value": value, "unit": "GPts/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},

@@ -477,9 +477,21 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
   const int tx = rt & 15, ty = rt >> 4;  // 4 k-points x rows 2ty, 2ty+1
   // tile order: order 0 = k fastest; order 1 = j fastest (the j neighbours,
   // which share 2R halo rows, are consecutive CTAs and so run at the same time)
+  // order >= 2: groups of `order` j-adjacent tiles are consecutive CTAs (and
+  // the groups run k-fastest), so most j and all k neighbours run together
   const int tiles_j = (n + Tl::TJ - 1) / Tl::TJ;
-  const int tk = order == 1 ? blockIdx.x / tiles_j : blockIdx.x % tiles_k;
-  const int tj = order == 1 ? blockIdx.x % tiles_j : blockIdx.x / tiles_k;
+  int tk, tj;
+  if (order == 1) {
+    tk = blockIdx.x / tiles_j;
+    tj = blockIdx.x % tiles_j;
+  } else if (order >= 2 && tiles_j % order == 0) {
+    const int grp = blockIdx.x / order, m = blockIdx.x % order;
+    tk = grp % tiles_k;
+    tj = order * (grp / tiles_k) + m;
+  } else {
+    tk = blockIdx.x % tiles_k;
+    tj = blockIdx.x / tiles_k;
+  }
   const int k0 = tk * TK, j0 = tj * Tl::TJ;
   const int o_begin = out_i0 + blockIdx.y * chunk;
   const int o_end = min(o_begin + chunk, out_i1);
@@ -532,6 +544,19 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
   for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
   const float gf = S3::kC2 ? 2.f * D : D;
 
+  // q-pass elements of this thread (fixed for all planes): smem offset in the
+  // box and, for centre elements, offset of its g in the 64x32 g tile
+  int qoff[Tl::EPT], goff[Tl::EPT];
+#pragma unroll
+  for (int m = 0; m < Tl::EPT; m++) {
+    const int e = tid + m * Tl::THREADS;
+    const int row = e / (BW / 4), c4 = e - row * (BW / 4);
+    qoff[m] = e < Tl::QELEMS ? row * BW + 4 * c4 : -1;
+    goff[m] = (e < Tl::QELEMS && row >= HJ && row < HJ + Tl::TJ && c4 >= 1 && c4 <= TK / 4)
+                  ? (row - HJ) * TK + 4 * (c4 - 1)
+                  : -1;
+  }
+
   float4 acc[RING][2];
 #pragma unroll
   for (int s = 0; s < RING; s++) acc[s][0] = acc[s][1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -565,11 +590,10 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
         // ---- q over the halo box; g for the centre elements
 #pragma unroll
         for (int m = 0; m < Tl::EPT; m++) {
-          const int e = tid + m * Tl::THREADS;
-          if (e < Tl::QELEMS) {
-            const int row = e / (BW / 4), c4 = e - row * (BW / 4);
-            const int qo = row * BW + 4 * c4;
-            const bool centre = row >= HJ && row < HJ + Tl::TJ && c4 >= 1 && c4 <= TK / 4;
+          if (qoff[m] >= 0) {
+            const int qo = qoff[m];
+            const int row = qo / BW, c4 = (qo - row * BW) >> 2;
+            const bool centre = goff[m] >= 0;
             float4 qv = make_float4(0.f, 0.f, 0.f, 0.f), gv = qv;
             if (pin) {
               const float4 cv = lds4(Cs + qo);
@@ -587,7 +611,7 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
               if (centre) gv = S3::kC2 ? mul4(muls4(2.f, cv), du) : du;
             }
             *reinterpret_cast<float4*>(Q + qo) = qv;
-            if (centre) *reinterpret_cast<float4*>(G + (row - HJ) * TK + 4 * (c4 - 1)) = gv;
+            if (centre) *reinterpret_cast<float4*>(G + goff[m]) = gv;
           }
         }
         // ---- q role: 2 u_b centre term (and u_2_b at plane p)
