@@ -181,6 +181,19 @@ void sgb_plan_destroy(sgb_plan* plan);
 int sgb_plan_run_adjoint_host(sgb_plan* plan, const double* scalars, void** arrays,
                               sgb_stream_t stream);
 
+/* ---- emitted kernels (runtime compilation) ----------------
+ * paper_1907_02818_b200/emitter.py generates CUDA source for the fused gather
+ * adjoint / primal of ANY problem the reference front end differentiates (its
+ * AdjointProgram: terms, offsets, partials); these entry points compile it
+ * with NVRTC for sm_100a (cached by source text) and launch it. */
+typedef struct sgb_jit_kernel sgb_jit_kernel;
+const char* sgb_jit_log(void);
+int sgb_jit_compile(const char* source, const char* name, sgb_jit_kernel** out);
+/* compile-only check (no GPU needed): 0 when the source compiles for sm_100a */
+int sgb_jit_check(const char* source);
+int sgb_jit_launch(sgb_jit_kernel* kernel, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+                   unsigned by, unsigned bz, void** args, sgb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@
 //                                             INTEGRATION.md binding, b200_binding.cpp)
 //                                             on the same Env; prints the max
 //                                             compare_grids error as JSON
+//   spec   <spec>                             serialize_spec (specfile.cpp:208-240)
 //   emit   <spec> <out_dir>                   emit_primal / emit_adjoint /
 //                                             emit_scatter_adjoint with restrict,
 //                                             exactly as cmd_bench does
@@ -236,6 +237,10 @@ int main(int argc, char** argv) {
       return cmd_verify(p, std::atoll(argv[3]), std::strtoull(argv[4], nullptr, 10),
                         std::atoi(argv[5]));
     if (cmd == "emit" && argc >= 4) return cmd_emit(p, argv[3]);
+    if (cmd == "spec") {
+      std::cout << sg::serialize_spec(p);
+      return 0;
+    }
     if (cmd == "b200" && argc >= 5) return cmd_b200(p, std::atoll(argv[3]), argv[4], argc - 5, argv + 5);
     std::cerr << "bad arguments\n";
     return 2;

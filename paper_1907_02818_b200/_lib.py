@@ -31,6 +31,9 @@ _CTYPES = {
     "void**": ctypes.c_void_p,
     "const char*": ctypes.c_char_p,
     "sgb_plan*": ctypes.c_void_p,
+    "sgb_jit_kernel*": ctypes.c_void_p,
+    "sgb_jit_kernel**": ctypes.c_void_p,
+    "unsigned": ctypes.c_uint,
     "void": None,
 }
 

@@ -1,0 +1,510 @@
+"""CUDA back-end emitter for arbitrary adjoint-stencil programs.
+
+The reference turns an ``AdjointProgram`` into C/OpenMP text with
+``emit_adjoint`` (codegen.cpp:332-382).  This module turns the same program
+-- the primal spec (counters, affine bounds, arrays, lhs, rhs) plus the
+derived terms (active read, offset, partial S_l printed by the reference's
+``to_input_string``, expr.cpp:261-397) -- into CUDA C for sm_100a, compiled at
+run time with NVRTC through the C ABI (``sgb_jit_compile`` / ``sgb_jit_launch``).
+
+Emitted gather kernel (one thread per point y of the write box):
+
+    for each target adjoint array A:
+        for l in ascending term order with target A:       (adjoint.cpp:85)
+            if y - o_l in B:  cell += S_l(y - o_l) * seed[perm(y - o_l)]
+        store cell if any term reached y                   (untouched otherwise)
+
+i.e. the predicate form of the reference's hierarchical core + boundary nests
+(SURVEY Appendix C), with the per-cell increments in the same order as
+``run_program`` (interp.cpp:153-198).  The primal kernel mirrors ``run_nest``.
+This general path covers every problem the front end accepts (lap1d,
+burgers1d, wave3d, the config families, the reference's fuzz problems); the
+hand-tuned TMA kernels remain the hot path for the BASELINE configs.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import re
+from dataclasses import dataclass
+
+from . import _lib
+
+# ------------------------------------------------------------------ parsing
+_TOK = re.compile(r"\s*(?:(\d+\.\d*(?:[eE][-+]?\d+)?|\d+(?:[eE][-+]?\d+)?|\.\d+(?:[eE][-+]?\d+)?)"
+                  r"|([A-Za-z_]\w*)|(>=|<=|[-+*/(),\[\]<>]))")
+
+
+def _tokens(text):
+    pos, out = 0, []
+    text = text.strip()
+    while pos < len(text):
+        m = _TOK.match(text, pos)
+        if not m or m.end() == pos:
+            raise ValueError(f"cannot tokenize {text[pos:]!r}")
+        num, ident, op = m.groups()
+        out.append(("num", num) if num else ("id", ident) if ident else ("op", op))
+        pos = m.end()
+    return out
+
+
+class _Parser:
+    """Precedence climbing over the reference's expression syntax
+    (parser.cpp:11-225 accepts it; to_input_string prints it)."""
+
+    def __init__(self, text):
+        self.t = _tokens(text)
+        self.i = 0
+
+    def peek(self):
+        return self.t[self.i] if self.i < len(self.t) else (None, None)
+
+    def take(self, val=None):
+        tok = self.peek()
+        if val is not None and tok[1] != val:
+            raise ValueError(f"expected {val!r}, got {tok}")
+        self.i += 1
+        return tok
+
+    def parse(self):
+        e = self.compare()
+        if self.i != len(self.t):
+            raise ValueError(f"trailing input at token {self.t[self.i]}")
+        return e
+
+    def compare(self):
+        a = self.additive()
+        if self.peek()[1] in (">=", "<=", ">", "<"):
+            op = self.take()[1]
+            return ("cmp", op, a, self.additive())
+        return a
+
+    def additive(self):
+        e = self.term()
+        while self.peek()[1] in ("+", "-"):
+            op = self.take()[1]
+            e = ("add" if op == "+" else "sub", e, self.term())
+        return e
+
+    def term(self):
+        e = self.unary()
+        while self.peek()[1] in ("*", "/"):
+            op = self.take()[1]
+            e = ("mul" if op == "*" else "div", e, self.unary())
+        return e
+
+    def unary(self):
+        if self.peek()[1] == "-":
+            self.take()
+            return ("neg", self.unary())
+        if self.peek()[1] == "+":
+            self.take()
+            return self.unary()
+        return self.atom()
+
+    def atom(self):
+        kind, val = self.take()
+        if kind == "num":
+            return ("num", val)
+        if kind == "op" and val == "(":
+            e = self.compare()
+            self.take(")")
+            return e
+        if kind == "id":
+            if self.peek()[1] == "(":
+                self.take("(")
+                args = [self.compare()]
+                while self.peek()[1] == ",":
+                    self.take(",")
+                    args.append(self.compare())
+                self.take(")")
+                if val in ("max", "min") and len(args) == 2:
+                    return (val, args[0], args[1])
+                if val == "pow" and len(args) == 2:
+                    k = args[1]
+                    sign = 1
+                    if k[0] == "neg":
+                        sign, k = -1, k[1]
+                    if k[0] != "num" or not re.fullmatch(r"\d+", k[1]):
+                        raise ValueError("pow exponent must be an integer literal")
+                    return ("pow", args[0], sign * int(k[1]))
+                if val == "select" and len(args) == 3 and args[0][0] == "cmp":
+                    return ("select", args[0], args[1], args[2])
+                raise ValueError(f"unsupported call {val}/{len(args)} (opaque calls have no "
+                                 "device implementation)")
+            if self.peek()[1] == "[":
+                idx = []
+                while self.peek()[1] == "[":
+                    self.take("[")
+                    c = self.take()
+                    if c[0] != "id":
+                        raise ValueError("array index must start with a counter")
+                    off = 0
+                    if self.peek()[1] in ("+", "-"):
+                        sgn = 1 if self.take()[1] == "+" else -1
+                        off = sgn * int(self.take()[1])
+                    self.take("]")
+                    idx.append((c[1], off))
+                return ("read", val, idx)
+            return ("sym", val)
+        raise ValueError(f"unexpected token {val!r}")
+
+
+def parse_expr(text):
+    return _Parser(text).parse()
+
+
+def parse_affine(text):
+    """'n - 2' -> ({'n': 1}, -2) (AffineExpr, affine.cpp:81-200)."""
+    coeff, const = {}, 0
+    e = parse_expr(text)
+
+    def walk(node, sign):
+        nonlocal const
+        k = node[0]
+        if k == "num":
+            const += sign * int(node[1])
+        elif k == "sym":
+            coeff[node[1]] = coeff.get(node[1], 0) + sign
+        elif k == "add":
+            walk(node[1], sign)
+            walk(node[2], sign)
+        elif k == "sub":
+            walk(node[1], sign)
+            walk(node[2], -sign)
+        elif k == "neg":
+            walk(node[1], -sign)
+        elif k == "mul" and node[1][0] == "num":
+            inner_c, inner_k = parse_affine_node(node[2])
+            f = int(node[1][1]) * sign
+            for s_, v in inner_c.items():
+                coeff[s_] = coeff.get(s_, 0) + f * v
+            const += f * inner_k
+        else:
+            raise ValueError(f"non-affine bound {text!r}")
+    walk(e, 1)
+    return coeff, const
+
+
+def parse_affine_node(node):
+    c, k = {}, 0
+    if node[0] == "sym":
+        c[node[1]] = 1
+    elif node[0] == "num":
+        k = int(node[1])
+    else:
+        raise ValueError("non-affine")
+    return c, k
+
+
+def affine_c(aff, sizes_var):
+    coeff, const = aff
+    parts = [f"({v} * {sizes_var[s]})" for s, v in coeff.items()]
+    return "(" + " + ".join(parts + [f"({const}LL)"]) + ")"
+
+
+# ------------------------------------------------------------------ codegen
+@dataclass
+class Term:
+    array: str
+    adjoint: str
+    offset: tuple
+    partial: str
+
+
+class _CGen:
+    def __init__(self, prob, counters, at):
+        self.p = prob
+        self.counters = counters  # counter name -> C expression of its value
+        self.at = at              # array name -> C flat-index function name
+
+    def e(self, node):
+        k = node[0]
+        if k == "num":
+            v = node[1]
+            return f"T({v})" if ("." in v or "e" in v or "E" in v) else f"T({v}.0)"
+        if k == "sym":
+            if node[1] not in self.p.scalars:
+                raise ValueError(f"unknown scalar {node[1]}")
+            return f"s_{node[1]}"
+        if k == "read":
+            name, idx = node[1], node[2]
+            args = ", ".join(f"({self.counters[c]} + ({o}))" for c, o in idx)
+            return f"a_{name}[{self.at[name]}({args})]"
+        if k in ("add", "sub", "mul", "div"):
+            op = {"add": "+", "sub": "-", "mul": "*", "div": "/"}[k]
+            return f"({self.e(node[1])} {op} {self.e(node[2])})"
+        if k == "neg":
+            return f"(-{self.e(node[1])})"
+        if k == "max":
+            return f"fmax({self.e(node[1])}, {self.e(node[2])})"
+        if k == "min":
+            return f"fmin({self.e(node[1])}, {self.e(node[2])})"
+        if k == "pow":
+            base, p_ = self.e(node[1]), node[2]
+            return f"ipow({base}, {p_})"
+        if k == "select":
+            c = node[1]
+            return f"(({self.e(c[2])} {c[1]} {self.e(c[3])}) ? {self.e(node[2])} : {self.e(node[3])})"
+        if k == "cmp":
+            raise ValueError("comparison outside select")
+        raise ValueError(k)
+
+
+class EmittedProblem:
+    """A reference problem (spec dict + terms) lowered to sm_100a kernels."""
+
+    def __init__(self, spec: dict, terms, dtype: str = "f64"):
+        self.spec = spec
+        self.name = spec["name"]
+        self.counters = list(spec["counters"])
+        self.d = len(self.counters)
+        self.sizes = list(spec["sizes"])
+        self.scalars = list(spec["scalars"])
+        self.bounds = [(parse_affine(spec["bounds"][c][0]), parse_affine(spec["bounds"][c][1]))
+                       for c in self.counters]
+        self.arrays = {}  # declaration order
+        for name, a in spec["arrays"].items():
+            self.arrays[name] = {"shape": [parse_affine(x) for x in a["shape"]],
+                                 "active": bool(a.get("active")), "adjoint": a.get("adjoint"),
+                                 "role": a.get("role", "input")}
+        m = re.fullmatch(r"\s*(\w+)((?:\[\s*\w+\s*\])+)\s*", spec["lhs"])
+        self.out = m.group(1)
+        self.lhs = re.findall(r"\[\s*(\w+)\s*\]", m.group(2))
+        self.seed = self.arrays[self.out]["adjoint"]
+        self.increment = spec.get("mode", "=") == "+="
+        self.rhs = parse_expr(spec["rhs"])
+        self.terms = [t if isinstance(t, Term) else
+                      Term(t["array"], t["adjoint"], tuple(t["offset"]), t["partial"])
+                      for t in terms]
+        self.partials = [parse_expr(t.partial) for t in self.terms]
+        self.T = {"f64": "double", "f32": "float"}[dtype]
+        self.dtype = dtype
+        self._kern = {}
+
+    # -- names and ABI order (codegen.cpp:198-211: declaration order, each
+    #    primal followed by its adjoint)
+    def param_arrays(self):
+        out = []
+        for name, a in self.arrays.items():
+            out.append(name)
+            if a["active"]:
+                out.append(a["adjoint"])
+        return out
+
+    def _shape_of(self, arr):
+        for name, a in self.arrays.items():
+            if arr == name or arr == a["adjoint"]:
+                return a["shape"]
+        raise KeyError(arr)
+
+    def _prelude(self):
+        szv = {s: f"z_{s}" for s in self.sizes}
+        lines = [f"typedef {self.T} T;",
+                 "__device__ __forceinline__ T ipow(T b, int p) {",
+                 "  T r = T(1); int q = p < 0 ? -p : p;",
+                 "  for (int i = 0; i < q; i++) r *= b;",
+                 "  return p < 0 ? T(1) / r : r; }"]
+        # flat index per array (row-major over its own shape)
+        fns = {}
+        for arr in self.param_arrays():
+            shp = self._shape_of(arr)
+            r = len(shp)
+            args = ", ".join(f"long long x{i}" for i in range(r))
+            body = "x0"
+            for i in range(1, r):
+                body = f"(({body}) * {affine_c(shp[i], szv)} + x{i})"
+            fn = f"ix_{arr}"
+            fns[arr] = fn
+            lines.append(f"__device__ __forceinline__ long long {fn}({args}, "
+                         + ", ".join(f"long long z_{s}" for s in self.sizes) + f") {{ return {body}; }}")
+        return lines, fns, szv
+
+    def _signature(self, kname):
+        ps = [f"long long z_{s}" for s in self.sizes]
+        ps += [f"T s_{s}" for s in self.scalars]
+        for arr in self.param_arrays():
+            ps.append(f"T* __restrict__ a_{arr}")
+        return f'extern "C" __global__ void {kname}(' + ", ".join(ps) + ")"
+
+    def _box_checks(self, xs, szv):
+        conds = []
+        for i, (lo, hi) in enumerate(self.bounds):
+            conds.append(f"({xs[i]} >= {affine_c(lo, szv)} && {xs[i]} <= {affine_c(hi, szv)})")
+        return " && ".join(conds) if conds else "true"
+
+    def _write_box(self, szv):
+        """Union of the target adjoint arrays' extents (per dimension)."""
+        ext = []
+        for i in range(self.d):
+            cands = [affine_c(self._shape_of(t.adjoint)[i], szv) for t in self.terms]
+            e = cands[0]
+            for c in cands[1:]:
+                e = f"max({e}, {c})"
+            ext.append(e)
+        return ext
+
+    def gather_source(self):
+        lines, fns, szv = self._prelude()
+        zargs = ", ".join(f"z_{s}" for s in self.sizes)
+        at = {arr: f"AT_{arr}" for arr in self.param_arrays()}
+        for arr, fn in fns.items():
+            lines.append(f"#define AT_{arr}(...) {fn}(__VA_ARGS__, {zargs})")
+        lines.append(self._signature("sgb_emitted_gather") + " {")
+        ext = self._write_box(szv)
+        lines.append("  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;")
+        for i in range(self.d):
+            lines.append(f"  const long long W{i} = {ext[i]};")
+        total = " * ".join(f"W{i}" for i in range(self.d))
+        lines.append(f"  if (t >= {total}) return;")
+        for i in reversed(range(self.d)):
+            if i == 0:
+                lines.append("  const long long y0 = t;")
+            else:
+                lines.append(f"  const long long y{i} = t % W{i}; t /= W{i};")
+        # group terms by target adjoint, ascending term order inside each
+        targets = []
+        for t in self.terms:
+            if t.adjoint not in targets:
+                targets.append(t.adjoint)
+        cidx = {c: i for i, c in enumerate(self.counters)}
+        for tgt in targets:
+            shp = self._shape_of(tgt)
+            inb = " && ".join(f"y{i} < {affine_c(shp[i], szv)}" for i in range(self.d))
+            lines.append(f"  if ({inb}) {{")
+            lines.append("    bool touched = false; T cell = T(0);")
+            ys = ", ".join(f"y{i}" for i in range(self.d))
+            for ti, (t, part) in enumerate(zip(self.terms, self.partials)):
+                if t.adjoint != tgt:
+                    continue
+                xs = [f"(y{i} - ({t.offset[i]}))" for i in range(self.d)]
+                cg = _CGen(self, {c: xs[cidx[c]] for c in self.counters}, at)
+                seed_idx = ", ".join(xs[cidx[c]] for c in self.lhs)
+                lines.append(f"    if ({self._box_checks(xs, szv)}) {{  // term {ti}: "
+                             f"{t.array}{list(t.offset)}")
+                lines.append(f"      if (!touched) {{ cell = a_{tgt}[AT_{tgt}({ys})]; touched = true; }}")
+                lines.append(f"      cell += ({cg.e(part)}) * a_{self.seed}[AT_{self.seed}({seed_idx})];")
+                lines.append("    }")
+            lines.append(f"    if (touched) a_{tgt}[AT_{tgt}({ys})] = cell;")
+            lines.append("  }")
+        lines.append("}")
+        return "\n".join(lines) + "\n"
+
+    def primal_source(self):
+        lines, fns, szv = self._prelude()
+        zargs = ", ".join(f"z_{s}" for s in self.sizes)
+        at = {arr: f"AT_{arr}" for arr in self.param_arrays()}
+        for arr, fn in fns.items():
+            lines.append(f"#define AT_{arr}(...) {fn}(__VA_ARGS__, {zargs})")
+        lines.append(self._signature("sgb_emitted_primal") + " {")
+        lines.append("  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;")
+        for i, (lo, hi) in enumerate(self.bounds):
+            lines.append(f"  const long long L{i} = {affine_c(lo, szv)}, "
+                         f"N{i} = {affine_c(hi, szv)} - L{i} + 1;")
+            lines.append(f"  if (N{i} <= 0) return;")
+        total = " * ".join(f"N{i}" for i in range(self.d))
+        lines.append(f"  if (t >= {total}) return;")
+        for i in reversed(range(self.d)):
+            if i == 0:
+                lines.append("  const long long x0 = L0 + t;")
+            else:
+                lines.append(f"  const long long x{i} = L{i} + t % N{i}; t /= N{i};")
+        xs = {c: f"x{i}" for i, c in enumerate(self.counters)}
+        cg = _CGen(self, xs, at)
+        lidx = ", ".join(xs[c] for c in self.lhs)
+        op = "+=" if self.increment else "="
+        lines.append(f"  a_{self.out}[AT_{self.out}({lidx})] {op} {cg.e(self.rhs)};")
+        lines.append("}")
+        return "\n".join(lines) + "\n"
+
+    # ------------------------------------------------------------ run
+    def check_compiles(self):
+        """NVRTC-compile both kernels for sm_100a without loading them (no GPU
+        needed); raises StencilError with the compiler log on failure."""
+        for src in (self.gather_source(), self.primal_source()):
+            if _lib.lib().sgb_jit_check(src.encode()) != 0:
+                raise _lib.StencilError(_lib.lib().sgb_jit_log().decode())
+
+    def _kernel(self, which):
+        if which not in self._kern:
+            src = self.gather_source() if which == "gather" else self.primal_source()
+            h = ctypes.c_void_p()
+            rc = _lib.lib().sgb_jit_compile(src.encode(), f"sgb_emitted_{which}".encode(),
+                                            ctypes.byref(h))
+            if rc != 0:
+                raise _lib.StencilError(_lib.lib().sgb_last_error().decode())
+            self._kern[which] = h
+        return self._kern[which]
+
+    def _launch(self, which, sizes, scalars, arrays, nthreads, stream=None):
+        import torch
+        from .api import _stream_ptr
+        keep = []
+        argv = []
+        for s in self.sizes:
+            v = ctypes.c_longlong(int(sizes[s]))
+            keep.append(v)
+        T = ctypes.c_double if self.T == "double" else ctypes.c_float
+        for s in self.scalars:
+            keep.append(T(float(scalars.get(s, 0.0))))
+        tdt = torch.float64 if self.T == "double" else torch.float32
+        for arr in self.param_arrays():
+            t = arrays.get(arr)
+            if t is None:
+                raise _lib.StencilError(f"{self.name}: missing array {arr}")
+            if not (t.is_cuda and t.is_contiguous() and t.dtype == tdt):
+                raise _lib.StencilError(f"{arr}: contiguous CUDA {tdt} tensor required")
+            keep.append(ctypes.c_void_p(t.data_ptr()))
+        argv = (ctypes.c_void_p * len(keep))(*[ctypes.cast(ctypes.pointer(k), ctypes.c_void_p)
+                                               for k in keep])
+        blocks = max(1, (nthreads + 255) // 256)
+        if blocks > 2 ** 31 - 1:
+            raise _lib.StencilError("grid too large")
+        rc = _lib.lib().sgb_jit_launch(self._kernel(which), blocks, 1, 1, 256, 1, 1, argv,
+                                       _stream_ptr(stream))
+        _lib.check(rc, f"{self.name} emitted {which}")
+
+    def _eval_aff(self, aff, sizes):
+        coeff, const = aff
+        return const + sum(v * int(sizes[s]) for s, v in coeff.items())
+
+    def guards_ok(self, sizes) -> bool:
+        """Minimum-extent guards of split_regions (adjoint.cpp:134-143)."""
+        for i in range(self.d):
+            offs = [t.offset[i] for t in self.terms]
+            if not offs:
+                continue
+            span = max(offs) - min(offs)
+            lo, hi = self.bounds[i]
+            if span >= 1 and self._eval_aff(hi, sizes) - self._eval_aff(lo, sizes) < span:
+                return False
+        return True
+
+    def adjoint(self, sizes, scalars, arrays, stream=None):
+        """Gather adjoint (+= into every adjoint array) on the device."""
+        if not self.terms:
+            return
+        if not self.guards_ok(sizes):
+            raise _lib.GuardViolation(f"{self.name}: minimum extent violated")
+        total = 1
+        for i in range(self.d):
+            total *= max(self._eval_aff(self._shape_of(t.adjoint)[i], sizes) for t in self.terms)
+        self._launch("gather", sizes, scalars, arrays, total, stream)
+
+    def primal(self, sizes, scalars, arrays, stream=None):
+        total = 1
+        for lo, hi in self.bounds:
+            total *= max(0, self._eval_aff(hi, sizes) - self._eval_aff(lo, sizes) + 1)
+        if total:
+            self._launch("primal", sizes, scalars, arrays, total, stream)
+
+
+def from_reference_info(spec: dict, info: dict, dtype="f64") -> EmittedProblem:
+    """Build from the reference's own program structure (`ref_harness info`:
+    terms in active_reads order with to_input_string partials)."""
+    return EmittedProblem(spec, info["terms"], dtype)
+
+
+def load_spec(path: str) -> dict:
+    with open(path) as fh:
+        return json.load(fh)
