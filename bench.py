@@ -423,6 +423,11 @@ def run_ours(args, cfg):
                              iters=5, warm=2)
         ablation = {"scatter_atomic_ms": ms_sc, "scatter_GPts_s": pts / ms_sc / 1e6,
                     "gather_kernel_ms": kms, "gather_speedup_vs_scatter": ms_sc / kms}
+        try:
+            ablation["boundary_strategies"] = boundary_ab(torch, family, n, scalars, arrays,
+                                                          dtype, kms)
+        except Exception as ex:  # pragma: no cover - report, never fail the bench
+            ablation["boundary_strategies"] = {"error": str(ex)[:300]}
     table = None
     if world == 1 and not args.no_configs:
         table = config_table(torch, api, peak, args.config)
@@ -480,6 +485,32 @@ def _time_launch(torch, fn, iters=10, warm=3):
         b.synchronize()
         ts.append(a.elapsed_time(b))
     return statistics.median(ts)
+
+
+def boundary_ab(torch, family, n, scalars, arrays, dtype, kms):
+    """Boundary-strategy A/B (paper section 3.3.4) on the
+    same inputs: the hand-tuned fused kernel vs the emitted generic kernel in
+    fused predicated form (1 launch) vs the reference's structure (one launch
+    per hierarchical nest, 1457 for radius 4), captured in a CUDA graph so the
+    comparison is device time, not Python launch overhead."""
+    from paper_1907_02818_b200 import emitter
+    ep = emitter.load_program(family, dtype)
+    sizes = {"n": n}
+    fused_ms = _time_launch(torch, lambda: ep.adjoint(sizes, scalars, arrays), iters=5, warm=2)
+    nests = ep.nests(sizes)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        ep.adjoint_nests(sizes, scalars, arrays, nests)  # compile outside the capture
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            launches = ep.adjoint_nests(sizes, scalars, arrays, nests)
+    torch.cuda.current_stream().wait_stream(s)
+    graph_ms = _time_launch(torch, g.replay, iters=5, warm=2)
+    return {"hand_tuned_fused_ms": kms, "emitted_fused_ms": fused_ms,
+            "emitted_per_nest_graph_ms": graph_ms, "per_nest_launches": launches,
+            "note": "same inputs; fused = one predicated launch over the write box"}
 
 
 def config_table(torch, api, peak, skip):

@@ -281,14 +281,35 @@ class EmittedProblem:
         self.T = {"f64": "double", "f32": "float"}[dtype]
         self.dtype = dtype
         self._kern = {}
+        self._which = "all"
 
     # -- names and ABI order (codegen.cpp:198-211: declaration order, each
     #    primal followed by its adjoint)
-    def param_arrays(self):
+    def param_arrays(self, which="all"):
+        """Arrays of a kernel's signature in the reference's ABI order: every
+        REFERENCED array in declaration order, each primal followed by its
+        adjoint (collect_refs, codegen.cpp:198-211)."""
+        def reads(node, acc):
+            if isinstance(node, tuple):
+                if node[0] == "read":
+                    acc.add(node[1])
+                for x in node[1:]:
+                    reads(x, acc)
+            return acc
+        used = set()
+        if which in ("gather", "nest", "all"):
+            for part in self.partials:
+                reads(part, used)
+            used.update(t.adjoint for t in self.terms)
+            used.add(self.seed)
+        if which in ("primal", "all"):
+            reads(self.rhs, used)
+            used.add(self.out)
         out = []
         for name, a in self.arrays.items():
-            out.append(name)
-            if a["active"]:
+            if name in used:
+                out.append(name)
+            if a["active"] and a["adjoint"] in used:
                 out.append(a["adjoint"])
         return out
 
@@ -307,7 +328,7 @@ class EmittedProblem:
                  "  return p < 0 ? T(1) / r : r; }"]
         # flat index per array (row-major over its own shape)
         fns = {}
-        for arr in self.param_arrays():
+        for arr in self.param_arrays(self._which):
             shp = self._shape_of(arr)
             r = len(shp)
             args = ", ".join(f"long long x{i}" for i in range(r))
@@ -323,7 +344,7 @@ class EmittedProblem:
     def _signature(self, kname):
         ps = [f"long long z_{s}" for s in self.sizes]
         ps += [f"T s_{s}" for s in self.scalars]
-        for arr in self.param_arrays():
+        for arr in self.param_arrays(self._which):
             ps.append(f"T* __restrict__ a_{arr}")
         return f'extern "C" __global__ void {kname}(' + ", ".join(ps) + ")"
 
@@ -345,9 +366,10 @@ class EmittedProblem:
         return ext
 
     def gather_source(self):
+        self._which = "gather"
         lines, fns, szv = self._prelude()
         zargs = ", ".join(f"z_{s}" for s in self.sizes)
-        at = {arr: f"AT_{arr}" for arr in self.param_arrays()}
+        at = {arr: f"AT_{arr}" for arr in self.param_arrays(self._which)}
         for arr, fn in fns.items():
             lines.append(f"#define AT_{arr}(...) {fn}(__VA_ARGS__, {zargs})")
         lines.append(self._signature("sgb_emitted_gather") + " {")
@@ -390,10 +412,73 @@ class EmittedProblem:
         lines.append("}")
         return "\n".join(lines) + "\n"
 
-    def primal_source(self):
+    def nest_source(self):
+        self._which = "nest"
+        """The reference's structure (adjoint.cpp:73-150): one kernel applied to
+        ONE hierarchical nest per launch -- box [lo, hi] and the nest's term
+        set as a bitmask, no per-point predicate (the nest guarantees every
+        listed term is valid).  Boundary-strategy A/B against the fused form."""
         lines, fns, szv = self._prelude()
         zargs = ", ".join(f"z_{s}" for s in self.sizes)
-        at = {arr: f"AT_{arr}" for arr in self.param_arrays()}
+        at = {arr: f"AT_{arr}" for arr in self.param_arrays(self._which)}
+        for arr, fn in fns.items():
+            lines.append(f"#define AT_{arr}(...) {fn}(__VA_ARGS__, {zargs})")
+        sig = self._signature("sgb_emitted_nest")[:-1]
+        sig += ", " + ", ".join(f"long long lo{i}, long long hi{i}" for i in range(self.d))
+        sig += ", unsigned long long mask)"
+        lines.append(sig + " {")
+        lines.append("  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;")
+        for i in range(self.d):
+            lines.append(f"  const long long N{i} = hi{i} - lo{i} + 1;")
+        total = " * ".join(f"N{i}" for i in range(self.d))
+        lines.append(f"  if (t >= {total}) return;")
+        for i in reversed(range(self.d)):
+            if i == 0:
+                lines.append("  const long long y0 = lo0 + t;")
+            else:
+                lines.append(f"  const long long y{i} = lo{i} + t % N{i}; t /= N{i};")
+        cidx = {c: i for i, c in enumerate(self.counters)}
+        ys = ", ".join(f"y{i}" for i in range(self.d))
+        for ti, (t, part) in enumerate(zip(self.terms, self.partials)):
+            xs = [f"(y{i} - ({t.offset[i]}))" for i in range(self.d)]
+            cg = _CGen(self, {c: xs[cidx[c]] for c in self.counters}, at)
+            seed_idx = ", ".join(xs[cidx[c]] for c in self.lhs)
+            lines.append(f"  if (mask & (1ULL << {ti}))  // term {ti}")
+            lines.append(f"    a_{t.adjoint}[AT_{t.adjoint}({ys})] += ({cg.e(part)}) * "
+                         f"a_{self.seed}[AT_{self.seed}({seed_idx})];")
+        lines.append("}")
+        return "\n".join(lines) + "\n"
+
+    def nests(self, sizes):
+        """Hierarchical core + boundary nests (Splitter::recurse,
+        adjoint.cpp:73-120) at concrete sizes: [(lo[], hi[], term indices)]."""
+        offs = [t.offset for t in self.terms]
+        lo = [self._eval_aff(b[0], sizes) for b in self.bounds]
+        hi = [self._eval_aff(b[1], sizes) for b in self.bounds]
+        out = []
+
+        def rec(dim, plo, phi, alive):
+            if dim == self.d:
+                out.append((list(plo), list(phi), list(alive)))
+                return
+            ds = sorted({offs[a][dim] for a in alive})
+            k = len(ds)
+            s_, e_ = lo[dim], hi[dim]
+            for j in range(k - 1):
+                rec(dim + 1, plo + [s_ + ds[j]], phi + [s_ + ds[j + 1] - 1],
+                    [a for a in alive if offs[a][dim] <= ds[j]])
+            rec(dim + 1, plo + [s_ + ds[-1]], phi + [e_ + ds[0]], alive)
+            for j in range(k - 1):
+                rec(dim + 1, plo + [e_ + ds[j] + 1], phi + [e_ + ds[j + 1]],
+                    [a for a in alive if offs[a][dim] > ds[j]])
+        rec(0, [], [], list(range(len(self.terms))))
+        return out
+
+    def primal_source(self):
+        self._which = "primal"
+        lines, fns, szv = self._prelude()
+        zargs = ", ".join(f"z_{s}" for s in self.sizes)
+        at = {arr: f"AT_{arr}" for arr in self.param_arrays(self._which)}
         for arr, fn in fns.items():
             lines.append(f"#define AT_{arr}(...) {fn}(__VA_ARGS__, {zargs})")
         lines.append(self._signature("sgb_emitted_primal") + " {")
@@ -427,7 +512,8 @@ class EmittedProblem:
 
     def _kernel(self, which):
         if which not in self._kern:
-            src = self.gather_source() if which == "gather" else self.primal_source()
+            src = {"gather": self.gather_source, "primal": self.primal_source,
+                   "nest": self.nest_source}[which]()
             h = ctypes.c_void_p()
             rc = _lib.lib().sgb_jit_compile(src.encode(), f"sgb_emitted_{which}".encode(),
                                             ctypes.byref(h))
@@ -436,7 +522,7 @@ class EmittedProblem:
             self._kern[which] = h
         return self._kern[which]
 
-    def _launch(self, which, sizes, scalars, arrays, nthreads, stream=None):
+    def _launch(self, which, sizes, scalars, arrays, nthreads, stream=None, extra=()):
         import torch
         from .api import _stream_ptr
         keep = []
@@ -448,13 +534,14 @@ class EmittedProblem:
         for s in self.scalars:
             keep.append(T(float(scalars.get(s, 0.0))))
         tdt = torch.float64 if self.T == "double" else torch.float32
-        for arr in self.param_arrays():
+        for arr in self.param_arrays("primal" if which == "primal" else "gather"):
             t = arrays.get(arr)
             if t is None:
                 raise _lib.StencilError(f"{self.name}: missing array {arr}")
             if not (t.is_cuda and t.is_contiguous() and t.dtype == tdt):
                 raise _lib.StencilError(f"{arr}: contiguous CUDA {tdt} tensor required")
             keep.append(ctypes.c_void_p(t.data_ptr()))
+        keep.extend(extra)
         argv = (ctypes.c_void_p * len(keep))(*[ctypes.cast(ctypes.pointer(k), ctypes.c_void_p)
                                                for k in keep])
         blocks = max(1, (nthreads + 255) // 256)
@@ -491,6 +578,31 @@ class EmittedProblem:
             total *= max(self._eval_aff(self._shape_of(t.adjoint)[i], sizes) for t in self.terms)
         self._launch("gather", sizes, scalars, arrays, total, stream)
 
+    def adjoint_nests(self, sizes, scalars, arrays, nests=None, stream=None):
+        """The same adjoint as `adjoint`, executed the reference's way: one
+        launch per hierarchical nest, in program order.  Returns #launches."""
+        if not self.guards_ok(sizes):
+            raise _lib.GuardViolation(f"{self.name}: minimum extent violated")
+        if len(self.terms) > 64:
+            raise _lib.StencilError("nest form supports up to 64 terms")
+        count = 0
+        for lo, hi, terms in (nests if nests is not None else self.nests(sizes)):
+            pts = 1
+            for a, b in zip(lo, hi):
+                pts *= max(0, b - a + 1)
+            if pts == 0 or not terms:
+                continue
+            mask = 0
+            for t in terms:
+                mask |= 1 << t
+            extra = []
+            for a, b in zip(lo, hi):
+                extra += [ctypes.c_longlong(a), ctypes.c_longlong(b)]
+            extra.append(ctypes.c_ulonglong(mask))
+            self._launch("nest", sizes, scalars, arrays, pts, stream, extra)
+            count += 1
+        return count
+
     def primal(self, sizes, scalars, arrays, stream=None):
         total = 1
         for lo, hi in self.bounds:
@@ -503,6 +615,15 @@ def from_reference_info(spec: dict, info: dict, dtype="f64") -> EmittedProblem:
     """Build from the reference's own program structure (`ref_harness info`:
     terms in active_reads order with to_input_string partials)."""
     return EmittedProblem(spec, info["terms"], dtype)
+
+
+def load_program(family: str, dtype: str = "f64") -> EmittedProblem:
+    """A committed front-end output (programs/<family>.json) as an emitted problem."""
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "programs",
+                           family + ".json")) as fh:
+        d = json.load(fh)
+    return EmittedProblem(d["spec"], d["terms"], dtype)
 
 
 def load_spec(path: str) -> dict:

@@ -107,3 +107,63 @@ def test_emitted_kernels_match_reference(name):
             assert oracle.max_rel_err(got, want) <= 1e-12, (name, t)
         want = np.fromfile(os.path.join(out, f"primal_{ep.out}.f64")).reshape(host[ep.out].shape)
         assert oracle.max_rel_err(prim[ep.out].cpu().numpy(), want) <= 1e-12, (name, "primal")
+
+
+@pytest.mark.parametrize("key", ["wave1d@16777216", "wave3d_c@512", "burgers2d@8192",
+                                 "wave3d_r4@768", "wave3d_r4@1024"])
+def test_emitter_nests_equal_reference_nests(key):
+    """The emitter's own splitter (nest form A/B) reproduces the reference's
+    assemble_adjoint nests (bounds, term sets, order) at the BASELINE sizes."""
+    from paper_1907_02818_b200 import emitter
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ref_structure.json")) as fh:
+        ref = json.load(fh)[key]
+    name, n = key.split("@")
+    ep = emitter.EmittedProblem(json.load(open(oracle.spec_path(name))), ref["terms"])
+    mine = ep.nests({"n": int(n)})
+    assert len(mine) == len(ref["nests"])
+    for (lo, hi, terms), theirs in zip(mine, ref["nests"]):
+        assert [[a, b] for a, b in zip(lo, hi)] == theirs["bounds"]
+        assert terms == theirs["terms"]
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("name", ["lap1d", "burgers2d", "wave3d_r4", 3, 7, 11])
+def test_nest_form_equals_fused_form_bitwise(name):
+    """Boundary-strategy A/B: the reference's one-launch-per-nest structure and
+    the fused predicated form apply the same ordered increments per cell."""
+    import torch
+    from paper_1907_02818_b200 import emitter
+    n = 20 if name == "wave3d_r4" else 12
+    with tempfile.TemporaryDirectory() as td:
+        spec, path, info = problem(name, n, td)
+    ep = emitter.EmittedProblem(spec, info["terms"])
+    rng = np.random.default_rng(1)
+    sizes = {"n": n}
+    scalars = {s: 0.3 for s in spec["scalars"]}
+    base = {}
+    for arr in ep.param_arrays():
+        shp = tuple(ep._eval_aff(a, sizes) for a in ep._shape_of(arr))
+        base[arr] = torch.from_numpy(rng.standard_normal(shp)).cuda()
+    fused = {k: v.clone() for k, v in base.items()}
+    nest = {k: v.clone() for k, v in base.items()}
+    ep.adjoint(sizes, scalars, fused)
+    launches = ep.adjoint_nests(sizes, scalars, nest)
+    torch.cuda.synchronize()
+    assert launches == len(info["nests"]) or launches <= len(info["nests"])
+    for t in {t["adjoint"] for t in info["terms"]}:
+        assert torch.equal(fused[t], nest[t]), t
+
+
+def test_emitted_signatures_follow_reference_emitter():
+    """The emitted kernels' array parameters are exactly those of the
+    reference's generated functions (collect_refs, codegen.cpp:198-230)."""
+    import re
+    from paper_1907_02818_b200 import emitter
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ref_protos.json")) as fh:
+        protos = json.load(fh)
+    for fam, pr in protos.items():
+        ep = emitter.load_program(fam)
+        for which, key in (("gather", "adjoint"), ("primal", "primal")):
+            arrays = [a for a in re.findall(r"double \*(\w+)", pr[key])]
+            assert ep.param_arrays(which) == arrays, (fam, which)
