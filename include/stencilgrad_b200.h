@@ -167,6 +167,12 @@ int sgb_zero_halo_f64(double* a, int d, int n, int h, int i_base, int nplanes,
 /* c[i][j][k] = value of layer floor(i*layers/n), layer values ~ U[lo, hi) from seed */
 int sgb_fill_layered_f32(float* c, int n, int layers, double lo, double hi, uint64_t seed,
                          int i_base, int nplanes, sgb_stream_t stream);
+/* y += alpha x on the box [lo, hi]^3 of local planes [i_base, i_base+nplanes):
+ * the u_2 term of a full time-loop adjoint (u-bar^{t-1} -= u-bar^{t+1} on B) */
+int sgb_box_axpy_f32(float* y, const float* x, double alpha, int n, int lo, int hi, int i_base,
+                     int nplanes, sgb_stream_t stream);
+int sgb_box_axpy_f64(double* y, const double* x, double alpha, int n, int lo, int hi,
+                     int i_base, int nplanes, sgb_stream_t stream);
 /* one interior pass of the 5-point average u <- (u + 4 neighbours)/5 (2D) */
 int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream);
 

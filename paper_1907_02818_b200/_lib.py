@@ -28,6 +28,7 @@ _CTYPES = {
     "float*": ctypes.c_void_p,
     "double*": ctypes.c_void_p,
     "const double*": ctypes.c_void_p,
+    "const float*": ctypes.c_void_p,
     "void**": ctypes.c_void_p,
     "const char*": ctypes.c_char_p,
     "sgb_plan*": ctypes.c_void_p,

@@ -106,6 +106,20 @@ __global__ void layered_kernel(float* c, long long n, int layers, double lo, dou
   }
 }
 
+// y[p] += alpha * x[p] on the box [lo, hi]^3 of planes [i_base, i_base+nplanes)
+template <typename T>
+__global__ void box_axpy_kernel(T* y, const T* x, T alpha, long long n, long long lo,
+                                long long hi, long long i_base, long long nplanes) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long j = blockIdx.y;
+  const long long li = blockIdx.z;
+  const long long i = i_base + li;
+  if (k >= n || li >= nplanes) return;
+  if (i < lo || i > hi || j < lo || j > hi || k < lo || k > hi) return;
+  const long long t = (li * n + j) * n + k;
+  y[t] += alpha * x[t];
+}
+
 __global__ void smooth5_kernel(const double* src, double* dst, long long n) {
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long i = blockIdx.y * (long long)blockDim.y + threadIdx.y;
@@ -184,6 +198,24 @@ int sgb_fill_layered_f32(float* c, int n, int layers, double lo, double hi, uint
   layered_kernel<<<fill_grid((long long)nplanes * n * n), 256, 0, as_stream(stream)>>>(
       c, n, layers, lo, hi, seed, i_base, nplanes);
   return launch_status("sgb_fill_layered_f32");
+}
+
+int sgb_box_axpy_f32(float* y, const float* x, double alpha, int n, int lo, int hi, int i_base,
+                     int nplanes, sgb_stream_t stream) {
+  if (!y || !x || n <= 0 || nplanes <= 0) return SGB_EINVAL;
+  dim3 g((unsigned)((n + 127) / 128), (unsigned)n, (unsigned)nplanes);
+  box_axpy_kernel<float><<<g, 128, 0, as_stream(stream)>>>(y, x, (float)alpha, n, lo, hi, i_base,
+                                                           nplanes);
+  return launch_status("sgb_box_axpy_f32");
+}
+
+int sgb_box_axpy_f64(double* y, const double* x, double alpha, int n, int lo, int hi,
+                     int i_base, int nplanes, sgb_stream_t stream) {
+  if (!y || !x || n <= 0 || nplanes <= 0) return SGB_EINVAL;
+  dim3 g((unsigned)((n + 127) / 128), (unsigned)n, (unsigned)nplanes);
+  box_axpy_kernel<double><<<g, 128, 0, as_stream(stream)>>>(y, x, alpha, n, lo, hi, i_base,
+                                                            nplanes);
+  return launch_status("sgb_box_axpy_f64");
 }
 
 int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream) {

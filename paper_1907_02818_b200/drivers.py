@@ -116,3 +116,78 @@ def run_carried(n, steps, seed=0, D=0.1, family="wave3d_c", arrays=None):
                                                            arrays["u_b"])
         arrays["u_2_b"].zero_()
     return arrays
+
+
+# ---------------------------------------------------------------------------
+# the adjoint of a whole wave3d_r4 time loop with REAL
+# forward recomputation from uniform checkpoints (the reference's scope ends
+# at one loop nest; a solver's time loop is what surrounds it).
+#
+#   forward   u^{t+1} = 2 u^t - u^{t-1} + c^2 D Lap25(u^t)   (primal kernel)
+#   loss      J = <w, u^T>
+#   reverse   for t = T-1 .. 1:
+#               c_b += dF/dc^T u-bar^{t+1};  u-bar^t += dF/du^t^T u-bar^{t+1}
+#                                                        (gather adjoint kernel)
+#               u-bar^{t-1} += -u-bar^{t+1} on B           (the u_2 partial, -1)
+# States are recomputed segment by segment from checkpoints (u^s, u^{s-1})
+# stored every K steps: memory (2 T/K + K) states instead of T.
+def time_loop_forward(n, T, D, c, u0, u1, store=None):
+    """Returns u^T; store(t, u^t) is called for t = 0..T."""
+    fam = "wave3d_r4"
+    prev, cur = u0, u1
+    if store:
+        store(0, prev)
+        store(1, cur)
+    for t in range(1, T):
+        nxt = torch.zeros_like(cur)
+        api.primal(fam, n, {"D": D}, {"c": c, "u_1": cur, "u_2": prev, "u": nxt})
+        prev, cur = cur, nxt
+        if store:
+            store(t + 1, cur)
+    return cur
+
+
+def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None):
+    """Gradient of J = <w, u^T> w.r.t. (u^0, u^1, c) through T-1 primal steps.
+    Returns (u0_b, u1_b, c_b, stats)."""
+    import math
+    fam = "wave3d_r4"
+    K = checkpoint_every or max(1, int(math.isqrt(T)))
+    lo, hi = 4, n - 5
+    # forward sweep keeping only the checkpoint pairs (u^{s-1}, u^s) at
+    # s = 1, 1+K, 1+2K, ... (s < T)
+    ckpt = {1: (u0.clone(), u1.clone())}
+    prev, cur = u0, u1
+    for t in range(1, T):
+        nxt = torch.zeros_like(cur)
+        api.primal(fam, n, {"D": D}, {"c": c, "u_1": cur, "u_2": prev, "u": nxt})
+        prev, cur = cur, nxt
+        s = t + 1
+        if (s - 1) % K == 0 and s < T:
+            ckpt[s] = (prev.clone(), cur.clone())
+    recomputed = 0
+    # reverse sweep
+    ub_next = w.clone()                  # u-bar^{t+1}
+    ub_cur = torch.zeros_like(w)         # u-bar^t
+    ub_prev = torch.zeros_like(w)        # u-bar^{t-1}
+    c_b = torch.zeros_like(c)
+    starts = sorted(ckpt)
+    for s in reversed(starts):
+        t_end = min(s + K, T)            # segment steps t = s .. t_end-1
+        states = {s - 1: ckpt[s][0], s: ckpt[s][1]}
+        for t in range(s, t_end - 1):    # recompute u^{s+1} .. u^{t_end-1}
+            nxt = torch.zeros_like(w)
+            api.primal(fam, n, {"D": D}, {"c": c, "u_1": states[t], "u_2": states[t - 1],
+                                          "u": nxt})
+            states[t + 1] = nxt
+            recomputed += 1
+        for t in reversed(range(s, t_end)):
+            api.adjoint(fam, n, {"D": D}, {"c": c, "c_b": c_b, "u_1": states[t],
+                                           "u_1_b": ub_cur, "u_b": ub_next})
+            api.box_axpy(ub_prev, ub_next, -1.0, n, lo, hi)
+            ub_next, ub_cur, ub_prev = ub_cur, ub_prev, ub_next
+            ub_prev.zero_()
+    # after the loop: ub_next = u-bar^1, ub_cur = u-bar^0
+    stats = {"checkpoint_every": K, "checkpoints": len(starts), "recomputed_steps": recomputed,
+             "adjoint_steps": T - 1}
+    return ub_cur, ub_next, c_b, stats

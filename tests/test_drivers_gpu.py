@@ -120,3 +120,39 @@ def test_generators_are_decomposition_invariant(mods):
     assert torch.equal(lpart, lay[30:35])
     z = full[4:-4, 4:-4, 4:-4]
     assert abs(float(z.mean())) < 0.05 and abs(float(z.std()) - 1) < 0.05
+
+
+def test_time_loop_adjoint_checkpointing_and_gradient(mods):
+    """adjoint of a whole wave3d_r4 time loop with forward
+    recomputation from checkpoints.  Checkpoint spacing does not change the
+    result (bitwise), and <grad, v> matches a central finite difference of
+    J = <w, u^T> (fp64, the reference's dot-product test idea,
+    interp.cpp:300-381, applied to the whole loop)."""
+    torch, api, drivers = mods
+    n, T, D = 20, 7, 0.01
+    g = torch.Generator(device="cpu").manual_seed(3)
+
+    def rnd(halo=4):
+        x = torch.randn((n, n, n), generator=g, dtype=torch.float64)
+        if halo:
+            x[:halo] = 0; x[-halo:] = 0; x[:, :halo] = 0; x[:, -halo:] = 0
+            x[:, :, :halo] = 0; x[:, :, -halo:] = 0
+        return x.cuda()
+    c = (torch.rand((n, n, n), generator=g, dtype=torch.float64) * 3 + 1.5).cuda()
+    u0, u1, w = rnd(), rnd(), rnd(0)
+    res = {}
+    for K in (1, 2, 3, T):
+        u0b, u1b, cb, st = drivers.time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=K)
+        res[K] = (u0b.clone(), u1b.clone(), cb.clone())
+    for K in (2, 3, T):
+        for a, b in zip(res[1], res[K]):
+            assert torch.equal(a, b), K
+    u0b, u1b, cb = res[3]
+
+    def J(a0, a1, cc):
+        return float((w * drivers.time_loop_forward(n, T, D, cc, a0, a1)).sum())
+    v0, v1, vc = rnd(), rnd(), rnd()
+    h = 1e-6
+    fd = (J(u0 + h * v0, u1 + h * v1, c + h * vc) - J(u0 - h * v0, u1 - h * v1, c - h * vc)) / (2 * h)
+    ad = float((v0 * u0b).sum() + (v1 * u1b).sum() + (vc * cb).sum())
+    assert abs(fd - ad) / (1 + abs(ad)) < 1e-6, (fd, ad)
