@@ -448,7 +448,46 @@ struct StarTile7 {
   static_assert(RING % NS == 0, "static stage index");
 };
 
-template <int MODE>
+// Tile map: interior tiles (halo box inside [lo, hi] in j and k) form the
+// rectangle tk in [ik0, ik1) x tj in [ij0, ij1); the rest is a frame.  The
+// INT=true instantiation runs the rectangle (k fastest) with no mask code at
+// all, INT=false the frame; both are launched back to back.
+struct TileMap {
+  int tiles_k, tiles_j, ik0, ik1, ij0, ij1;
+  __host__ __device__ int n_interior() const {
+    return (ik1 > ik0 && ij1 > ij0) ? (ik1 - ik0) * (ij1 - ij0) : 0;
+  }
+  __host__ __device__ int n_frame() const { return tiles_k * tiles_j - n_interior(); }
+  __device__ void interior(int t, int& tk, int& tj) const {
+    const int w = ik1 - ik0;
+    tk = ik0 + t % w;
+    tj = ij0 + t / w;
+  }
+  __device__ void frame(int b, int& tk, int& tj) const {
+    if (n_interior() == 0) {
+      tk = b % tiles_k;
+      tj = b / tiles_k;
+      return;
+    }
+    const int top = ij0 * tiles_k;
+    const int side = ik0 + (tiles_k - ik1);
+    const int mid = (ij1 - ij0) * side;
+    if (b < top) {
+      tk = b % tiles_k;
+      tj = b / tiles_k;
+    } else if (b < top + mid) {
+      const int m = b - top, r = m % side;
+      tj = ij0 + m / side;
+      tk = r < ik0 ? r : ik1 + (r - ik0);
+    } else {
+      const int m = b - top - mid;
+      tk = m % tiles_k;
+      tj = ij1 + m / tiles_k;
+    }
+  }
+};
+
+template <int MODE, bool INT>
 __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
     star3_v7_kernel(const __grid_constant__ CUtensorMap tm_c,
                     const __grid_constant__ CUtensorMap tm_ub,
@@ -457,8 +496,7 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
                     const __grid_constant__ CUtensorMap tm_u1b,
                     const __grid_constant__ CUtensorMap tm_u2b, float* __restrict__ c_b,
                     float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n, int i_base,
-                    int lo, int hi, int out_i0, int out_i1, int chunk, int tiles_k, float D,
-                    int order) {
+                    int lo, int hi, int out_i0, int out_i1, int chunk, TileMap tm, float D) {
   using Tl = StarTile7<MODE>;
   using S3 = Star3<MODE>;
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
@@ -475,23 +513,11 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
   const bool q_role = tid >= ROLE;  // warp-uniform
   const int rt = q_role ? tid - ROLE : tid;
   const int tx = rt & 15, ty = rt >> 4;  // 4 k-points x rows 2ty, 2ty+1
-  // tile order: order 0 = k fastest; order 1 = j fastest (the j neighbours,
-  // which share 2R halo rows, are consecutive CTAs and so run at the same time)
-  // order >= 2: groups of `order` j-adjacent tiles are consecutive CTAs (and
-  // the groups run k-fastest), so most j and all k neighbours run together
-  const int tiles_j = (n + Tl::TJ - 1) / Tl::TJ;
   int tk, tj;
-  if (order == 1) {
-    tk = blockIdx.x / tiles_j;
-    tj = blockIdx.x % tiles_j;
-  } else if (order >= 2 && tiles_j % order == 0) {
-    const int grp = blockIdx.x / order, m = blockIdx.x % order;
-    tk = grp % tiles_k;
-    tj = order * (grp / tiles_k) + m;
-  } else {
-    tk = blockIdx.x % tiles_k;
-    tj = blockIdx.x / tiles_k;
-  }
+  if (INT)
+    tm.interior(blockIdx.x, tk, tj);
+  else
+    tm.frame(blockIdx.x, tk, tj);
   const int k0 = tk * TK, j0 = tj * Tl::TJ;
   const int o_begin = out_i0 + blockIdx.y * chunk;
   const int o_end = min(o_begin + chunk, out_i1);
@@ -536,12 +562,7 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
   const int r0 = 2 * ty + HJ, col = HK + 4 * tx;
   const int trow = 2 * ty * TK + 4 * tx;  // offset of row 2ty in a 64x32 tile
   const long long plane = (long long)n * n;
-  const long long coff = (long long)jr0 * n + kc;
-  const bool interior = j0 - HJ >= lo && j0 + Tl::TJ + HJ - 1 <= hi && k0 - HK >= lo &&
-                        k0 + TK + HK - 1 <= hi && j0 + Tl::TJ <= n && k0 + TK <= n;
-  bool kin[4];
-#pragma unroll
-  for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
+  const int coff = jr0 * n + kc;  // in-plane offset (n*n < 2^31)
   const float gf = S3::kC2 ? 2.f * D : D;
 
   // q-pass elements of this thread (fixed for all planes): smem offset in the
@@ -572,7 +593,7 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
         const float* Cs = stage + s * SF;
         const float* UBs = Cs + BF;
         const float* U1s = Cs + 2 * BF;
-        float* Q = qbuf + (it % NQB) * BF;
+        float* Q = qbuf + ((it & 1) ? BF : 0);
         float* G = gq + (it % QD) * TILE;
         const bool emit = it >= 2 * R;
         const int o = p - R;
@@ -592,13 +613,13 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
         for (int m = 0; m < Tl::EPT; m++) {
           if (qoff[m] >= 0) {
             const int qo = qoff[m];
-            const int row = qo / BW, c4 = (qo - row * BW) >> 2;
             const bool centre = goff[m] >= 0;
             float4 qv = make_float4(0.f, 0.f, 0.f, 0.f), gv = qv;
             if (pin) {
               const float4 cv = lds4(Cs + qo);
               float4 uv = lds4(UBs + qo);
-              if (!interior) {
+              if (!INT) {
+                const int row = qo / BW, c4 = (qo - row * BW) >> 2;
                 const int jg = j0 - HJ + row, kg = k0 - HK + 4 * c4;
                 const bool rm = jg >= lo && jg <= hi;
                 if (!(rm && kg >= lo && kg <= hi)) uv.x = 0.f;
@@ -616,18 +637,23 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
         }
         // ---- q role: 2 u_b centre term (and u_2_b at plane p)
         if (q_role && pin) {
+          float* u2_plane = u_2_b + (long long)(p - i_base) * plane;
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            const bool jin = jr0 + h >= lo && jr0 + h <= hi;
             float4 ubm = lds4(UBs + (r0 + h) * BW + col);
-            if (!interior)
+            bool kin[4] = {true, true, true, true}, jin = true;
+            if (!INT) {
+              jin = jr0 + h >= lo && jr0 + h <= hi;
+#pragma unroll
+              for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
               ubm = make_float4(jin && kin[0] ? ubm.x : 0.f, jin && kin[1] ? ubm.y : 0.f,
                                 jin && kin[2] ? ubm.z : 0.f, jin && kin[3] ? ubm.w : 0.f);
+            }
             acc[ph][h] = fmas4(2.f, ubm, acc[ph][h]);
-            if (S3::kU2 && jin && jr0 + h < n && kc < n && p >= o_begin && p < o_end) {
+            if (S3::kU2 && jin && (INT || (jr0 + h < n && kc < n)) && p >= o_begin &&
+                p < o_end) {
               const float4 u2 = lds4(Cs + 3 * BF + 2 * TILE + trow + h * TK);
-              float* ptr = u_2_b + (long long)(p - i_base) * plane + coff + (long long)h * n;
-              __stcs(reinterpret_cast<float4*>(ptr),
+              __stcs(reinterpret_cast<float4*>(u2_plane + coff + h * n),
                      make_float4(kin[0] ? u2.x - ubm.x : u2.x, kin[1] ? u2.y - ubm.y : u2.y,
                                  kin[2] ? u2.z - ubm.z : u2.z, kin[3] ? u2.w - ubm.w : u2.w));
             }
@@ -641,36 +667,45 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
         // ---- emit output plane o = p - R
         if (emit) {
           const int es = (ph + R + 1) % RING;
-          const long long obase = (long long)(o - i_base) * plane + coff;
+          const long long obase = (long long)(o - i_base) * plane;
           if (!q_role) {
             if (oin) {
               const float* Go = gq + ((it - R) % QD) * TILE + trow;
+              float* cb_plane = c_b + obase;
 #pragma unroll
               for (int h = 0; h < 2; h++) {
-                const bool jin = jr0 + h >= lo && jr0 + h <= hi;
-                if (!jin || jr0 + h >= n || kc >= n) continue;
                 float4 nv = fma4(lds4(Go + h * TK), acc[es][h], old[h]);
-                if (!interior)
+                if (!INT) {
+                  const int j = jr0 + h;
+                  if (!(j >= lo && j <= hi) || j >= n || kc >= n) continue;
+                  bool kin[4];
+#pragma unroll
+                  for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
                   nv = make_float4(kin[0] ? nv.x : old[h].x, kin[1] ? nv.y : old[h].y,
                                    kin[2] ? nv.z : old[h].z, kin[3] ? nv.w : old[h].w);
-                __stcs(reinterpret_cast<float4*>(c_b + obase + (long long)h * n), nv);
+                }
+                __stcs(reinterpret_cast<float4*>(cb_plane + coff + h * n), nv);
               }
             }
           } else {
             const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
+            float* u1b_plane = u_1_b + obase;
+            if (INT) {
+              if (oout <= R) {
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
-              const int j = jr0 + h;
-              if (j >= n || kc >= n) continue;
-              float4 nv;
-              if (interior) {
-                if (oout > R) continue;
-                nv = add4(old[h], acc[es][h]);
-              } else {
+                for (int h = 0; h < 2; h++)
+                  __stcs(reinterpret_cast<float4*>(u1b_plane + coff + h * n),
+                         add4(old[h], acc[es][h]));
+              }
+            } else {
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                const int j = jr0 + h;
+                if (j >= n || kc >= n) continue;
                 const int jout = j < lo ? lo - j : (j > hi ? j - hi : 0);
                 const float4 a = acc[es][h];
                 const float av[4] = {a.x, a.y, a.z, a.w};
-                nv = old[h];
+                float4 nv = old[h];
                 float* nvp = reinterpret_cast<float*>(&nv);
                 bool any = false;
 #pragma unroll
@@ -683,9 +718,8 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
                   if (reach) nvp[m] = nvp[m] + av[m];
                   any |= reach;
                 }
-                if (!any) continue;
+                if (any) __stcs(reinterpret_cast<float4*>(u1b_plane + coff + h * n), nv);
               }
-              __stcs(reinterpret_cast<float4*>(u_1_b + obase + (long long)h * n), nv);
             }
           }
         }
@@ -712,25 +746,47 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   if (rc) return SGB_EINVAL;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(star3_v7_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(star3_v7_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Tl::SMEM);
+    cudaFuncSetAttribute(star3_v7_kernel<MODE, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
     attr_set = true;
   }
-  const int tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
-  const int tiles_j = (int)((g.n + Tl::TJ - 1) / Tl::TJ);
+  TileMap tm;
+  tm.tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
+  tm.tiles_j = (int)((g.n + Tl::TJ - 1) / Tl::TJ);
+  // interior: the whole halo box inside [lo, hi] (and inside the grid)
+  auto first_in = [&](int T, int H) {  // smallest tile index t with t*T - H >= lo
+    long long t = (lo + H + T - 1) / T;
+    return (int)t;
+  };
+  auto end_in = [&](int T, int H, int tiles) {  // one past the last t with t*T+T+H-1 <= hi
+    long long t = (hi - H + 1) / T;             // t*T + T + H - 1 <= hi  <=> t <= (hi-H+1)/T - 1
+    return (int)std::min<long long>(t, tiles);
+  };
+  tm.ik0 = first_in(Tl::TK, Tl::HK);
+  tm.ik1 = end_in(Tl::TK, Tl::HK, tm.tiles_k);
+  tm.ij0 = first_in(Tl::TJ, Tl::HJ);
+  tm.ij1 = end_in(Tl::TJ, Tl::HJ, tm.tiles_j);
+  if (tm.ik1 <= tm.ik0 || tm.ij1 <= tm.ij0) tm.ik0 = tm.ik1 = tm.ij0 = tm.ij1 = 0;
   const long long nout = out_i1 - out_i0;
-  const int chunks = choose_chunks((long long)tiles_k * tiles_j, nout, Tl::R, 1);
+  const int chunks = choose_chunks((long long)tm.tiles_k * tm.tiles_j, nout, Tl::R, 1);
   const int chunk = (int)((nout + chunks - 1) / chunks);
-  dim3 grid((unsigned)(tiles_k * tiles_j), (unsigned)((nout + chunk - 1) / chunk));
-  static int order = -1;
-  if (order < 0) {
-    const char* e = std::getenv("SGB_TILE_ORDER");
-    order = e ? std::atoi(e) : 0;
+  const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
+  if (tm.n_interior() > 0) {
+    star3_v7_kernel<MODE, true><<<dim3((unsigned)tm.n_interior(), gy), Tl::THREADS, Tl::SMEM, s>>>(
+        maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tm, D);
+    const int st = launch_status(name);
+    if (st) return st;
   }
-  star3_v7_kernel<MODE><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
-      maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-      (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D, order);
-  return launch_status(name);
+  if (tm.n_frame() > 0) {
+    star3_v7_kernel<MODE, false><<<dim3((unsigned)tm.n_frame(), gy), Tl::THREADS, Tl::SMEM, s>>>(
+        maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tm, D);
+    return launch_status(name);
+  }
+  return 0;
 }
 
 }  // namespace sgb
