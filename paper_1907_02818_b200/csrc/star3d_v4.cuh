@@ -18,6 +18,8 @@
 //   * the adjoint read-modify-write uses streaming 128-bit loads (issued a
 //     full plane ahead of use) and stores.
 #pragma once
+#include <mutex>
+#include <utility>
 
 #include "star3d_v3.cuh"
 
@@ -448,6 +450,31 @@ struct StarTile7 {
   static_assert(RING % NS == 0, "static stage index");
 };
 
+// One non-blocking side stream (+ fork/join events) per device, created on
+// first use; lets the frame kernel overlap the interior kernel.  Fork/join by
+// events, so it is legal inside CUDA graph capture.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+inline SideStream* side_stream() {
+  static SideStream per_dev[64];
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  SideStream& ss = per_dev[dev];
+  if (!ss.s) {
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+      ss.s = nullptr;
+      return nullptr;
+    }
+  }
+  return &ss;
+}
+
 // Tile map: interior tiles (halo box inside [lo, hi] in j and k) form the
 // rectangle tk in [ik0, ik1) x tj in [ij0, ij1); the rest is a frame.  The
 // INT=true instantiation runs the rectangle (k fastest) with no mask code at
@@ -488,15 +515,11 @@ struct TileMap {
 };
 
 template <int MODE, bool INT>
-__global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
-    star3_v7_kernel(const __grid_constant__ CUtensorMap tm_c,
-                    const __grid_constant__ CUtensorMap tm_ub,
-                    const __grid_constant__ CUtensorMap tm_u1,
-                    const __grid_constant__ CUtensorMap tm_cb,
-                    const __grid_constant__ CUtensorMap tm_u1b,
-                    const __grid_constant__ CUtensorMap tm_u2b, float* __restrict__ c_b,
-                    float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n, int i_base,
-                    int lo, int hi, int out_i0, int out_i1, int chunk, TileMap tm, float D) {
+__device__ __forceinline__ void star3_v7_body(
+    const CUtensorMap& tm_c, const CUtensorMap& tm_ub, const CUtensorMap& tm_u1,
+    const CUtensorMap& tm_cb, const CUtensorMap& tm_u1b, const CUtensorMap& tm_u2b,
+    float* __restrict__ c_b, float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n,
+    int i_base, int lo, int hi, int out_i0, int out_i1, int chunk, int tk, int tj, float D) {
   using Tl = StarTile7<MODE>;
   using S3 = Star3<MODE>;
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
@@ -513,11 +536,6 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
   const bool q_role = tid >= ROLE;  // warp-uniform
   const int rt = q_role ? tid - ROLE : tid;
   const int tx = rt & 15, ty = rt >> 4;  // 4 k-points x rows 2ty, 2ty+1
-  int tk, tj;
-  if (INT)
-    tm.interior(blockIdx.x, tk, tj);
-  else
-    tm.frame(blockIdx.x, tk, tj);
   const int k0 = tk * TK, j0 = tj * Tl::TJ;
   const int o_begin = out_i0 + blockIdx.y * chunk;
   const int o_end = min(o_begin + chunk, out_i1);
@@ -577,6 +595,46 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
                   ? (row - HJ) * TK + 4 * (c4 - 1)
                   : -1;
   }
+  // Frame tiles: every (j, k) predicate is plane-independent, so it is
+  // evaluated once here into bit masks (only the i terms vary per plane).
+  //   qmask bit 4m+x : u_b element x of q-pass element m inside [lo, hi]^2
+  //   fm bits 0-7   : centre (h, x) with j, k in [lo, hi]          (set A)
+  //   fm bits 8-15  : centre (h, x) one coordinate out by <= R     (set B)
+  //   fm bits 16-19 : k = kc + x in [lo, hi]
+  //   fm bits 20-21 : row h in [lo, hi] and inside the grid
+  //   fm bits 22-23 : row h inside the grid
+  uint32_t qmask = 0, fm = 0;
+  if (!INT) {
+#pragma unroll
+    for (int m = 0; m < Tl::EPT; m++) {
+      if (qoff[m] < 0) continue;
+      const int row = qoff[m] / BW, c4 = (qoff[m] - row * BW) >> 2;
+      const int jg = j0 - HJ + row, kg = k0 - HK + 4 * c4;
+      const bool rm = jg >= lo && jg <= hi;
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+        if (rm && kg + x >= lo && kg + x <= hi) qmask |= 1u << (4 * m + x);
+    }
+#pragma unroll
+    for (int x = 0; x < 4; x++)
+      if (kc + x >= lo && kc + x <= hi) fm |= 1u << (16 + x);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int j = jr0 + h;
+      const bool grid = j < n && kc < n;
+      const bool jin = j >= lo && j <= hi;
+      const int jout = j < lo ? lo - j : (j > hi ? j - hi : 0);
+      if (grid) fm |= 1u << (22 + h);
+      if (grid && jin) fm |= 1u << (20 + h);
+#pragma unroll
+      for (int x = 0; x < 4; x++) {
+        const int k = kc + x;
+        const int kout = k < lo ? lo - k : (k > hi ? k - hi : 0);
+        if (jout == 0 && kout == 0) fm |= 1u << (4 * h + x);
+        if ((jout > 0) + (kout > 0) == 1 && jout <= R && kout <= R) fm |= 1u << (8 + 4 * h + x);
+      }
+    }
+  }
 
   float4 acc[RING][2];
 #pragma unroll
@@ -619,13 +677,9 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
               const float4 cv = lds4(Cs + qo);
               float4 uv = lds4(UBs + qo);
               if (!INT) {
-                const int row = qo / BW, c4 = (qo - row * BW) >> 2;
-                const int jg = j0 - HJ + row, kg = k0 - HK + 4 * c4;
-                const bool rm = jg >= lo && jg <= hi;
-                if (!(rm && kg >= lo && kg <= hi)) uv.x = 0.f;
-                if (!(rm && kg + 1 >= lo && kg + 1 <= hi)) uv.y = 0.f;
-                if (!(rm && kg + 2 >= lo && kg + 2 <= hi)) uv.z = 0.f;
-                if (!(rm && kg + 3 >= lo && kg + 3 <= hi)) uv.w = 0.f;
+                const uint32_t mk = qmask >> (4 * m);
+                uv = make_float4(mk & 1 ? uv.x : 0.f, mk & 2 ? uv.y : 0.f, mk & 4 ? uv.z : 0.f,
+                                 mk & 8 ? uv.w : 0.f);
               }
               const float4 du = muls4(D, uv);
               qv = mul4(S3::kC2 ? mul4(cv, cv) : cv, du);
@@ -643,14 +697,15 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
             float4 ubm = lds4(UBs + (r0 + h) * BW + col);
             bool kin[4] = {true, true, true, true}, jin = true;
             if (!INT) {
-              jin = jr0 + h >= lo && jr0 + h <= hi;
+              const uint32_t mk = fm >> (4 * h);
+              jin = (fm >> (20 + h)) & 1;
 #pragma unroll
-              for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
-              ubm = make_float4(jin && kin[0] ? ubm.x : 0.f, jin && kin[1] ? ubm.y : 0.f,
-                                jin && kin[2] ? ubm.z : 0.f, jin && kin[3] ? ubm.w : 0.f);
+              for (int x = 0; x < 4; x++) kin[x] = (fm >> (16 + x)) & 1;
+              ubm = make_float4(mk & 1 ? ubm.x : 0.f, mk & 2 ? ubm.y : 0.f, mk & 4 ? ubm.z : 0.f,
+                                mk & 8 ? ubm.w : 0.f);
             }
             acc[ph][h] = fmas4(2.f, ubm, acc[ph][h]);
-            if (S3::kU2 && jin && (INT || (jr0 + h < n && kc < n)) && p >= o_begin &&
+            if (S3::kU2 && jin && p >= o_begin &&
                 p < o_end) {
               const float4 u2 = lds4(Cs + 3 * BF + 2 * TILE + trow + h * TK);
               __stcs(reinterpret_cast<float4*>(u2_plane + coff + h * n),
@@ -676,13 +731,10 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
               for (int h = 0; h < 2; h++) {
                 float4 nv = fma4(lds4(Go + h * TK), acc[es][h], old[h]);
                 if (!INT) {
-                  const int j = jr0 + h;
-                  if (!(j >= lo && j <= hi) || j >= n || kc >= n) continue;
-                  bool kin[4];
-#pragma unroll
-                  for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
-                  nv = make_float4(kin[0] ? nv.x : old[h].x, kin[1] ? nv.y : old[h].y,
-                                   kin[2] ? nv.z : old[h].z, kin[3] ? nv.w : old[h].w);
+                  if (!((fm >> (20 + h)) & 1)) continue;
+                  const uint32_t mk = fm >> 16;
+                  nv = make_float4(mk & 1 ? nv.x : old[h].x, mk & 2 ? nv.y : old[h].y,
+                                   mk & 4 ? nv.z : old[h].z, mk & 8 ? nv.w : old[h].w);
                 }
                 __stcs(reinterpret_cast<float4*>(cb_plane + coff + h * n), nv);
               }
@@ -698,27 +750,19 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
                          add4(old[h], acc[es][h]));
               }
             } else {
+              // reached iff at most one coordinate is outside [lo, hi], by <= R
+              const uint32_t reach =
+                  oout == 0 ? (fm | (fm >> 8)) & 0xff : (oout <= R ? fm & 0xff : 0u);
 #pragma unroll
               for (int h = 0; h < 2; h++) {
-                const int j = jr0 + h;
-                if (j >= n || kc >= n) continue;
-                const int jout = j < lo ? lo - j : (j > hi ? j - hi : 0);
+                const uint32_t mk = reach >> (4 * h);
+                if (!((fm >> (22 + h)) & 1) || !(mk & 0xf)) continue;
                 const float4 a = acc[es][h];
-                const float av[4] = {a.x, a.y, a.z, a.w};
-                float4 nv = old[h];
-                float* nvp = reinterpret_cast<float*>(&nv);
-                bool any = false;
-#pragma unroll
-                for (int m = 0; m < 4; m++) {
-                  const int k = kc + m;
-                  const int kout = k < lo ? lo - k : (k > hi ? k - hi : 0);
-                  const int nout = (oout > 0) + (jout > 0) + (kout > 0);
-                  const bool reach =
-                      nout == 0 || (nout == 1 && oout <= R && jout <= R && kout <= R);
-                  if (reach) nvp[m] = nvp[m] + av[m];
-                  any |= reach;
-                }
-                if (any) __stcs(reinterpret_cast<float4*>(u1b_plane + coff + h * n), nv);
+                const float4 nv = make_float4(mk & 1 ? old[h].x + a.x : old[h].x,
+                                              mk & 2 ? old[h].y + a.y : old[h].y,
+                                              mk & 4 ? old[h].z + a.z : old[h].z,
+                                              mk & 8 ? old[h].w + a.w : old[h].w);
+                __stcs(reinterpret_cast<float4*>(u1b_plane + coff + h * n), nv);
               }
             }
           }
@@ -726,6 +770,38 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
       }
     }
   }
+}
+
+#define SGB_V7_PARAMS                                                                   \
+  const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_ub,     \
+      const __grid_constant__ CUtensorMap tm_u1, const __grid_constant__ CUtensorMap tm_cb, \
+      const __grid_constant__ CUtensorMap tm_u1b,                                          \
+      const __grid_constant__ CUtensorMap tm_u2b, float *__restrict__ c_b,                 \
+      float *__restrict__ u_1_b, float *__restrict__ u_2_b, int n, int i_base, int lo,     \
+      int hi, int out_i0, int out_i1, int chunk, TileMap tm, float D
+#define SGB_V7_ARGS                                                                    \
+  tm_c, tm_ub, tm_u1, tm_cb, tm_u1b, tm_u2b, c_b, u_1_b, u_2_b, n, i_base, lo, hi, out_i0, \
+      out_i1, chunk
+
+// Split launch: INT=true runs the interior rectangle, INT=false the frame.
+template <int MODE, bool INT>
+__global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_kernel(SGB_V7_PARAMS) {
+  int tk, tj;
+  if (INT)
+    tm.interior(blockIdx.x, tk, tj);
+  else
+    tm.frame(blockIdx.x, tk, tj);
+  star3_v7_body<MODE, INT>(SGB_V7_ARGS, tk, tj, D);
+}
+
+// Unified launch: row-major tile order, each CTA picks its specialised body.
+template <int MODE>
+__global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_unified(SGB_V7_PARAMS) {
+  const int tk = blockIdx.x % tm.tiles_k, tj = blockIdx.x / tm.tiles_k;
+  if (tk >= tm.ik0 && tk < tm.ik1 && tj >= tm.ij0 && tj < tm.ij1)
+    star3_v7_body<MODE, true>(SGB_V7_ARGS, tk, tj, D);
+  else
+    star3_v7_body<MODE, false>(SGB_V7_ARGS, tk, tj, D);
 }
 
 template <int MODE>
@@ -750,6 +826,8 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
                          (int)Tl::SMEM);
     cudaFuncSetAttribute(star3_v7_kernel<MODE, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
+    cudaFuncSetAttribute(star3_v7_unified<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Tl::SMEM);
     attr_set = true;
   }
   TileMap tm;
@@ -770,21 +848,62 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   tm.ij1 = end_in(Tl::TJ, Tl::HJ, tm.tiles_j);
   if (tm.ik1 <= tm.ik0 || tm.ij1 <= tm.ij0) tm.ik0 = tm.ik1 = tm.ij0 = tm.ij1 = 0;
   const long long nout = out_i1 - out_i0;
-  const int chunks = choose_chunks((long long)tm.tiles_k * tm.tiles_j, nout, Tl::R, 1);
-  const int chunk = (int)((nout + chunks - 1) / chunks);
-  const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
-  if (tm.n_interior() > 0) {
-    star3_v7_kernel<MODE, true><<<dim3((unsigned)tm.n_interior(), gy), Tl::THREADS, Tl::SMEM, s>>>(
-        maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tm, D);
+  // i-chunk count per launch from a wave model: CTAs are equal-length
+  // (one tile column over chunk + 2R planes), one resident per SM, so a launch
+  // takes ceil(tiles*c / SMs) * (ceil(nout/c) + 2R) plane-times.  Minimising it
+  // reproduced the measured best chunking at 768^3 and 1024^3.
+  const int sms = num_sms();
+  auto chunking = [&](const char* env, long long tiles) {
+    int c = 0;
+    if (const char* e = std::getenv(env)) c = std::max(1, std::atoi(e));
+    if (c == 0) {
+      long long best = -1;
+      for (int cc = 1; cc <= 64 && cc <= nout; cc++) {
+        const long long len = (nout + cc - 1) / cc;
+        const long long waves = (tiles * cc + sms - 1) / sms;
+        const long long cost = waves * (len + 2 * Tl::R);
+        if (best < 0 || cost < best) best = cost, c = cc;
+      }
+    }
+    const int len = (int)((nout + c - 1) / c);
+    return std::make_pair(len, (unsigned)((nout + len - 1) / len));
+  };
+  const auto ci = chunking("SGB_ICHUNKS", tm.n_interior());
+  const auto cf = chunking("SGB_ICHUNKS_F", tm.n_frame());
+  if (std::getenv("SGB_V7_UNIFIED")) {
+    star3_v7_unified<MODE><<<dim3((unsigned)(tm.tiles_k * tm.tiles_j), ci.second), Tl::THREADS,
+                             Tl::SMEM, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
+                                            c_b, u_1_b, u_2_b, (int)g.n, (int)g.i_base, (int)lo,
+                                            (int)hi, (int)out_i0, (int)out_i1, ci.first, tm, D);
+    return launch_status(name);
+  }
+  const bool fork = tm.n_interior() > 0 && tm.n_frame() > 0 && std::getenv("SGB_FORK");
+  SideStream* ss = fork ? side_stream() : nullptr;
+  if (ss) {
+    if (cudaEventRecord(ss->fork, s) != cudaSuccess ||
+        cudaStreamWaitEvent(ss->s, ss->fork, 0) != cudaSuccess)
+      return launch_status(name);
+  }
+  if (tm.n_frame() > 0) {
+    star3_v7_kernel<MODE, false>
+        <<<dim3((unsigned)tm.n_frame(), cf.second), Tl::THREADS, Tl::SMEM, ss ? ss->s : s>>>(
+            maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cf.first, tm, D);
     const int st = launch_status(name);
     if (st) return st;
   }
-  if (tm.n_frame() > 0) {
-    star3_v7_kernel<MODE, false><<<dim3((unsigned)tm.n_frame(), gy), Tl::THREADS, Tl::SMEM, s>>>(
-        maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tm, D);
-    return launch_status(name);
+  if (tm.n_interior() > 0) {
+    star3_v7_kernel<MODE, true>
+        <<<dim3((unsigned)tm.n_interior(), ci.second), Tl::THREADS, Tl::SMEM, s>>>(
+            maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, ci.first, tm, D);
+    const int st = launch_status(name);
+    if (st) return st;
+  }
+  if (ss) {
+    if (cudaEventRecord(ss->join, ss->s) != cudaSuccess ||
+        cudaStreamWaitEvent(s, ss->join, 0) != cudaSuccess)
+      return launch_status(name);
   }
   return 0;
 }
