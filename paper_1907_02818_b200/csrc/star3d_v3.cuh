@@ -343,6 +343,33 @@ inline int encode_3d(CUtensorMap* map, const float* base, long long n, long long
   return 0;
 }
 
+// Same, restricted to the window [off, off+ext) in j and k: TMA zero-fills
+// every element outside it, which is exactly the primal-box mask on the seed
+// (u_b is defined on [lo, hi]^3 only).  Needs a 16-byte aligned window base;
+// returns 1 (no map) when it is not.
+inline int encode_3d_window(CUtensorMap* map, const float* base, long long n, long long nplanes,
+                            long long off, long long ext, int box0, int box1, const char* name) {
+  const float* wb = base + off * n + off;
+  if ((reinterpret_cast<uintptr_t>(wb) & 15) != 0 || ext < 1) return 1;
+  auto encode = get_encode();
+  if (!encode) {
+    set_error(std::string(name) + ": cuTensorMapEncodeTiled unavailable");
+    return SGB_EINVAL;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)ext, (cuuint64_t)ext, (cuuint64_t)nplanes};
+  cuuint64_t strides[2] = {(cuuint64_t)n * 4, (cuuint64_t)n * n * 4};
+  cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)wb, dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(std::string(name) + ": tensor map encode failed (" + std::to_string((int)r) + ")");
+    return SGB_EINVAL;
+  }
+  return 0;
+}
+
 template <int MODE>
 inline int star3_v3_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
                            long long out_i1, float D, const float* c, float* c_b,

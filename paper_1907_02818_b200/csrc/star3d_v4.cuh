@@ -514,7 +514,7 @@ struct TileMap {
   }
 };
 
-template <int MODE, bool INT>
+template <int MODE, bool INT, bool UBW>
 __device__ __forceinline__ void star3_v7_body(
     const CUtensorMap& tm_c, const CUtensorMap& tm_ub, const CUtensorMap& tm_u1,
     const CUtensorMap& tm_cb, const CUtensorMap& tm_u1b, const CUtensorMap& tm_u2b,
@@ -555,6 +555,7 @@ __device__ __forceinline__ void star3_v7_body(
     tma::fence_barrier_init();
   }
   __syncthreads();
+  const int ulo = UBW ? lo : 0;  // u_b map origin (windowed map: TMA does the mask)
   auto issue = [&](int it) {
     const int s = it % NS;
     float* dst = stage + s * SF;
@@ -565,7 +566,7 @@ __device__ __forceinline__ void star3_v7_body(
     tma::mbar_arrive_expect_tx(&bars[s], 3 * Tl::BOX_BYTES +
                                              ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE * 4);
     tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
-    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK - ulo, j0 - HJ - ulo, pl);
     tma::load_3d(dst + 2 * BF, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
     if (emit) {
       tma::load_3d(dst + 3 * BF, &tm_cb, &bars[s], k0, j0, pl - R);
@@ -607,7 +608,7 @@ __device__ __forceinline__ void star3_v7_body(
   if (!INT) {
 #pragma unroll
     for (int m = 0; m < Tl::EPT; m++) {
-      if (qoff[m] < 0) continue;
+      if (qoff[m] < 0 || UBW) continue;
       const int row = qoff[m] / BW, c4 = (qoff[m] - row * BW) >> 2;
       const int jg = j0 - HJ + row, kg = k0 - HK + 4 * c4;
       const bool rm = jg >= lo && jg <= hi;
@@ -676,7 +677,7 @@ __device__ __forceinline__ void star3_v7_body(
             if (pin) {
               const float4 cv = lds4(Cs + qo);
               float4 uv = lds4(UBs + qo);
-              if (!INT) {
+              if (!INT && !UBW) {
                 const uint32_t mk = qmask >> (4 * m);
                 uv = make_float4(mk & 1 ? uv.x : 0.f, mk & 2 ? uv.y : 0.f, mk & 4 ? uv.z : 0.f,
                                  mk & 8 ? uv.w : 0.f);
@@ -701,7 +702,8 @@ __device__ __forceinline__ void star3_v7_body(
               jin = (fm >> (20 + h)) & 1;
 #pragma unroll
               for (int x = 0; x < 4; x++) kin[x] = (fm >> (16 + x)) & 1;
-              ubm = make_float4(mk & 1 ? ubm.x : 0.f, mk & 2 ? ubm.y : 0.f, mk & 4 ? ubm.z : 0.f,
+              if (!UBW)
+                ubm = make_float4(mk & 1 ? ubm.x : 0.f, mk & 2 ? ubm.y : 0.f, mk & 4 ? ubm.z : 0.f,
                                 mk & 8 ? ubm.w : 0.f);
             }
             acc[ph][h] = fmas4(2.f, ubm, acc[ph][h]);
@@ -783,25 +785,16 @@ __device__ __forceinline__ void star3_v7_body(
   tm_c, tm_ub, tm_u1, tm_cb, tm_u1b, tm_u2b, c_b, u_1_b, u_2_b, n, i_base, lo, hi, out_i0, \
       out_i1, chunk
 
-// Split launch: INT=true runs the interior rectangle, INT=false the frame.
-template <int MODE, bool INT>
+// INT=true runs the interior rectangle, INT=false the frame; UBW: u_b map is
+// windowed to [lo, hi]^2 (TMA zero fill replaces the seed mask).
+template <int MODE, bool INT, bool UBW>
 __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_kernel(SGB_V7_PARAMS) {
   int tk, tj;
   if (INT)
     tm.interior(blockIdx.x, tk, tj);
   else
     tm.frame(blockIdx.x, tk, tj);
-  star3_v7_body<MODE, INT>(SGB_V7_ARGS, tk, tj, D);
-}
-
-// Unified launch: row-major tile order, each CTA picks its specialised body.
-template <int MODE>
-__global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_unified(SGB_V7_PARAMS) {
-  const int tk = blockIdx.x % tm.tiles_k, tj = blockIdx.x / tm.tiles_k;
-  if (tk >= tm.ik0 && tk < tm.ik1 && tj >= tm.ij0 && tj < tm.ij1)
-    star3_v7_body<MODE, true>(SGB_V7_ARGS, tk, tj, D);
-  else
-    star3_v7_body<MODE, false>(SGB_V7_ARGS, tk, tj, D);
+  star3_v7_body<MODE, INT, UBW>(SGB_V7_ARGS, tk, tj, D);
 }
 
 template <int MODE>
@@ -813,7 +806,14 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   CUtensorMap maps[6];
   int rc = 0;
   rc |= encode_3d(&maps[0], c, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
-  rc |= encode_3d(&maps[1], u_b, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
+  int ubwin = 0;
+  if (!std::getenv("SGB_NO_UBWIN")) {
+    const int w = encode_3d_window(&maps[1], u_b, g.n, g.nplanes, lo, hi - lo + 1, Tl::BW, Tl::BJ,
+                                   name);
+    if (w < 0) return w;
+    ubwin = w == 0;
+  }
+  if (!ubwin) rc |= encode_3d(&maps[1], u_b, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
   rc |= encode_3d(&maps[2], u_1, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
   rc |= encode_3d(&maps[3], c_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
   rc |= encode_3d(&maps[4], u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
@@ -822,12 +822,12 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   if (rc) return SGB_EINVAL;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(star3_v7_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Tl::SMEM);
-    cudaFuncSetAttribute(star3_v7_kernel<MODE, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
-    cudaFuncSetAttribute(star3_v7_unified<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Tl::SMEM);
+    const void* ks[] = {(const void*)star3_v7_kernel<MODE, true, true>,
+                        (const void*)star3_v7_kernel<MODE, true, false>,
+                        (const void*)star3_v7_kernel<MODE, false, true>,
+                        (const void*)star3_v7_kernel<MODE, false, false>};
+    for (const void* k : ks)
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
     attr_set = true;
   }
   TileMap tm;
@@ -870,13 +870,6 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   };
   const auto ci = chunking("SGB_ICHUNKS", tm.n_interior());
   const auto cf = chunking("SGB_ICHUNKS_F", tm.n_frame());
-  if (std::getenv("SGB_V7_UNIFIED")) {
-    star3_v7_unified<MODE><<<dim3((unsigned)(tm.tiles_k * tm.tiles_j), ci.second), Tl::THREADS,
-                             Tl::SMEM, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
-                                            c_b, u_1_b, u_2_b, (int)g.n, (int)g.i_base, (int)lo,
-                                            (int)hi, (int)out_i0, (int)out_i1, ci.first, tm, D);
-    return launch_status(name);
-  }
   const bool fork = tm.n_interior() > 0 && tm.n_frame() > 0 && std::getenv("SGB_FORK");
   SideStream* ss = fork ? side_stream() : nullptr;
   if (ss) {
@@ -885,18 +878,18 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
       return launch_status(name);
   }
   if (tm.n_frame() > 0) {
-    star3_v7_kernel<MODE, false>
-        <<<dim3((unsigned)tm.n_frame(), cf.second), Tl::THREADS, Tl::SMEM, ss ? ss->s : s>>>(
-            maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cf.first, tm, D);
+    auto k = ubwin ? star3_v7_kernel<MODE, false, true> : star3_v7_kernel<MODE, false, false>;
+    k<<<dim3((unsigned)tm.n_frame(), cf.second), Tl::THREADS, Tl::SMEM, ss ? ss->s : s>>>(
+        maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cf.first, tm, D);
     const int st = launch_status(name);
     if (st) return st;
   }
   if (tm.n_interior() > 0) {
-    star3_v7_kernel<MODE, true>
-        <<<dim3((unsigned)tm.n_interior(), ci.second), Tl::THREADS, Tl::SMEM, s>>>(
-            maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, ci.first, tm, D);
+    auto k = ubwin ? star3_v7_kernel<MODE, true, true> : star3_v7_kernel<MODE, true, false>;
+    k<<<dim3((unsigned)tm.n_interior(), ci.second), Tl::THREADS, Tl::SMEM, s>>>(
+        maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, ci.first, tm, D);
     const int st = launch_status(name);
     if (st) return st;
   }

@@ -228,3 +228,26 @@ def test_host_buffer_plan_entry(api, name, n, dtype):
     for k in adjs:
         got = host[k].astype(np.float64)
         assert np.array_equal(got, want[k]), k
+
+
+@pytest.mark.parametrize("n", [68, 97, 136])
+def test_r4_launch_variants_bitwise_equal(api, n, monkeypatch):
+    """The radius-4 launch knobs (windowed seed map vs in-kernel mask, wave-model
+    vs forced i-chunking, frame on a side stream) change only scheduling: every
+    point's arithmetic is the same, so the results are bitwise identical, and
+    the default matches the oracle."""
+    name = "wave3d_r4"
+    scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 1, accumulate=True)
+    g, a = _round(grids, "f32"), _round(adjs, "f32")
+    base = api.run_program(name, n, scalars, g, a, dtype="f32")
+    want = oracle_gather(name, n, scalars, g, a)
+    for adj in ("c_b", "u_1_b"):
+        check_close(base[adj], want[adj], "f32", f"{name} n={n} {adj}")
+    for env in ({"SGB_NO_UBWIN": "1"}, {"SGB_ICHUNKS": "3", "SGB_ICHUNKS_F": "5"},
+                {"SGB_FORK": "1"}, {"SGB_ICHUNKS": "1", "SGB_ICHUNKS_F": "1"}):
+        with monkeypatch.context() as m:
+            for k, v in env.items():
+                m.setenv(k, v)
+            got = api.run_program(name, n, scalars, g, a, dtype="f32")
+        for adj in ("c_b", "u_1_b"):
+            assert np.array_equal(got[adj], base[adj]), (env, adj)
