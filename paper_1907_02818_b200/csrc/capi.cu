@@ -190,6 +190,40 @@ static int burgers2d_gather(long long n, double C, double D, const T* u_1, T* u_
   if (n <= 0) return einval("burgers2d_b: n must be positive");
   if (!guard_ok(BURGERS2D, n)) return SGB_GUARD;
   if (!u_1 || !u_1_b || !u_b) return einval("burgers2d_b: null array");
+  if ((n * (long long)sizeof(T)) % 16 == 0 && n <= (1 << 30) && aligned16(u_1, u_1_b, u_b, u_b) &&
+      !std::getenv("SGB_BURGERS_NORING")) {
+    // rows per CTA / ring stages: measured defaults, env overrides (read per call)
+    int rb = 32, stages = 5;
+    if (const char* e = std::getenv("SGB_BURGERS_RING_RB")) rb = std::max(1, std::atoi(e));
+    if (const char* f = std::getenv("SGB_BURGERS_RING_S")) stages = std::atoi(f);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(burgers2d_ring_kernel<T, 4>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, BurgRing<T, 4>::SMEM);
+      cudaFuncSetAttribute(burgers2d_ring_kernel<T, 5>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, BurgRing<T, 5>::SMEM);
+      cudaFuncSetAttribute(burgers2d_ring_kernel<T, 6>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, BurgRing<T, 6>::SMEM);
+      cudaFuncSetAttribute(burgers2d_ring_kernel<T, 8>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, BurgRing<T, 8>::SMEM);
+      attr = true;
+    }
+    constexpr int W = BurgRing<T>::W, TH = BurgRing<T>::THREADS;
+    dim3 g((unsigned)((n + W - 1) / W), (unsigned)((n + rb - 1) / rb));
+    if (stages == 4)
+      burgers2d_ring_kernel<T, 4><<<g, TH, BurgRing<T, 4>::SMEM, s>>>((int)n, (T)C, (T)D, u_1,
+                                                                      u_1_b, u_b, rb);
+    else if (stages == 5)
+      burgers2d_ring_kernel<T, 5><<<g, TH, BurgRing<T, 5>::SMEM, s>>>((int)n, (T)C, (T)D, u_1,
+                                                                      u_1_b, u_b, rb);
+    else if (stages == 6)
+      burgers2d_ring_kernel<T, 6><<<g, TH, BurgRing<T, 6>::SMEM, s>>>((int)n, (T)C, (T)D, u_1,
+                                                                      u_1_b, u_b, rb);
+    else
+      burgers2d_ring_kernel<T, 8><<<g, TH, BurgRing<T, 8>::SMEM, s>>>((int)n, (T)C, (T)D, u_1,
+                                                                      u_1_b, u_b, rb);
+    return launch_status("burgers2d_b");
+  }
   if (n % 2 == 0 && aligned16(u_1, u_1_b, u_b, u_b)) {
     static int rb = -1;  // rows per block (SGB_BURGERS_RB), measured default
     if (rb < 0) {

@@ -13,6 +13,7 @@
 #pragma once
 
 #include "generic_kernels.cuh"
+#include "star3d_tma.cuh"
 
 namespace sgb {
 
@@ -174,6 +175,161 @@ __global__ void __launch_bounds__(128) burgers2d_stream_kernel(long long n, T C,
     b0 = bp;
     bp = bp2;
     o0 = o1;
+  }
+}
+
+// ------------------------------------------------------------------ burgers2d (ring)
+// Strip-streaming form: a CTA owns a W-column strip and rows [i0, i1).  One
+// thread streams the row segments of u_1 and u_b (with a 16-byte halo each
+// side) and of u_1_b into an S-stage shared-memory ring with 1D bulk copies
+// (cp.async.bulk, mbarrier complete_tx), S-3 rows ahead of the consumers, so
+// memory-level parallelism no longer depends on registers or occupancy.
+// Every thread then evaluates its two points from shared memory (no shuffles,
+// no 64-bit index math in the loop); term order and predicates as above.
+namespace tma {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+}  // namespace tma
+
+template <typename T, int S_ = 4>
+struct BurgRing {
+  static constexpr int THREADS = 128, W = 2 * THREADS;  // strip width (columns)
+  static constexpr int H = 16 / (int)sizeof(T);          // halo columns: one 16-B granule
+  static constexpr int UW = W + 2 * H;                   // u_1 / u_b row segment
+  static constexpr int S = S_;                           // ring stages (rows)
+  static constexpr int STAGE = 2 * UW + W;               // u_1, u_b, u_1_b (elements)
+  static constexpr int SMEM = S * STAGE * (int)sizeof(T) + S * 8;
+};
+
+template <typename T>
+__device__ __forceinline__ void st2cs(T* p, T a, T b) {
+  typename Vec2<T>::type v;
+  v.x = a;
+  v.y = b;
+  __stcs(reinterpret_cast<typename Vec2<T>::type*>(p), v);
+}
+// max(0, u) / min(0, u) as one compare + select: equal to fmax / fmin for
+// every u up to the sign of a zero result (absorbed by the + D / the sums
+// they enter), and for NaN u (both give 0)
+template <typename T>
+__device__ __forceinline__ T pos0(T u) { return u > T(0) ? u : T(0); }
+template <typename T>
+__device__ __forceinline__ T neg0(T u) { return u < T(0) ? u : T(0); }
+
+// Strip-streaming form: a CTA owns a W-column strip and rows [i0, i1).  One
+// thread streams the row segments of u_1 and u_b (with a 16-byte halo each
+// side) and of u_1_b into an S-stage shared-memory ring with 1D bulk copies
+// (cp.async.bulk, mbarrier complete_tx), S-3 rows ahead of the consumers;
+// stages are small (6 KB fp64) so 8 CTAs (32 warps) stay resident per SM.
+// Every thread evaluates its two points from shared memory (no shuffles, no
+// 64-bit index math in the loop) in the reference's term order
+// (symdiff.cpp:204): (-1,0), (0,-1), (0,0), (0,1), (1,0).
+template <typename T, int S_>
+__global__ void __launch_bounds__(BurgRing<T, S_>::THREADS, 8)
+    burgers2d_ring_kernel(int n, T C, T D, const T* __restrict__ u1, T* __restrict__ u1b,
+                          const T* __restrict__ ub, int rows_per_block) {
+  using Rg = BurgRing<T, S_>;
+  using V = typename Vec2<T>::type;
+  constexpr int W = Rg::W, H = Rg::H, UW = Rg::UW, S = Rg::S, ST = Rg::STAGE;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + S * ST);
+  const int tid = threadIdx.x;
+  const int j0 = blockIdx.x * W;
+  const int i0 = blockIdx.y * rows_per_block;
+  const int i1 = min(i0 + rows_per_block, n);
+  const int lo = 1, hi = n - 2;
+  const int ca = max(j0 - H, 0), cb = min(j0 + W + H, n), oa = j0, ob = min(j0 + W, n);
+  const uint32_t ubytes = (uint32_t)(cb - ca) * sizeof(T), obytes = (uint32_t)(ob - oa) * sizeof(T);
+  const int uoff = ca - (j0 - H);
+  const int r_first = i0 - 1, nrows = i1 - i0 + 2;  // rows i0-1 .. i1
+
+  for (int e = tid; e < S * ST; e += Rg::THREADS) ring[e] = T(0);
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before bulk writes
+  __syncthreads();
+
+  auto issue = [&](int k) {
+    const int s = k % S, r = r_first + k;
+    T* st = ring + s * ST;
+    const bool valid = r >= 0 && r < n, own = r >= i0 && r < i1;
+    tma::mbar_arrive_expect_tx(&bars[s], valid ? 2 * ubytes + (own ? obytes : 0u) : 0u);
+    if (valid) {
+      const size_t rb = (size_t)r * n;
+      tma::bulk_g2s(st + uoff, u1 + rb + ca, ubytes, &bars[s]);
+      tma::bulk_g2s(st + UW + uoff, ub + rb + ca, ubytes, &bars[s]);
+      if (own) tma::bulk_g2s(st + 2 * UW, u1b + rb + oa, obytes, &bars[s]);
+    }
+  };
+  if (tid == 0)
+    for (int k = 0; k < S && k < nrows; k++) issue(k);
+
+  const int jl = 2 * tid, j = j0 + jl;
+  const bool active = j < n;
+  auto inB = [&](int x) { return x >= lo && x <= hi; };
+  const bool jin[2] = {inB(j), inB(j + 1)};
+  const bool jl_[2] = {inB(j - 1), jin[0]}, jr_[2] = {jin[1], inB(j + 2)};
+  const bool jreach[2] = {j >= lo - 1 && j <= hi + 1, j + 1 >= lo - 1 && j + 1 <= hi + 1};
+  T* orow = u1b + (size_t)i0 * n + j;
+  tma::mbar_wait(&bars[0], 0);
+  for (int r = i0; r < i1; r++, orow += n) {
+    const int k = r - r_first;
+    tma::mbar_wait(&bars[k % S], (k / S) & 1);
+    tma::mbar_wait(&bars[(k + 1) % S], ((k + 1) / S) & 1);
+    if (active) {
+      const T* Um = ring + ((k - 1) % S) * ST + H + jl;
+      const T* Uc = ring + (k % S) * ST + H + jl;
+      const T* Up = ring + ((k + 1) % S) * ST + H + jl;
+      const V um = *reinterpret_cast<const V*>(Um), uc = *reinterpret_cast<const V*>(Uc),
+              up = *reinterpret_cast<const V*>(Up);
+      const V bm = *reinterpret_cast<const V*>(Um + UW), bc = *reinterpret_cast<const V*>(Uc + UW),
+              bp = *reinterpret_cast<const V*>(Up + UW);
+      const V oc = *reinterpret_cast<const V*>(Uc - H + 2 * UW);  // u_1_b at (r, j)
+      const T ul = Uc[-1], ur = Uc[2], bl = Uc[UW - 1], br = Uc[UW + 2];
+      const bool iin = inB(r), iin_m = inB(r - 1), iin_p = inB(r + 1);
+      const bool ireach = r >= lo - 1 && r <= hi + 1;
+      const T ucv[2] = {uc.x, uc.y}, bcv[2] = {bc.x, bc.y};
+      const T uL[2] = {ul, uc.x}, uR[2] = {uc.y, ur};
+      const T bL[2] = {bl, bc.x}, bR[2] = {bc.y, br};
+      const T uM[2] = {um.x, um.y}, uP[2] = {up.x, up.y}, bM[2] = {bm.x, bm.y},
+              bP[2] = {bp.x, bp.y};
+      T acc[2];
+      bool reach[2];
+#pragma unroll
+      for (int m = 0; m < 2; m++) {
+        const T u = ucv[m];
+        const T ge = u >= T(0) ? T(1) : T(0), le = -u >= T(0) ? T(1) : T(0);
+        const T cen = -C * ((u - uM[m]) * ge + (u - uL[m]) * ge + (uR[m] - u) * le +
+                            (uP[m] - u) * le + T(2) * pos0(u) - T(2) * neg0(u)) -
+                      T(4) * D + T(1);
+        const T t1 = (C * pos0(uP[m]) + D) * bP[m];
+        const T t2 = (C * pos0(uR[m]) + D) * bR[m];
+        const T t4 = (-C * neg0(uL[m]) + D) * bL[m];
+        const T t5 = (-C * neg0(uM[m]) + D) * bM[m];
+        T a = T(0);
+        a += jin[m] && iin_p ? t1 : T(0);
+        a += iin && jr_[m] ? t2 : T(0);
+        a += iin && jin[m] ? cen * bcv[m] : T(0);
+        a += iin && jl_[m] ? t4 : T(0);
+        a += jin[m] && iin_m ? t5 : T(0);
+        acc[m] = a;
+        reach[m] = (iin && jreach[m]) || (jin[m] && ireach);
+      }
+      if (reach[0] || reach[1])
+        st2cs(orow, reach[0] ? oc.x + acc[0] : oc.x, reach[1] ? oc.y + acc[1] : oc.y);
+    }
+    __syncthreads();  // row r-1's stage is free
+    if (tid == 0 && k - 1 + S < nrows) issue(k - 1 + S);
   }
 }
 

@@ -92,7 +92,7 @@ SIZES = {
     "wave3d_c": [5, 16, 33, 40, 68],
     "wave3d_c2": [20, 41],
     "wave1d": [5, 1000, 4099],
-    "burgers2d": [5, 64, 203],
+    "burgers2d": [5, 64, 203, 300, 1030],
 }
 
 
@@ -251,3 +251,26 @@ def test_r4_launch_variants_bitwise_equal(api, n, monkeypatch):
             got = api.run_program(name, n, scalars, g, a, dtype="f32")
         for adj in ("c_b", "u_1_b"):
             assert np.array_equal(got[adj], base[adj]), (env, adj)
+
+
+@pytest.mark.parametrize("n", [64, 300, 1030])
+def test_burgers_ring_variants_bitwise_equal(api, n, monkeypatch):
+    """burgers2d ring kernel: stage count and rows per CTA change only the
+    schedule, so results are bitwise identical; the register-streaming kernel
+    it replaced agrees to fp64 rounding."""
+    name = "burgers2d"
+    scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 3, accumulate=True)
+    base = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
+    want = oracle_gather(name, n, scalars, grids, adjs)
+    check_close(base["u_1_b"], want["u_1_b"], "f64", f"{name} n={n}")
+    for env in ({"SGB_BURGERS_RING_S": "4"}, {"SGB_BURGERS_RING_S": "8"},
+                {"SGB_BURGERS_RING_RB": "7"}, {"SGB_BURGERS_RING_RB": "256"}):
+        with monkeypatch.context() as m:
+            for k, v in env.items():
+                m.setenv(k, v)
+            got = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
+        assert np.array_equal(got["u_1_b"], base["u_1_b"]), env
+    with monkeypatch.context() as m:
+        m.setenv("SGB_BURGERS_NORING", "1")
+        old = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
+    assert oracle.max_rel_err(old["u_1_b"], base["u_1_b"]) <= 1e-14
