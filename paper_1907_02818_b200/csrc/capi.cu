@@ -7,10 +7,8 @@
 
 #include "generic_kernels.cuh"
 #include "lowdim.cuh"
+#include "star3d_r4.cuh"
 #include "star3d_tma.cuh"
-#include "star3d_v2.cuh"
-#include "star3d_v3.cuh"
-#include "star3d_v4.cuh"
 
 namespace sgb {
 
@@ -49,26 +47,15 @@ static bool guard_ok(int fam, long long n) {
 }
 
 // ------------------------------------------------------------------ 3D stars
-// Kernel selection for the TMA path ("Measured path"): v7 for
-// radius 4, v1 for radius 1 by default; SGB_STAR_KERNEL=1..7 and
-// SGB_TJ=16|24|32 select the earlier designs for A/B measurements.
+// Kernel selection for the TMA path ("Measured path"): the
+// radius-4 streaming kernel (v7) for radius 4, the v1 streaming kernel for
+// radius 1 (measured faster there); SGB_STAR_KERNEL=1|7 forces one of them.
 static int star_kernel_version(int mode) {
-  static int forced = -1;
-  if (forced < 0) {
-    const char* e = std::getenv("SGB_STAR_KERNEL");
-    forced = e ? std::atoi(e) : 0;
+  if (const char* e = std::getenv("SGB_STAR_KERNEL")) {
+    const int v = std::atoi(e);
+    if (v == 1 || v == 7) return v;
   }
-  if (forced >= 1 && forced <= 7) return forced;
   return mode == 2 ? 7 : 1;
-}
-static int star_tile_rows() {
-  static int tj = -1;
-  if (tj < 0) {
-    const char* e = std::getenv("SGB_TJ");
-    tj = e ? std::atoi(e) : 32;
-    if (tj != 16 && tj != 24) tj = 32;
-  }
-  return tj;
 }
 
 template <int MODE, typename T>
@@ -93,37 +80,10 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
   const long long lo = R, hi = n - 1 - R;
   Slab3 g{n, i_base, nplanes};
   if (star3_tma_supported<MODE, T>(n)) {
-    const int ver = star_kernel_version(MODE);
-    if (ver == 7)
+    if (star_kernel_version(MODE) == 7)
       return star3_v7_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
                                    (float*)c_b, (const float*)u_1, (float*)u_1_b, (float*)u_2_b,
                                    (const float*)u_b, s, name);
-    if (ver >= 4 && ver <= 6) {
-#define SGB_V4(TJ, RMWT, ROLES)                                                              \
-  return star3_v4_gather<MODE, TJ, RMWT, ROLES>(g, lo, hi, out_i0, out_i1, (float)D,           \
-                                                (const float*)c, (float*)c_b, (const float*)u_1, \
-                                                (float*)u_1_b, (float*)u_2_b,                    \
-                                                (const float*)u_b, s, name)
-      if (ver == 4) SGB_V4(16, false, false);
-      if (ver == 6) SGB_V4(32, true, true);
-      if (star_tile_rows() == 16) SGB_V4(16, true, false);
-      if (star_tile_rows() == 24) SGB_V4(24, true, false);
-      SGB_V4(32, true, false);
-#undef SGB_V4
-    }
-    if (ver == 3)
-      return star3_v3_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
-                                   (float*)c_b, (const float*)u_1, (float*)u_1_b, (float*)u_2_b,
-                                   (const float*)u_b, s, name);
-    if (ver == 2) {
-      if (star_tile_rows() == 32)
-        return star3_v2_gather<MODE, 32>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
-                                         (float*)c_b, (const float*)u_1, (float*)u_1_b,
-                                         (float*)u_2_b, (const float*)u_b, s, name);
-      return star3_v2_gather<MODE, 16>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
-                                       (float*)c_b, (const float*)u_1, (float*)u_1_b,
-                                       (float*)u_2_b, (const float*)u_b, s, name);
-    }
     return star3_tma_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
                                   (float*)c_b, (const float*)u_1, (float*)u_1_b,
                                   (float*)u_2_b, (const float*)u_b, s, name);

@@ -1,62 +1,50 @@
-// Streaming gather-adjoint kernel v4 for the 3D star families (sm_100a).
+// Radius-4 streaming gather-adjoint kernel (the hot kernel; sm_100a).
 //
 // Mathematics and boundary predicate: star3d_tma.cuh header (SURVEY
-// Appendix C; reference adjoint.cpp:73-163 / interp.cpp:189-198).
-//
-// Structure (chosen from ncu evidence on v1..v3):
-//   * 256 threads, 2 CTAs per SM, one 64 (k) x 16 (j) column tile per CTA,
-//     streaming over i; each thread owns 4 consecutive k points of one row and
-//     BOTH fields' rotating i-accumulators (2 x (2R+1) float4);
-//   * c, u_b, u_1 halo boxes arrive by TMA (cp.async.bulk.tensor.3d) into a
-//     3-stage ring; the plane loop is unrolled by 2R+1 (a multiple of the 3
-//     stages and of the 3 q buffers), so every stage / buffer / accumulator
-//     index is a compile-time constant;
-//   * arithmetic is packed fp32x2 (FFMA2 / FADD2 / FMUL2) wherever the lanes
-//     align, which halves the FP instruction count of v1;
-//   * CTAs whose halo box lies inside [lo, hi] in j and k ("interior", ~80%
-//     at 768^3) skip every mask; only boundary CTAs evaluate the predicate;
-//   * the adjoint read-modify-write uses streaming 128-bit loads (issued a
-//     full plane ahead of use) and stores.
+// Appendix C; reference adjoint.cpp:73-163 / interp.cpp:189-198).  Design,
+// measurements and the path from the earlier versions: DESIGN.md ("Radius-4
+// streaming kernel") and profiles/.
 #pragma once
 #include <mutex>
 #include <utility>
 
-#include "star3d_v3.cuh"
-
-#ifndef SGB_TREE_SUM
-#define SGB_TREE_SUM 1
-#endif
+#include "star3d_tma.cuh"
 
 namespace sgb {
 
-template <int MODE, int TJ_, bool RMW_TMA_, bool ROLES_ = false>
-struct StarTile4 {
-  static constexpr int R = Star3<MODE>::R;
-  static constexpr bool RMW_TMA = RMW_TMA_;  // old adjoint values staged by TMA
-  static constexpr int TK = 64, TJ = TJ_, HK = 4, HJ = R;
-  static constexpr int BW = TK + 2 * HK;  // 72 floats = 288 B rows
-  static constexpr int BJ = TJ + 2 * HJ;
-  static constexpr int RING = 2 * R + 1;  // 9 or 3
-  // 3 stages (RING % 3 == 0: static stage index); the 2-CTA/SM variant
-  // (TJ 16 with TMA-staged RMW) needs 2 stages to fit two CTAs' smem.
-  static constexpr int NS = (TJ_ == 16 && RMW_TMA_) ? 2 : 3;
-  static constexpr int NQB = 2;
-  static constexpr bool ROLES = ROLES_;  // field-specialised warp halves
-  static constexpr int HALF = 16 * TJ;   // threads covering the tile once
-  static constexpr int THREADS = ROLES ? 2 * HALF : HALF;
-  static constexpr int MINB = THREADS <= 256 ? 2 : 1;
-  static constexpr bool STATIC_STAGE = RING % NS == 0;
-  static constexpr int BOX_BYTES = BW * BJ * 4;
-  static constexpr int BF = ((BOX_BYTES + 127) / 128) * 128 / 4;
-  static constexpr int TILE = TK * TJ;  // floats of one adjoint tile
-  static constexpr int NT = RMW_TMA ? (Star3<MODE>::kU2 ? 3 : 2) : 0;  // c_b, u_1_b (, u_2_b)
-  static constexpr int SF = 3 * BF + NT * TILE;  // floats per stage
-  static constexpr int QD = R + 1;
-  static constexpr int QELEMS = (BW / 4) * BJ;
-  static constexpr int EPT = (QELEMS + THREADS - 1) / THREADS;
-  static constexpr size_t SMEM =
-      (size_t)(NS * SF + NQB * BF) * 4 + (size_t)QD * HALF * 16 + NS * 8;
-};
+// ---- packed fp32x2 helpers on float4 (FFMA2 / FMUL2 / FADD2)
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float4 cat4(const float2& a, const float2& b) {
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+// a*b + c on float4 via two FFMA2
+__device__ __forceinline__ float4 fma4(const float4& a, const float4& b, const float4& c) {
+  return cat4(__ffma2_rn(lo2(a), lo2(b), lo2(c)), __ffma2_rn(hi2(a), hi2(b), hi2(c)));
+}
+__device__ __forceinline__ float4 fmas4(float w, const float4& b, const float4& c) {
+  const float2 ww = make_float2(w, w);
+  return cat4(__ffma2_rn(ww, lo2(b), lo2(c)), __ffma2_rn(ww, hi2(b), hi2(c)));
+}
+__device__ __forceinline__ float4 mul4(const float4& a, const float4& b) {
+  return cat4(__fmul2_rn(lo2(a), lo2(b)), __fmul2_rn(hi2(a), hi2(b)));
+}
+__device__ __forceinline__ float4 muls4(float w, const float4& b) {
+  const float2 ww = make_float2(w, w);
+  return cat4(__fmul2_rn(ww, lo2(b)), __fmul2_rn(ww, hi2(b)));
+}
+__device__ __forceinline__ float4 add4(const float4& a, const float4& b) {
+  return cat4(__fadd2_rn(lo2(a), lo2(b)), __fadd2_rn(hi2(a), hi2(b)));
+}
+__device__ __forceinline__ float4 lds4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+
+__device__ __forceinline__ float4 sel4(const bool (&m)[4], const float4& yes, const float4& no) {
+  return make_float4(m[0] ? yes.x : no.x, m[1] ? yes.y : no.y, m[2] ? yes.z : no.z,
+                     m[3] ? yes.w : no.w);
+}
+
 
 // in-plane k-direction stencil for 4 points: window a|b|c = k0-4 .. k0+7
 template <int R>
@@ -81,304 +69,60 @@ __device__ __forceinline__ float4 kstencil2(const float4& a, const float4& b, co
   return cat4(p0, p1);
 }
 
-// One field, one plane, 4 points of one row: in-plane stencil into acc[ph],
-// centre into the i-neighbour accumulators (output p+R is initialised here).
-template <int R, int RING>
-__device__ __forceinline__ void field1(const float* F, int crow, int col, float w0,
-                                       const float (&wr)[R + 1], float4 (&acc)[RING], int ph) {
-  constexpr int BW = 72;
-  const float* cp = F + crow + col;
-  const float4 a = lds4(cp - 4), b = lds4(cp), c = lds4(cp + 4);
-#if SGB_TREE_SUM
-  // j direction as a short tree (independent partial sums) to cut the
-  // dependent FFMA2 chain behind each shared-memory load
-  float4 jp[2];
-  jp[0] = muls4(wr[1], add4(lds4(cp - BW), lds4(cp + BW)));
-  jp[1] = R >= 2 ? muls4(wr[2], add4(lds4(cp - 2 * BW), lds4(cp + 2 * BW)))
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int r = 3; r <= R; r++)
-    jp[r & 1] = fmas4(wr[r], add4(lds4(cp - r * BW), lds4(cp + r * BW)), jp[r & 1]);
-  const float4 in = add4(kstencil2<R>(a, b, c, w0, wr), R >= 2 ? add4(jp[0], jp[1]) : jp[0]);
-#else
-  float4 in = kstencil2<R>(a, b, c, w0, wr);
-#pragma unroll
-  for (int r = 1; r <= R; r++) in = fmas4(wr[r], add4(lds4(cp - r * BW), lds4(cp + r * BW)), in);
-#endif
-  acc[ph] = add4(acc[ph], in);
-  acc[(ph + R) % RING] = muls4(wr[R], b);
-#pragma unroll
-  for (int r = 1; r <= R; r++) {
-    if (r < R) acc[(ph + r) % RING] = fmas4(wr[r], b, acc[(ph + r) % RING]);
-    acc[(ph + RING - r) % RING] = fmas4(wr[r], b, acc[(ph + RING - r) % RING]);
+// ---- 3D tensor maps over a slab of n x n planes
+inline int encode_3d(CUtensorMap* map, const float* base, long long n, long long nplanes,
+                     int box0, int box1, const char* name) {
+  auto encode = get_encode();
+  if (!encode) {
+    set_error(std::string(name) + ": cuTensorMapEncodeTiled unavailable");
+    return SGB_EINVAL;
   }
+  cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)nplanes};
+  cuuint64_t strides[2] = {(cuuint64_t)n * 4, (cuuint64_t)n * n * 4};
+  cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(std::string(name) + ": tensor map encode failed (" + std::to_string((int)r) + ")");
+    return SGB_EINVAL;
+  }
+  return 0;
 }
 
-template <int MODE, int TJ, bool RMWT, bool ROLES>
-__global__ void __launch_bounds__(StarTile4<MODE, TJ, RMWT, ROLES>::THREADS,
-                                  StarTile4<MODE, TJ, RMWT, ROLES>::MINB)
-    star3_v4_kernel(const __grid_constant__ CUtensorMap tm_c,
-                    const __grid_constant__ CUtensorMap tm_ub,
-                    const __grid_constant__ CUtensorMap tm_u1,
-                    const __grid_constant__ CUtensorMap tm_cb,
-                    const __grid_constant__ CUtensorMap tm_u1b,
-                    const __grid_constant__ CUtensorMap tm_u2b, float* __restrict__ c_b,
-                    float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n, int i_base,
-                    int lo, int hi, int out_i0, int out_i1, int chunk, int tiles_k, float D) {
-  using Tl = StarTile4<MODE, TJ, RMWT, ROLES>;
-  using S3 = Star3<MODE>;
-  constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
-  constexpr int HALF = Tl::HALF;
-  constexpr int RING = Tl::RING, NS = Tl::NS, NQB = Tl::NQB, BF = Tl::BF, QD = Tl::QD;
-  constexpr int SF = Tl::SF, TILE = Tl::TILE;
-
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* stage = reinterpret_cast<float*>(smem_raw);  // [NS][c, ub, u1, (cb, u1b, u2b)]
-  float* qbuf = stage + NS * SF;                       // [NQB]
-  float4* gq = reinterpret_cast<float4*>(qbuf + NQB * BF);  // [QD][HALF]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(gq + QD * HALF);
-
-  const int tid = threadIdx.x;
-  // ROLES: threads [0, HALF) carry Lap(u_1) and emit c_b, [HALF, 2 HALF) carry
-  // the q stencil and emit u_1_b; otherwise every thread carries both fields.
-  const bool lap_part = !ROLES || tid < HALF;  // warp-uniform
-  const bool q_part = !ROLES || tid >= HALF;
-  const int rt = ROLES ? (tid % HALF) : tid;
-  const int tx = rt & 15, ty = rt >> 4;
-  const int tk = blockIdx.x % tiles_k, tj = blockIdx.x / tiles_k;
-  const int k0 = tk * Tl::TK, j0 = tj * Tl::TJ;
-  const int o_begin = out_i0 + blockIdx.y * chunk;
-  const int o_end = min(o_begin + chunk, out_i1);
-  if (o_begin >= o_end) return;
-  const int pstart = o_begin - R;
-  const int P = (o_end - o_begin) + 2 * R;
-
-  const float w0 = S3::template w<float>(0);
-  float wr[R + 1];
-  wr[0] = w0;
-#pragma unroll
-  for (int r = 1; r <= R; r++) wr[r] = S3::template w<float>(r);
-
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < NS; s++) tma::mbar_init(&bars[s], 1);
-    tma::fence_barrier_init();
+// Same, restricted to the window [off, off+ext) in j and k: TMA zero-fills
+// every element outside it, which is exactly the primal-box mask on the seed
+// (u_b is defined on [lo, hi]^3 only).  Needs a 16-byte aligned window base;
+// returns 1 (no map) when it is not.
+inline int encode_3d_window(CUtensorMap* map, const float* base, long long n, long long nplanes,
+                            long long off, long long ext, int box0, int box1, const char* name) {
+  const float* wb = base + off * n + off;
+  if ((reinterpret_cast<uintptr_t>(wb) & 15) != 0 || ext < 1) return 1;
+  auto encode = get_encode();
+  if (!encode) {
+    set_error(std::string(name) + ": cuTensorMapEncodeTiled unavailable");
+    return SGB_EINVAL;
   }
-  __syncthreads();
-  auto issue = [&](int it) {
-    const int s = it % NS;
-    float* dst = stage + s * SF;
-    const int p = pstart + it;
-    const int pl = p - i_base;  // out of the slab -> TMA zero fill
-    const bool emit = it >= 2 * R;
-    const bool u2 = S3::kU2 && p >= o_begin && p < o_end;
-    const int bytes = 3 * Tl::BOX_BYTES +
-                      (Tl::RMW_TMA ? ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE * 4 : 0);
-    tma::mbar_arrive_expect_tx(&bars[s], bytes);
-    tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
-    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK, j0 - HJ, pl);
-    tma::load_3d(dst + 2 * BF, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
-    if (Tl::RMW_TMA) {
-      if (emit) {
-        tma::load_3d(dst + 3 * BF, &tm_cb, &bars[s], k0, j0, pl - R);
-        tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
-      }
-      if (u2) tma::load_3d(dst + 3 * BF + 2 * TILE, &tm_u2b, &bars[s], k0, j0, pl);
-    }
-  };
-  if (tid == 0)
-    for (int it = 0; it < NS && it < P; it++) issue(it);
-
-  const int jc = j0 + ty, kc = k0 + 4 * tx;
-  const bool col_ok = jc < n && kc < n;  // n % 4 == 0: all 4 points or none
-  const bool jin = jc >= lo && jc <= hi;
-  const int jout = jc < lo ? lo - jc : (jc > hi ? jc - hi : 0);
-  const int crow = (ty + HJ) * BW, col = HK + 4 * tx;
-  const long long plane = (long long)n * n;
-  const long long coff = (long long)jc * n + kc;
-  const bool interior = j0 - HJ >= lo && j0 + Tl::TJ + HJ - 1 <= hi && k0 - HK >= lo &&
-                        k0 + Tl::TK + HK - 1 <= hi && j0 + Tl::TJ <= n && k0 + Tl::TK <= n;
-  bool kin[4];
-#pragma unroll
-  for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
-  const float4 kmask = make_float4(kin[0] && jin ? 1.f : 0.f, kin[1] && jin ? 1.f : 0.f,
-                                   kin[2] && jin ? 1.f : 0.f, kin[3] && jin ? 1.f : 0.f);
-  const float gf = S3::kC2 ? 2.f * D : D;
-
-  float4 accL[RING], accQ[RING];
-#pragma unroll
-  for (int s = 0; s < RING; s++) accL[s] = accQ[s] = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4(&AQ)[RING] = ROLES ? accL : accQ;  // the q role reuses the one array
-
-  for (int base = 0; base < P; base += RING) {
-    const int par0 = base / NS;  // used when RING % NS == 0
-#pragma unroll
-    for (int ph = 0; ph < RING; ph++) {
-      const int it = base + ph;
-      if (it < P) {
-        const int s = Tl::STATIC_STAGE ? ph % NS : it % NS;
-        const int p = pstart + it;
-        const float* Cs = stage + s * SF;
-        const float* UBs = Cs + BF;
-        const float* U1s = Cs + 2 * BF;
-        const float* OLD = Cs + 3 * BF + ty * TK + 4 * tx;  // this thread's 4 points
-        float* Q = qbuf + (it % NQB) * BF;
-        const bool emit = it >= 2 * R;
-        const int o = p - R;
-        const bool pin = p >= lo && p <= hi;
-        const bool oin = o >= lo && o <= hi;
-        const long long gidx = (long long)(o - i_base) * plane + coff;
-
-        // prefetch the adjoint values this plane's emit updates
-        float4 cb_old = make_float4(0.f, 0.f, 0.f, 0.f), u1b_old = cb_old;
-        if (!Tl::RMW_TMA && emit && col_ok) {
-          u1b_old = __ldcs(reinterpret_cast<const float4*>(u_1_b + gidx));
-          if (oin && jin) cb_old = __ldcs(reinterpret_cast<const float4*>(c_b + gidx));
-        }
-
-        tma::mbar_wait(&bars[s], Tl::STATIC_STAGE ? ((par0 + ph / NS) & 1) : ((it / NS) & 1));
-        if (Tl::RMW_TMA && emit) {
-          if (lap_part) cb_old = lds4(OLD);
-          if (q_part) u1b_old = lds4(OLD + TILE);
-        }
-
-        // ---- q = D c(^2) u_b [x in B] over the halo box
-#pragma unroll
-        for (int m = 0; m < Tl::EPT; m++) {
-          const int e = tid + m * Tl::THREADS;
-          if (e < Tl::QELEMS) {
-            const int row = e / (BW / 4), c4 = e - row * (BW / 4);
-            const int qo = row * BW + 4 * c4;
-            float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (pin) {
-              const float4 cv = lds4(Cs + qo);
-              const float4 uv = lds4(UBs + qo);
-              qv = mul4(S3::kC2 ? mul4(cv, cv) : cv, muls4(D, uv));
-              if (!interior) {
-                const int jg = j0 - HJ + row, kg = k0 - HK + 4 * c4;
-                const bool rm = jg >= lo && jg <= hi;
-                if (!(rm && kg >= lo && kg <= hi)) qv.x = 0.f;
-                if (!(rm && kg + 1 >= lo && kg + 1 <= hi)) qv.y = 0.f;
-                if (!(rm && kg + 2 >= lo && kg + 2 <= hi)) qv.z = 0.f;
-                if (!(rm && kg + 3 >= lo && kg + 3 <= hi)) qv.w = 0.f;
-              }
-            }
-            *reinterpret_cast<float4*>(Q + qo) = qv;
-          }
-        }
-        // ---- own centre: g (queued R planes), 2 u_b into accQ, u_2_b at p
-        {
-          float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (pin) {
-            float4 ubm = lds4(UBs + crow + col);
-            if (!interior) ubm = mul4(ubm, kmask);
-            if (lap_part)
-              g = S3::kC2 ? mul4(muls4(gf, lds4(Cs + crow + col)), ubm) : muls4(gf, ubm);
-            if (q_part) {
-              AQ[ph] = fmas4(2.f, ubm, AQ[ph]);
-              if (S3::kU2 && col_ok && jin && p >= o_begin && p < o_end) {
-                float* ptr = u_2_b + (long long)(p - i_base) * plane + coff;
-                const float4 u2 = Tl::RMW_TMA ? lds4(OLD + 2 * TILE)
-                                              : __ldcs(reinterpret_cast<const float4*>(ptr));
-                __stcs(reinterpret_cast<float4*>(ptr),
-                       make_float4(kin[0] ? u2.x - ubm.x : u2.x, kin[1] ? u2.y - ubm.y : u2.y,
-                                   kin[2] ? u2.z - ubm.z : u2.z, kin[3] ? u2.w - ubm.w : u2.w));
-              }
-            }
-          }
-          if (lap_part) gq[(it % QD) * HALF + rt] = g;
-        }
-        __syncthreads();
-        // the stage read by the previous plane is free now: refill it
-        if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
-
-        if (ROLES) {
-          field1<R, RING>(q_part ? Q : U1s, crow, col, w0, wr, accL, ph);
-        } else {
-          field1<R, RING>(U1s, crow, col, w0, wr, accL, ph);
-          field1<R, RING>(Q, crow, col, w0, wr, accQ, ph);
-        }
-
-        // ---- emit output plane o = p - R (all of its contributions are in)
-        if (emit && col_ok) {
-          const int es = (ph + R + 1) % RING;
-          if (lap_part && oin && jin) {
-            const float4 g = gq[((it - R) % QD) * HALF + rt];
-            float4 nv = fma4(g, accL[es], cb_old);
-            if (!interior)
-              nv = make_float4(kin[0] ? nv.x : cb_old.x, kin[1] ? nv.y : cb_old.y,
-                               kin[2] ? nv.z : cb_old.z, kin[3] ? nv.w : cb_old.w);
-            __stcs(reinterpret_cast<float4*>(c_b + gidx), nv);
-          }
-          const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
-          if (!q_part) {
-          } else if (interior) {
-            if (oout <= R) __stcs(reinterpret_cast<float4*>(u_1_b + gidx), add4(u1b_old, AQ[es]));
-          } else {
-            const float4 a = AQ[es];
-            const float av[4] = {a.x, a.y, a.z, a.w};
-            float4 nv = u1b_old;
-            float* nvp = reinterpret_cast<float*>(&nv);
-            bool any = false;
-#pragma unroll
-            for (int m = 0; m < 4; m++) {
-              const int k = kc + m;
-              const int kout = k < lo ? lo - k : (k > hi ? k - hi : 0);
-              const int nout = (oout > 0) + (jout > 0) + (kout > 0);
-              const bool reach = nout == 0 || (nout == 1 && oout <= R && jout <= R && kout <= R);
-              if (reach) nvp[m] = nvp[m] + av[m];
-              any |= reach;
-            }
-            if (any) __stcs(reinterpret_cast<float4*>(u_1_b + gidx), nv);
-          }
-        }
-      }
-    }
+  cuuint64_t dims[3] = {(cuuint64_t)ext, (cuuint64_t)ext, (cuuint64_t)nplanes};
+  cuuint64_t strides[2] = {(cuuint64_t)n * 4, (cuuint64_t)n * n * 4};
+  cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)wb, dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(std::string(name) + ": tensor map encode failed (" + std::to_string((int)r) + ")");
+    return SGB_EINVAL;
   }
+  return 0;
 }
-
-template <int MODE, int TJ, bool RMWT, bool ROLES = false>
-inline int star3_v4_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
-                           long long out_i1, float D, const float* c, float* c_b,
-                           const float* u_1, float* u_1_b, float* u_2_b, const float* u_b,
-                           cudaStream_t s, const char* name) {
-  using Tl = StarTile4<MODE, TJ, RMWT, ROLES>;
-  CUtensorMap maps[6];
-  int rc = 0;
-  rc |= encode_3d(&maps[0], c, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
-  rc |= encode_3d(&maps[1], u_b, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
-  rc |= encode_3d(&maps[2], u_1, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
-  rc |= encode_3d(&maps[3], c_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
-  rc |= encode_3d(&maps[4], u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
-  rc |= encode_3d(&maps[5], Star3<MODE>::kU2 ? u_2_b : u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ,
-                  name);
-  if (rc) return SGB_EINVAL;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(star3_v4_kernel<MODE, TJ, RMWT, ROLES>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
-    attr_set = true;
-  }
-  const int tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
-  const int tiles_j = (int)((g.n + Tl::TJ - 1) / Tl::TJ);
-  const long long nout = out_i1 - out_i0;
-  const int chunks = choose_chunks((long long)tiles_k * tiles_j, nout, Tl::R, Tl::MINB);
-  const int chunk = (int)((nout + chunks - 1) / chunks);
-  dim3 grid((unsigned)(tiles_k * tiles_j), (unsigned)((nout + chunk - 1) / chunk));
-  star3_v4_kernel<MODE, TJ, RMWT, ROLES><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
-      maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-      (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D);
-  return launch_status(name);
-}
-
-}  // namespace sgb
-
-namespace sgb {
 
 // ---------------------------------------------------------------------------
-// v7: shared-memory-traffic-lean variant of v5 (same TMA pipeline, 64x32
-// tile, TMA-staged adjoint tiles).  ncu on v5 shows the kernel bound by the
-// shared-memory crossbar (~160 B/pt incl. TMA fills).  v7 cuts it to ~115 B/pt:
+// The kernel (v7 in DESIGN.md's history): one CTA per SM, 512 threads, a 64x32
+// column tile streamed over i through a 3-stage TMA ring (c, u_b, u_1 halo
+// boxes + the c_b / u_1_b tiles).  The shared-memory crossbar bounded the
+// earlier single-role design (~160 B/pt incl. TMA fills); this one needs ~115:
 //   * warps [0,8) carry Lap(u_1) (emit c_b), warps [8,16) the q stencil
 //     (emit u_1_b); every thread owns 2 rows x 4 k-points of ONE field, so the
 //     j-direction reads (2R+2 rows per 8 points instead of 4R+2) are shared
@@ -582,7 +326,6 @@ __device__ __forceinline__ void star3_v7_body(
   const int trow = 2 * ty * TK + 4 * tx;  // offset of row 2ty in a 64x32 tile
   const long long plane = (long long)n * n;
   const int coff = jr0 * n + kc;  // in-plane offset (n*n < 2^31)
-  const float gf = S3::kC2 ? 2.f * D : D;
 
   // q-pass elements of this thread (fixed for all planes): smem offset in the
   // box and, for centre elements, offset of its g in the 64x32 g tile
@@ -900,5 +643,6 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   }
   return 0;
 }
+
 
 }  // namespace sgb
