@@ -7,6 +7,8 @@
 // synchronisation so the call returns with results in host memory like the
 // CPU function does.  The plan owns the device workspace (no allocation in
 // the call).  One cudaMemcpyAsync per array (no batched-copy APIs).
+#include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -81,8 +83,11 @@ sgb_plan* sgb_plan_create(const char* family, int n, int dtype_bytes) {
     p->rmw.push_back(fs->rmw[a]);
   }
   if (fs->dims == 3 && p->dtype == 4) {
-    // pipelined host path: ~8 i-chunks (at least 2R planes each)
-    p->chunks = n >= 128 ? 8 : 1;
+    // pipelined host path: C i-chunks (at least 2R planes each); the call
+    // costs ~ H2D(all) + D2H(one chunk), so more chunks shorten the tail
+    int c = n >= 128 ? 32 : 1;
+    if (const char* e = std::getenv("SGB_PLAN_CHUNKS")) c = std::max(1, std::atoi(e));
+    p->chunks = std::min(c, std::max(1, n / 16));
     cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p->s_cmp, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
