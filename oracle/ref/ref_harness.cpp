@@ -21,8 +21,13 @@
 //                                             exactly as cmd_bench does
 //                                             (tools/stencilgrad.cpp:285-301)
 //
-// <spec> is a path to a JSON spec, or "example:<name>" for a bundled example
-// (examples.cpp:79).  Grids are raw little-endian fp64, row-major, named
+// <spec> is a path to a JSON spec, "example:<name>" for a bundled example
+// (examples.cpp:79), or "opaque:<name>" for an opaque-call problem built
+// through the reference's expression builders (the JSON front end has no
+// syntax for opaque calls, parser.cpp:210): "opaque:paper2d" is the paper's
+// f(a = u[i-1][j], b = u[i][j-1]) example, "opaque:line1d" a 1D
+// two-argument call; `emit` declares C prototypes for f / f_d_a / f_d_b (g /
+// g_d_x / g_d_y) as the reference requires (codegen.cpp:153-158, :290-300).  Grids are raw little-endian fp64, row-major, named
 // <array>.f64.  Nothing here is shipped or timed.
 #include <cstdio>
 #include <cstdlib>
@@ -35,6 +40,7 @@
 #include "stencilgrad/codegen.hpp"
 #include "stencilgrad/examples.hpp"
 #include "stencilgrad/interp.hpp"
+#include "stencilgrad/parser.hpp"
 #include "stencilgrad/specfile.hpp"
 
 namespace sg = stencilgrad;
@@ -51,8 +57,54 @@ static std::string slurp(const std::string& path) {
   return os.str();
 }
 
+static sg::ExprPtr P(const char* text) {
+  std::string err;
+  auto e = sg::parse_expr(text, &err);
+  if (!e) throw sg::Error(std::string("parse_expr: ") + err);
+  return e;
+}
+
+static sg::Problem opaque_problem(const std::string& name) {
+  std::string spec;
+  sg::ExprPtr rhs;
+  if (name == "paper2d") {
+    spec = R"({"name": "opq2d", "counters": ["i", "j"],
+      "bounds": {"i": ["1", "n - 2"], "j": ["1", "n - 2"]}, "sizes": ["n"], "scalars": ["a"],
+      "arrays": {"u": {"rank": 2, "shape": ["n", "n"], "active": true, "adjoint": "u_b",
+                       "role": "input"},
+                 "c": {"rank": 2, "shape": ["n", "n"], "active": false, "role": "coefficient"},
+                 "r": {"rank": 2, "shape": ["n", "n"], "active": true, "adjoint": "r_b",
+                       "role": "output"}},
+      "lhs": "r[i][j]", "mode": "=", "rhs": "a*u[i][j]"})";
+    // r = c * f(a = u[i-1][j], b = u[i][j-1]) + a * u
+    rhs = sg::add({sg::mul({P("c[i][j]"),
+                            sg::opaque_call("f", {{"a", P("u[i - 1][j]")}, {"b", P("u[i][j - 1]")}})}),
+                   P("a*u[i][j]")});
+  } else if (name == "line1d") {
+    spec = R"({"name": "opq1d", "counters": ["i"], "bounds": {"i": ["2", "n - 3"]},
+      "sizes": ["n"], "scalars": ["a"],
+      "arrays": {"u": {"rank": 1, "shape": ["n"], "active": true, "adjoint": "u_b",
+                       "role": "input"},
+                 "r": {"rank": 1, "shape": ["n"], "active": true, "adjoint": "r_b",
+                       "role": "output"}},
+      "lhs": "r[i]", "mode": "+=", "rhs": "a*u[i]"})";
+    // r += g(x = u[i-2], y = u[i+1]) * u[i] + a * g(x = u[i], y = u[i])
+    rhs = sg::add({sg::mul({sg::opaque_call("g", {{"x", P("u[i - 2]")}, {"y", P("u[i + 1]")}}),
+                            P("u[i]")}),
+                   sg::mul({P("a"), sg::opaque_call("g", {{"x", P("u[i]")}, {"y", P("u[i]")}})})});
+  } else {
+    throw sg::Error("unknown opaque example " + name);
+  }
+  auto r = sg::parse_spec(spec);
+  if (!r.problem) throw sg::Error("spec rejected:\n" + r.report.str());
+  sg::Problem p = *r.problem;
+  p.nest.body[0].rhs = rhs;
+  return p;
+}
+
 static sg::Problem load(const std::string& spec) {
   if (spec.rfind("example:", 0) == 0) return sg::example_problem(spec.substr(8));
+  if (spec.rfind("opaque:", 0) == 0) return opaque_problem(spec.substr(7));
   auto r = sg::parse_spec(slurp(spec));
   if (!r.problem) throw sg::Error("spec rejected:\n" + r.report.str());
   return *r.problem;
@@ -212,6 +264,10 @@ static int cmd_verify(const sg::Problem& p, long long n, unsigned long long seed
 static int cmd_emit(const sg::Problem& p, const std::string& out_dir) {
   sg::EmitOptions opts;
   opts.restrict_pointers = true;  // as cmd_bench (tools/stencilgrad.cpp:286)
+  for (const char* fn : {"f", "f_d_a", "f_d_b"})
+    opts.opaque_prototypes[fn] = std::string("double ") + fn + "(double a, double b)";
+  for (const char* fn : {"g", "g_d_x", "g_d_y"})
+    opts.opaque_prototypes[fn] = std::string("double ") + fn + "(double x, double y)";
   auto prog = sg::assemble_adjoint(p);
   std::ofstream(out_dir + "/" + p.name + "_primal.c") << sg::emit_primal(p, opts);
   std::ofstream(out_dir + "/" + p.name + "_adjoint.c") << sg::emit_adjoint(p, prog, opts);

@@ -32,7 +32,7 @@ from . import _lib
 
 # ------------------------------------------------------------------ parsing
 _TOK = re.compile(r"\s*(?:(\d+\.\d*(?:[eE][-+]?\d+)?|\d+(?:[eE][-+]?\d+)?|\.\d+(?:[eE][-+]?\d+)?)"
-                  r"|([A-Za-z_]\w*)|(>=|<=|[-+*/(),\[\]<>]))")
+                  r"|([A-Za-z_]\w*)|(>=|<=|[-+*/(),\[\]<>=]))")
 
 
 def _tokens(text):
@@ -58,6 +58,11 @@ class _Parser:
 
     def peek(self):
         return self.t[self.i] if self.i < len(self.t) else (None, None)
+
+    def at(self, k):
+        """Value of the token k positions ahead (None past the end)."""
+        j = self.i + k
+        return self.t[j][1] if j < len(self.t) else None
 
     def take(self, val=None):
         tok = self.peek()
@@ -111,6 +116,17 @@ class _Parser:
             self.take(")")
             return e
         if kind == "id":
+            if val == "derivative" and self.peek()[1] == "(":
+                # OpaqueDeriv as printed by to_input_string (expr.cpp:374-388):
+                # derivative(f, a)(a=<expr>, b=<expr>) -> call f_d_a(...)
+                self.take("(")
+                fn = self.take()[1]
+                self.take(",")
+                wrt = self.take()[1]
+                self.take(")")
+                return ("opaque", f"{fn}_d_{wrt}", self.kwargs())
+            if self.peek()[1] == "(" and self.at(2) == "=":
+                return ("opaque", val, self.kwargs())  # OpaqueCall f(a=.., b=..)
             if self.peek()[1] == "(":
                 self.take("(")
                 args = [self.compare()]
@@ -130,8 +146,8 @@ class _Parser:
                     return ("pow", args[0], sign * int(k[1]))
                 if val == "select" and len(args) == 3 and args[0][0] == "cmp":
                     return ("select", args[0], args[1], args[2])
-                raise ValueError(f"unsupported call {val}/{len(args)} (opaque calls have no "
-                                 "device implementation)")
+                raise ValueError(f"unsupported call {val}/{len(args)} (opaque calls take "
+                                 "named arguments: {val}(a=..., b=...))")
             if self.peek()[1] == "[":
                 idx = []
                 while self.peek()[1] == "[":
@@ -148,6 +164,23 @@ class _Parser:
                 return ("read", val, idx)
             return ("sym", val)
         raise ValueError(f"unexpected token {val!r}")
+
+
+    def kwargs(self):
+        """(name=expr, ...) argument list of an opaque call, in printed
+        (argument-name) order, which is also the C call order
+        (codegen.cpp:153-168)."""
+        self.take("(")
+        out = []
+        while True:
+            name = self.take()[1]
+            self.take("=")
+            out.append((name, self.compare()))
+            if self.peek()[1] != ",":
+                break
+            self.take(",")
+        self.take(")")
+        return out
 
 
 def parse_expr(text):
@@ -248,14 +281,23 @@ class _CGen:
             return f"(({self.e(c[2])} {c[1]} {self.e(c[3])}) ? {self.e(node[2])} : {self.e(node[3])})"
         if k == "cmp":
             raise ValueError("comparison outside select")
+        if k == "opaque":
+            # user-supplied __device__ function (EmittedProblem(device_functions=)),
+            # arguments positional in argument-name order like the reference's C
+            return f"{node[1]}(" + ", ".join(self.e(x) for _, x in node[2]) + ")"
         raise ValueError(k)
 
 
 class EmittedProblem:
     """A reference problem (spec dict + terms) lowered to sm_100a kernels."""
 
-    def __init__(self, spec: dict, terms, dtype: str = "f64"):
+    def __init__(self, spec: dict, terms, dtype: str = "f64", device_functions: str = ""):
+        """`device_functions`: CUDA source defining every opaque function and
+        derivative the program calls (e.g. ``__device__ T f_d_a(T a, T b)``,
+        T = the kernel's element type) -- the device counterpart of the
+        reference's `EmitOptions.opaque_prototypes` (codegen.hpp:17-18)."""
         self.spec = spec
+        self.device_functions = device_functions
         self.name = spec["name"]
         self.counters = list(spec["counters"])
         self.d = len(self.counters)
@@ -291,9 +333,12 @@ class EmittedProblem:
         adjoint (collect_refs, codegen.cpp:198-211)."""
         def reads(node, acc):
             if isinstance(node, tuple):
-                if node[0] == "read":
+                if node and node[0] == "read":
                     acc.add(node[1])
                 for x in node[1:]:
+                    reads(x, acc)
+            elif isinstance(node, list):  # opaque-call arguments
+                for x in node:
                     reads(x, acc)
             return acc
         used = set()
@@ -326,6 +371,8 @@ class EmittedProblem:
                  "  T r = T(1); int q = p < 0 ? -p : p;",
                  "  for (int i = 0; i < q; i++) r *= b;",
                  "  return p < 0 ? T(1) / r : r; }"]
+        if self.device_functions:
+            lines.append(self.device_functions)
         # flat index per array (row-major over its own shape)
         fns = {}
         for arr in self.param_arrays(self._which):
