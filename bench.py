@@ -245,36 +245,38 @@ def cpu_arrays(family, n):
     return out
 
 
-def time_cpu(family, scalars, n_full, target_s=6.0, calls=3):
-    """Best-of-`calls` time of one reference adjoint call on a bounded cube
-    sample sized so each call takes about target_s / calls seconds."""
+def time_cpu(family, scalars, n_full, target_s=4.0, calls=3):
+    """Best-of-`calls` time of one reference adjoint call on the full workload
+    grid (or, if one call there exceeds target_s, the largest cube that fits;
+    see run_reference_arm for why the sample must not be small)."""
     threads = _omp_env()
     kind, call, label = cpu_reference_runner(family)
     d = DIMS[family]
-    # calibrate on a small sample
-    n0 = {3: 96, 2: 1024, 1: 1 << 20}[d]
-    a = cpu_arrays(family, n0)
-    t0 = time.perf_counter()
-    call(n0, scalars, a)
-    dt = max(time.perf_counter() - t0, 1e-4)
-    rate = n0 ** d / dt
-    n = int(round((rate * target_s / calls) ** (1.0 / d)))
-    n = max(n0, min(n, n_full))
-    if d == 3:
-        n -= n % 4
+    n = n_full
+    if os.environ.get("SGB_REF_N"):
+        n = int(os.environ["SGB_REF_N"])
     a = cpu_arrays(family, n)
-    call(n, scalars, a)  # warm-up / first touch
-    best = float("inf")
-    for _ in range(calls):
+    call(n, scalars, a)  # first touch
+    t0 = time.perf_counter()
+    call(n, scalars, a)
+    t = time.perf_counter() - t0
+    if t > target_s and n == n_full:
+        n = int(n_full * (target_s / t) ** (1.0 / 2.5))
+        if d == 3:
+            n -= n % 4
+        a = cpu_arrays(family, n)
+        call(n, scalars, a)
+    best = t if n == n_full else float("inf")
+    for _ in range(calls - (1 if n == n_full else 0)):
         t0 = time.perf_counter()
         call(n, scalars, a)
         best = min(best, time.perf_counter() - t0)
     pts = n ** d
     return {"value": pts / best / 1e9, "unit": "GPts/s", "cores": threads, "kind": kind,
             "cpu_model": cpu_model(), "nproc": os.cpu_count(),
-            "sample": f"{label}; one call over the full {n}^{d} grid (bounded sample of the "
-                      f"{n_full}^{d} workload), best of {calls}", "seconds_per_call": best,
-            "n": n}
+            "sample": f"{label}; one call over a {n}^{d} grid "
+                      f"({'the full workload' if n == n_full else 'bounded sample of the ' + str(n_full) + '^' + str(d) + ' workload'}), best of {calls}",
+            "seconds_per_call": best, "n": n}
 
 
 def run_reference_arm(args, cfg):
@@ -285,19 +287,31 @@ def run_reference_arm(args, cfg):
     threads = _omp_env()
     kind, call, label = cpu_reference_runner(family)
     d = DIMS[family]
-    # size each step so that warmup + steps end within ~2 minutes
-    budget = float(os.environ.get("SGB_REF_BUDGET_S", "90"))
+    # size each step so that warmup + steps end within ~3 minutes
+    budget = float(os.environ.get("SGB_REF_BUDGET_S", "180"))
     per_call = budget / max(1, args.steps + args.warmup)
-    n0 = {3: 96, 2: 1024, 1: 1 << 20}[d]
-    a = cpu_arrays(family, n0)
-    t0 = time.perf_counter()
-    call(n0, scalars, a)
-    rate = n0 ** d / max(time.perf_counter() - t0, 1e-4)
-    n = int((rate * per_call) ** (1.0 / d))
-    n = max(min(n, n_full), {3: 24, 2: 64, 1: 4096}[d])
-    if d == 3:
+    # Calibrate at the FULL workload size: the reference's time per point falls
+    # with n (its boundary nests run serially and scale like n^(d-1); measured
+    # on the B200 host at radius 4: 0.17 GPts/s at 256^3, 0.37 at 748^3), so a
+    # small calibration cube would pick an unrepresentatively small sample.
+    # Shrink only as far as the budget requires (time ~ n^2.5 measured).
+    a = None
+    if os.environ.get("SGB_REF_N"):  # fixed sample size (tests)
+        n = int(os.environ["SGB_REF_N"])
+    else:
+        a = cpu_arrays(family, n_full)
+        call(n_full, scalars, a)  # first touch
+        t0 = time.perf_counter()
+        call(n_full, scalars, a)
+        t_full = max(time.perf_counter() - t0, 1e-4)
+        n = n_full if t_full <= per_call else int(n_full * (per_call / t_full) ** (1.0 / 2.5))
+        n = max(min(n, n_full), min(n_full, {3: 256, 2: 2048, 1: 1 << 20}[d]))
+    if n != n_full:
+        a = None
+    if d == 3 and n != n_full:
         n -= n % 4
-    a = cpu_arrays(family, n)
+    if a is None:
+        a = cpu_arrays(family, n)
     for _ in range(args.warmup):
         call(n, scalars, a)
     t0 = time.perf_counter()

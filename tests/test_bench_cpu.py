@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("config", ["4", "2"])
 def test_reference_arm_prints_contract_line(config):
-    env = dict(os.environ, SGB_REF_BUDGET_S="2", OMP_NUM_THREADS="2")
+    env = dict(os.environ, SGB_REF_BUDGET_S="2", OMP_NUM_THREADS="2", SGB_REF_N="64")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
                         "--config", config, "--steps", "2", "--warmup", "3"],
                        capture_output=True, text=True, env=env, timeout=300)
