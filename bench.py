@@ -590,8 +590,26 @@ def run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d):
     ms = float(ms[0]) / k
     if sl is None:
         plan.close()
+    # the bound this path runs into: this box's pinned PCIe copy bandwidth
+    nm0 = names[0]
+    hb, db = host[nm0].view(-1), arrays[nm0].view(-1)
+    gb = hb.numel() * hb.element_size() / 1e9
+
+    def copy_gbs(dst, src):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        s.record()
+        dst.copy_(src, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        return gb / (s.elapsed_time(e) / 1e3)
+    h2d_gbs = copy_gbs(db, hb)
+    d2h_gbs = copy_gbs(hb, db)
+    floor_ms = max(h2d / 1e9 / h2d_gbs, d2h / 1e9 / d2h_gbs) * 1e3
     return {"value": pts / (ms / 1e3) / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k,
+            "pcie_h2d_GBps": h2d_gbs, "pcie_d2h_GBps": d2h_gbs,
+            "copy_floor_ms": floor_ms, "frac_of_copy_floor": floor_ms / ms,
             "path": "sgb_plan_run_adjoint_host (pinned host buffers)" if sl is None
             else "per-rank pinned H2D + halo exchange + slab kernel + D2H"}
 

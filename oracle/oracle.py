@@ -232,6 +232,8 @@ def run_program_predicate(name, n, scalars, grids, adjs):
 
 
 def run_program_omp(name, n, scalars, grids, adjs):
+    """OpenMP predicate form; returns the number of threads used (>= 1), or
+    -1 on a guard violation."""
     return _run("sg_run_program_omp", name, n, scalars, grids, adjs)
 
 

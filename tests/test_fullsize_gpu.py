@@ -50,7 +50,7 @@ def _oracle(family, n, scalars, arrays):
     host = {k: v.double().cpu().numpy() for k, v in arrays.items()}
     grids = {a: host[a] for a in f.arrays if a in host}
     adjs = {b: host[b] for b in f.adjoints if b and b in host}
-    assert oracle.run_program_omp(family, n, scalars, grids, adjs) == 0
+    assert oracle.run_program_omp(family, n, scalars, grids, adjs) >= 1  # threads used
     return adjs
 
 
