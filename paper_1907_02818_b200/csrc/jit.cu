@@ -90,8 +90,12 @@ int sgb_jit_compile(const char* source, const char* name, sgb_jit_kernel** out) 
     sgb::set_error("nvrtcCreateProgram failed");
     return SGB_EINVAL;
   }
-  const char* opts[] = {"-arch=sm_100a", "--std=c++17", "-default-device", "-lineinfo"};
-  const int rc = nv.compile(prog, 4, opts);
+  // --fmad=false: every product and sum rounded separately, like the
+  // reference's emitted C (gcc -O2, x86-64 baseline: no FMA contraction), so
+  // emitted variants of one program (fused / per-nest) are bitwise equal
+  const char* opts[] = {"-arch=sm_100a", "--std=c++17", "-default-device", "-lineinfo",
+                        "--fmad=false"};
+  const int rc = nv.compile(prog, 5, opts);
   size_t ls = 0;
   nv.log_size(prog, &ls);
   g_log.assign(ls, '\0');
@@ -131,8 +135,8 @@ int sgb_jit_check(const char* source) {
   }
   void* prog = nullptr;
   if (nv.create(&prog, source, "sgb_emitted.cu", 0, nullptr, nullptr) != 0) return SGB_EINVAL;
-  const char* opts[] = {"-arch=sm_100a", "--std=c++17", "-default-device"};
-  const int rc = nv.compile(prog, 3, opts);
+  const char* opts[] = {"-arch=sm_100a", "--std=c++17", "-default-device", "--fmad=false"};
+  const int rc = nv.compile(prog, 4, opts);
   size_t ls = 0;
   nv.log_size(prog, &ls);
   g_log.assign(ls, '\0');

@@ -26,6 +26,8 @@ from __future__ import annotations
 import ctypes
 import json
 import re
+
+import numpy as np
 from dataclasses import dataclass
 
 from . import _lib
@@ -233,7 +235,10 @@ def parse_affine_node(node):
 def affine_c(aff, sizes_var):
     coeff, const = aff
     parts = [f"({v} * {sizes_var[s]})" for s, v in coeff.items()]
-    return "(" + " + ".join(parts + [f"({const}LL)"]) + ")"
+    # plain int literal: the arithmetic takes the size variables' type
+    # (I = int or long long), so a 32-bit kernel stays 32-bit
+    lit = f"({const})" if -2 ** 31 < const < 2 ** 31 else f"({const}LL)"
+    return "(" + " + ".join(parts + [lit]) + ")"
 
 
 # ------------------------------------------------------------------ codegen
@@ -364,9 +369,9 @@ class EmittedProblem:
                 return a["shape"]
         raise KeyError(arr)
 
-    def _prelude(self):
+    def _prelude(self, index="long long"):
         szv = {s: f"z_{s}" for s in self.sizes}
-        lines = [f"typedef {self.T} T;",
+        lines = [f"typedef {self.T} T;", f"typedef {index} I;",
                  "__device__ __forceinline__ T ipow(T b, int p) {",
                  "  T r = T(1); int q = p < 0 ? -p : p;",
                  "  for (int i = 0; i < q; i++) r *= b;",
@@ -378,18 +383,18 @@ class EmittedProblem:
         for arr in self.param_arrays(self._which):
             shp = self._shape_of(arr)
             r = len(shp)
-            args = ", ".join(f"long long x{i}" for i in range(r))
+            args = ", ".join(f"I x{i}" for i in range(r))
             body = "x0"
             for i in range(1, r):
                 body = f"(({body}) * {affine_c(shp[i], szv)} + x{i})"
             fn = f"ix_{arr}"
             fns[arr] = fn
-            lines.append(f"__device__ __forceinline__ long long {fn}({args}, "
-                         + ", ".join(f"long long z_{s}" for s in self.sizes) + f") {{ return {body}; }}")
+            lines.append(f"__device__ __forceinline__ I {fn}({args}, "
+                         + ", ".join(f"I z_{s}" for s in self.sizes) + f") {{ return {body}; }}")
         return lines, fns, szv
 
-    def _signature(self, kname):
-        ps = [f"long long z_{s}" for s in self.sizes]
+    def _signature(self, kname, index="long long"):
+        ps = [f"{index} z_{s}" for s in self.sizes]
         ps += [f"T s_{s}" for s in self.scalars]
         for arr in self.param_arrays(self._which):
             ps.append(f"T* __restrict__ a_{arr}")
@@ -405,57 +410,89 @@ class EmittedProblem:
         """Union of the target adjoint arrays' extents (per dimension)."""
         ext = []
         for i in range(self.d):
-            cands = [affine_c(self._shape_of(t.adjoint)[i], szv) for t in self.terms]
+            cands = []
+            for t in self.terms:
+                c = affine_c(self._shape_of(t.adjoint)[i], szv)
+                if c not in cands:
+                    cands.append(c)
             e = cands[0]
             for c in cands[1:]:
                 e = f"max({e}, {c})"
             ext.append(e)
         return ext
 
-    def gather_source(self):
+    def gather_source(self, index="long long"):
+        """Fused predicated gather.  Threads map to (.., j, k) = (z, y, x) of a
+        3D launch with grid-stride outer loops (no div/mod); per target array
+        a point inside the target's core box -- the intersection of its terms'
+        valid boxes B + o_l -- applies every term unpredicated, any other point
+        tests each term (same per-cell order either way, so bitwise equal)."""
         self._which = "gather"
-        lines, fns, szv = self._prelude()
+        lines, fns, szv = self._prelude(index)
         zargs = ", ".join(f"z_{s}" for s in self.sizes)
         at = {arr: f"AT_{arr}" for arr in self.param_arrays(self._which)}
         for arr, fn in fns.items():
             lines.append(f"#define AT_{arr}(...) {fn}(__VA_ARGS__, {zargs})")
-        lines.append(self._signature("sgb_emitted_gather") + " {")
+        lines.append(self._signature("sgb_emitted_gather", index) + " {")
         ext = self._write_box(szv)
-        lines.append("  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;")
         for i in range(self.d):
-            lines.append(f"  const long long W{i} = {ext[i]};")
-        total = " * ".join(f"W{i}" for i in range(self.d))
-        lines.append(f"  if (t >= {total}) return;")
-        for i in reversed(range(self.d)):
-            if i == 0:
-                lines.append("  const long long y0 = t;")
-            else:
-                lines.append(f"  const long long y{i} = t % W{i}; t /= W{i};")
+            lines.append(f"  const I W{i} = {ext[i]};")
+        d = self.d
+        inner = d - 1
+        lines.append(f"  const I y{inner} = blockIdx.x * (I)blockDim.x + threadIdx.x;")
+        lines.append(f"  if (y{inner} >= W{inner}) return;")
+        depth = 1
+        if d >= 2:
+            lines.append(f"  for (I y{d - 2} = blockIdx.y * (I)blockDim.y + threadIdx.y; "
+                         f"y{d - 2} < W{d - 2}; y{d - 2} += gridDim.y * (I)blockDim.y) {{")
+            depth += 1
+        if d >= 3:
+            lines.append(f"  for (I y{d - 3} = blockIdx.z * (I)blockDim.z + threadIdx.z; "
+                         f"y{d - 3} < W{d - 3}; y{d - 3} += gridDim.z * (I)blockDim.z) {{")
+            depth += 1
         # group terms by target adjoint, ascending term order inside each
         targets = []
         for t in self.terms:
             if t.adjoint not in targets:
                 targets.append(t.adjoint)
         cidx = {c: i for i, c in enumerate(self.counters)}
+        ys = ", ".join(f"y{i}" for i in range(d))
         for tgt in targets:
             shp = self._shape_of(tgt)
-            inb = " && ".join(f"y{i} < {affine_c(shp[i], szv)}" for i in range(self.d))
+            inb = " && ".join(f"y{i} < {affine_c(shp[i], szv)}" for i in range(d))
+            mine = [(ti, t, part) for ti, (t, part) in enumerate(zip(self.terms, self.partials))
+                    if t.adjoint == tgt]
+            core = []
+            for i in range(d):
+                lo, hi = self.bounds[i]
+                omax = max(t.offset[i] for _, t, _ in mine)
+                omin = min(t.offset[i] for _, t, _ in mine)
+                core.append(f"y{i} >= {affine_c(lo, szv)} + ({omax}) && "
+                            f"y{i} <= {affine_c(hi, szv)} + ({omin})")
             lines.append(f"  if ({inb}) {{")
-            lines.append("    bool touched = false; T cell = T(0);")
-            ys = ", ".join(f"y{i}" for i in range(self.d))
-            for ti, (t, part) in enumerate(zip(self.terms, self.partials)):
-                if t.adjoint != tgt:
-                    continue
-                xs = [f"(y{i} - ({t.offset[i]}))" for i in range(self.d)]
+            lines.append(f"    if ({' && '.join(core)}) {{  // core of {tgt}: every term valid")
+            lines.append(f"      T cell = a_{tgt}[AT_{tgt}({ys})];")
+            exprs = []
+            for ti, t, part in mine:
+                xs = [f"(y{i} - ({t.offset[i]}))" for i in range(d)]
                 cg = _CGen(self, {c: xs[cidx[c]] for c in self.counters}, at)
                 seed_idx = ", ".join(xs[cidx[c]] for c in self.lhs)
-                lines.append(f"    if ({self._box_checks(xs, szv)}) {{  // term {ti}: "
+                exprs.append((ti, t, xs, f"({cg.e(part)}) * a_{self.seed}[AT_{self.seed}({seed_idx})]"))
+            for ti, t, xs, ex in exprs:
+                lines.append(f"      cell += {ex};  // term {ti}")
+            lines.append(f"      a_{tgt}[AT_{tgt}({ys})] = cell;")
+            lines.append("    } else {")
+            lines.append("      bool touched = false; T cell = T(0);")
+            for ti, t, xs, ex in exprs:
+                lines.append(f"      if ({self._box_checks(xs, szv)}) {{  // term {ti}: "
                              f"{t.array}{list(t.offset)}")
-                lines.append(f"      if (!touched) {{ cell = a_{tgt}[AT_{tgt}({ys})]; touched = true; }}")
-                lines.append(f"      cell += ({cg.e(part)}) * a_{self.seed}[AT_{self.seed}({seed_idx})];")
-                lines.append("    }")
-            lines.append(f"    if (touched) a_{tgt}[AT_{tgt}({ys})] = cell;")
+                lines.append(f"        if (!touched) {{ cell = a_{tgt}[AT_{tgt}({ys})]; touched = true; }}")
+                lines.append(f"        cell += {ex};")
+                lines.append("      }")
+            lines.append(f"      if (touched) a_{tgt}[AT_{tgt}({ys})] = cell;")
+            lines.append("    }")
             lines.append("  }")
+        lines.append("  }" * (depth - 1))
         lines.append("}")
         return "\n".join(lines) + "\n"
 
@@ -557,25 +594,29 @@ class EmittedProblem:
             if _lib.lib().sgb_jit_check(src.encode()) != 0:
                 raise _lib.StencilError(_lib.lib().sgb_jit_log().decode())
 
-    def _kernel(self, which):
-        if which not in self._kern:
-            src = {"gather": self.gather_source, "primal": self.primal_source,
-                   "nest": self.nest_source}[which]()
+    def _kernel(self, which, index="long long"):
+        key = (which, index)
+        if key not in self._kern:
+            if which == "gather":
+                src = self.gather_source(index)
+            else:
+                src = {"primal": self.primal_source, "nest": self.nest_source}[which]()
             h = ctypes.c_void_p()
             rc = _lib.lib().sgb_jit_compile(src.encode(), f"sgb_emitted_{which}".encode(),
                                             ctypes.byref(h))
             if rc != 0:
                 raise _lib.StencilError(_lib.lib().sgb_last_error().decode())
-            self._kern[which] = h
-        return self._kern[which]
+            self._kern[key] = h
+        return self._kern[key]
 
-    def _launch(self, which, sizes, scalars, arrays, nthreads, stream=None, extra=()):
+    def _launch(self, which, sizes, scalars, arrays, nthreads, stream=None, extra=(),
+                grid=None, index="long long"):
         import torch
         from .api import _stream_ptr
         keep = []
         argv = []
         for s in self.sizes:
-            v = ctypes.c_longlong(int(sizes[s]))
+            v = (ctypes.c_int if index == "int" else ctypes.c_longlong)(int(sizes[s]))
             keep.append(v)
         T = ctypes.c_double if self.T == "double" else ctypes.c_float
         for s in self.scalars:
@@ -591,10 +632,12 @@ class EmittedProblem:
         keep.extend(extra)
         argv = (ctypes.c_void_p * len(keep))(*[ctypes.cast(ctypes.pointer(k), ctypes.c_void_p)
                                                for k in keep])
-        blocks = max(1, (nthreads + 255) // 256)
-        if blocks > 2 ** 31 - 1:
-            raise _lib.StencilError("grid too large")
-        rc = _lib.lib().sgb_jit_launch(self._kernel(which), blocks, 1, 1, 256, 1, 1, argv,
+        if grid is None:
+            blocks = max(1, (nthreads + 255) // 256)
+            if blocks > 2 ** 31 - 1:
+                raise _lib.StencilError("grid too large")
+            grid = (blocks, 1, 1, 256, 1, 1)
+        rc = _lib.lib().sgb_jit_launch(self._kernel(which, index), *grid, argv,
                                        _stream_ptr(stream))
         _lib.check(rc, f"{self.name} emitted {which}")
 
@@ -620,10 +663,21 @@ class EmittedProblem:
             return
         if not self.guards_ok(sizes):
             raise _lib.GuardViolation(f"{self.name}: minimum extent violated")
-        total = 1
-        for i in range(self.d):
-            total *= max(self._eval_aff(self._shape_of(t.adjoint)[i], sizes) for t in self.terms)
-        self._launch("gather", sizes, scalars, arrays, total, stream)
+        W = [max(self._eval_aff(self._shape_of(t.adjoint)[i], sizes) for t in self.terms)
+             for i in range(self.d)]
+        # 32-bit indices when every referenced array fits
+        big = max(int(np.prod([self._eval_aff(a, sizes) for a in self._shape_of(arr)]))
+                  for arr in self.param_arrays("gather"))
+        index = "int" if big < 2 ** 31 - 1 else "long long"
+        bx = 32 if self.d > 1 else 256
+        by = 8 if self.d > 1 else 1
+        gx = (W[-1] + bx - 1) // bx
+        gy = min((W[-2] + by - 1) // by, 65535) if self.d >= 2 else 1
+        gz = min(W[0], 65535) if self.d >= 3 else 1
+        if gx > 2 ** 31 - 1:
+            raise _lib.StencilError("grid too large")
+        self._launch("gather", sizes, scalars, arrays, 0, stream,
+                     grid=(max(1, gx), max(1, gy), max(1, gz), bx, by, 1), index=index)
 
     def adjoint_nests(self, sizes, scalars, arrays, nests=None, stream=None):
         """The same adjoint as `adjoint`, executed the reference's way: one
