@@ -251,10 +251,14 @@ class Term:
 
 
 class _CGen:
-    def __init__(self, prob, counters, at):
+    def __init__(self, prob, counters, at, flat=None):
         self.p = prob
         self.counters = counters  # counter name -> C expression of its value
         self.at = at              # array name -> C flat-index function name
+        # flat addressing (gather): {"shift": {counter: s}, "arrays": set} -- a
+        # read A[c_0 + k_0]..[c_r + k_r] of an array laid out in counter order
+        # at x = y + shift is fy_A + sum_i (k_i + shift_i) * sd_A_i
+        self.flat = flat
 
     def e(self, node):
         k = node[0]
@@ -267,6 +271,17 @@ class _CGen:
             return f"s_{node[1]}"
         if k == "read":
             name, idx = node[1], node[2]
+            if self.flat is not None and name in self.flat["arrays"] and \
+                    [c for c, _ in idx] == self.p.counters:
+                sh = self.flat["shift"]
+                r = len(idx)
+                terms = []
+                for dim, (c, o) in enumerate(idx):
+                    dd = o + sh[c]
+                    if dd:
+                        terms.append(f"{dd}" if dim == r - 1 else f"({dd}) * sd_{name}_{dim}")
+                off = " + ".join(terms)
+                return f"a_{name}[fy_{name}" + (f" + ({off})" if off else "") + "]"
             args = ", ".join(f"({self.counters[c]} + ({o}))" for c, o in idx)
             return f"a_{name}[{self.at[name]}({args})]"
         if k in ("add", "sub", "mul", "div"):
@@ -438,6 +453,15 @@ class EmittedProblem:
         for i in range(self.d):
             lines.append(f"  const I W{i} = {ext[i]};")
         d = self.d
+        # arrays laid out in counter order (rank d): flat base index per point
+        # plus per-dimension strides, so every shifted read is base + const
+        flat_arrays = [a for a in self.param_arrays(self._which)
+                       if len(self._shape_of(a)) == d]
+        for a in flat_arrays:
+            shp = self._shape_of(a)
+            for dim in range(d - 1):
+                st = " * ".join(affine_c(shp[q], szv) for q in range(dim + 1, d))
+                lines.append(f"  const I sd_{a}_{dim} = {st};")
         inner = d - 1
         lines.append(f"  const I y{inner} = blockIdx.x * (I)blockDim.x + threadIdx.x;")
         lines.append(f"  if (y{inner} >= W{inner}) return;")
@@ -457,6 +481,8 @@ class EmittedProblem:
                 targets.append(t.adjoint)
         cidx = {c: i for i, c in enumerate(self.counters)}
         ys = ", ".join(f"y{i}" for i in range(d))
+        for a in flat_arrays:
+            lines.append(f"  const I fy_{a} = AT_{a}({ys});")
         for tgt in targets:
             shp = self._shape_of(tgt)
             inb = " && ".join(f"y{i} < {affine_c(shp[i], szv)}" for i in range(d))
@@ -471,25 +497,28 @@ class EmittedProblem:
                             f"y{i} <= {affine_c(hi, szv)} + ({omin})")
             lines.append(f"  if ({inb}) {{")
             lines.append(f"    if ({' && '.join(core)}) {{  // core of {tgt}: every term valid")
-            lines.append(f"      T cell = a_{tgt}[AT_{tgt}({ys})];")
+            tix = f"fy_{tgt}" if tgt in flat_arrays else f"AT_{tgt}({ys})"
+            lines.append(f"      T cell = a_{tgt}[{tix}];")
             exprs = []
             for ti, t, part in mine:
                 xs = [f"(y{i} - ({t.offset[i]}))" for i in range(d)]
-                cg = _CGen(self, {c: xs[cidx[c]] for c in self.counters}, at)
-                seed_idx = ", ".join(xs[cidx[c]] for c in self.lhs)
-                exprs.append((ti, t, xs, f"({cg.e(part)}) * a_{self.seed}[AT_{self.seed}({seed_idx})]"))
+                flat = {"shift": {c: -t.offset[cidx[c]] for c in self.counters},
+                        "arrays": set(flat_arrays)}
+                cg = _CGen(self, {c: xs[cidx[c]] for c in self.counters}, at, flat)
+                seed_read = ("read", self.seed, [(c, 0) for c in self.lhs])
+                exprs.append((ti, t, xs, f"({cg.e(part)}) * {cg.e(seed_read)}"))
             for ti, t, xs, ex in exprs:
                 lines.append(f"      cell += {ex};  // term {ti}")
-            lines.append(f"      a_{tgt}[AT_{tgt}({ys})] = cell;")
+            lines.append(f"      a_{tgt}[{tix}] = cell;")
             lines.append("    } else {")
             lines.append("      bool touched = false; T cell = T(0);")
             for ti, t, xs, ex in exprs:
                 lines.append(f"      if ({self._box_checks(xs, szv)}) {{  // term {ti}: "
                              f"{t.array}{list(t.offset)}")
-                lines.append(f"        if (!touched) {{ cell = a_{tgt}[AT_{tgt}({ys})]; touched = true; }}")
+                lines.append(f"        if (!touched) {{ cell = a_{tgt}[{tix}]; touched = true; }}")
                 lines.append(f"        cell += {ex};")
                 lines.append("      }")
-            lines.append(f"      if (touched) a_{tgt}[AT_{tgt}({ys})] = cell;")
+            lines.append(f"      if (touched) a_{tgt}[{tix}] = cell;")
             lines.append("    }")
             lines.append("  }")
         lines.append("  }" * (depth - 1))

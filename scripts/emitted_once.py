@@ -1,0 +1,17 @@
+"""One launch of the emitted generic gather at cfg 4 (768^3 fp32) on
+benchmark inputs (for ncu; developer aid)."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_1907_02818_b200 import api, emitter  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 768
+arrays = bench.gen_inputs(api, torch, "wave3d_r4", n)
+ep = emitter.load_program("wave3d_r4", "f32")
+for _ in range(3):
+    ep.adjoint({"n": n}, {"D": 0.01}, arrays)
+torch.cuda.synchronize()
+print("ok")
