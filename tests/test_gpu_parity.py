@@ -232,8 +232,9 @@ def test_host_buffer_plan_entry(api, name, n, dtype):
 
 @pytest.mark.parametrize("n", [68, 97, 136])
 def test_r4_launch_variants_bitwise_equal(api, n, monkeypatch):
-    """The radius-4 launch knobs (windowed seed map vs in-kernel mask, wave-model
-    vs forced i-chunking, frame on a side stream) change only scheduling: every
+    """The radius-4 launch knobs (windowed seed map vs in-kernel mask, one
+    launch vs interior/frame launches, wave-model vs forced i-chunking, frame
+    on a side stream) change only scheduling: every
     point's arithmetic is the same, so the results are bitwise identical, and
     the default matches the oracle."""
     name = "wave3d_r4"
@@ -243,8 +244,9 @@ def test_r4_launch_variants_bitwise_equal(api, n, monkeypatch):
     want = oracle_gather(name, n, scalars, g, a)
     for adj in ("c_b", "u_1_b"):
         check_close(base[adj], want[adj], "f32", f"{name} n={n} {adj}")
-    for env in ({"SGB_NO_UBWIN": "1"}, {"SGB_ICHUNKS": "3", "SGB_ICHUNKS_F": "5"},
-                {"SGB_FORK": "1"}, {"SGB_ICHUNKS": "1", "SGB_ICHUNKS_F": "1"}):
+    for env in ({"SGB_NO_UBWIN": "1"}, {"SGB_ICHUNKS": "3"}, {"SGB_ICHUNKS": "1"},
+                {"SGB_V7_SPLIT": "1", "SGB_ICHUNKS": "3", "SGB_ICHUNKS_F": "5"},
+                {"SGB_V7_SPLIT": "1", "SGB_FORK": "1"}):
         with monkeypatch.context() as m:
             for k, v in env.items():
                 m.setenv(k, v)
