@@ -156,3 +156,25 @@ def test_time_loop_adjoint_checkpointing_and_gradient(mods):
     fd = (J(u0 + h * v0, u1 + h * v1, c + h * vc) - J(u0 - h * v0, u1 - h * v1, c - h * vc)) / (2 * h)
     ad = float((v0 * u0b).sum() + (v1 * u1b).sum() + (vc * cb).sum())
     assert abs(fd - ad) / (1 + abs(ad)) < 1e-6, (fd, ad)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("n,lo,hi,base,npl", [(40, 4, 35, 0, 40), (37, 1, 35, 0, 37),
+                                              (64, 4, 59, 10, 30), (33, 3, 30, 5, 9)])
+def test_box_axpy_matches_numpy(mods, n, lo, hi, base, npl, dtype):
+    """y[B] += a * x[B] on a slab of planes, box edges and slab offsets that
+    break 16-byte alignment included (vector and element paths)."""
+    torch, api, _ = mods
+    dt = torch.float32 if dtype == "f32" else torch.float64
+    g = torch.Generator(device="cpu").manual_seed(n + lo)
+    y = torch.randn(npl, n, n, generator=g, dtype=dt)
+    x = torch.randn(npl, n, n, generator=g, dtype=dt)
+    want = y.clone()
+    for li in range(npl):
+        i = base + li
+        if lo <= i <= hi:
+            want[li, lo:hi + 1, lo:hi + 1] += -0.5 * x[li, lo:hi + 1, lo:hi + 1]
+    yd, xd = y.cuda(), x.cuda()
+    api.box_axpy(yd, xd, -0.5, n, lo, hi, base, npl)
+    torch.cuda.synchronize()
+    assert torch.allclose(yd.cpu(), want, rtol=0, atol=1e-6 if dtype == "f32" else 1e-14)
