@@ -1,12 +1,14 @@
 // extern "C" entry points (include/stencilgrad_b200.h): argument checks, the
 // reference's minimum-extent guards, and dispatch to the sm_100a kernels.
 #include <cstdio>
+#include <type_traits>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "generic_kernels.cuh"
 #include "lowdim.cuh"
+#include "star3d_primal.cuh"
 #include "star3d_r4.cuh"
 #include "star3d_tma.cuh"
 
@@ -102,6 +104,11 @@ static int star3_primal(const char* name, long long n, double D, const T* c, con
   if (n <= 0) return einval(std::string(name) + ": n must be positive");
   if (!c || !u_1 || !u_2 || !u) return einval(std::string(name) + ": null array");
   if (n < 2 * R + 1) return 0;  // empty primal box
+  if (std::is_same<T, float>::value && !std::getenv("SGB_PRIMAL_GENERIC")) {
+    const int rc = star3_primal_tma<MODE>(n, (float)D, (const float*)c, (const float*)u_1,
+                                          (const float*)u_2, (float*)u, s, name);
+    if (rc != 1) return rc;  // 1: TMA path not applicable (alignment / size)
+  }
   const long long lo = R, hi = n - 1 - R;
   dim3 b(32, 4), gr((unsigned)((n + 31) / 32), (unsigned)((n + 3) / 4), (unsigned)n);
   star3_primal_kernel<MODE, T><<<gr, b, 0, s>>>(Slab3{n, 0, n}, lo, hi, 0, n, (T)D, c, u_1,

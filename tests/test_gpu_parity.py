@@ -292,3 +292,21 @@ def test_verify_problem_equivalence_on_gpu(api, name, n):
         if adj != f.seed:
             e = oracle.max_rel_err(gat[adj], sca[adj])
             assert e <= 1e-12, (name, adj, e)
+
+
+@pytest.mark.parametrize("name", ["wave3d_r4", "wave3d_c", "wave3d_c2"])
+@pytest.mark.parametrize("n", [17, 24, 36, 68, 97, 136, 200])
+def test_primal_f32_matches_oracle(api, name, n):
+    """fp32 primal (TMA streaming kernel where n % 4 == 0, per-point kernel
+    otherwise) against the oracle's run_nest on the fp32-rounded inputs; the
+    output array starts non-zero, so '+=' families and the untouched points
+    outside the primal box are checked too."""
+    scalars, grids, _ = gen.family_inputs(name, n, seed=n + 7)
+    f = oracle.family(name)
+    out = f.arrays[f.output]
+    grids[out] = np.random.default_rng(n).standard_normal(grids[out].shape)
+    g = _round(grids, "f32")
+    got = api.run_nest(name, n, scalars, g, dtype="f32")
+    want = {k: v.copy() for k, v in g.items()}
+    assert oracle.run_primal(name, n, scalars, want) == 0
+    check_close(got[out], want[out], "f32", f"{name} n={n} primal")
