@@ -442,6 +442,11 @@ def run_ours(args, cfg):
                                                           dtype, kms)
         except Exception as ex:  # pragma: no cover - report, never fail the bench
             ablation["boundary_strategies"] = {"error": str(ex)[:300]}
+        if family == "wave3d_r4":
+            try:
+                ablation["time_loop_adjoint"] = time_loop_bench(torch, api, n, scalars, arrays)
+            except Exception as ex:  # pragma: no cover
+                ablation["time_loop_adjoint"] = {"error": str(ex)[:300]}
     table = None
     if world == 1 and not args.no_configs:
         table = config_table(torch, api, peak, args.config)
@@ -544,6 +549,39 @@ def config_table(torch, api, peak, skip):
         del arrays
         torch.cuda.empty_cache()
     return out
+
+
+def time_loop_bench(torch, api, n, scalars, arrays, T=16, K=4):
+    """SURVEY 8(f) item 2 at the cfg-4 size: gradient of <w, u^T> through T-1
+    primal steps, checkpoints every K steps, forward recomputation per segment
+    (drivers.time_loop_adjoint).  Timed once after one full-size warm-up."""
+    from paper_1907_02818_b200 import drivers
+    D = float(scalars["D"])
+    c = arrays["c"]
+    u0 = arrays["u_1"]
+    u1 = torch.empty_like(u0)
+    api.fill_normal3d(u1, n, 4, 0, 5, 0, n)
+    w = arrays["u_b"]
+    # warm-up at full size: the caching allocator then holds the state buffers
+    drivers.time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=K)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    _, _, _, stats = drivers.time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=K)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    pts = n ** 3
+    primal_steps = (T - 1) + stats["recomputed_steps"]
+    adj_steps = stats["adjoint_steps"]
+    # kernels' algorithmic bytes: primal 16, gather 28, box axpy 12 B/pt
+    alg = pts * (16 * primal_steps + (28 + 12) * adj_steps)
+    return {"n": n, "T": T, "checkpoint_every": K, "ms": ms,
+            "ms_per_reverse_step": ms / max(1, adj_steps), **stats,
+            "primal_launches": primal_steps,
+            "alg_GB_s_kernels": alg / (ms / 1e3) / 1e9,
+            "note": "includes checkpoint copies and state zeroing; alg bytes count "
+                    "the primal/gather/axpy kernels only"}
 
 
 def run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d):
