@@ -296,6 +296,12 @@ int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float
 #define SGB_BURGERS(T, SFX)                                                                    \
   int burgers2d_##SFX(int n, double C, double D, T* u_1, T* u, sgb_stream_t stream) {          \
     if (n <= 0 || !u_1 || !u) return einval("burgers2d: bad arguments");                       \
+    if (n % 2 == 0 && aligned16(u_1, u, u_1, u)) {                                             \
+      dim3 g((unsigned)((n / 2 + 127) / 128), (unsigned)((n + 31) / 32));                      \
+      burgers2d_primal_stream_kernel<T>                                                        \
+          <<<g, 128, 0, as_stream(stream)>>>(n, (T)C, (T)D, u_1, u, 32);                       \
+      return launch_status("burgers2d");                                                       \
+    }                                                                                          \
     dim3 b(64, 4), g((unsigned)((n + 63) / 64), (unsigned)((n + 3) / 4));                      \
     burgers2d_primal_kernel<T><<<g, b, 0, as_stream(stream)>>>(n, (T)C, (T)D, u_1, u);         \
     return launch_status("burgers2d");                                                         \

@@ -178,6 +178,58 @@ __global__ void __launch_bounds__(128) burgers2d_stream_kernel(long long n, T C,
   }
 }
 
+// ------------------------------------------------------------------ burgers2d primal
+// run_nest of the Burgers spec on [1, n-2]^2 (interp.cpp:153-173): each thread
+// owns 2 consecutive j of a column strip and streams down rows_per_block
+// rows with a 3-row register window (row i+1 requested one row ahead);
+// j-1 / j+2 from the neighbouring lanes.  Same expression and grouping as
+// the per-point kernel (generic_kernels.cuh).  16 B/pt: u_1 read, u written.
+template <typename T>
+__global__ void __launch_bounds__(128) burgers2d_primal_stream_kernel(long long n, T C, T D,
+                                                                      const T* __restrict__ u1,
+                                                                      T* __restrict__ u,
+                                                                      int rows_per_block) {
+  using V = typename Vec2<T>::type;
+  const int lane = threadIdx.x & 31;
+  const long long j = 2 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+  const bool active = j < n;
+  const long long i0 = (long long)blockIdx.y * rows_per_block;
+  const long long i1 = min(i0 + rows_per_block, n);
+  auto row = [&](long long i) { return (active && i >= 0 && i < n) ? ld2(u1 + i * n + j) : V{}; };
+  V um = row(i0 - 1), u0 = row(i0), up = row(i0 + 1);
+  const bool jin[2] = {j >= 1 && j <= n - 2, j + 1 >= 1 && j + 1 <= n - 2};
+  for (long long i = i0; i < i1; i++) {
+    const V up2 = row(i + 2);
+    const T* urow = u1 + i * n;
+    const bool rowok = i >= 0 && i < n;
+    const T ul = left_of(u0.y, urow, j, n, lane, active && rowok);
+    const T ur = right_of(u0.x, urow, j, n, lane, active && rowok);
+    if (active && i >= 1 && i <= n - 2 && (jin[0] || jin[1])) {
+      const T vv[2] = {u0.x, u0.y}, mm[2] = {um.x, um.y}, pp[2] = {up.x, up.y};
+      const T vl[2] = {ul, u0.x}, vr[2] = {u0.y, ur};
+      T out[2];
+#pragma unroll
+      for (int m = 0; m < 2; m++) {
+        const T v = vv[m];
+        out[m] = v -
+                 C * (fmax(v, T(0)) * (v - mm[m]) + fmin(v, T(0)) * (pp[m] - v) +
+                      fmax(v, T(0)) * (v - vl[m]) + fmin(v, T(0)) * (vr[m] - v)) +
+                 D * (pp[m] + mm[m] + vr[m] + vl[m] - T(4) * v);
+      }
+      T* orow = u + i * n + j;
+      if (jin[0] && jin[1]) {
+        st2(orow, out[0], out[1]);
+      } else {
+        if (jin[0]) orow[0] = out[0];
+        if (jin[1]) orow[1] = out[1];
+      }
+    }
+    um = u0;
+    u0 = up;
+    up = up2;
+  }
+}
+
 // ------------------------------------------------------------------ burgers2d (ring)
 // Strip-streaming form: a CTA owns a W-column strip and rows [i0, i1).  One
 // thread streams the row segments of u_1 and u_b (with a 16-byte halo each

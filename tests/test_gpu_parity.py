@@ -310,3 +310,18 @@ def test_primal_f32_matches_oracle(api, name, n):
     want = {k: v.copy() for k, v in g.items()}
     assert oracle.run_primal(name, n, scalars, want) == 0
     check_close(got[out], want[out], "f32", f"{name} n={n} primal")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("n", [5, 64, 203, 300, 1030])
+def test_burgers_primal_matches_oracle(api, n, dtype):
+    """burgers2d primal (row-streaming kernel for even n, per-point otherwise)
+    against the oracle's run_nest; untouched ring keeps its values."""
+    name = "burgers2d"
+    scalars, grids, _ = gen.family_inputs(name, n, seed=n + 11)
+    grids["u"] = np.random.default_rng(n).standard_normal(grids["u"].shape)
+    g = _round(grids, dtype)
+    got = api.run_nest(name, n, scalars, g, dtype=dtype)
+    want = {k: v.copy() for k, v in g.items()}
+    assert oracle.run_primal(name, n, scalars, want) == 0
+    check_close(got["u"], want["u"], dtype, f"burgers2d n={n} primal")
