@@ -17,8 +17,23 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // splitmix64 finaliser
   return x;
 }
 
+__device__ __forceinline__ uint64_t hash_key(uint64_t seed, uint64_t stream) {
+  return seed * 0x9E3779B97F4A7C15ull + mix64(stream + 0xD1B54A32D192ED03ull);
+}
 __device__ __forceinline__ uint64_t hash3(uint64_t seed, uint64_t stream, uint64_t ctr) {
-  return mix64(seed * 0x9E3779B97F4A7C15ull + mix64(stream + 0xD1B54A32D192ED03ull) + ctr);
+  return mix64(hash_key(seed, stream) + ctr);
+}
+
+// One Box-Muller pair from the hash of pair index m: (cos branch, sin branch)
+// = the values of flat indices 2m and 2m+1.
+__device__ __forceinline__ float2 normal_pair(uint64_t key, uint64_t m) {
+  const uint64_t h = mix64(key + m);
+  const float u1 = ((float)(uint32_t)(h >> 40) + 1.0f) * 0x1.0p-24f;  // (0, 1]
+  const float u2 = (float)(uint32_t)(h & 0xFFFFFFu) * 0x1.0p-24f;     // [0, 1)
+  const float rad = sqrtf(-2.0f * __logf(u1));
+  float sn, cs;
+  __sincosf(6.283185307179586f * u2, &sn, &cs);
+  return make_float2(rad * cs, rad * sn);
 }
 
 // kind 0: N(mean, scale^2); kind 1: U[mean, mean + scale).
@@ -26,13 +41,8 @@ __device__ __forceinline__ uint64_t hash3(uint64_t seed, uint64_t stream, uint64
 // (cos / sin branch), so value(index) is still a pure function of the index.
 __device__ __forceinline__ double draw(uint64_t seed, uint64_t stream, uint64_t idx, int kind) {
   if (kind == 1) return (double)(hash3(seed, stream, idx) >> 11) * 0x1.0p-53;
-  const uint64_t h = hash3(seed, stream, idx >> 1);
-  const float u1 = ((float)(uint32_t)(h >> 40) + 1.0f) * 0x1.0p-24f;  // (0, 1]
-  const float u2 = (float)(uint32_t)(h & 0xFFFFFFu) * 0x1.0p-24f;     // [0, 1)
-  const float rad = sqrtf(-2.0f * __logf(u1));
-  float sn, cs;
-  __sincosf(6.283185307179586f * u2, &sn, &cs);
-  return (double)((idx & 1) ? rad * sn : rad * cs);
+  const float2 z = normal_pair(hash_key(seed, stream), idx >> 1);
+  return (double)((idx & 1) ? z.y : z.x);
 }
 
 template <typename T>
@@ -47,22 +57,38 @@ __global__ void fill_random_kernel(T* dst, long long count, long long base, uint
 
 // 3D fill with a fused zero halo: planes [i_base, i_base+nplanes) of an n^3
 // grid, h-point zero shell, N(mean, scale^2) elsewhere; 4 points per thread.
+// With n even the 4 points are two whole Box-Muller pairs, each computed once
+// (same values as draw()).
 __global__ void fill_normal3d_f32_kernel(float* dst, long long n, long long i_base,
                                          long long nplanes, int h, uint64_t seed,
                                          uint64_t stream, float mean, float scale) {
   const long long k = 4 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
   const long long j = blockIdx.y;
   if (k >= n) return;
+  const uint64_t key = hash_key(seed, stream);
+  const bool jh = j < h || j >= n - h;
   for (long long li = blockIdx.z; li < nplanes; li += gridDim.z) {
     const long long i = i_base + li;
     const long long g = (i * n + j) * n + k;
+    const bool rowh = jh || i < h || i >= n - h;
     float v[4];
+    if ((g & 1) == 0 && k + 3 < n) {
+      const float2 a = normal_pair(key, (uint64_t)g >> 1);
+      const float2 b = normal_pair(key, ((uint64_t)g >> 1) + 1);
+      const float z[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
-    for (int m = 0; m < 4; m++) {
-      const long long kk = k + m;
-      const bool halo = i < h || i >= n - h || j < h || j >= n - h || kk < h || kk >= n - h;
-      v[m] = (halo || kk >= n) ? 0.f
-                               : mean + scale * (float)draw(seed, stream, (uint64_t)(g + m), 0);
+      for (int m = 0; m < 4; m++) {
+        const long long kk = k + m;
+        v[m] = (rowh || kk < h || kk >= n - h) ? 0.f : mean + scale * z[m];
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; m++) {
+        const long long kk = k + m;
+        const bool halo = rowh || kk < h || kk >= n - h;
+        v[m] = (halo || kk >= n) ? 0.f
+                                 : mean + scale * (float)draw(seed, stream, (uint64_t)(g + m), 0);
+      }
     }
     float* p = dst + (li * n + j) * n + k;
     if (n % 4 == 0) {

@@ -178,3 +178,17 @@ def test_box_axpy_matches_numpy(mods, n, lo, hi, base, npl, dtype):
     api.box_axpy(yd, xd, -0.5, n, lo, hi, base, npl)
     torch.cuda.synchronize()
     assert torch.allclose(yd.cpu(), want, rtol=0, atol=1e-6 if dtype == "f32" else 1e-14)
+
+
+@pytest.mark.parametrize("n", [64, 37])
+def test_fill_normal3d_equals_elementwise_draw(mods, n):
+    """The pairwise 3D generator (each Box-Muller pair computed once) yields
+    exactly the values of the element-wise generator at the same global
+    indices (odd n exercises the unpaired path)."""
+    torch, api, _ = mods
+    a = torch.empty((n, n, n), dtype=torch.float32, device="cuda")
+    b = torch.empty_like(a)
+    api.fill_normal3d(a, n, 0, 5, 3)
+    api.fill_random(b, 0, 5, 3, "normal", 0.0, 1.0)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
