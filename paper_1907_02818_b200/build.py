@@ -28,7 +28,7 @@ def sources():
 
 def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + \
-        sorted(glob.glob(os.path.join(INCLUDE, "*.h"))) + [os.path.abspath(__file__)]
+        sorted(glob.glob(os.path.join(INCLUDE, "*.h*"))) + [os.path.abspath(__file__)]
 
 
 def stale() -> bool:
