@@ -57,8 +57,12 @@ def _stream_ptr(stream=None):
 
 
 def _call(family, kind, n, scalars, arrays, stream=None, extra=()):
-    import torch
     names = array_params(family, kind)
+    d = FAMILIES[family]
+    # every array holds the full n^d grid (a slab: nplanes whole planes); a
+    # short buffer would be read out of bounds, so it is rejected here like
+    # the reference's bounds error (interp.cpp:30-35)
+    want = int(extra[1]) * int(n) ** (d - 1) if kind == "slab" else int(n) ** d
     dtype = None
     ptrs = []
     for nm in names:
@@ -67,6 +71,8 @@ def _call(family, kind, n, scalars, arrays, stream=None, extra=()):
             raise _lib.StencilError(f"{family}{_SUFFIX[kind]}: missing array '{nm}'")
         if not (t.is_cuda and t.is_contiguous()):
             raise _lib.StencilError(f"array '{nm}' must be a contiguous CUDA tensor")
+        if t.numel() != want:
+            raise _lib.StencilError(f"array '{nm}' has {t.numel()} elements, expected {want}")
         if dtype is None:
             dtype = t.dtype
         elif t.dtype != dtype:
@@ -77,7 +83,6 @@ def _call(family, kind, n, scalars, arrays, stream=None, extra=()):
     sc = [float(scalars[s]) for s in SCALARS[family]]
     rc = fn(int(n), *sc, *ptrs, *extra, _stream_ptr(stream))
     _lib.check(rc, fname)
-    del torch
 
 
 def primal(family, n, scalars, arrays, stream=None):

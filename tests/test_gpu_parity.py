@@ -325,3 +325,19 @@ def test_burgers_primal_matches_oracle(api, n, dtype):
     want = {k: v.copy() for k, v in g.items()}
     assert oracle.run_primal(name, n, scalars, want) == 0
     check_close(got["u"], want["u"], dtype, f"burgers2d n={n} primal")
+
+
+def test_short_buffers_are_rejected(api):
+    """A device array smaller than the grid is refused before any launch (the
+    reference raises on out-of-bounds access) and nothing is written."""
+    import torch
+    from paper_1907_02818_b200 import _lib
+    n = 24
+    arrays = {nm: torch.zeros((n, n, n), device="cuda")
+              for nm in api.array_params("wave3d_r4", "adjoint")}
+    arrays["u_1_b"] = torch.zeros((n - 1, n, n), device="cuda")
+    before = _lib.launch_count()
+    with pytest.raises(_lib.StencilError):
+        api.adjoint("wave3d_r4", n, {"D": 0.01}, arrays)
+    assert _lib.launch_count() == before
+    assert not arrays["c_b"].any()
