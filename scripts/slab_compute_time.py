@@ -1,0 +1,35 @@
+"""Per-rank compute of the z-slab adjoint step on ONE GPU (developer aid):
+the launches drivers.adjoint_step issues for an interior rank of an N-way
+decomposition (interior planes + two edge bands), halo exchange omitted, vs
+the single-GPU step / N.  Estimates the compute side of N-GPU efficiency."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_1907_02818_b200 import api, slab  # noqa: E402
+from scripts.quick_time import time_it  # noqa: E402
+
+fam, n = sys.argv[1] if len(sys.argv) > 1 else "wave3d_r4", int(sys.argv[2]) if len(sys.argv) > 2 else 768
+R = bench.RADIUS[fam]
+sc = {"D": 0.01} if fam == "wave3d_r4" else {"D": 0.1}
+full = bench.gen_inputs(api, torch, fam, n)
+t1 = time_it(lambda: api.adjoint(fam, n, sc, full))
+print(f"{fam} {n}^3 single GPU {t1:.3f} ms")
+for N in (2, 4, 8):
+    sl = slab.decompose(n, R, N, N // 2)
+    loc = bench.gen_inputs(api, torch, fam, n, sl)
+    lo_in, hi_in = sl.own0 + R, sl.own1 - R
+
+    def step():
+        api.adjoint_slab(fam, n, sc, loc, sl.base, sl.nplanes, lo_in, hi_in)
+        api.adjoint_slab(fam, n, sc, loc, sl.base, sl.nplanes, sl.own0, lo_in)
+        api.adjoint_slab(fam, n, sc, loc, sl.base, sl.nplanes, hi_in, sl.own1)
+
+    def whole():
+        api.adjoint_slab(fam, n, sc, loc, sl.base, sl.nplanes, sl.own0, sl.own1)
+    tn = time_it(step)
+    tw = time_it(whole)
+    print(f"  N={N}: rank {N // 2} owns {sl.own1 - sl.own0} planes: overlapped-form compute "
+          f"{tn:.3f} ms (eff {t1 / N / tn:.2f}), one launch {tw:.3f} ms (eff {t1 / N / tw:.2f})")
