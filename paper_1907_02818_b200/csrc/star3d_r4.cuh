@@ -540,12 +540,12 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_kernel(S
   star3_v7_body<MODE, INT, UBW>(SGB_V7_ARGS, tk, tj, D);
 }
 
-// Alternative launch (SGB_V7_UNIFIED=1): all tiles in row-major order in ONE
-// grid, each CTA running the body specialised for its tile, so frame and
-// interior neighbours stream the same planes concurrently and share halo rows
-// in L2.  1.2% faster than the split launch with the GPU at full clock, but
-// 1.5% slower in a sustained (power-capped, ~1.6 GHz) 200-step run, which is
-// what bench.py measures -- so the split launch stays the default.
+// One launch over all tiles in row-major order, each CTA running the body
+// specialised for its tile, so frame and interior neighbours stream the same
+// planes concurrently and share halo rows in L2.  Used for partial plane
+// ranges (z-slabs, edge bands); for the full grid it is 1.2% faster at full
+// clock but 1.5% slower in the sustained (power-capped) 200-step run
+// bench.py measures, so the full grid keeps the split launch.
 template <int MODE, bool UBW>
 __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_unified(SGB_V7_PARAMS) {
   const int tk = blockIdx.x % tm.tiles_k, tj = blockIdx.x / tm.tiles_k;
@@ -630,7 +630,13 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   };
   const auto ci = chunking("SGB_ICHUNKS", tm.n_interior());
   const auto cf = chunking("SGB_ICHUNKS_F", tm.n_frame());
-  if (ubwin && std::getenv("SGB_V7_UNIFIED")) {
+  // one launch for partial plane ranges (z-slabs, edge bands: measured 5-12%
+  // faster there, fewer CTA waves); two launches for the full grid (faster in
+  // the sustained single-GPU run); SGB_V7_UNIFIED / SGB_V7_SPLIT force either
+  const bool partial = out_i0 != 0 || out_i1 != g.n;
+  const bool unified = std::getenv("SGB_V7_UNIFIED") ||
+                       (partial && !std::getenv("SGB_V7_SPLIT"));
+  if (ubwin && unified) {
     const auto cu = chunking("SGB_ICHUNKS", (long long)tm.tiles_k * tm.tiles_j);
     star3_v7_unified<MODE, true>
         <<<dim3((unsigned)(tm.tiles_k * tm.tiles_j), cu.second), Tl::THREADS, Tl::SMEM, s>>>(
