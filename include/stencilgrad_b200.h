@@ -182,6 +182,12 @@ int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream);
  * A plan owns the device workspace so the call itself does not allocate. */
 typedef struct sgb_plan sgb_plan;
 sgb_plan* sgb_plan_create(const char* family, int n, int dtype_bytes);
+/* z-slab plan (multi-GPU host-buffer path): the host arrays hold local planes
+ * [i_base, i_base + nplanes) of the global n^3 grid; the call computes the
+ * gather adjoint of global output planes [out_i0, out_i1) (wave3d_r4 /
+ * wave3d_c, fp32), H2D / kernel / D2H pipelined over i-chunks */
+sgb_plan* sgb_plan_create_slab(const char* family, int n, int dtype_bytes, int i_base,
+                               int nplanes, int out_i0, int out_i1);
 void sgb_plan_destroy(sgb_plan* plan);
 /* arrays[] in the reference prototype order of <family>_b (host pointers) */
 int sgb_plan_run_adjoint_host(sgb_plan* plan, const double* scalars, void** arrays,

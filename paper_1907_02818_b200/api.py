@@ -198,10 +198,17 @@ def run_scatter_adjoint(family, n, scalars, grids, adjs, dtype="f64"):
 class Plan:
     """Device workspace for the host-buffer entry point (sgb_plan_*)."""
 
-    def __init__(self, family: str, n: int, dtype="f32"):
+    def __init__(self, family: str, n: int, dtype="f32", slab=None):
+        """slab: a slab.Slab (multi-GPU host-buffer path: host arrays hold the
+        local planes, outputs are the owned planes); None = the full grid."""
         self.family, self.n = family, n
         self.dtype_bytes = 4 if _sfx(dtype) == "f32" else 8
-        self._p = _lib.lib().sgb_plan_create(family.encode(), n, self.dtype_bytes)
+        if slab is None:
+            self._p = _lib.lib().sgb_plan_create(family.encode(), n, self.dtype_bytes)
+        else:
+            self._p = _lib.lib().sgb_plan_create_slab(family.encode(), n, self.dtype_bytes,
+                                                      slab.base, slab.nplanes, slab.own0,
+                                                      slab.own1)
         if not self._p:
             raise _lib.StencilError(_lib.lib().sgb_last_error().decode())
         self.names = array_params(family, "adjoint")

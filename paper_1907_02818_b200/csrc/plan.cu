@@ -17,6 +17,9 @@
 struct sgb_plan {
   std::string family;
   int n = 0, dtype = 0, dims = 0;
+  // z-slab: local planes [i_base, i_base + nplanes), outputs [out_i0, out_i1)
+  // (the full grid: 0, n, 0, n)
+  int i_base = 0, nplanes = 0, out_i0 = 0, out_i1 = 0;
   size_t bytes = 0;
   std::vector<void*> dev;
   std::vector<bool> rmw;  // accumulated adjoint arrays (copied back)
@@ -57,10 +60,20 @@ const FamSpec* find_fam(const std::string& f) {
 
 extern "C" {
 
-sgb_plan* sgb_plan_create(const char* family, int n, int dtype_bytes) {
+sgb_plan* sgb_plan_create_slab(const char* family, int n, int dtype_bytes, int i_base,
+                               int nplanes, int out_i0, int out_i1) {
   const FamSpec* fs = family ? find_fam(family) : nullptr;
   if (!fs || n <= 0 || (dtype_bytes != 4 && dtype_bytes != 8)) {
     sgb::set_error("sgb_plan_create: unsupported family/n/dtype");
+    return nullptr;
+  }
+  const bool full = i_base == 0 && nplanes == n && out_i0 == 0 && out_i1 == n;
+  const bool has_slab = std::string(family) == "wave3d_r4" || std::string(family) == "wave3d_c";
+  if (!full && (!has_slab || dtype_bytes != 4 || i_base < 0 || nplanes <= 0 ||
+                i_base + nplanes > n || out_i0 < i_base || out_i1 > i_base + nplanes ||
+                out_i0 >= out_i1)) {
+    sgb::set_error("sgb_plan_create_slab: slabs need wave3d_r4 / wave3d_c in fp32 and "
+                   "i_base <= out_i0 < out_i1 <= i_base + nplanes <= n");
     return nullptr;
   }
   auto* p = new sgb_plan;
@@ -68,8 +81,13 @@ sgb_plan* sgb_plan_create(const char* family, int n, int dtype_bytes) {
   p->n = n;
   p->dtype = dtype_bytes;
   p->dims = fs->dims;
+  p->i_base = i_base;
+  p->nplanes = nplanes;
+  p->out_i0 = out_i0;
+  p->out_i1 = out_i1;
   size_t elems = 1;
-  for (int d = 0; d < fs->dims; d++) elems *= (size_t)n;
+  for (int d = 0; d < fs->dims - 1; d++) elems *= (size_t)n;
+  elems *= (size_t)(fs->dims == 3 ? nplanes : n);
   p->bytes = elems * dtype_bytes;
   for (int a = 0; a < fs->narr; a++) {
     void* d = nullptr;
@@ -83,22 +101,27 @@ sgb_plan* sgb_plan_create(const char* family, int n, int dtype_bytes) {
     p->rmw.push_back(fs->rmw[a]);
   }
   if (fs->dims == 3 && p->dtype == 4) {
-    // pipelined host path: C i-chunks (at least 2R planes each); the call
-    // costs ~ H2D(all) + D2H(one chunk), so more chunks shorten the tail
-    int c = n >= 128 ? 32 : 1;
+    // pipelined host path: C chunks of the local planes (at least 2R planes
+    // each); the call costs ~ H2D(all) + D2H(one chunk), so more chunks
+    // shorten the tail
+    int c = nplanes >= 128 ? 32 : 1;
     if (const char* e = std::getenv("SGB_PLAN_CHUNKS")) c = std::max(1, std::atoi(e));
-    p->chunks = std::min(c, std::max(1, n / 16));
+    p->chunks = std::min(c, std::max(1, nplanes / 16));
     cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p->s_cmp, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
     p->ev_in.resize(p->chunks);
     p->ev_out.resize(p->chunks);
-    for (int c = 0; c < p->chunks; c++) {
-      cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&p->ev_out[c], cudaEventDisableTiming);
+    for (int k = 0; k < p->chunks; k++) {
+      cudaEventCreateWithFlags(&p->ev_in[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&p->ev_out[k], cudaEventDisableTiming);
     }
   }
   return p;
+}
+
+sgb_plan* sgb_plan_create(const char* family, int n, int dtype_bytes) {
+  return sgb_plan_create_slab(family, n, dtype_bytes, 0, n, 0, n);
 }
 
 void sgb_plan_destroy(sgb_plan* plan) {
@@ -113,14 +136,13 @@ void sgb_plan_destroy(sgb_plan* plan) {
 }
 
 // 3D fp32 families: H2D of chunk c+1 (copy engine), the slab adjoint of
-// chunk c (SMs) and D2H of chunk c-1 (other copy engine) overlap.  Output
-// planes [o_c, o_{c+1}) need input planes up to o_{c+1} + R - 1, so chunk c's
-// kernel waits for the H2D of chunks c and c+1.
+// chunk c (SMs) and D2H of chunk c-1 (other copy engine) overlap.  Local
+// planes are split into C chunks; the outputs inside chunk c need input planes
+// up to R beyond it, so chunk c's kernel waits for the H2D of chunks c and c+1.
 static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
-  const int n = p->n, C = p->chunks;
-  const int R = p->family == "wave3d_r4" ? 4 : 1;
+  const int n = p->n, C = p->chunks, L = p->nplanes, base = p->i_base;
   const size_t plane = (size_t)n * n * 4;
-  auto bound = [&](int c) { return (int)((long long)n * c / C); };
+  auto bound = [&](int c) { return (int)((long long)L * c / C); };  // local plane
   const size_t na = p->dev.size();
   for (int c = 0; c < C; c++) {
     const int a = bound(c), b = bound(c + 1);
@@ -134,27 +156,32 @@ static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
     cudaEventRecord(p->ev_in[c], p->s_h2d);
   }
   for (int c = 0; c < C; c++) {
-    const int a = bound(c), b = bound(c + 1);
+    // output planes of this chunk (global indices)
+    const int a = std::max(p->out_i0, base + bound(c));
+    const int b = std::min(p->out_i1, base + bound(c + 1));
     cudaStreamWaitEvent(p->s_cmp, p->ev_in[c], 0);
     if (c + 1 < C) cudaStreamWaitEvent(p->s_cmp, p->ev_in[c + 1], 0);
-    (void)R;
-    float** d = reinterpret_cast<float**>(p->dev.data());
-    int rc;
-    if (p->family == "wave3d_r4")
-      rc = wave3d_r4_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], 0, n, a, b,
-                                p->s_cmp);
-    else if (p->family == "wave3d_c")
-      rc = wave3d_c_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], 0, n, a, b,
-                               p->s_cmp);
-    else
-      return SGB_EINVAL;
-    if (rc != 0) return rc;
+    if (a < b) {
+      float** d = reinterpret_cast<float**>(p->dev.data());
+      int rc;
+      if (p->family == "wave3d_r4")
+        rc = wave3d_r4_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L, a, b,
+                                  p->s_cmp);
+      else if (p->family == "wave3d_c")
+        rc = wave3d_c_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], base, L, a,
+                                 b, p->s_cmp);
+      else
+        return SGB_EINVAL;
+      if (rc != 0) return rc;
+    }
     cudaEventRecord(p->ev_out[c], p->s_cmp);
     cudaStreamWaitEvent(p->s_d2h, p->ev_out[c], 0);
+    if (a >= b) continue;
+    const size_t off = (size_t)(a - base) * plane, len = (size_t)(b - a) * plane;
     for (size_t k = 0; k < na; k++) {
       if (!p->rmw[k]) continue;
-      if (cudaMemcpyAsync((char*)arrays[k] + a * plane, (const char*)p->dev[k] + a * plane,
-                          (b - a) * plane, cudaMemcpyDeviceToHost, p->s_d2h) != cudaSuccess) {
+      if (cudaMemcpyAsync((char*)arrays[k] + off, (const char*)p->dev[k] + off, len,
+                          cudaMemcpyDeviceToHost, p->s_d2h) != cudaSuccess) {
         sgb::set_error("sgb_plan_run_adjoint_host: D2H copy failed");
         return -1;
       }
@@ -173,7 +200,7 @@ int sgb_plan_run_adjoint_host(sgb_plan* p, const double* scalars, void** arrays,
     sgb::set_error("sgb_plan_run_adjoint_host: null argument");
     return SGB_EINVAL;
   }
-  if (p->chunks > 1 && (p->family == "wave3d_r4" || p->family == "wave3d_c")) {
+  if (p->s_cmp && (p->family == "wave3d_r4" || p->family == "wave3d_c")) {
     for (size_t a = 0; a < p->dev.size(); a++)
       if (!arrays[a]) {
         sgb::set_error("sgb_plan_run_adjoint_host: null host array");

@@ -342,3 +342,30 @@ def test_short_buffers_are_rejected(api):
         api.adjoint("wave3d_r4", n, {"D": 0.01}, arrays)
     assert _lib.launch_count() == before
     assert not arrays["c_b"].any()
+
+
+@pytest.mark.parametrize("name,n,nslabs", [("wave3d_r4", 136, 3), ("wave3d_r4", 68, 2),
+                                           ("wave3d_c", 128, 4)])
+def test_slab_plans_reassemble_full_plan(api, name, n, nslabs):
+    """sgb_plan_create_slab: each rank's host-buffer call on its local planes
+    (owned + halos) returns the owned planes of the full-grid plan bit for bit."""
+    from paper_1907_02818_b200 import slab
+    scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 2, accumulate=True)
+    host = {k: np.ascontiguousarray(v.astype(np.float32)) for k, v in {**grids, **adjs}.items()}
+    names = api.array_params(name, "adjoint")
+    full = {k: host[k].copy() for k in names}
+    plan = api.Plan(name, n, "f32")
+    plan.run_adjoint_host(scalars, full)
+    plan.close()
+    R = 4 if name == "wave3d_r4" else 1
+    f = oracle.family(name)
+    for rank in range(nslabs):
+        sl = slab.decompose(n, R, nslabs, rank)
+        loc = {k: np.ascontiguousarray(host[k][sl.base:sl.base + sl.nplanes]) for k in names}
+        p = api.Plan(name, n, "f32", slab=sl)
+        p.run_adjoint_host(scalars, loc)
+        p.close()
+        a, b = sl.own0 - sl.base, sl.own1 - sl.base
+        for k in names:
+            if k in adjs and k != f.seed:
+                assert np.array_equal(loc[k][a:b], full[k][sl.own0:sl.own1]), (rank, k)
