@@ -93,9 +93,15 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
   }
   // plane-streaming kernel for radius 4 (measured: fp64 768^3 29 -> ~12 ms);
   // radius 1 keeps the per-point kernel (measured faster there)
-  if (MODE == 2 && !std::getenv("SGB_GENERIC_POINT") && n <= 46340)
+  if (MODE == 2 && !std::getenv("SGB_GENERIC_POINT") && n <= 46340) {
+    if (!std::getenv("SGB_PLANE_NO_TMA")) {
+      const int rc = star3_plane_tma_gather<MODE, T>(g, lo, hi, out_i0, out_i1, (T)D, c, c_b,
+                                                     u_1, u_1_b, u_2_b, u_b, s, name);
+      if (rc != 1) return rc;
+    }
     return star3_plane_gather<MODE, T>(g, lo, hi, out_i0, out_i1, (T)D, c, c_b, u_1, u_1_b,
                                        u_2_b, u_b, s, name);
+  }
   dim3 b(32, 4), gr((unsigned)((n + 31) / 32), (unsigned)((n + 3) / 4),
                     (unsigned)(out_i1 - out_i0));
   star3_gather_kernel<MODE, T>

@@ -369,3 +369,21 @@ def test_slab_plans_reassemble_full_plan(api, name, n, nslabs):
         for k in names:
             if k in adjs and k != f.seed:
                 assert np.array_equal(loc[k][a:b], full[k][sl.own0:sl.own1]), (rank, k)
+
+
+@pytest.mark.parametrize("n", [24, 40, 68, 97])
+def test_plane_kernels_tma_equals_plain_fp64(api, n, monkeypatch):
+    """fp64 radius-4 gather: the TMA-fed plane kernel (even n) and the
+    plain-load plane kernel apply the same arithmetic per point (bitwise
+    equal); both match the oracle at 1e-12.  Odd n takes the plain kernel."""
+    name = "wave3d_r4"
+    scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 9, accumulate=True)
+    base = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
+    want = oracle_gather(name, n, scalars, grids, adjs)
+    for adj in ("c_b", "u_1_b"):
+        check_close(base[adj], want[adj], "f64", f"n={n} {adj}")
+    with monkeypatch.context() as m:
+        m.setenv("SGB_PLANE_NO_TMA", "1")
+        plain = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
+    for adj in ("c_b", "u_1_b"):
+        assert np.array_equal(plain[adj], base[adj]), adj
