@@ -1,3 +1,4 @@
+"""Scratch timing of the fp64 3D gather adjoints at full size (developer aid)."""
 import sys, torch
 sys.path.insert(0, ".")
 from paper_1907_02818_b200 import api

@@ -1,3 +1,5 @@
+"""One host-API gather adjoint call on oracle-style inputs (developer aid):
+    python scripts/one_call.py <family> <n>"""
 import sys
 import numpy as np
 sys.path.insert(0, ".")

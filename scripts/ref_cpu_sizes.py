@@ -1,3 +1,5 @@
+"""The reference CPU gather (oracle/_ref) timed at several cube sizes on the
+host cores (developer aid; shows its time per point falling with n)."""
 import os, sys, time
 sys.path.insert(0, ".")
 import bench

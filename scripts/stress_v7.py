@@ -1,3 +1,6 @@
+"""Repeat the radius-4 gather many times on the same inputs and count runs that
+differ from the first (developer aid for races):
+    python scripts/stress_v7.py wave3d_r4 <n> <reps>"""
 import os, sys
 import numpy as np
 sys.path.insert(0, ".")
