@@ -173,6 +173,12 @@ int sgb_box_axpy_f32(float* y, const float* x, double alpha, int n, int lo, int 
                      int nplanes, sgb_stream_t stream);
 int sgb_box_axpy_f64(double* y, const double* x, double alpha, int n, int lo, int hi,
                      int i_base, int nplanes, sgb_stream_t stream);
+/* y = alpha x on the box, 0 elsewhere (a zeroed y followed by box_axpy, in one
+ * pass) on local planes [i_base, i_base+nplanes) */
+int sgb_box_set_f32(float* y, const float* x, double alpha, int n, int lo, int hi, int i_base,
+                    int nplanes, sgb_stream_t stream);
+int sgb_box_set_f64(double* y, const double* x, double alpha, int n, int lo, int hi, int i_base,
+                    int nplanes, sgb_stream_t stream);
 /* one interior pass of the 5-point average u <- (u + 4 neighbours)/5 (2D) */
 int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream);
 

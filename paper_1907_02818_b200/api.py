@@ -155,6 +155,16 @@ def box_axpy(y, x, alpha: float, n: int, lo: int, hi: int, i_base: int = 0,
                "box_axpy")
 
 
+def box_set(y, x, alpha: float, n: int, lo: int, hi: int, i_base: int = 0,
+            nplanes: int | None = None, stream=None):
+    """y = alpha * x on the box B = [lo, hi]^3, 0 elsewhere (3D grids)."""
+    import torch
+    fn = _lib.lib().sgb_box_set_f32 if y.dtype == torch.float32 else _lib.lib().sgb_box_set_f64
+    _lib.check(fn(ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(x.data_ptr()), float(alpha), n,
+                  lo, hi, i_base, n if nplanes is None else nplanes, _stream_ptr(stream)),
+               "box_set")
+
+
 def smooth5(src, dst, n: int, stream=None):
     _lib.check(_lib.lib().sgb_smooth5_f64(ctypes.c_void_p(src.data_ptr()),
                                           ctypes.c_void_p(dst.data_ptr()), n,

@@ -154,29 +154,48 @@ def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None):
     fam = "wave3d_r4"
     K = checkpoint_every or max(1, int(math.isqrt(T)))
     lo, hi = 4, n - 5
+    # state buffers: the primal writes only the box, so a buffer this driver
+    # allocated (zero outside the box) can be reused without re-zeroing; the
+    # caller's u0 / u1 are read, never written or recycled
+    pool = []
+    owned = set()
+
+    def fresh():
+        if pool:
+            return pool.pop()
+        t = torch.zeros_like(u1)
+        owned.add(id(t))
+        return t
+
+    def release(t, keep):
+        if id(t) in owned and not any(t is k for k in keep):
+            pool.append(t)
+
     # forward sweep keeping only the checkpoint pairs (u^{s-1}, u^s) at
-    # s = 1, 1+K, 1+2K, ... (s < T)
-    ckpt = {1: (u0.clone(), u1.clone())}
+    # s = 1, 1+K, 1+2K, ... (s < T), by reference (they are never written)
+    ckpt = {1: (u0, u1)}
     prev, cur = u0, u1
     for t in range(1, T):
-        nxt = torch.zeros_like(cur)
+        nxt = fresh()
         api.primal(fam, n, {"D": D}, {"c": c, "u_1": cur, "u_2": prev, "u": nxt})
+        release(prev, [x for pair in ckpt.values() for x in pair])
         prev, cur = cur, nxt
         s = t + 1
         if (s - 1) % K == 0 and s < T:
-            ckpt[s] = (prev.clone(), cur.clone())
+            ckpt[s] = (prev, cur)
     recomputed = 0
     # reverse sweep
     ub_next = w.clone()                  # u-bar^{t+1}
     ub_cur = torch.zeros_like(w)         # u-bar^t
-    ub_prev = torch.zeros_like(w)        # u-bar^{t-1}
+    ub_prev = torch.zeros_like(w)        # u-bar^{t-1} (fully overwritten each step)
     c_b = torch.zeros_like(c)
     starts = sorted(ckpt)
+    keep = [x for pair in ckpt.values() for x in pair]
     for s in reversed(starts):
         t_end = min(s + K, T)            # segment steps t = s .. t_end-1
         states = {s - 1: ckpt[s][0], s: ckpt[s][1]}
         for t in range(s, t_end - 1):    # recompute u^{s+1} .. u^{t_end-1}
-            nxt = torch.zeros_like(w)
+            nxt = fresh()
             api.primal(fam, n, {"D": D}, {"c": c, "u_1": states[t], "u_2": states[t - 1],
                                           "u": nxt})
             states[t + 1] = nxt
@@ -184,9 +203,11 @@ def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None):
         for t in reversed(range(s, t_end)):
             api.adjoint(fam, n, {"D": D}, {"c": c, "c_b": c_b, "u_1": states[t],
                                            "u_1_b": ub_cur, "u_b": ub_next})
-            api.box_axpy(ub_prev, ub_next, -1.0, n, lo, hi)
+            # u-bar^{t-1} = -u-bar^{t+1} on B (the u_2 partial), 0 elsewhere
+            api.box_set(ub_prev, ub_next, -1.0, n, lo, hi)
             ub_next, ub_cur, ub_prev = ub_cur, ub_prev, ub_next
-            ub_prev.zero_()
+        for t, st in states.items():
+            release(st, keep)
     # after the loop: ub_next = u-bar^1, ub_cur = u-bar^0
     stats = {"checkpoint_every": K, "checkpoints": len(starts), "recomputed_steps": recomputed,
              "adjoint_steps": T - 1}
