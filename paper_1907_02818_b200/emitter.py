@@ -436,6 +436,10 @@ class EmittedProblem:
             ext.append(e)
         return ext
 
+    def _unroll(self):
+        import os
+        return max(1, int(os.environ.get("SGB_EMIT_UNROLL", "2"))) if self.d >= 3 else 1
+
     def gather_source(self, index="long long"):
         """Fused predicated gather.  Threads map to (.., j, k) = (z, y, x) of a
         3D launch with grid-stride outer loops (no div/mod); per target array
@@ -471,9 +475,16 @@ class EmittedProblem:
                          f"y{d - 2} < W{d - 2}; y{d - 2} += gridDim.y * (I)blockDim.y) {{")
             depth += 1
         if d >= 3:
-            lines.append(f"  for (I y{d - 3} = blockIdx.z * (I)blockDim.z + threadIdx.z; "
-                         f"y{d - 3} < W{d - 3}; y{d - 3} += gridDim.z * (I)blockDim.z) {{")
-            depth += 1
+            # UF consecutive outer-dimension points per thread, unrolled, so
+            # their independent load streams overlap (memory-level parallelism)
+            uf = self._unroll()
+            lines.append(f"  for (I yb = (blockIdx.z * (I)blockDim.z + threadIdx.z) * {uf}; "
+                         f"yb < W{d - 3}; yb += gridDim.z * (I)blockDim.z * {uf}) {{")
+            lines.append("#pragma unroll")
+            lines.append(f"  for (int uu = 0; uu < {uf}; uu++) {{")
+            lines.append(f"  const I y{d - 3} = yb + uu;")
+            lines.append(f"  if (y{d - 3} < W{d - 3}) {{")
+            depth += 3
         # group terms by target adjoint, ascending term order inside each
         targets = []
         for t in self.terms:
@@ -702,7 +713,7 @@ class EmittedProblem:
         by = 8 if self.d > 1 else 1
         gx = (W[-1] + bx - 1) // bx
         gy = min((W[-2] + by - 1) // by, 65535) if self.d >= 2 else 1
-        gz = min(W[0], 65535) if self.d >= 3 else 1
+        gz = min((W[0] + self._unroll() - 1) // self._unroll(), 65535) if self.d >= 3 else 1
         if gx > 2 ** 31 - 1:
             raise _lib.StencilError("grid too large")
         self._launch("gather", sizes, scalars, arrays, 0, stream,
