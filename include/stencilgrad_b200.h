@@ -138,6 +138,24 @@ int wave3d_r4_scatter_b_f64(int n, double D, double* c, double* c_b, double* u_1
 int wave3d_r4_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
                          float* u_b, int i_base, int nplanes, int out_i0, int out_i1,
                          sgb_stream_t stream);
+/* Fused halo exchange: the same z-slab adjoint, but the local arrays hold
+ * exactly the planes [i_base, i_base + nplanes) and every input plane below /
+ * above them is read straight from the lower / upper neighbour's arrays
+ * (lo_* / hi_*, holding global planes [lo_base, lo_base + lo_nplanes) /
+ * [hi_base, ...); NULL at a grid end) by the kernel's own TMA loads -- peer
+ * memory over NVLink when the pointers come from sgb_ipc_open, no separate
+ * send/recv.  The neighbours' planes must be final before the call. */
+int wave3d_r4_b_slab_peer_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                              float* u_b, int i_base, int nplanes, int out_i0, int out_i1,
+                              const float* lo_c, const float* lo_u_1, const float* lo_u_b,
+                              int lo_base, int lo_nplanes, const float* hi_c,
+                              const float* hi_u_1, const float* hi_u_b, int hi_base,
+                              int hi_nplanes, sgb_stream_t stream);
+/* CUDA IPC for the fused path: a 64-byte handle (+ byte offset) of the device
+ * allocation holding ptr; open maps a peer's allocation into this process */
+int sgb_ipc_handle(const void* ptr, void* handle64, long long* offset);
+int sgb_ipc_open(const void* handle64, long long offset, void** ptr);
+int sgb_ipc_close(void* ptr, long long offset);
 int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
                         float* u_2_b, float* u_b, int i_base, int nplanes, int out_i0,
                         int out_i1, sgb_stream_t stream);

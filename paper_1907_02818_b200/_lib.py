@@ -30,6 +30,9 @@ _CTYPES = {
     "const double*": ctypes.c_void_p,
     "const float*": ctypes.c_void_p,
     "void**": ctypes.c_void_p,
+    "void*": ctypes.c_void_p,
+    "const void*": ctypes.c_void_p,
+    "long long*": ctypes.c_void_p,
     "const char*": ctypes.c_char_p,
     "sgb_plan*": ctypes.c_void_p,
     "sgb_jit_kernel*": ctypes.c_void_p,

@@ -297,6 +297,71 @@ int wave3d_r4_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, floa
                                 i_base, nplanes, out_i0, out_i1, as_stream(stream));
 }
 
+int wave3d_r4_b_slab_peer_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                              float* u_b, int i_base, int nplanes, int out_i0, int out_i1,
+                              const float* lo_c, const float* lo_u_1, const float* lo_u_b,
+                              int lo_base, int lo_nplanes, const float* hi_c,
+                              const float* hi_u_1, const float* hi_u_b, int hi_base,
+                              int hi_nplanes, sgb_stream_t stream) {
+  const char* name = "wave3d_r4_b_slab_peer";
+  if (n <= 0 || nplanes <= 0) return einval(std::string(name) + ": bad sizes");
+  if (!guard_ok(WAVE3D_R4, n)) return SGB_GUARD;
+  if (!c || !c_b || !u_1 || !u_1_b || !u_b) return einval(std::string(name) + ": null array");
+  if (!star3_tma_supported<2, float>(n))
+    return einval(std::string(name) + ": needs n % 4 == 0 (TMA rows)");
+  if (out_i1 == out_i0) return 0;
+  const float* nc[2] = {lo_c, hi_c};
+  const float* nu1[2] = {lo_u_1, hi_u_1};
+  const float* nub[2] = {lo_u_b, hi_u_b};
+  const int nb[2] = {lo_base, hi_base}, nn[2] = {lo_nplanes, hi_nplanes};
+  return star3_v7_gather_peer<2>(Slab3{n, i_base, nplanes}, 4, n - 5, out_i0, out_i1, (float)D,
+                                 c, c_b, u_1, u_1_b, u_b, nc, nu1, nub, nb, nn,
+                                 as_stream(stream), name);
+}
+
+int sgb_ipc_handle(const void* ptr, void* handle64, long long* offset) {
+  if (!ptr || !handle64 || !offset) return SGB_EINVAL;
+  // allocation base of ptr (driver entry point, so the library keeps no hard
+  // dependency on libcuda)
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      get_range = reinterpret_cast<GetRange>(f);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (!get_range || get_range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+    return einval("sgb_ipc_handle: not a device allocation");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+  if (e != cudaSuccess) return -static_cast<int>(e);
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = (long long)((CUdeviceptr)ptr - base);
+  return 0;
+}
+
+int sgb_ipc_open(const void* handle64, long long offset, void** ptr) {
+  if (!handle64 || !ptr) return SGB_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  const cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return -static_cast<int>(e);
+  *ptr = (char*)base + offset;
+  return 0;
+}
+
+int sgb_ipc_close(void* ptr, long long offset) {
+  if (!ptr) return SGB_EINVAL;
+  const cudaError_t e = cudaIpcCloseMemHandle((char*)ptr - offset);
+  return e == cudaSuccess ? 0 : -static_cast<int>(e);
+}
+
 int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
                         float* u_2_b, float* u_b, int i_base, int nplanes, int out_i0,
                         int out_i1, sgb_stream_t stream) {

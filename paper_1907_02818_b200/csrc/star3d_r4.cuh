@@ -5,6 +5,7 @@
 // measurements and the path from the earlier versions: DESIGN.md ("Radius-4
 // streaming kernel") and profiles/.
 #pragma once
+#include <cstring>
 #include <mutex>
 #include <utility>
 
@@ -258,12 +259,24 @@ struct TileMap {
   }
 };
 
+// Halo planes read straight from the neighbouring ranks' arrays (fused
+// exchange: peer memory over NVLink via CUDA IPC, or any device-visible
+// pointer): input planes below the local planes come from the lower
+// neighbour's maps, above them from the upper neighbour's.
+struct PeerHalo {
+  CUtensorMap c[2], ub[2], u1[2];  // [0] lower neighbour, [1] upper neighbour
+  int base[2];                     // global plane of the neighbour's array plane 0
+  int has[2];
+  int own0, own1;                  // planes held locally (global)
+};
+
 template <int MODE, bool INT, bool UBW>
 __device__ __forceinline__ void star3_v7_body(
     const CUtensorMap& tm_c, const CUtensorMap& tm_ub, const CUtensorMap& tm_u1,
     const CUtensorMap& tm_cb, const CUtensorMap& tm_u1b, const CUtensorMap& tm_u2b,
     float* __restrict__ c_b, float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n,
-    int i_base, int lo, int hi, int out_i0, int out_i1, int chunk, int tk, int tj, float D) {
+    int i_base, int lo, int hi, int out_i0, int out_i1, int chunk, int tk, int tj, float D,
+    const PeerHalo* peer = nullptr) {
   using Tl = StarTile7<MODE>;
   using S3 = Star3<MODE>;
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
@@ -309,9 +322,20 @@ __device__ __forceinline__ void star3_v7_body(
     const bool u2 = S3::kU2 && p >= o_begin && p < o_end;
     tma::mbar_arrive_expect_tx(&bars[s], 3 * Tl::BOX_BYTES +
                                              ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE * 4);
-    tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
-    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK - ulo, j0 - HJ - ulo, pl);
-    tma::load_3d(dst + 2 * BF, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
+    const CUtensorMap *mc = &tm_c, *mub = &tm_ub, *mu1 = &tm_u1;
+    int pin = pl;
+    if (peer) {  // uniform per plane: which array holds input plane p
+      const int side = p < peer->own0 ? 0 : (p >= peer->own1 ? 1 : -1);
+      if (side >= 0 && peer->has[side]) {
+        mc = &peer->c[side];
+        mub = &peer->ub[side];
+        mu1 = &peer->u1[side];
+        pin = p - peer->base[side];
+      }
+    }
+    tma::load_3d(dst + 0 * BF, mc, &bars[s], k0 - HK, j0 - HJ, pin);
+    tma::load_3d(dst + 1 * BF, mub, &bars[s], k0 - HK - ulo, j0 - HJ - ulo, pin);
+    tma::load_3d(dst + 2 * BF, mu1, &bars[s], k0 - HK, j0 - HJ, pin);
     if (emit) {
       tma::load_3d(dst + 3 * BF, &tm_cb, &bars[s], k0, j0, pl - R);
       tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
@@ -555,11 +579,22 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_unified(
     star3_v7_body<MODE, false, UBW>(SGB_V7_ARGS, tk, tj, D);
 }
 
+// The same, with the halo planes read from the neighbours' arrays.
+template <int MODE, bool UBW>
+__global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
+    star3_v7_unified_peer(SGB_V7_PARAMS, const __grid_constant__ PeerHalo peer) {
+  const int tk = blockIdx.x % tm.tiles_k, tj = blockIdx.x / tm.tiles_k;
+  if (tk >= tm.ik0 && tk < tm.ik1 && tj >= tm.ij0 && tj < tm.ij1)
+    star3_v7_body<MODE, true, UBW>(SGB_V7_ARGS, tk, tj, D, &peer);
+  else
+    star3_v7_body<MODE, false, UBW>(SGB_V7_ARGS, tk, tj, D, &peer);
+}
+
 template <int MODE>
 inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
                            long long out_i1, float D, const float* c, float* c_b,
                            const float* u_1, float* u_1_b, float* u_2_b, const float* u_b,
-                           cudaStream_t s, const char* name) {
+                           cudaStream_t s, const char* name, const PeerHalo* peer = nullptr) {
   using Tl = StarTile7<MODE>;
   CUtensorMap maps[6];
   int rc = 0;
@@ -587,6 +622,8 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     for (const void* k : ks)
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
     cudaFuncSetAttribute((const void*)star3_v7_unified<MODE, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
+    cudaFuncSetAttribute((const void*)star3_v7_unified_peer<MODE, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
     attr_set = true;
   }
@@ -633,6 +670,18 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   // one launch for partial plane ranges (z-slabs, edge bands: measured 5-12%
   // faster there, fewer CTA waves); two launches for the full grid (faster in
   // the sustained single-GPU run); SGB_V7_UNIFIED / SGB_V7_SPLIT force either
+  if (peer) {  // fused halo: one launch, halo planes from the neighbours' arrays
+    if (!ubwin) {
+      set_error(std::string(name) + ": peer halo path needs 16-byte aligned arrays");
+      return SGB_EINVAL;
+    }
+    const auto cu = chunking("SGB_ICHUNKS", (long long)tm.tiles_k * tm.tiles_j);
+    star3_v7_unified_peer<MODE, true>
+        <<<dim3((unsigned)(tm.tiles_k * tm.tiles_j), cu.second), Tl::THREADS, Tl::SMEM, s>>>(
+            maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cu.first, tm, D, *peer);
+    return launch_status(name);
+  }
   const bool partial = out_i0 != 0 || out_i1 != g.n;
   const bool unified = std::getenv("SGB_V7_UNIFIED") ||
                        (partial && !std::getenv("SGB_V7_SPLIT"));
@@ -675,5 +724,53 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   return 0;
 }
 
+
+// Local arrays hold exactly the global planes [g.i_base, g.i_base + g.nplanes);
+// neighbour side k (0 lower, 1 upper) holds planes [nb_base[k], nb_base[k] +
+// nb_np[k]) of arrays nb_c / nb_u1 / nb_ub (nullptr: no neighbour, grid end).
+template <int MODE>
+inline int star3_v7_gather_peer(const Slab3& g, long long lo, long long hi, long long out_i0,
+                                long long out_i1, float D, const float* c, float* c_b,
+                                const float* u_1, float* u_1_b, const float* u_b,
+                                const float* const nb_c[2], const float* const nb_u1[2],
+                                const float* const nb_ub[2], const int nb_base[2],
+                                const int nb_np[2], cudaStream_t s, const char* name) {
+  using Tl = StarTile7<MODE>;
+  constexpr int R = Tl::R;
+  PeerHalo ph;
+  std::memset(&ph, 0, sizeof(ph));
+  ph.own0 = (int)g.i_base;
+  ph.own1 = (int)(g.i_base + g.nplanes);
+  for (int k = 0; k < 2; k++) {
+    if (!nb_c[k]) continue;
+    if (!nb_u1[k] || !nb_ub[k] || nb_np[k] <= 0) return SGB_EINVAL;
+    ph.has[k] = 1;
+    ph.base[k] = nb_base[k];
+    int rc = encode_3d(&ph.c[k], nb_c[k], g.n, nb_np[k], Tl::BW, Tl::BJ, name);
+    rc |= encode_3d(&ph.u1[k], nb_u1[k], g.n, nb_np[k], Tl::BW, Tl::BJ, name);
+    const int w = encode_3d_window(&ph.ub[k], nb_ub[k], g.n, nb_np[k], lo, hi - lo + 1, Tl::BW,
+                                   Tl::BJ, name);
+    if (rc || w != 0) {
+      set_error(std::string(name) + ": peer maps (16-byte aligned neighbour arrays needed)");
+      return SGB_EINVAL;
+    }
+  }
+  // every input plane the outputs need must be held locally or by a neighbour
+  const long long need_lo = std::max<long long>(0, out_i0 - R);
+  const long long need_hi = std::min<long long>(g.n - 1, out_i1 - 1 + R);
+  for (long long p = need_lo; p <= need_hi; p++) {
+    const bool local = p >= ph.own0 && p < ph.own1;
+    const bool low = ph.has[0] && p < ph.own0 && p >= ph.base[0] && p < ph.base[0] + nb_np[0];
+    const bool up = ph.has[1] && p >= ph.own1 && p >= ph.base[1] && p < ph.base[1] + nb_np[1];
+    if (!local && !low && !up) {
+      set_error(std::string(name) + ": input plane " + std::to_string(p) +
+                " held by no rank (local + neighbours must cover the R halo)");
+      return SGB_EINVAL;
+    }
+  }
+  if (out_i0 < ph.own0 || out_i1 > ph.own1) return SGB_EINVAL;
+  return star3_v7_gather<MODE>(g, lo, hi, out_i0, out_i1, D, c, c_b, u_1, u_1_b, nullptr, u_b, s,
+                               name, &ph);
+}
 
 }  // namespace sgb

@@ -43,11 +43,19 @@ def regen_seed(u_b, n, t, seed, sl=None):
     api.fill_normal3d(u_b, n, 0, seed, 1001 + 2 * t, base, npl)
 
 
-def adjoint_step(family, n, scalars, arrays, sl=None, exchange=("u_1", "u_b"), overlap=True):
+def adjoint_step(family, n, scalars, arrays, sl=None, exchange=("u_1", "u_b"), overlap=True,
+                 link=None):
     """One gather-adjoint step; with a slab, halos of `exchange` are refreshed
-    first -- overlapped with the interior planes when `overlap`."""
+    first -- overlapped with the interior planes when `overlap` -- or, with a
+    peer `link` (peer.try_connect), read by the kernel straight from the
+    neighbours' arrays after a stream-ordered cross-rank sync."""
     if sl is None:
         api.adjoint(family, n, scalars, arrays)
+        return 1
+    if link is not None:
+        from . import peer
+        peer.step_sync()
+        peer.adjoint(n, scalars, arrays, link)
         return 1
     R = sl.radius
     lo_in, hi_in = sl.own0 + (R if sl.rank > 0 else 0), sl.own1 - (R if sl.rank < sl.world - 1 else 0)
