@@ -270,6 +270,39 @@ struct PeerHalo {
   int own0, own1;                  // planes held locally (global)
 };
 
+// One plane's TMA issue (elected thread): the c / u_b / u_1 halo boxes of
+// input plane p -- from the neighbour's arrays when p lies outside the local
+// planes and a PeerHalo is given -- and the c_b / u_1_b (/ u_2_b) tiles.  Kept
+// out of line: it runs once per plane in one thread, and inlining it into
+// every unrolled plane of both tile bodies costs instruction-cache misses.
+__device__ __noinline__ void v7_issue(float* dst, uint64_t* bar, const CUtensorMap* tm_c,
+                                      const CUtensorMap* tm_ub, const CUtensorMap* tm_u1,
+                                      const CUtensorMap* tm_cb, const CUtensorMap* tm_u1b,
+                                      const CUtensorMap* tm_u2b, const PeerHalo* peer, int p,
+                                      int pl, int k0, int j0, int HK, int HJ, int ulo, int R,
+                                      int BF, int TILE, int box_bytes, bool emit, bool u2) {
+  tma::mbar_arrive_expect_tx(bar, 3 * box_bytes + ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE * 4);
+  const CUtensorMap *mc = tm_c, *mub = tm_ub, *mu1 = tm_u1;
+  int pin = pl;
+  if (peer) {  // uniform per plane: which array holds input plane p
+    const int side = p < peer->own0 ? 0 : (p >= peer->own1 ? 1 : -1);
+    if (side >= 0 && peer->has[side]) {
+      mc = &peer->c[side];
+      mub = &peer->ub[side];
+      mu1 = &peer->u1[side];
+      pin = p - peer->base[side];
+    }
+  }
+  tma::load_3d(dst + 0 * BF, mc, bar, k0 - HK, j0 - HJ, pin);
+  tma::load_3d(dst + 1 * BF, mub, bar, k0 - HK - ulo, j0 - HJ - ulo, pin);
+  tma::load_3d(dst + 2 * BF, mu1, bar, k0 - HK, j0 - HJ, pin);
+  if (emit) {
+    tma::load_3d(dst + 3 * BF, tm_cb, bar, k0, j0, pl - R);
+    tma::load_3d(dst + 3 * BF + TILE, tm_u1b, bar, k0, j0, pl - R);
+  }
+  if (u2) tma::load_3d(dst + 3 * BF + 2 * TILE, tm_u2b, bar, k0, j0, pl);
+}
+
 template <int MODE, bool INT, bool UBW>
 __device__ __forceinline__ void star3_v7_body(
     const CUtensorMap& tm_c, const CUtensorMap& tm_ub, const CUtensorMap& tm_u1,
@@ -320,22 +353,16 @@ __device__ __forceinline__ void star3_v7_body(
     const int pl = p - i_base;
     const bool emit = it >= 2 * R;
     const bool u2 = S3::kU2 && p >= o_begin && p < o_end;
+    if (peer) {  // fused-halo launches only (out of line: I-cache, see v7_issue)
+      v7_issue(dst, &bars[s], &tm_c, &tm_ub, &tm_u1, &tm_cb, &tm_u1b, &tm_u2b, peer, p, pl, k0,
+               j0, HK, HJ, ulo, R, BF, TILE, Tl::BOX_BYTES, emit, u2);
+      return;
+    }
     tma::mbar_arrive_expect_tx(&bars[s], 3 * Tl::BOX_BYTES +
                                              ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE * 4);
-    const CUtensorMap *mc = &tm_c, *mub = &tm_ub, *mu1 = &tm_u1;
-    int pin = pl;
-    if (peer) {  // uniform per plane: which array holds input plane p
-      const int side = p < peer->own0 ? 0 : (p >= peer->own1 ? 1 : -1);
-      if (side >= 0 && peer->has[side]) {
-        mc = &peer->c[side];
-        mub = &peer->ub[side];
-        mu1 = &peer->u1[side];
-        pin = p - peer->base[side];
-      }
-    }
-    tma::load_3d(dst + 0 * BF, mc, &bars[s], k0 - HK, j0 - HJ, pin);
-    tma::load_3d(dst + 1 * BF, mub, &bars[s], k0 - HK - ulo, j0 - HJ - ulo, pin);
-    tma::load_3d(dst + 2 * BF, mu1, &bars[s], k0 - HK, j0 - HJ, pin);
+    tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK - ulo, j0 - HJ - ulo, pl);
+    tma::load_3d(dst + 2 * BF, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
     if (emit) {
       tma::load_3d(dst + 3 * BF, &tm_cb, &bars[s], k0, j0, pl - R);
       tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);

@@ -9,7 +9,13 @@ import torch
 sys.path.insert(0, ".")
 import bench  # noqa: E402
 from paper_1907_02818_b200 import api, slab  # noqa: E402
-from scripts.quick_time import time_it  # noqa: E402
+from scripts.quick_time import time_it as _time_one  # noqa: E402
+
+
+def time_it(fn, reps=20):
+    """ms per call over `reps` back-to-back calls (host launch overhead hidden
+    behind queued work, as in a step loop)."""
+    return _time_one(lambda: [fn() for _ in range(reps)]) / reps
 
 fam, n = sys.argv[1] if len(sys.argv) > 1 else "wave3d_r4", int(sys.argv[2]) if len(sys.argv) > 2 else 768
 R = bench.RADIUS[fam]
@@ -31,5 +37,17 @@ for N in (2, 4, 8):
         api.adjoint_slab(fam, n, sc, loc, sl.base, sl.nplanes, sl.own0, sl.own1)
     tn = time_it(step)
     tw = time_it(whole)
-    print(f"  N={N}: rank {N // 2} owns {sl.own1 - sl.own0} planes: overlapped-form compute "
-          f"{tn:.3f} ms (eff {t1 / N / tn:.2f}), one launch {tw:.3f} ms (eff {t1 / N / tw:.2f})")
+    line = (f"  N={N}: rank {N // 2} owns {sl.own1 - sl.own0} planes: overlapped-form compute "
+            f"{tn:.3f} ms (eff {t1 / N / tn:.2f}), one launch {tw:.3f} ms (eff {t1 / N / tw:.2f})")
+    if fam == "wave3d_r4":
+        # fused peer halo: the neighbours emulated as separate buffers on this GPU
+        from paper_1907_02818_b200 import peer
+        r = N // 2
+        ranks = [q for q in (r - 1, r, r + 1) if 0 <= q < N]
+        slabs = [slab.decompose(n, R, N, q) for q in ranks]
+        arrs = [bench.gen_inputs(api, torch, fam, n, s2) for s2 in slabs]
+        me = ranks.index(r)
+        link = peer.emulate(slabs, arrs)[me]
+        tp = time_it(lambda: peer.adjoint(n, sc, arrs[me], link))
+        line += f", peer {tp:.3f} ms (eff {t1 / N / tp:.2f})"
+    print(line)
