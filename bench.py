@@ -71,6 +71,7 @@ class ClockSampler:
 
     def __init__(self, device_index: int):
         self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.power_w, self.power_limit_w = [], None
         self._stop = threading.Event()
         try:
             import pynvml
@@ -78,6 +79,10 @@ class ClockSampler:
             self._nv = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1e3
+            except Exception:
+                pass
         except Exception as e:  # pragma: no cover
             log("clock sampling unavailable:", e)
             self._nv = None
@@ -87,6 +92,10 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                try:
+                    self.power_w.append(nv.nvmlDeviceGetPowerUsage(self._h) / 1e3)
+                except Exception:
+                    pass
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
@@ -109,7 +118,9 @@ class ClockSampler:
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples),
+                "power_w": statistics.median(self.power_w) if self.power_w else None,
+                "power_limit_w": self.power_limit_w}
 
 
 # ------------------------------------------------------------------ helpers
