@@ -219,6 +219,45 @@ static int burgers2d_gather(long long n, double C, double D, const T* u_1, T* u_
   return launch_status("burgers2d_b");
 }
 
+// burgers2d primal, strip-streaming ring kernel (lowdim.cuh).  Returns true
+// when it launched (the caller checks the launch status), false when the
+// shape needs the register-streaming / per-point kernels.
+template <typename T>
+static bool burgers2d_primal_ring(long long n, double C, double D, const T* u_1, T* u,
+                                  cudaStream_t s) {
+  if ((n * (long long)sizeof(T)) % 16 != 0 || n > (1 << 30) || !aligned16(u_1, u, u_1, u) ||
+      std::getenv("SGB_BURGERS_NORING"))
+    return false;
+  int rb = 16, stages = 6;  // measured at 8192^2; env overrides per call
+  if (const char* e = std::getenv("SGB_BURGERS_PRIMAL_RB")) rb = std::max(1, std::atoi(e));
+  if (const char* f = std::getenv("SGB_BURGERS_PRIMAL_S")) {
+    const int v = std::atoi(f);
+    stages = v <= 4 ? 4 : (v >= 8 ? 8 : 6);
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(burgers2d_primal_ring_kernel<T, 4>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, BurgPrimalRing<T, 4>::SMEM);
+    cudaFuncSetAttribute(burgers2d_primal_ring_kernel<T, 6>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, BurgPrimalRing<T, 6>::SMEM);
+    cudaFuncSetAttribute(burgers2d_primal_ring_kernel<T, 8>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, BurgPrimalRing<T, 8>::SMEM);
+    attr = true;
+  }
+  constexpr int W = BurgPrimalRing<T, 4>::W, TH = BurgPrimalRing<T, 4>::THREADS;
+  dim3 g((unsigned)((n + W - 1) / W), (unsigned)((n + rb - 1) / rb));
+  if (stages == 4)
+    burgers2d_primal_ring_kernel<T, 4>
+        <<<g, TH, BurgPrimalRing<T, 4>::SMEM, s>>>((int)n, (T)C, (T)D, u_1, u, rb);
+  else if (stages == 6)
+    burgers2d_primal_ring_kernel<T, 6>
+        <<<g, TH, BurgPrimalRing<T, 6>::SMEM, s>>>((int)n, (T)C, (T)D, u_1, u, rb);
+  else
+    burgers2d_primal_ring_kernel<T, 8>
+        <<<g, TH, BurgPrimalRing<T, 8>::SMEM, s>>>((int)n, (T)C, (T)D, u_1, u, rb);
+  return true;
+}
+
 }  // namespace sgb
 
 using namespace sgb;
@@ -373,6 +412,8 @@ int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float
 #define SGB_BURGERS(T, SFX)                                                                    \
   int burgers2d_##SFX(int n, double C, double D, T* u_1, T* u, sgb_stream_t stream) {          \
     if (n <= 0 || !u_1 || !u) return einval("burgers2d: bad arguments");                       \
+    if (burgers2d_primal_ring<T>(n, C, D, u_1, u, as_stream(stream)))                          \
+      return launch_status("burgers2d");                                                       \
     if (n % 2 == 0 && aligned16(u_1, u, u_1, u)) {                                             \
       dim3 g((unsigned)((n / 2 + 127) / 128), (unsigned)((n + 31) / 32));                      \
       burgers2d_primal_stream_kernel<T>                                                        \

@@ -385,4 +385,100 @@ __global__ void __launch_bounds__(BurgRing<T, S_>::THREADS, 8)
   }
 }
 
+// ------------------------------------------------------------------ burgers2d primal (ring)
+// The primal in the strip-streaming form of the adjoint ring kernel: one
+// thread streams the u_1 row segments (W columns + a 16-byte halo each side)
+// of rows i0-1 .. i1 into an S-stage ring with 1D bulk copies, S-3 rows
+// ahead; every thread evaluates its two points of row r from shared memory
+// (rows r-1, r, r+1) with the same expression and grouping as
+// burgers2d_primal_stream_kernel / the per-point kernel (bitwise equal).
+// The register-streaming form it replaces was issue-bound on row-index math
+// and waited on its own loads (profiles/).  16 B/pt: u_1 read, u written.
+template <typename T, int S_>
+struct BurgPrimalRing {
+  static constexpr int THREADS = 128, W = 2 * THREADS;
+  static constexpr int H = 16 / (int)sizeof(T);
+  static constexpr int UW = W + 2 * H;
+  static constexpr int S = S_;
+  static constexpr int SMEM = S * UW * (int)sizeof(T) + S * 8;
+};
+
+template <typename T, int S_>
+__global__ void __launch_bounds__(128, 8)
+    burgers2d_primal_ring_kernel(int n, T C, T D, const T* __restrict__ u1, T* __restrict__ u,
+                                 int rows_per_block) {
+  using Rg = BurgPrimalRing<T, S_>;
+  using V = typename Vec2<T>::type;
+  constexpr int W = Rg::W, H = Rg::H, UW = Rg::UW, S = Rg::S;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + S * UW);
+  const int tid = threadIdx.x;
+  const int j0 = blockIdx.x * W;
+  const int i0 = blockIdx.y * rows_per_block;
+  const int i1 = min(i0 + rows_per_block, n);
+  const int ca = max(j0 - H, 0), cb = min(j0 + W + H, n);
+  const uint32_t ubytes = (uint32_t)(cb - ca) * sizeof(T);
+  const int uoff = ca - (j0 - H);
+  const int r_first = i0 - 1, nrows = i1 - i0 + 2;  // rows i0-1 .. i1
+
+  // columns outside the grid are never loaded: zero once (never read for an
+  // output point either, the outputs are j in [1, n-2])
+  for (int e = tid; e < S * UW; e += Rg::THREADS) ring[e] = T(0);
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  auto issue = [&](int k) {
+    const int s = k % S, r = r_first + k;
+    const bool valid = r >= 0 && r < n;
+    tma::mbar_arrive_expect_tx(&bars[s], valid ? ubytes : 0u);
+    if (valid) tma::bulk_g2s(ring + s * UW + uoff, u1 + (size_t)r * n + ca, ubytes, &bars[s]);
+  };
+  if (tid == 0)
+    for (int k = 0; k < S && k < nrows; k++) issue(k);
+
+  const int jl = 2 * tid, j = j0 + jl;
+  const bool active = j < n;
+  const bool jin[2] = {j >= 1 && j <= n - 2, j + 1 >= 1 && j + 1 <= n - 2};
+  T* orow = u + (size_t)i0 * n + j;
+  tma::mbar_wait(&bars[0], 0);
+  for (int r = i0; r < i1; r++, orow += n) {
+    const int k = r - r_first;
+    tma::mbar_wait(&bars[k % S], (k / S) & 1);
+    tma::mbar_wait(&bars[(k + 1) % S], ((k + 1) / S) & 1);
+    if (active && r >= 1 && r <= n - 2 && (jin[0] || jin[1])) {
+      const T* Um = ring + ((k - 1) % S) * UW + H + jl;
+      const T* Uc = ring + (k % S) * UW + H + jl;
+      const T* Up = ring + ((k + 1) % S) * UW + H + jl;
+      const V um = *reinterpret_cast<const V*>(Um), u0 = *reinterpret_cast<const V*>(Uc),
+              up = *reinterpret_cast<const V*>(Up);
+      const T ul = Uc[-1], ur = Uc[2];
+      const T vv[2] = {u0.x, u0.y}, mm[2] = {um.x, um.y}, pp[2] = {up.x, up.y};
+      const T vl[2] = {ul, u0.x}, vr[2] = {u0.y, ur};
+      T out[2];
+#pragma unroll
+      for (int m = 0; m < 2; m++) {
+        const T v = vv[m];
+        out[m] = v -
+                 C * (fmax(v, T(0)) * (v - mm[m]) + fmin(v, T(0)) * (pp[m] - v) +
+                      fmax(v, T(0)) * (v - vl[m]) + fmin(v, T(0)) * (vr[m] - v)) +
+                 D * (pp[m] + mm[m] + vr[m] + vl[m] - T(4) * v);
+      }
+      if (jin[0] && jin[1]) {
+        st2cs(orow, out[0], out[1]);
+      } else {
+        if (jin[0]) orow[0] = out[0];
+        if (jin[1]) orow[1] = out[1];
+      }
+    }
+    __syncthreads();  // row r-1's stage is free
+    if (tid == 0 && k - 1 + S < nrows) issue(k - 1 + S);
+  }
+}
+
 }  // namespace sgb

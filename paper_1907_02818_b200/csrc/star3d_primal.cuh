@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(PrimalTile<MODE>::THREADS, 2)
   for (int h = 0; h < 2; h++) jin[h] = jr0 + h >= lo && jr0 + h <= hi;
 #pragma unroll
   for (int m = 0; m < 4; m++) kin[m] = kc + m >= lo && kc + m <= hi;
+  const bool kall = kin[0] && kin[3] && kc + 3 < n;  // all 4 k points written: one 16-byte store
 
   float4 acc[RING][2];
 #pragma unroll
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(PrimalTile<MODE>::THREADS, 2)
             // (2 u_1 - u_2) + (cc D) Lap, the generic kernel's grouping
             float4 v = add4(fmas4(2.f, u1, muls4(-1.f, u2)), mul4(muls4(D, cc), acc[es][h]));
             if (NT == 4) v = add4(lds4(F + BF + 3 * TILE + trow + h * TK), v);
-            if (tile_in) {
+            if (tile_in || (jin[h] && kall)) {
               __stcs(reinterpret_cast<float4*>(urow + h * n), v);
             } else if (jin[h]) {
               const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -186,6 +187,13 @@ inline int star3_primal_tma(long long n, float D, const float* c, const float* u
     const long long cost = ((tiles * cc + slots - 1) / slots) * (len + 2 * R);
     if (best < 0 || cost < best) best = cost, nch = cc;
   }
+  // Radius 4: short chunks (~48 planes) keep the resident CTAs streaming
+  // nearly the same planes, so the u_1 halo rows a tile shares with its
+  // neighbours and the u_1 centre tile (re-read R planes after its box) are
+  // still in L2: 768^3 1.34 -> 1.11 ms although every chunk re-reads 2R halo
+  // planes.  Radius 1 keeps the wave model (measured best there).
+  if (R >= 2) nch = (int)std::max<long long>(nch, (nout + 47) / 48);
+  if (const char* e = std::getenv("SGB_PRIMAL_CHUNKS")) nch = std::max(1, std::atoi(e));
   const int chunk = (int)((nout + nch - 1) / nch);
   const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
   star3_primal_tma_kernel<MODE><<<dim3((unsigned)tiles, gy), Tl::THREADS, Tl::SMEM, s>>>(

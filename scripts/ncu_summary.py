@@ -32,12 +32,23 @@ for vals in rows[2:]:
 if len(sys.argv) > 2:
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
                           "sass"], capture_output=True, text=True).stdout
-    r = list(csv.reader(src.splitlines()))
-    h = r[1]
-    data = r[2:]
-    iS = h.index("Warp Stall Sampling (All Samples)")
-    iE = h.index("Instructions Executed")
-    iSrc = h.index("Source")
+    # one section per kernel: a "Kernel Name" line, a header line, then rows;
+    # argv[3] (optional) selects the sections whose kernel name contains it
+    want = sys.argv[3] if len(sys.argv) > 3 else None
+    h, data, keep = None, [], True
+    for x in csv.reader(src.splitlines()):
+        if x and x[0] == "Kernel Name":
+            keep = want is None or want in x[1]
+            h = None
+            continue
+        if x and x[0] == "Address":
+            h = x
+            iS = h.index("Warp Stall Sampling (All Samples)")
+            iE = h.index("Instructions Executed")
+            iSrc = h.index("Source")
+            continue
+        if keep and h and len(x) == len(h):
+            data.append(x)
     tot = sum(float(x[iS] or 0) for x in data)
     totE = sum(float(x[iE] or 0) for x in data)
     c, s = Counter(), Counter()

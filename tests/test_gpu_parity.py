@@ -256,6 +256,26 @@ def test_r4_launch_variants_bitwise_equal(api, n, monkeypatch):
             assert np.array_equal(got[adj], base[adj]), (env, adj)
 
 
+@pytest.mark.parametrize("name,n", [("wave3d_r4", 68), ("wave3d_r4", 136), ("wave3d_r4", 200),
+                                    ("wave3d_c", 136)])
+def test_primal_chunking_bitwise_equal(api, name, n, monkeypatch):
+    """The streaming primal's i-chunk count (default: ~48-plane chunks at
+    radius 4, wave model at radius 1) changes only which CTA streams which
+    planes: results are bitwise identical for any count, incl. one chunk per
+    column and chunks shorter than the 2R halo."""
+    scalars, grids, _ = gen.family_inputs(name, n, seed=n + 11)
+    f = oracle.family(name)
+    out = f.arrays[f.output]
+    grids[out] = np.random.default_rng(n + 1).standard_normal(grids[out].shape)
+    g = _round(grids, "f32")
+    base = api.run_nest(name, n, scalars, g, dtype="f32")[out]
+    for chunks in ("1", "2", "5", "64"):
+        with monkeypatch.context() as m:
+            m.setenv("SGB_PRIMAL_CHUNKS", chunks)
+            got = api.run_nest(name, n, scalars, g, dtype="f32")[out]
+        assert np.array_equal(got, base), chunks
+
+
 @pytest.mark.parametrize("n", [64, 300, 1030])
 def test_burgers_ring_variants_bitwise_equal(api, n, monkeypatch):
     """burgers2d ring kernel: stage count and rows per CTA change only the
@@ -314,10 +334,32 @@ def test_primal_f32_matches_oracle(api, name, n):
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("n", [64, 300, 1032])
+def test_burgers_primal_ring_variants_bitwise_equal(api, n, dtype, monkeypatch):
+    """The ring primal evaluates the register-streaming kernel's expression
+    with the same grouping: bitwise equal to it, for every stage count and
+    rows-per-CTA (incl. a strip taller than the grid)."""
+    name = "burgers2d"
+    scalars, grids, _ = gen.family_inputs(name, n, seed=n + 13)
+    grids["u"] = np.random.default_rng(n + 2).standard_normal(grids["u"].shape)
+    g = _round(grids, dtype)
+    base = api.run_nest(name, n, scalars, g, dtype=dtype)["u"]
+    for env in ({"SGB_BURGERS_NORING": "1"}, {"SGB_BURGERS_PRIMAL_S": "4"},
+                {"SGB_BURGERS_PRIMAL_S": "8"}, {"SGB_BURGERS_PRIMAL_RB": "7"},
+                {"SGB_BURGERS_PRIMAL_RB": "5000"}):
+        with monkeypatch.context() as m:
+            for k, v in env.items():
+                m.setenv(k, v)
+            got = api.run_nest(name, n, scalars, g, dtype=dtype)["u"]
+        assert np.array_equal(got, base), env
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("n", [5, 64, 203, 300, 1030])
 def test_burgers_primal_matches_oracle(api, n, dtype):
-    """burgers2d primal (row-streaming kernel for even n, per-point otherwise)
-    against the oracle's run_nest; untouched ring keeps its values."""
+    """burgers2d primal (strip ring kernel where rows are 16-byte multiples,
+    row-streaming kernel for other even n, per-point otherwise) against the
+    oracle's run_nest; untouched ring keeps its values."""
     name = "burgers2d"
     scalars, grids, _ = gen.family_inputs(name, n, seed=n + 11)
     grids["u"] = np.random.default_rng(n).standard_normal(grids["u"].shape)
