@@ -393,7 +393,27 @@ def run_ours(args, cfg):
         from paper_1907_02818_b200 import peer as peermod
         link = peermod.try_connect(sl, arrays)
 
+    pf_sel = [False]     # cross-step pipelined exchange (drivers.HaloPrefetch)
+    pf = [None]
+    if sl is not None and world > 1 and halo_mode in ("auto", "prefetch"):
+        def pf_regen(fs, t):
+            drivers.regen_state(fs["u_1"], n, t, 0, R, sl)
+            drivers.regen_seed(fs["u_b"], n, t, 0, sl)
+        pf[0] = drivers.HaloPrefetch(family, n, scalars, arrays, sl,
+                                     regen=pf_regen if regen else None)
+
     def step(record):
+        if pf_sel[0]:
+            if regen:
+                arrays["u_1_b"].zero_()
+            if record:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            nl = pf[0].step()
+            if record:
+                b.record(stream)
+                kev.append((a, b, nl))
+            return
         if regen:
             if peer_sel[0]:  # neighbours finished reading the planes regen overwrites
                 peermod.step_sync()
@@ -447,12 +467,38 @@ def run_ours(args, cfg):
                 link.close()
                 link = None
                 probe["peer"] = "disabled: result differed from the exchange path"
-        modes = [("overlapped", True, False), ("exchange_then_compute", False, False)]
+        if pf[0] is not None:
+            # the pipelined exchange must reproduce the exchange path bit for
+            # bit: step 0 of the pipeline vs the exchange path on its inputs
+            stream.wait_event(pf[0].ready[0])
+            snap = {k: arrays[k].clone() for k in ("c_b", "u_1_b", "u_1", "u_b")}
+            for k in ("u_1", "u_b"):
+                arrays[k].copy_(pf[0].sets[0][k])
+            drivers.adjoint_step(family, n, scalars, arrays, sl, overlap=False)
+            want = {k: arrays[k].clone() for k in ("c_b", "u_1_b")}
+            for k in snap:
+                arrays[k].copy_(snap[k])
+            pf[0].step(0)
+            a0, a1 = sl.own0 - sl.base, sl.own1 - sl.base
+            same = all(torch.equal(arrays[k][a0:a1], want[k][a0:a1]) for k in want)
+            for k in ("c_b", "u_1_b"):
+                arrays[k].copy_(snap[k])
+            flag = torch.tensor([1 if same else 0], device="cuda", dtype=torch.int32)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag[0]) == 0:
+                pf[0].close()
+                pf[0] = None
+                probe["prefetch"] = "disabled: result differed from the exchange path"
+        modes = [("overlapped", True, False, False),
+                 ("exchange_then_compute", False, False, False)]
         if link is not None:
-            modes.append(("peer", False, True))
-        for label, mode, use_peer in modes:
+            modes.append(("peer", False, True, False))
+        if pf[0] is not None:
+            modes.append(("prefetch", False, False, True))
+        for label, mode, use_peer, use_pf in modes:
             overlap_sel[0] = mode
             peer_sel[0] = use_peer
+            pf_sel[0] = use_pf
             step(False)
             barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -468,9 +514,15 @@ def run_ours(args, cfg):
         best = min(timed, key=timed.get)
         overlap_sel[0] = best == "overlapped"
         peer_sel[0] = best == "peer"
+        pf_sel[0] = best == "prefetch"
         halo_probe = probe
     elif link is not None and halo_mode == "peer":
         peer_sel[0] = True
+    elif pf[0] is not None and halo_mode == "prefetch":
+        pf_sel[0] = True
+    if pf[0] is not None and not pf_sel[0]:
+        pf[0].close()
+        pf[0] = None
     l0 = _lib.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
@@ -541,7 +593,12 @@ def run_ours(args, cfg):
                    "algorithmic_bytes_per_point": bpp,
                    "l2": "no flush: every step streams >= 12.7 GB (inputs >> 126 MB L2)"
                    if family == "wave3d_r4" else "inputs larger than L2",
-                   "halo_exchange": (("fused: the kernel's TMA loads read the radius-R halo "
+                   "halo_exchange": ("NCCL batch_isend_irecv u_1,u_b radius-R per step on a "
+                                     "side stream, pipelined one step ahead (double-buffered "
+                                     "inputs; step t's exchange behind step t-1's compute), "
+                                     "then one launch over the owned planes"
+                                     if pf_sel[0] else
+                                     ("fused: the kernel's TMA loads read the radius-R halo "
                                       "planes from the neighbours' arrays over NVLink (CUDA "
                                       "IPC), stream-ordered NCCL sync per step")
                                      if peer_sel[0] else
@@ -735,7 +792,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="exchange, then compute")
-    ap.add_argument("--halo", default="auto", choices=["auto", "overlap", "serial", "peer"],
+    ap.add_argument("--halo", default="auto",
+                    choices=["auto", "overlap", "serial", "peer", "prefetch"],
                     help="N>1 halo strategy: auto = time each after warm-up, keep the fastest "
                          "(peer only if it reproduces the exchange path bitwise)")
     ap.add_argument("--no-ablation", action="store_true")

@@ -81,6 +81,80 @@ def adjoint_step(family, n, scalars, arrays, sl=None, exchange=("u_1", "u_b"), o
     return launches
 
 
+class HaloPrefetch:
+    """Cross-step pipelined halo exchange for z-slab steps whose
+    inputs do not depend on the previous step's outputs -- cfg 4 (the same
+    forward state and seed every step) and cfg 5 (both regenerated from
+    (seed, step)).  The exchanged fields (u_1, u_b) get two buffer sets: while
+    the gather adjoint of step t reads set t % 2 in ONE launch over the owned
+    planes (halos already in place), a high-priority side stream regenerates
+    step t+1's owned planes into the other set (cfg 5) and exchanges that
+    set's halo planes with the neighbours (NCCL over NVLink), so the exchange
+    -- and the regeneration -- run behind the compute instead of before it.
+    Step t still consumes exactly the planes the exchange-then-compute path
+    gives it, so the outputs are bitwise identical (tests/test_drivers_gpu.py).
+
+    regen(fields, t): writes step t's owned planes of the exchanged fields
+    (None: inputs static); exchange(tensors): refreshes their halo planes
+    (default: slab.exchange_halos, one batched NCCL isend/irecv round).
+    Call step(t) for t = 0, 1, 2, ... on the compute stream; close() drains
+    the side stream."""
+
+    def __init__(self, family, n, scalars, arrays, sl, fields=("u_1", "u_b"), regen=None,
+                 exchange=None):
+        self.family, self.n, self.scalars, self.arrays, self.sl = family, n, scalars, arrays, sl
+        self.fields = tuple(fields)
+        self.regen = regen
+        self.exchange = exchange or (lambda ts: slabmod.exchange_halos(sl, ts))
+        # both sets are private copies (initialised from `arrays`), so the
+        # side stream never writes a tensor the caller may still use
+        self.sets = [{f: arrays[f].clone() for f in self.fields} for _ in range(2)]
+        self.side = torch.cuda.Stream(priority=-1)
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+        self.side.wait_stream(torch.cuda.current_stream())  # arrays initialised
+        self._t = 0
+        self._prepare(0)
+        self._prepare(1)
+
+    def _prepare(self, t):
+        s = t % 2
+        with torch.cuda.stream(self.side):
+            if t >= 2:  # step t-2 finished reading this set
+                self.side.wait_event(self.free[s])
+            if self.regen is not None:
+                self.regen(self.sets[s], t)
+            self.exchange([self.sets[s][f] for f in self.fields])
+            self.ready[s].record(self.side)
+
+    def inputs(self, t):
+        """The arrays step t reads (the static ones + set t % 2)."""
+        a = dict(self.arrays)
+        a.update(self.sets[t % 2])
+        return a
+
+    def step(self, t=None):
+        """Step t's gather adjoint (one launch over the owned planes) on the
+        current stream; enqueues step t+2's input preparation behind it."""
+        t = self._t if t is None else t
+        if t != self._t:
+            raise ValueError(f"HaloPrefetch steps run in order: expected {self._t}, got {t}")
+        s = t % 2
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self.ready[s])
+        sl = self.sl
+        api.adjoint_slab(self.family, self.n, self.scalars, self.inputs(t), sl.base, sl.nplanes,
+                         sl.own0, sl.own1)
+        self.free[s].record(cur)
+        self._t = t + 1
+        self._prepare(t + 2)
+        return 1
+
+    def close(self):
+        torch.cuda.current_stream().wait_stream(self.side)
+        self.side.synchronize()
+
+
 def alloc(family, n, sl=None, dtype=torch.float32):
     shape = (sl.nplanes, n, n) if sl is not None else (n, n, n)
     return {nm: torch.zeros(shape, dtype=dtype, device="cuda")

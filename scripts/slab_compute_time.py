@@ -1,14 +1,17 @@
 """Per-rank compute of the z-slab adjoint step on ONE GPU (developer aid):
 the launches drivers.adjoint_step issues for an interior rank of an N-way
 decomposition (interior planes + two edge bands), halo exchange omitted, vs
-the single-GPU step / N.  Estimates the compute side of N-GPU efficiency."""
+the single-GPU step / N.  Estimates the compute side of N-GPU efficiency.
+The pipelined form (drivers.HaloPrefetch) is timed with its exchange
+emulated by device copies of the same volume on its side stream (the halo
+planes in, the owned edge planes out), so HBM / SM contention is included."""
 import sys
 
 import torch
 
 sys.path.insert(0, ".")
 import bench  # noqa: E402
-from paper_1907_02818_b200 import api, slab  # noqa: E402
+from paper_1907_02818_b200 import api, drivers, slab  # noqa: E402
 from scripts.quick_time import time_it as _time_one  # noqa: E402
 
 
@@ -37,8 +40,24 @@ for N in (2, 4, 8):
         api.adjoint_slab(fam, n, sc, loc, sl.base, sl.nplanes, sl.own0, sl.own1)
     tn = time_it(step)
     tw = time_it(whole)
+    top = sl.halo_lo + sl.owned
+    nbr = {k: torch.randn((2, R, n, n), device="cuda") for k in ("u_1", "u_b")}
+
+    def exch(ts):  # what NCCL moves: R planes in and out per interior side and field
+        for t_, k in zip(ts, ("u_1", "u_b")):
+            if sl.halo_lo:
+                nbr[k][0].copy_(t_[sl.halo_lo:sl.halo_lo + R])
+                t_[:sl.halo_lo].copy_(nbr[k][0])
+            if sl.halo_hi:
+                nbr[k][1].copy_(t_[top - R:top])
+                t_[top:].copy_(nbr[k][1])
+    pf = drivers.HaloPrefetch(fam, n, sc, loc, sl, exchange=exch)
+    tf = time_it(pf.step)
+    pf.close()
     line = (f"  N={N}: rank {N // 2} owns {sl.own1 - sl.own0} planes: overlapped-form compute "
-            f"{tn:.3f} ms (eff {t1 / N / tn:.2f}), one launch {tw:.3f} ms (eff {t1 / N / tw:.2f})")
+            f"{tn:.3f} ms (eff {t1 / N / tn:.2f}), one launch {tw:.3f} ms (eff {t1 / N / tw:.2f}), "
+            f"pipelined (exchange emulated on the side stream) {tf:.3f} ms "
+            f"(eff {t1 / N / tf:.2f})")
     if fam == "wave3d_r4":
         # fused peer halo: the neighbours emulated as separate buffers on this GPU
         from paper_1907_02818_b200 import peer

@@ -99,6 +99,79 @@ def test_interior_edge_split_equals_single_launch(mods, family, n, world):
             assert torch.equal(loc[k], one[k]), (family, r, k)
 
 
+@pytest.mark.parametrize("n,world,regen", [(40, 2, True), (52, 3, True), (40, 2, False),
+                                           (44, 4, False)])
+def test_halo_prefetch_pipeline_bitwise(mods, n, world, regen):
+    """HaloPrefetch (exchange of step t+1's halos on a side stream behind step
+    t's compute, double-buffered u_1 / u_b) on emulated ranks of one GPU:
+    every rank's owned planes of c_b / u_1_b after T steps are bitwise the
+    single-GPU run's.  Each rank's regeneration writes its owned planes only
+    (halo planes poisoned with NaN), and the emulated exchange fills the halo
+    planes from the step's global field, so a step that read a set before its
+    exchange, or a set already overwritten for a later step, shows up as
+    NaN or as a wrong step's values."""
+    torch, api, drivers = mods
+    from paper_1907_02818_b200 import slab as slabmod
+    fam, seed, D, T, R = "wave3d_r4", 5, 0.01, 5, 4
+    sc = {"D": D}
+    full = drivers.alloc(fam, n)
+    drivers.init_static(fam, full, n, seed)
+    api.fill_normal3d(full["u_1"], n, R, seed, 1)   # static inputs (cfg 4 style)
+    api.fill_normal3d(full["u_b"], n, 0, seed, 3)
+    static = {k: full[k].clone() for k in ("u_1", "u_b")}
+    for t in range(T):
+        if regen:
+            drivers.regen_state(full["u_1"], n, t, seed, R)
+            drivers.regen_seed(full["u_b"], n, t, seed)
+            full["u_1_b"].zero_()
+        api.adjoint(fam, n, sc, full)
+    nan = float("nan")
+    for r in range(world):
+        sl = slabmod.decompose(n, R, world, r)
+        loc = drivers.alloc(fam, n, sl)
+        drivers.init_static(fam, loc, n, seed, sl)
+        scratch = {k: torch.empty((n, n, n), device="cuda") for k in ("u_1", "u_b")}
+        step_of = [0]
+        top = sl.halo_lo + sl.owned
+
+        def poison(t_):
+            t_[:sl.halo_lo] = nan
+            t_[top:] = nan
+
+        for k in ("u_1", "u_b"):
+            loc[k].copy_(static[k][sl.base:sl.base + sl.nplanes])
+            poison(loc[k])
+
+        def regen_fn(fs, t, sl=sl, step_of=step_of):
+            drivers.regen_state(fs["u_1"], n, t, seed, R, sl)
+            drivers.regen_seed(fs["u_b"], n, t, seed, sl)
+            for k in fs:
+                poison(fs[k])
+            step_of[0] = t
+
+        def exchange_fn(ts, sl=sl, step_of=step_of, scratch=scratch):
+            if regen:
+                drivers.regen_state(scratch["u_1"], n, step_of[0], seed, R)
+                drivers.regen_seed(scratch["u_b"], n, step_of[0], seed)
+                src = [scratch["u_1"], scratch["u_b"]]
+            else:
+                src = [static["u_1"], static["u_b"]]
+            for dst, g in zip(ts, src):
+                dst[:sl.halo_lo].copy_(g[sl.base:sl.own0])
+                dst[top:].copy_(g[sl.own1:sl.base + sl.nplanes])
+
+        pf = drivers.HaloPrefetch(fam, n, sc, loc, sl, regen=regen_fn if regen else None,
+                                  exchange=exchange_fn)
+        for t in range(T):
+            if regen:
+                loc["u_1_b"].zero_()
+            pf.step(t)
+        torch.cuda.synchronize()
+        own = slice(sl.halo_lo, top)
+        for k in ("c_b", "u_1_b"):
+            assert torch.equal(loc[k][own], full[k][sl.own0:sl.own1]), (r, k)
+
+
 def test_generators_are_decomposition_invariant(mods):
     """fill_normal3d / fill_random / fill_layered values depend only on the
     global index: a slab regenerates exactly the single-GPU planes."""
