@@ -189,10 +189,12 @@ struct PlaneTmaTile {
   static constexpr int NS = 3;
   static constexpr int THREADS = TK * TJ;
   static constexpr int BOX = BK * BJ, TILE = TK * TJ;
+  // box slot stride: every TMA destination 128-byte aligned (radius 1: 34 x 10)
+  static constexpr int BP = ((BOX * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
   static constexpr int EPT = (BOX + THREADS - 1) / THREADS;
   // stage: [u_1 box | c box | u_b box | c tile | u_b tile | c_b tile | u_1_b tile]
-  static constexpr int SF = 3 * BOX + 4 * TILE;
-  static constexpr int SMEM = (NS * SF + BOX) * (int)sizeof(T) + NS * 8;
+  static constexpr int SF = 3 * BP + 4 * TILE;
+  static constexpr int SMEM = (NS * SF + BP) * (int)sizeof(T) + NS * 8;
   static_assert(RING % NS == 0, "static stage index");
   static constexpr bool kTmaRows = (BK * sizeof(T)) % 16 == 0 && (TK * sizeof(T)) % 16 == 0;
 };
@@ -211,11 +213,11 @@ __global__ void __launch_bounds__(PlaneTmaTile<MODE, T>::THREADS)
   using Tl = PlaneTmaTile<MODE, T>;
   using S = Star3<MODE>;
   constexpr int R = Tl::R, BK = Tl::BK, RING = Tl::RING, TK = Tl::TK, NS = Tl::NS;
-  constexpr int BOX = Tl::BOX, TILE = Tl::TILE, SF = Tl::SF;
+  constexpr int BOX = Tl::BOX, BP = Tl::BP, TILE = Tl::TILE, SF = Tl::SF;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* stage = reinterpret_cast<T*>(smem_raw);
   T* Q = stage + NS * SF;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Q + BOX);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Q + BP);
 
   const int n = (int)g.n;
   const int tid = threadIdx.x;
@@ -262,14 +264,14 @@ __global__ void __launch_bounds__(PlaneTmaTile<MODE, T>::THREADS)
     const bool emit = it >= 2 * R;
     tma::mbar_arrive_expect_tx(&bars[s], (3 * BOX + (emit ? 4 * TILE : 0)) * (int)sizeof(T));
     tma::load_3d(dst, &tm_u1, &bars[s], k0 - R, j0 - R, pl);
-    tma::load_3d(dst + BOX, &tm_c, &bars[s], k0 - R, j0 - R, pl);
-    tma::load_3d(dst + 2 * BOX, &tm_ub, &bars[s], k0 - R, j0 - R, pl);
+    tma::load_3d(dst + BP, &tm_c, &bars[s], k0 - R, j0 - R, pl);
+    tma::load_3d(dst + 2 * BP, &tm_ub, &bars[s], k0 - R, j0 - R, pl);
     if (emit) {
       const int ol = pl - R;
-      tma::load_3d(dst + 3 * BOX, &tm_ct, &bars[s], k0, j0, ol);
-      tma::load_3d(dst + 3 * BOX + TILE, &tm_ubt, &bars[s], k0, j0, ol);
-      tma::load_3d(dst + 3 * BOX + 2 * TILE, &tm_cbt, &bars[s], k0, j0, ol);
-      tma::load_3d(dst + 3 * BOX + 3 * TILE, &tm_u1bt, &bars[s], k0, j0, ol);
+      tma::load_3d(dst + 3 * BP, &tm_ct, &bars[s], k0, j0, ol);
+      tma::load_3d(dst + 3 * BP + TILE, &tm_ubt, &bars[s], k0, j0, ol);
+      tma::load_3d(dst + 3 * BP + 2 * TILE, &tm_cbt, &bars[s], k0, j0, ol);
+      tma::load_3d(dst + 3 * BP + 3 * TILE, &tm_u1bt, &bars[s], k0, j0, ol);
     }
   };
   if (tid == 0)
@@ -288,8 +290,8 @@ __global__ void __launch_bounds__(PlaneTmaTile<MODE, T>::THREADS)
         const int s = ph % NS;
         const int p = pstart + it;
         const T* U = stage + s * SF;
-        const T* Cb = U + BOX;
-        const T* Ub = U + 2 * BOX;
+        const T* Cb = U + BP;
+        const T* Ub = U + 2 * BP;
         tma::mbar_wait(&bars[s], (par0 + ph / NS) & 1);
         const bool pB = p >= lo && p <= hi;
 #pragma unroll
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(PlaneTmaTile<MODE, T>::THREADS)
           const int nout = (oout > 0) + (jout > 0) + (kout > 0);
           const bool reach = nout == 0 || (nout == 1 && oout <= R && jout <= R && kout <= R);
           if (reach) {
-            const T* tiles = U + 3 * BOX;
+            const T* tiles = U + 3 * BP;
             const long long y = (long long)(o - (int)g.i_base) * plane + (long long)j * n + k;
             const bool inB = nout == 0;
             T add = aq[es];

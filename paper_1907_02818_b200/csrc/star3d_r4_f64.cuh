@@ -1,0 +1,371 @@
+// fp64 radius-4 streaming gather adjoint (sm_100a): the reference's own
+// precision on the cfg 4 / 5 stencil.
+//
+// Mathematics and boundary predicate as every 3D gather kernel here (SURVEY
+// Appendix C; reference adjoint.cpp:73-163 / interp.cpp:189-198):
+//   u_1_b[o] += sum_l w_l q(o - o_l) + 2 u_b[o] [o in B],  q = D c^2 u_b [x in B]
+//   c_b[o]   += g[o] Lap25(u_1)[o],                         g = 2 D c u_b [o in B]
+// Structure of the fp32 v7 kernel (star3d_r4.cuh) re-balanced for doubles,
+// where the shared-memory pipe -- not DRAM -- bounded the plane kernel it
+// replaces (star3d_plane.cuh: one point per thread, 17 shared loads per
+// point and field, ncu mio_throttle / barrier stalls, profiles/):
+//   * one CTA per SM (512 threads) owns a 32 (k) x 32 (j) column tile and
+//     streams over i; per plane one elected thread issues TMA loads of the
+//     c / u_b / u_1 halo boxes (40 x 40) and the c_b / u_1_b tiles of the
+//     output plane o = p - R into a 3-stage mbarrier ring;
+//   * the seed map is windowed to the primal box, so TMA's zero fill is the
+//     seed mask in j and k (the i test is per plane);
+//   * warps 0-7 carry Lap(u_1) (emit c_b), warps 8-15 the q stencil (emit
+//     u_1_b); each thread owns 2 rows x 2 k points of one field: k neighbours
+//     from a 10-double window (5 LDS.128 per row), j neighbours from shared
+//     rows common to its two rows, i in 2R+1 rotating accumulators -- 4.5
+//     16-byte shared loads per point and field instead of 17 8-byte ones;
+//   * g is formed in the q-pass; one q buffer and an R+1-slot g ring (smem
+//     budget), so a second barrier per plane closes the q / g reuse.
+#pragma once
+
+#include "star3d_plane.cuh"
+#include "star3d_r4.cuh"
+
+namespace sgb {
+
+struct StarTileD {
+  static constexpr int R = 4;
+  static constexpr int TK = 32, TJ = 32, HK = 4, HJ = 4;
+  static constexpr int BW = TK + 2 * HK;  // 40 doubles: 320-byte box rows
+  static constexpr int BJ = TJ + 2 * HJ;
+  static constexpr int RING = 2 * R + 1;
+  static constexpr int NS = 3;
+  static constexpr int QD = R + 1;
+  static constexpr int ROLE = (TK / 2) * (TJ / 2);  // 256 threads per field
+  static constexpr int THREADS = 2 * ROLE;
+  static constexpr int BOX = BW * BJ;  // 1600 doubles = 12800 B (128-byte multiple)
+  static constexpr int TILE = TK * TJ;
+  static constexpr int SF = 3 * BOX + 2 * TILE;
+  static constexpr int QPAIRS = BOX / 2;
+  static constexpr int EPT = (QPAIRS + THREADS - 1) / THREADS;
+  static constexpr size_t SMEM = (size_t)(NS * SF + BOX + QD * TILE) * 8 + NS * 8;
+  static_assert(RING % NS == 0, "static stage index");
+  static_assert((BOX * 8) % 128 == 0 && (TILE * 8) % 128 == 0, "TMA destinations 128-B aligned");
+};
+
+__device__ __forceinline__ double2 ldd2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ double2 fmad2(double w, const double2& v, const double2& a) {
+  return make_double2(fma(w, v.x, a.x), fma(w, v.y, a.y));
+}
+
+// in-plane k stencil of 2 points (k, k+1) of one row: window k-4 .. k+5
+__device__ __forceinline__ double2 kstencil_d(const double* row, double w0,
+                                              const double (&wr)[5]) {
+  const double2 a = ldd2(row - 4), b = ldd2(row - 2), c = ldd2(row), d = ldd2(row + 2),
+                e = ldd2(row + 4);
+  const double w[10] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
+  double p0 = w0 * w[4], p1 = w0 * w[5];
+#pragma unroll
+  for (int r = 1; r <= 4; r++) {
+    p0 = fma(wr[r], w[4 - r] + w[4 + r], p0);
+    p1 = fma(wr[r], w[5 - r] + w[5 + r], p1);
+  }
+  return make_double2(p0, p1);
+}
+
+// 2 rows x 2 k of one field, plane phase ph: in-plane stencil into acc[ph],
+// the plane's centre values into the i-neighbours' accumulators.
+__device__ __forceinline__ void field2x2_d(const double* F, int r0, int col, double w0,
+                                           const double (&wr)[5], double2 (&acc)[9][2],
+                                           int ph) {
+  constexpr int BW = StarTileD::BW, R = 4, RING = 9;
+  const double* row0 = F + r0 * BW + col;
+  const double2 b0 = ldd2(row0), b1 = ldd2(row0 + BW);
+  double2 in0 = kstencil_d(row0, w0, wr);
+  double2 in1 = kstencil_d(row0 + BW, w0, wr);
+  in0 = fmad2(wr[1], b1, in0);
+  in1 = fmad2(wr[1], b0, in1);
+#pragma unroll
+  for (int t = -R; t <= R + 1; t++) {
+    if (t == 0 || t == 1) continue;
+    const double2 v = ldd2(row0 + t * BW);
+    const int d0 = t < 0 ? -t : t, d1 = t - 1 < 0 ? 1 - t : t - 1;
+    if (d0 <= R) in0 = fmad2(wr[d0], v, in0);
+    if (d1 <= R) in1 = fmad2(wr[d1], v, in1);
+  }
+  acc[ph][0] = make_double2(acc[ph][0].x + in0.x, acc[ph][0].y + in0.y);
+  acc[ph][1] = make_double2(acc[ph][1].x + in1.x, acc[ph][1].y + in1.y);
+  acc[(ph + R) % RING][0] = make_double2(wr[R] * b0.x, wr[R] * b0.y);
+  acc[(ph + R) % RING][1] = make_double2(wr[R] * b1.x, wr[R] * b1.y);
+#pragma unroll
+  for (int r = 1; r <= R; r++) {
+    if (r < R) {
+      acc[(ph + r) % RING][0] = fmad2(wr[r], b0, acc[(ph + r) % RING][0]);
+      acc[(ph + r) % RING][1] = fmad2(wr[r], b1, acc[(ph + r) % RING][1]);
+    }
+    acc[(ph + RING - r) % RING][0] = fmad2(wr[r], b0, acc[(ph + RING - r) % RING][0]);
+    acc[(ph + RING - r) % RING][1] = fmad2(wr[r], b1, acc[(ph + RING - r) % RING][1]);
+  }
+}
+
+__global__ void __launch_bounds__(StarTileD::THREADS, 1)
+    star3_r4_f64_kernel(const __grid_constant__ CUtensorMap tm_c,
+                        const __grid_constant__ CUtensorMap tm_ub,
+                        const __grid_constant__ CUtensorMap tm_u1,
+                        const __grid_constant__ CUtensorMap tm_cb,
+                        const __grid_constant__ CUtensorMap tm_u1b, double* __restrict__ c_b,
+                        double* __restrict__ u_1_b, int n, int i_base, int lo, int hi,
+                        int out_i0, int out_i1, int chunk, int tiles_k, double D) {
+  using Tl = StarTileD;
+  using S3 = Star3<2>;
+  constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
+  constexpr int RING = Tl::RING, NS = Tl::NS, BOX = Tl::BOX, QD = Tl::QD;
+  constexpr int SF = Tl::SF, TILE = Tl::TILE, ROLE = Tl::ROLE;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stage = reinterpret_cast<double*>(smem_raw);  // [NS][c, ub, u1 boxes | cb, u1b tiles]
+  double* Q = stage + NS * SF;                          // q box
+  double* gq = Q + BOX;                                 // [QD][TJ][TK] g of centres
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gq + QD * TILE);
+
+  const int tid = threadIdx.x;
+  const bool q_role = tid >= ROLE;  // warp-uniform
+  const int rt = q_role ? tid - ROLE : tid;
+  const int tx = rt & 15, ty = rt >> 4;  // 2 k-points x rows 2ty, 2ty+1
+  const int tk = blockIdx.x % tiles_k, tj = blockIdx.x / tiles_k;
+  const int k0 = tk * TK, j0 = tj * Tl::TJ;
+  const int o_begin = out_i0 + blockIdx.y * chunk;
+  const int o_end = min(o_begin + chunk, out_i1);
+  if (o_begin >= o_end) return;
+  const int pstart = o_begin - R;
+  const int P = (o_end - o_begin) + 2 * R;
+
+  const double w0 = S3::template w<double>(0);
+  double wr[R + 1];
+  wr[0] = w0;
+#pragma unroll
+  for (int r = 1; r <= R; r++) wr[r] = S3::template w<double>(r);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int it) {
+    const int s = it % NS;
+    double* dst = stage + s * SF;
+    const int pl = pstart + it - i_base;
+    const bool emit = it >= 2 * R;
+    tma::mbar_arrive_expect_tx(&bars[s], (3 * BOX + (emit ? 2 * TILE : 0)) * 8);
+    tma::load_3d(dst, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + BOX, &tm_ub, &bars[s], k0 - HK - lo, j0 - HJ - lo, pl);
+    tma::load_3d(dst + 2 * BOX, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
+    if (emit) {
+      tma::load_3d(dst + 3 * BOX, &tm_cb, &bars[s], k0, j0, pl - R);
+      tma::load_3d(dst + 3 * BOX + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
+    }
+  };
+  if (tid == 0)
+    for (int it = 0; it < NS && it < P; it++) issue(it);
+
+  const int jr0 = j0 + 2 * ty, kc = k0 + 2 * tx;
+  const int r0 = 2 * ty + HJ, col = HK + 2 * tx;
+  const int trow = 2 * ty * TK + 2 * tx;  // row 2ty of a 32x32 tile
+  const long long plane = (long long)n * n;
+  const long long coff = (long long)jr0 * n + kc;
+
+  // q-pass pairs of this thread: box offset and, for centres, g-tile offset
+  int qoff[Tl::EPT], goff[Tl::EPT];
+#pragma unroll
+  for (int m = 0; m < Tl::EPT; m++) {
+    const int e = tid + m * Tl::THREADS;
+    const int row = e / (BW / 2), c2 = e - row * (BW / 2);
+    qoff[m] = e < Tl::QPAIRS ? row * BW + 2 * c2 : -1;
+    goff[m] = (e < Tl::QPAIRS && row >= HJ && row < HJ + Tl::TJ && c2 >= HK / 2 &&
+               c2 < HK / 2 + TK / 2)
+                  ? (row - HJ) * TK + 2 * (c2 - HK / 2)
+                  : -1;
+  }
+  // per-point masks (plane-independent): bit 2h+x for point (jr0+h, kc+x)
+  //   inb : j, k in [lo, hi];  one : exactly one of j, k outside, by <= R
+  //   grid (bits 4, 5): row h inside the grid (kc < n, n even: kc+1 < n too)
+  uint32_t inb = 0, one = 0, grid = 0;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int j = jr0 + h;
+    if (j < n && kc < n) grid |= 1u << h;
+    const int jout = j < lo ? lo - j : (j > hi ? j - hi : 0);
+#pragma unroll
+    for (int x = 0; x < 2; x++) {
+      const int k = kc + x;
+      const int kout = k < lo ? lo - k : (k > hi ? k - hi : 0);
+      if (jout == 0 && kout == 0) inb |= 1u << (2 * h + x);
+      if ((jout > 0) + (kout > 0) == 1 && jout <= R && kout <= R) one |= 1u << (2 * h + x);
+    }
+  }
+
+  double2 acc[RING][2];
+#pragma unroll
+  for (int s = 0; s < RING; s++) acc[s][0] = acc[s][1] = make_double2(0.0, 0.0);
+
+  for (int base = 0; base < P; base += RING) {
+    const int par0 = base / NS;
+#pragma unroll
+    for (int ph = 0; ph < RING; ph++) {
+      const int it = base + ph;
+      if (it < P) {
+        const int s = ph % NS;
+        const int p = pstart + it;
+        const double* Cs = stage + s * SF;
+        const double* UBs = Cs + BOX;
+        const double* U1s = Cs + 2 * BOX;
+        double* G = gq + (it % QD) * TILE;
+        const int o = p - R;
+        const bool pin = p >= lo && p <= hi;
+
+        tma::mbar_wait(&bars[s], (par0 + ph / NS) & 1);
+        // ---- q over the halo box; g for the centre pairs
+#pragma unroll
+        for (int m = 0; m < Tl::EPT; m++) {
+          if (qoff[m] >= 0) {
+            const int qo = qoff[m];
+            double2 qv = make_double2(0.0, 0.0), gv = qv;
+            if (pin) {
+              const double2 cv = ldd2(Cs + qo), uv = ldd2(UBs + qo);
+              const double2 du = make_double2(D * uv.x, D * uv.y);
+              qv = make_double2(cv.x * cv.x * du.x, cv.y * cv.y * du.y);
+              gv = make_double2(2.0 * cv.x * du.x, 2.0 * cv.y * du.y);
+            }
+            *reinterpret_cast<double2*>(Q + qo) = qv;
+            if (goff[m] >= 0) *reinterpret_cast<double2*>(G + goff[m]) = gv;
+          }
+        }
+        // ---- q role: the 2 u_b centre term of output plane p
+        if (q_role && pin) {
+#pragma unroll
+          for (int h = 0; h < 2; h++)
+            acc[ph][h] = fmad2(2.0, ldd2(UBs + (r0 + h) * BW + col), acc[ph][h]);
+        }
+        __syncthreads();  // Q / G of plane p complete; stage of plane p-1 free
+        if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
+
+        field2x2_d(q_role ? Q : U1s, r0, col, w0, wr, acc, ph);
+
+        // ---- emit output plane o = p - R
+        if (it >= 2 * R) {
+          const int es = (ph + R + 1) % RING;
+          const long long obase = (long long)(o - i_base) * plane;
+          const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
+          const double* OLD = Cs + 3 * BOX + (q_role ? TILE : 0) + trow;
+          if (!q_role) {
+            if (oout == 0) {
+              const double* Go = gq + ((it - R) % QD) * TILE + trow;
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                const uint32_t mk = inb >> (2 * h);
+                if (!((grid >> h) & 1) || !(mk & 3)) continue;
+                const double2 old = ldd2(OLD + h * TK), g = ldd2(Go + h * TK);
+                const double2 a = acc[es][h];
+                const double2 nv = make_double2((mk & 1) ? fma(g.x, a.x, old.x) : old.x,
+                                                (mk & 2) ? fma(g.y, a.y, old.y) : old.y);
+                __stcs(reinterpret_cast<double2*>(c_b + obase + coff + h * n), nv);
+              }
+            }
+          } else {
+            // reached iff at most one coordinate is outside [lo, hi], by <= R
+            const uint32_t reach = oout == 0 ? (inb | one) : (oout <= R ? inb : 0u);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const uint32_t mk = reach >> (2 * h);
+              if (!((grid >> h) & 1) || !(mk & 3)) continue;
+              const double2 old = ldd2(OLD + h * TK);
+              const double2 a = acc[es][h];
+              const double2 nv = make_double2((mk & 1) ? old.x + a.x : old.x,
+                                              (mk & 2) ? old.y + a.y : old.y);
+              __stcs(reinterpret_cast<double2*>(u_1_b + obase + coff + h * n), nv);
+            }
+          }
+        }
+        __syncthreads();  // Q and the emitted g slot free for the next plane
+      }
+    }
+  }
+}
+
+// Same-shape TMA map restricted to the window [off, off+ext) in j and k
+// (TMA zero fill outside = the seed mask); needs a 16-byte aligned window base.
+inline int encode_3d_window_f64(CUtensorMap* map, const double* base, long long n,
+                                long long nplanes, long long off, long long ext, int box0,
+                                int box1, const char* name) {
+  const double* wb = base + off * n + off;
+  if ((reinterpret_cast<uintptr_t>(wb) & 15) != 0 || ext < 1) return 1;
+  auto encode = get_encode();
+  if (!encode) {
+    set_error(std::string(name) + ": cuTensorMapEncodeTiled unavailable");
+    return SGB_EINVAL;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)ext, (cuuint64_t)ext, (cuuint64_t)nplanes};
+  cuuint64_t strides[2] = {(cuuint64_t)n * 8, (cuuint64_t)n * n * 8};
+  cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)wb, dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(std::string(name) + ": tensor map encode failed (" + std::to_string((int)r) + ")");
+    return SGB_EINVAL;
+  }
+  return 0;
+}
+
+// Host launcher; returns 1 when the shape does not fit this kernel (the
+// caller uses the plane kernels), 0 / negative like the other entries.
+inline int star3_r4_f64_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
+                               long long out_i1, double D, const double* c, double* c_b,
+                               const double* u_1, double* u_1_b, const double* u_b,
+                               cudaStream_t s, const char* name) {
+  using Tl = StarTileD;
+  if (g.n % 2 != 0 || g.n > (1 << 20) || g.n < 2 * Tl::R + 2 || hi < lo) return 1;
+  for (const void* p : {(const void*)c, (const void*)c_b, (const void*)u_1, (const void*)u_1_b,
+                        (const void*)u_b})
+    if (reinterpret_cast<uintptr_t>(p) & 15) return 1;
+  CUtensorMap maps[5];
+  int rc = encode_3d_t(&maps[0], c, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
+  const int w = encode_3d_window_f64(&maps[1], u_b, g.n, g.nplanes, lo, hi - lo + 1, Tl::BW,
+                                     Tl::BJ, name);
+  if (w < 0) return w;
+  if (w == 1) return 1;  // unaligned seed window: plane kernels
+  rc |= encode_3d_t(&maps[2], u_1, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
+  rc |= encode_3d_t(&maps[3], (const double*)c_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
+  rc |= encode_3d_t(&maps[4], (const double*)u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
+  if (rc) return SGB_EINVAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(star3_r4_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Tl::SMEM);
+    attr = true;
+  }
+  const int tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
+  const long long tiles = (long long)tiles_k * ((g.n + Tl::TJ - 1) / Tl::TJ);
+  const long long nout = out_i1 - out_i0;
+  // i-chunks: the wave model of star3d_r4.cuh (one CTA per SM, equal-length CTAs)
+  int nch = 0;
+  if (const char* e = std::getenv("SGB_F64_ICHUNKS")) nch = std::max(1, std::atoi(e));
+  if (nch == 0) {
+    const int sms = num_sms();
+    long long best = -1;
+    for (int cc = 1; cc <= 64 && cc <= nout; cc++) {
+      const long long len = (nout + cc - 1) / cc;
+      const long long waves = (tiles * cc + sms - 1) / sms;
+      const long long cost = waves * (len + 2 * Tl::R);
+      if (best < 0 || cost < best) best = cost, nch = cc;
+    }
+  }
+  const int chunk = (int)((nout + nch - 1) / nch);
+  const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
+  star3_r4_f64_kernel<<<dim3((unsigned)tiles, gy), Tl::THREADS, Tl::SMEM, s>>>(
+      maps[0], maps[1], maps[2], maps[3], maps[4], c_b, u_1_b, (int)g.n, (int)g.i_base, (int)lo,
+      (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D);
+  return launch_status(name);
+}
+
+}  // namespace sgb

@@ -9,14 +9,15 @@ import subprocess
 import sys
 
 CHILD = r"""
-import sys, torch
+import os, sys, torch
 sys.path.insert(0, ".")
 from paper_1907_02818_b200 import api
 from scripts.quick_time import time_it
 n = int(sys.argv[1]); fam = sys.argv[2]; kind = sys.argv[3]
 g = torch.Generator(device="cuda"); g.manual_seed(0)
 names = api.array_params(fam, kind)
-a = {nm: torch.randn((n, n, n), device="cuda", generator=g) for nm in names}
+dt = torch.float64 if os.environ.get("AB_F64") else torch.float32
+a = {nm: torch.randn((n, n, n), device="cuda", generator=g, dtype=dt) for nm in names}
 sc = {"D": 0.01 if fam == "wave3d_r4" else 0.1}
 fn = getattr(api, "primal" if kind == "primal" else "adjoint")
 ms = time_it(lambda: fn(fam, n, sc, a), iters=30, warm=5)
@@ -46,6 +47,8 @@ def main():
     if args and args[0].startswith("kind="):
         kind = args.pop(0)[5:]
     bpp = {"primal": 16, "adjoint": {"wave3d_r4": 28}.get(fam, 36)}[kind]
+    if os.environ.get("AB_F64"):
+        bpp *= 2
     variants = args or [""]
     for v in variants:
         env = dict(os.environ)

@@ -415,17 +415,38 @@ def test_slab_plans_reassemble_full_plan(api, name, n, nslabs):
 
 @pytest.mark.parametrize("n", [24, 40, 68, 97])
 def test_plane_kernels_tma_equals_plain_fp64(api, n, monkeypatch):
-    """fp64 radius-4 gather: the TMA-fed plane kernel (even n) and the
+    """fp64 radius-4 plane kernels (the general-shape path behind the
+    register-blocked kernel): the TMA-fed plane kernel (even n) and the
     plain-load plane kernel apply the same arithmetic per point (bitwise
     equal); both match the oracle at 1e-12.  Odd n takes the plain kernel."""
     name = "wave3d_r4"
     scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 9, accumulate=True)
-    base = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
     want = oracle_gather(name, n, scalars, grids, adjs)
-    for adj in ("c_b", "u_1_b"):
-        check_close(base[adj], want[adj], "f64", f"n={n} {adj}")
     with monkeypatch.context() as m:
+        m.setenv("SGB_F64_PLANE", "1")
+        base = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
         m.setenv("SGB_PLANE_NO_TMA", "1")
         plain = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
     for adj in ("c_b", "u_1_b"):
+        check_close(base[adj], want[adj], "f64", f"n={n} {adj}")
         assert np.array_equal(plain[adj], base[adj]), adj
+
+
+@pytest.mark.parametrize("n", [20, 24, 40, 66, 98, 136])
+def test_r4_f64_streaming_kernel(api, n, monkeypatch):
+    """fp64 radius-4 register-blocked streaming kernel (even n): matches the
+    oracle at 1e-12 per point on the accumulated adjoints (partial tiles,
+    frame tiles, one-tile grids); the i-chunk count changes only which CTA
+    streams which planes (bitwise equal)."""
+    name = "wave3d_r4"
+    scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 21, accumulate=True)
+    want = oracle_gather(name, n, scalars, grids, adjs)
+    base = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
+    for adj in ("c_b", "u_1_b"):
+        check_close(base[adj], want[adj], "f64", f"n={n} {adj}")
+    for chunks in ("1", "3", "7"):
+        with monkeypatch.context() as m:
+            m.setenv("SGB_F64_ICHUNKS", chunks)
+            got = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
+        for adj in ("c_b", "u_1_b"):
+            assert np.array_equal(got[adj], base[adj]), (chunks, adj)
