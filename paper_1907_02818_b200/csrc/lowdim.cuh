@@ -334,14 +334,18 @@ __global__ void __launch_bounds__(BurgRing<T, S_>::THREADS, 8)
   const bool jreach[2] = {j >= lo - 1 && j <= hi + 1, j + 1 >= lo - 1 && j + 1 <= hi + 1};
   T* orow = u1b + (size_t)i0 * n + j;
   tma::mbar_wait(&bars[0], 0);
+  // stages of rows r-1, r, r+1 (row r is ring row k = r - r_first) and the
+  // parities of the latter two, advanced incrementally (no k % S per row)
+  int sm = 0, sc = 1 % S, sp = 2 % S;
+  uint32_t phc = 0, php = S > 2 ? 0u : 1u;
   for (int r = i0; r < i1; r++, orow += n) {
     const int k = r - r_first;
-    tma::mbar_wait(&bars[k % S], (k / S) & 1);
-    tma::mbar_wait(&bars[(k + 1) % S], ((k + 1) / S) & 1);
+    tma::mbar_wait(&bars[sc], phc);
+    tma::mbar_wait(&bars[sp], php);
     if (active) {
-      const T* Um = ring + ((k - 1) % S) * ST + H + jl;
-      const T* Uc = ring + (k % S) * ST + H + jl;
-      const T* Up = ring + ((k + 1) % S) * ST + H + jl;
+      const T* Um = ring + sm * ST + H + jl;
+      const T* Uc = ring + sc * ST + H + jl;
+      const T* Up = ring + sp * ST + H + jl;
       const V um = *reinterpret_cast<const V*>(Um), uc = *reinterpret_cast<const V*>(Uc),
               up = *reinterpret_cast<const V*>(Up);
       const V bm = *reinterpret_cast<const V*>(Um + UW), bc = *reinterpret_cast<const V*>(Uc + UW),
@@ -382,6 +386,10 @@ __global__ void __launch_bounds__(BurgRing<T, S_>::THREADS, 8)
     }
     __syncthreads();  // row r-1's stage is free
     if (tid == 0 && k - 1 + S < nrows) issue(k - 1 + S);
+    sm = sc;
+    sc = sp;
+    phc = php;
+    if (++sp == S) sp = 0, php ^= 1u;
   }
 }
 
@@ -447,14 +455,16 @@ __global__ void __launch_bounds__(128, 8)
   const bool jin[2] = {j >= 1 && j <= n - 2, j + 1 >= 1 && j + 1 <= n - 2};
   T* orow = u + (size_t)i0 * n + j;
   tma::mbar_wait(&bars[0], 0);
+  int sm = 0, sc = 1 % S, sp = 2 % S;  // as in burgers2d_ring_kernel
+  uint32_t phc = 0, php = S > 2 ? 0u : 1u;
   for (int r = i0; r < i1; r++, orow += n) {
     const int k = r - r_first;
-    tma::mbar_wait(&bars[k % S], (k / S) & 1);
-    tma::mbar_wait(&bars[(k + 1) % S], ((k + 1) / S) & 1);
+    tma::mbar_wait(&bars[sc], phc);
+    tma::mbar_wait(&bars[sp], php);
     if (active && r >= 1 && r <= n - 2 && (jin[0] || jin[1])) {
-      const T* Um = ring + ((k - 1) % S) * UW + H + jl;
-      const T* Uc = ring + (k % S) * UW + H + jl;
-      const T* Up = ring + ((k + 1) % S) * UW + H + jl;
+      const T* Um = ring + sm * UW + H + jl;
+      const T* Uc = ring + sc * UW + H + jl;
+      const T* Up = ring + sp * UW + H + jl;
       const V um = *reinterpret_cast<const V*>(Um), u0 = *reinterpret_cast<const V*>(Uc),
               up = *reinterpret_cast<const V*>(Up);
       const T ul = Uc[-1], ur = Uc[2];
@@ -478,6 +488,10 @@ __global__ void __launch_bounds__(128, 8)
     }
     __syncthreads();  // row r-1's stage is free
     if (tid == 0 && k - 1 + S < nrows) issue(k - 1 + S);
+    sm = sc;
+    sc = sp;
+    phc = php;
+    if (++sp == S) sp = 0, php ^= 1u;
   }
 }
 
