@@ -11,7 +11,7 @@
 #include "star3d_plane.cuh"
 #include "star3d_primal.cuh"
 #include "star3d_r4.cuh"
-#include "star3d_r4_f64.cuh"
+#include "star3d_f64.cuh"
 #include "star3d_tma.cuh"
 
 namespace sgb {
@@ -94,12 +94,11 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
   }
   // plane-streaming kernel for radius 4 (measured: fp64 768^3 29 -> ~12 ms);
   // radius 1 keeps the per-point kernel (measured faster there)
-  if constexpr (MODE == 2 && std::is_same<T, double>::value) {
-    // fp64 radius 4: the register-blocked streaming kernel (star3d_r4_f64.cuh)
+  if constexpr (std::is_same<T, double>::value) {
+    // fp64: the register-blocked streaming kernel (star3d_f64.cuh)
     if (!std::getenv("SGB_F64_PLANE") && !std::getenv("SGB_GENERIC_POINT") && n <= 46340) {
-      const int rc = star3_r4_f64_gather(g, lo, hi, out_i0, out_i1, D, (const double*)c,
-                                         (double*)c_b, (const double*)u_1, (double*)u_1_b,
-                                         (const double*)u_b, s, name);
+      const int rc = star3_f64_stream_gather<MODE>(g, lo, hi, out_i0, out_i1, D, c, c_b, u_1,
+                                                   u_1_b, u_2_b, u_b, s, name);
       if (rc != 1) return rc;
     }
   }

@@ -1,25 +1,27 @@
-// fp64 radius-4 streaming gather adjoint (sm_100a): the reference's own
-// precision on the cfg 4 / 5 stencil.
+// fp64 streaming gather adjoint for the 3D stars (sm_100a): the reference's
+// own precision on the cfg 2 (radius 1, c or c^2, u_2 active) and cfg 4 / 5
+// (radius 4, c^2) stencils.
 //
 // Mathematics and boundary predicate as every 3D gather kernel here (SURVEY
 // Appendix C; reference adjoint.cpp:73-163 / interp.cpp:189-198):
-//   u_1_b[o] += sum_l w_l q(o - o_l) + 2 u_b[o] [o in B],  q = D c^2 u_b [x in B]
-//   c_b[o]   += g[o] Lap25(u_1)[o],                         g = 2 D c u_b [o in B]
+//   u_1_b[o] += sum_l w_l q(o - o_l) + 2 u_b[o] [o in B],  q = D c^(1|2) u_b [x in B]
+//   c_b[o]   += g[o] Lap(u_1)[o],      g = D u_b | 2 D c u_b  [o in B]
+//   u_2_b[o] -= u_b[o] [o in B]        (radius-1 specs)
 // Structure of the fp32 v7 kernel (star3d_r4.cuh) re-balanced for doubles,
 // where the shared-memory pipe -- not DRAM -- bounded the plane kernel it
 // replaces (star3d_plane.cuh: one point per thread, 17 shared loads per
 // point and field, ncu mio_throttle / barrier stalls, profiles/):
 //   * one CTA per SM (512 threads) owns a 32 (k) x 32 (j) column tile and
 //     streams over i; per plane one elected thread issues TMA loads of the
-//     c / u_b / u_1 halo boxes (40 x 40) and the c_b / u_1_b tiles of the
-//     output plane o = p - R into a 3-stage mbarrier ring;
+//     c / u_b / u_1 halo boxes and the c_b / u_1_b tiles of the output plane
+//     o = p - R (and the u_2_b tile of plane p) into a 3-stage mbarrier ring;
 //   * the seed map is windowed to the primal box, so TMA's zero fill is the
 //     seed mask in j and k (the i test is per plane);
 //   * warps 0-7 carry Lap(u_1) (emit c_b), warps 8-15 the q stencil (emit
 //     u_1_b); each thread owns 2 rows x 2 k points of one field: k neighbours
-//     from a 10-double window (5 LDS.128 per row), j neighbours from shared
-//     rows common to its two rows, i in 2R+1 rotating accumulators -- 4.5
-//     16-byte shared loads per point and field instead of 17 8-byte ones;
+//     from a 16-byte-load window per row, j neighbours from shared rows
+//     common to its two rows, i in 2R+1 rotating accumulators -- at radius 4
+//     4.5 16-byte shared loads per point and field instead of 17 8-byte ones;
 //   * g is formed in the q-pass; one q buffer and an R+1-slot g ring (smem
 //     budget), so a second barrier per plane closes the q / g reuse.
 #pragma once
@@ -29,24 +31,29 @@
 
 namespace sgb {
 
+template <int MODE>
 struct StarTileD {
-  static constexpr int R = 4;
-  static constexpr int TK = 32, TJ = 32, HK = 4, HJ = 4;
-  static constexpr int BW = TK + 2 * HK;  // 40 doubles: 320-byte box rows
+  static constexpr int R = Star3<MODE>::R;
+  static constexpr int TK = 32, TJ = 32, HJ = R;
+  static constexpr int HK = R > 2 ? R : 2;  // k halo: >= R, even (16-byte loads)
+  static constexpr int BW = TK + 2 * HK;    // box row (40 / 36 doubles)
   static constexpr int BJ = TJ + 2 * HJ;
   static constexpr int RING = 2 * R + 1;
   static constexpr int NS = 3;
   static constexpr int QD = R + 1;
   static constexpr int ROLE = (TK / 2) * (TJ / 2);  // 256 threads per field
   static constexpr int THREADS = 2 * ROLE;
-  static constexpr int BOX = BW * BJ;  // 1600 doubles = 12800 B (128-byte multiple)
+  static constexpr int BOX = BW * BJ;
+  static constexpr int BP = (BOX + 15) / 16 * 16;  // box slot stride: 128-byte aligned
   static constexpr int TILE = TK * TJ;
-  static constexpr int SF = 3 * BOX + 2 * TILE;
+  static constexpr int NT = Star3<MODE>::kU2 ? 3 : 2;  // c_b, u_1_b (, u_2_b) tiles
+  static constexpr int SF = 3 * BP + NT * TILE;
   static constexpr int QPAIRS = BOX / 2;
   static constexpr int EPT = (QPAIRS + THREADS - 1) / THREADS;
-  static constexpr size_t SMEM = (size_t)(NS * SF + BOX + QD * TILE) * 8 + NS * 8;
+  static constexpr size_t SMEM = (size_t)(NS * SF + BP + QD * TILE) * 8 + NS * 8;
   static_assert(RING % NS == 0, "static stage index");
-  static_assert((BOX * 8) % 128 == 0 && (TILE * 8) % 128 == 0, "TMA destinations 128-B aligned");
+  static_assert((TILE * 8) % 128 == 0, "TMA destinations 128-B aligned");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
 __device__ __forceinline__ double2 ldd2(const double* p) {
@@ -56,31 +63,38 @@ __device__ __forceinline__ double2 fmad2(double w, const double2& v, const doubl
   return make_double2(fma(w, v.x, a.x), fma(w, v.y, a.y));
 }
 
-// in-plane k stencil of 2 points (k, k+1) of one row: window k-4 .. k+5
+// in-plane k stencil of 2 points (k, k+1) of one row: window k-HK .. k+HK+1
+template <int R, int HK>
 __device__ __forceinline__ double2 kstencil_d(const double* row, double w0,
-                                              const double (&wr)[5]) {
-  const double2 a = ldd2(row - 4), b = ldd2(row - 2), c = ldd2(row), d = ldd2(row + 2),
-                e = ldd2(row + 4);
-  const double w[10] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
-  double p0 = w0 * w[4], p1 = w0 * w[5];
+                                              const double (&wr)[R + 1]) {
+  double kw[2 * HK + 2];
 #pragma unroll
-  for (int r = 1; r <= 4; r++) {
-    p0 = fma(wr[r], w[4 - r] + w[4 + r], p0);
-    p1 = fma(wr[r], w[5 - r] + w[5 + r], p1);
+  for (int q = 0; q <= HK; q++) {
+    const double2 v = ldd2(row - HK + 2 * q);
+    kw[2 * q] = v.x;
+    kw[2 * q + 1] = v.y;
+  }
+  double p0 = w0 * kw[HK], p1 = w0 * kw[HK + 1];
+#pragma unroll
+  for (int r = 1; r <= R; r++) {
+    p0 = fma(wr[r], kw[HK - r] + kw[HK + r], p0);
+    p1 = fma(wr[r], kw[HK + 1 - r] + kw[HK + 1 + r], p1);
   }
   return make_double2(p0, p1);
 }
 
 // 2 rows x 2 k of one field, plane phase ph: in-plane stencil into acc[ph],
 // the plane's centre values into the i-neighbours' accumulators.
+template <int MODE>
 __device__ __forceinline__ void field2x2_d(const double* F, int r0, int col, double w0,
-                                           const double (&wr)[5], double2 (&acc)[9][2],
-                                           int ph) {
-  constexpr int BW = StarTileD::BW, R = 4, RING = 9;
+                                           const double (&wr)[StarTileD<MODE>::R + 1],
+                                           double2 (&acc)[StarTileD<MODE>::RING][2], int ph) {
+  constexpr int BW = StarTileD<MODE>::BW, HK = StarTileD<MODE>::HK;
+  constexpr int R = StarTileD<MODE>::R, RING = StarTileD<MODE>::RING;
   const double* row0 = F + r0 * BW + col;
   const double2 b0 = ldd2(row0), b1 = ldd2(row0 + BW);
-  double2 in0 = kstencil_d(row0, w0, wr);
-  double2 in1 = kstencil_d(row0 + BW, w0, wr);
+  double2 in0 = kstencil_d<R, HK>(row0, w0, wr);
+  double2 in1 = kstencil_d<R, HK>(row0 + BW, w0, wr);
   in0 = fmad2(wr[1], b1, in0);
   in1 = fmad2(wr[1], b0, in1);
 #pragma unroll
@@ -106,24 +120,29 @@ __device__ __forceinline__ void field2x2_d(const double* F, int r0, int col, dou
   }
 }
 
-__global__ void __launch_bounds__(StarTileD::THREADS, 1)
-    star3_r4_f64_kernel(const __grid_constant__ CUtensorMap tm_c,
-                        const __grid_constant__ CUtensorMap tm_ub,
-                        const __grid_constant__ CUtensorMap tm_u1,
-                        const __grid_constant__ CUtensorMap tm_cb,
-                        const __grid_constant__ CUtensorMap tm_u1b, double* __restrict__ c_b,
-                        double* __restrict__ u_1_b, int n, int i_base, int lo, int hi,
-                        int out_i0, int out_i1, int chunk, int tiles_k, double D) {
-  using Tl = StarTileD;
-  using S3 = Star3<2>;
+// UBW: the u_b map is windowed to [lo, hi]^2 (TMA zero fill = seed mask);
+// otherwise the mask is applied in the q-pass and the centre term.
+template <int MODE, bool UBW>
+__global__ void __launch_bounds__(StarTileD<MODE>::THREADS, 1)
+    star3_f64_stream_kernel(const __grid_constant__ CUtensorMap tm_c,
+                            const __grid_constant__ CUtensorMap tm_ub,
+                            const __grid_constant__ CUtensorMap tm_u1,
+                            const __grid_constant__ CUtensorMap tm_cb,
+                            const __grid_constant__ CUtensorMap tm_u1b,
+                            const __grid_constant__ CUtensorMap tm_u2b,
+                            double* __restrict__ c_b, double* __restrict__ u_1_b,
+                            double* __restrict__ u_2_b, int n, int i_base, int lo, int hi,
+                            int out_i0, int out_i1, int chunk, int tiles_k, double D) {
+  using Tl = StarTileD<MODE>;
+  using S3 = Star3<MODE>;
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
-  constexpr int RING = Tl::RING, NS = Tl::NS, BOX = Tl::BOX, QD = Tl::QD;
+  constexpr int RING = Tl::RING, NS = Tl::NS, BOX = Tl::BOX, BP = Tl::BP, QD = Tl::QD;
   constexpr int SF = Tl::SF, TILE = Tl::TILE, ROLE = Tl::ROLE;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* stage = reinterpret_cast<double*>(smem_raw);  // [NS][c, ub, u1 boxes | cb, u1b tiles]
+  double* stage = reinterpret_cast<double*>(smem_raw);  // [NS][c, ub, u1 boxes | tiles]
   double* Q = stage + NS * SF;                          // q box
-  double* gq = Q + BOX;                                 // [QD][TJ][TK] g of centres
+  double* gq = Q + BP;                                  // [QD][TJ][TK] g of centres
   uint64_t* bars = reinterpret_cast<uint64_t*>(gq + QD * TILE);
 
   const int tid = threadIdx.x;
@@ -155,14 +174,19 @@ __global__ void __launch_bounds__(StarTileD::THREADS, 1)
     double* dst = stage + s * SF;
     const int pl = pstart + it - i_base;
     const bool emit = it >= 2 * R;
-    tma::mbar_arrive_expect_tx(&bars[s], (3 * BOX + (emit ? 2 * TILE : 0)) * 8);
+    const int p = pstart + it;
+    const bool u2 = S3::kU2 && p >= o_begin && p < o_end;  // u_2_b tile of plane p
+    tma::mbar_arrive_expect_tx(&bars[s],
+                               (3 * BOX + ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE) * 8);
     tma::load_3d(dst, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
-    tma::load_3d(dst + BOX, &tm_ub, &bars[s], k0 - HK - lo, j0 - HJ - lo, pl);
-    tma::load_3d(dst + 2 * BOX, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + BP, &tm_ub, &bars[s], k0 - HK - (UBW ? lo : 0), j0 - HJ - (UBW ? lo : 0),
+                 pl);
+    tma::load_3d(dst + 2 * BP, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
     if (emit) {
-      tma::load_3d(dst + 3 * BOX, &tm_cb, &bars[s], k0, j0, pl - R);
-      tma::load_3d(dst + 3 * BOX + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
+      tma::load_3d(dst + 3 * BP, &tm_cb, &bars[s], k0, j0, pl - R);
+      tma::load_3d(dst + 3 * BP + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
     }
+    if (u2) tma::load_3d(dst + 3 * BP + 2 * TILE, &tm_u2b, &bars[s], k0, j0, pl);
   };
   if (tid == 0)
     for (int it = 0; it < NS && it < P; it++) issue(it);
@@ -175,11 +199,16 @@ __global__ void __launch_bounds__(StarTileD::THREADS, 1)
 
   // q-pass pairs of this thread: box offset and, for centres, g-tile offset
   int qoff[Tl::EPT], goff[Tl::EPT];
+  uint32_t qmask = 0;  // !UBW: bit 2m+x = element x of pair m inside [lo, hi]^2
 #pragma unroll
   for (int m = 0; m < Tl::EPT; m++) {
     const int e = tid + m * Tl::THREADS;
     const int row = e / (BW / 2), c2 = e - row * (BW / 2);
     qoff[m] = e < Tl::QPAIRS ? row * BW + 2 * c2 : -1;
+    const int jg = j0 - HJ + row, kg = k0 - HK + 2 * c2;
+#pragma unroll
+    for (int x = 0; x < 2; x++)
+      if (jg >= lo && jg <= hi && kg + x >= lo && kg + x <= hi) qmask |= 1u << (2 * m + x);
     goff[m] = (e < Tl::QPAIRS && row >= HJ && row < HJ + Tl::TJ && c2 >= HK / 2 &&
                c2 < HK / 2 + TK / 2)
                   ? (row - HJ) * TK + 2 * (c2 - HK / 2)
@@ -216,8 +245,8 @@ __global__ void __launch_bounds__(StarTileD::THREADS, 1)
         const int s = ph % NS;
         const int p = pstart + it;
         const double* Cs = stage + s * SF;
-        const double* UBs = Cs + BOX;
-        const double* U1s = Cs + 2 * BOX;
+        const double* UBs = Cs + BP;
+        const double* U1s = Cs + 2 * BP;
         double* G = gq + (it % QD) * TILE;
         const int o = p - R;
         const bool pin = p >= lo && p <= hi;
@@ -230,32 +259,58 @@ __global__ void __launch_bounds__(StarTileD::THREADS, 1)
             const int qo = qoff[m];
             double2 qv = make_double2(0.0, 0.0), gv = qv;
             if (pin) {
-              const double2 cv = ldd2(Cs + qo), uv = ldd2(UBs + qo);
+              const double2 cv = ldd2(Cs + qo);
+              double2 uv = ldd2(UBs + qo);
+              if (!UBW)
+                uv = make_double2((qmask >> (2 * m)) & 1 ? uv.x : 0.0,
+                                  (qmask >> (2 * m + 1)) & 1 ? uv.y : 0.0);
               const double2 du = make_double2(D * uv.x, D * uv.y);
-              qv = make_double2(cv.x * cv.x * du.x, cv.y * cv.y * du.y);
-              gv = make_double2(2.0 * cv.x * du.x, 2.0 * cv.y * du.y);
+              if (S3::kC2) {  // q = D c^2 u_b, g = 2 D c u_b
+                qv = make_double2(cv.x * cv.x * du.x, cv.y * cv.y * du.y);
+                gv = make_double2(2.0 * cv.x * du.x, 2.0 * cv.y * du.y);
+              } else {        // q = D c u_b, g = D u_b
+                qv = make_double2(cv.x * du.x, cv.y * du.y);
+                gv = du;
+              }
             }
             *reinterpret_cast<double2*>(Q + qo) = qv;
             if (goff[m] >= 0) *reinterpret_cast<double2*>(G + goff[m]) = gv;
           }
         }
-        // ---- q role: the 2 u_b centre term of output plane p
+        // ---- q role: the 2 u_b centre term of output plane p, and the u_2
+        // partial u_2_b[p] -= u_b[p] on B (radius-1 specs) at plane p itself
         if (q_role && pin) {
 #pragma unroll
-          for (int h = 0; h < 2; h++)
-            acc[ph][h] = fmad2(2.0, ldd2(UBs + (r0 + h) * BW + col), acc[ph][h]);
+          for (int h = 0; h < 2; h++) {
+            double2 ubm = ldd2(UBs + (r0 + h) * BW + col);
+            if (!UBW)
+              ubm = make_double2((inb >> (2 * h)) & 1 ? ubm.x : 0.0,
+                                 (inb >> (2 * h + 1)) & 1 ? ubm.y : 0.0);
+            acc[ph][h] = fmad2(2.0, ubm, acc[ph][h]);
+            if (S3::kU2 && p >= o_begin && p < o_end) {
+              const uint32_t mk = inb >> (2 * h);
+              if (((grid >> h) & 1) && (mk & 3)) {
+                const double2 u2 = ldd2(Cs + 3 * BP + 2 * TILE + trow + h * TK);
+                const double2 nv = make_double2((mk & 1) ? u2.x + -ubm.x : u2.x,
+                                                (mk & 2) ? u2.y + -ubm.y : u2.y);
+                __stcs(reinterpret_cast<double2*>(u_2_b + (long long)(p - i_base) * plane +
+                                                  coff + h * n),
+                       nv);
+              }
+            }
+          }
         }
         __syncthreads();  // Q / G of plane p complete; stage of plane p-1 free
         if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
 
-        field2x2_d(q_role ? Q : U1s, r0, col, w0, wr, acc, ph);
+        field2x2_d<MODE>(q_role ? Q : U1s, r0, col, w0, wr, acc, ph);
 
         // ---- emit output plane o = p - R
         if (it >= 2 * R) {
           const int es = (ph + R + 1) % RING;
           const long long obase = (long long)(o - i_base) * plane;
           const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
-          const double* OLD = Cs + 3 * BOX + (q_role ? TILE : 0) + trow;
+          const double* OLD = Cs + 3 * BP + (q_role ? TILE : 0) + trow;
           if (!q_role) {
             if (oout == 0) {
               const double* Go = gq + ((it - R) % QD) * TILE + trow;
@@ -318,30 +373,37 @@ inline int encode_3d_window_f64(CUtensorMap* map, const double* base, long long 
 }
 
 // Host launcher; returns 1 when the shape does not fit this kernel (the
-// caller uses the plane kernels), 0 / negative like the other entries.
-inline int star3_r4_f64_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
-                               long long out_i1, double D, const double* c, double* c_b,
-                               const double* u_1, double* u_1_b, const double* u_b,
-                               cudaStream_t s, const char* name) {
-  using Tl = StarTileD;
+// caller uses the plane / per-point kernels), 0 / negative like the others.
+template <int MODE>
+inline int star3_f64_stream_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
+                                   long long out_i1, double D, const double* c, double* c_b,
+                                   const double* u_1, double* u_1_b, double* u_2_b,
+                                   const double* u_b, cudaStream_t s, const char* name) {
+  using Tl = StarTileD<MODE>;
+  constexpr bool kU2 = Star3<MODE>::kU2;
   if (g.n % 2 != 0 || g.n > (1 << 20) || g.n < 2 * Tl::R + 2 || hi < lo) return 1;
   for (const void* p : {(const void*)c, (const void*)c_b, (const void*)u_1, (const void*)u_1_b,
-                        (const void*)u_b})
+                        (const void*)u_b, (const void*)(kU2 ? u_2_b : u_1_b)})
     if (reinterpret_cast<uintptr_t>(p) & 15) return 1;
-  CUtensorMap maps[5];
+  CUtensorMap maps[6];
   int rc = encode_3d_t(&maps[0], c, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
   const int w = encode_3d_window_f64(&maps[1], u_b, g.n, g.nplanes, lo, hi - lo + 1, Tl::BW,
                                      Tl::BJ, name);
   if (w < 0) return w;
-  if (w == 1) return 1;  // unaligned seed window: plane kernels
+  const bool ubw = w == 0;  // else (odd lo*(n+1)): full map, mask in the kernel
+  if (!ubw) rc |= encode_3d_t(&maps[1], u_b, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
   rc |= encode_3d_t(&maps[2], u_1, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
   rc |= encode_3d_t(&maps[3], (const double*)c_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
   rc |= encode_3d_t(&maps[4], (const double*)u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
+  rc |= encode_3d_t(&maps[5], (const double*)(kU2 ? u_2_b : u_1_b), g.n, g.nplanes, Tl::TK,
+                    Tl::TJ, name);
   if (rc) return SGB_EINVAL;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(star3_r4_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Tl::SMEM);
+    cudaFuncSetAttribute(star3_f64_stream_kernel<MODE, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
+    cudaFuncSetAttribute(star3_f64_stream_kernel<MODE, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
     attr = true;
   }
   const int tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
@@ -362,9 +424,10 @@ inline int star3_r4_f64_gather(const Slab3& g, long long lo, long long hi, long 
   }
   const int chunk = (int)((nout + nch - 1) / nch);
   const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
-  star3_r4_f64_kernel<<<dim3((unsigned)tiles, gy), Tl::THREADS, Tl::SMEM, s>>>(
-      maps[0], maps[1], maps[2], maps[3], maps[4], c_b, u_1_b, (int)g.n, (int)g.i_base, (int)lo,
-      (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D);
+  auto kern = ubw ? star3_f64_stream_kernel<MODE, true> : star3_f64_stream_kernel<MODE, false>;
+  kern<<<dim3((unsigned)tiles, gy), Tl::THREADS, Tl::SMEM, s>>>(
+      maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
+      (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D);
   return launch_status(name);
 }
 
