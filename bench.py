@@ -710,13 +710,15 @@ def time_loop_bench(torch, api, n, scalars, arrays, T=16, K=4):
     pts = n ** 3
     primal_steps = (T - 1) + stats["recomputed_steps"]
     adj_steps = stats["adjoint_steps"]
-    # kernels' algorithmic bytes: primal 16, gather 28, box set 8 B/pt
-    alg = pts * (16 * primal_steps + (28 + 8) * adj_steps)
+    # kernels' algorithmic bytes: primal 16, fused reverse step 32 B/pt (the
+    # gather's 28 + the u_2 partial written; unfused it was gather + an 8 B/pt
+    # box set)
+    alg = pts * (16 * primal_steps + 32 * adj_steps)
     return {"n": n, "T": T, "checkpoint_every": K, "ms": ms,
             "ms_per_reverse_step": ms / max(1, adj_steps), **stats,
             "primal_launches": primal_steps,
             "alg_GB_s_kernels": alg / (ms / 1e3) / 1e9,
-            "note": "alg bytes count the primal / gather / box-set kernels only"}
+            "note": "alg bytes count the primal and fused reverse-step kernels only"}
 
 
 def run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d):
@@ -771,10 +773,34 @@ def run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d):
     h2d_gbs = copy_gbs(db, hb)
     d2h_gbs = copy_gbs(hb, db)
     floor_ms = max(h2d / 1e9 / h2d_gbs, d2h / 1e9 / d2h_gbs) * 1e3
+    # the same step's copies with both directions in flight at once (no
+    # kernel): PCIe is full duplex, but the D2H traffic slows the H2D side
+    # (~7% here), so this -- not the one-way figure -- is what a pipelined
+    # step can reach
+    dev = {nm: torch.empty_like(arrays[nm]) for nm in names}
+    side = torch.cuda.Stream()
+
+    def copies():
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for nm in rmw:
+                host[nm].copy_(dev[nm], non_blocking=True)
+        for nm in names:
+            dev[nm].copy_(host[nm], non_blocking=True)
+        torch.cuda.current_stream().wait_stream(side)
+    copies()
+    torch.cuda.synchronize()
+    s.record()
+    copies()
+    e.record()
+    torch.cuda.synchronize()
+    both_ms = s.elapsed_time(e)
+    del dev
     return {"value": pts / (ms / 1e3) / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k,
             "pcie_h2d_GBps": h2d_gbs, "pcie_d2h_GBps": d2h_gbs,
             "copy_floor_ms": floor_ms, "frac_of_copy_floor": floor_ms / ms,
+            "copy_floor_concurrent_ms": both_ms, "frac_of_concurrent_copy_floor": both_ms / ms,
             "path": "sgb_plan_run_adjoint_host (pinned host buffers)" if sl is None
             else "per-rank sgb_plan_create_slab + run_adjoint_host (pinned local planes incl. "
                  "halos; owned planes returned)"}

@@ -197,6 +197,13 @@ int sgb_box_set_f32(float* y, const float* x, double alpha, int n, int lo, int h
                     int nplanes, sgb_stream_t stream);
 int sgb_box_set_f64(double* y, const double* x, double alpha, int n, int lo, int hi, int i_base,
                     int nplanes, sgb_stream_t stream);
+/* One reverse step of a wave3d_r4 time loop (drivers.time_loop_adjoint; no
+ * reference counterpart -- the reference's scope ends at one loop nest,
+ * SPEC.md:8): the gather adjoint wave3d_r4_b (c_b, u_1_b accumulated) and
+ * the u_2 partial u_2_b = -u_b on [4, n-5]^3, 0 elsewhere, in one pass
+ * (bitwise = wave3d_r4_b_f32 followed by sgb_box_set_f32(u_2_b, u_b, -1)). */
+int sgb_wave3d_r4_b_step_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                             float* u_b, float* u_2_b, sgb_stream_t stream);
 /* one interior pass of the 5-point average u <- (u + 4 neighbours)/5 (2D) */
 int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream);
 

@@ -165,6 +165,25 @@ def box_set(y, x, alpha: float, n: int, lo: int, hi: int, i_base: int = 0,
                "box_set")
 
 
+def adjoint_time_step(n: int, scalars, arrays, u_2_b, stream=None):
+    """One reverse step of a wave3d_r4 time loop (fp32, device arrays): the
+    gather adjoint (c_b, u_1_b accumulated from the seed u_b) and the u_2
+    partial u_2_b = -u_b on [4, n-5]^3, 0 elsewhere, fused into the gather
+    kernel (sgb_wave3d_r4_b_step_f32)."""
+    import torch
+    names = array_params("wave3d_r4", "adjoint")
+    ts = [arrays.get(k) for k in names] + [u_2_b]
+    for nm, t in zip(names + ["u_2_b"], ts):
+        if t is None or not (t.is_cuda and t.is_contiguous()) or t.dtype != torch.float32 \
+                or t.numel() != int(n) ** 3:
+            raise _lib.StencilError(f"adjoint_time_step: '{nm}' must be a contiguous fp32 "
+                                    f"CUDA tensor of {n}^3 elements")
+    ptr = [ctypes.c_void_p(t.data_ptr()) for t in ts[:-1]]
+    _lib.check(_lib.lib().sgb_wave3d_r4_b_step_f32(
+        n, float(scalars["D"]), *ptr, ctypes.c_void_p(u_2_b.data_ptr()), _stream_ptr(stream)),
+        "sgb_wave3d_r4_b_step_f32")
+
+
 def smooth5(src, dst, n: int, stream=None):
     _lib.check(_lib.lib().sgb_smooth5_f64(ctypes.c_void_p(src.data_ptr()),
                                           ctypes.c_void_p(dst.data_ptr()), n,

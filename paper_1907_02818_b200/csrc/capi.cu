@@ -345,6 +345,25 @@ int wave3d_r4_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, floa
                                 i_base, nplanes, out_i0, out_i1, as_stream(stream));
 }
 
+int sgb_wave3d_r4_b_step_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                             float* u_b, float* u_2_b, sgb_stream_t stream) {
+  const char* name = "sgb_wave3d_r4_b_step";
+  if (n <= 0) return einval(std::string(name) + ": n must be positive");
+  if (!guard_ok(WAVE3D_R4, n)) return SGB_GUARD;
+  if (!c || !c_b || !u_1 || !u_1_b || !u_b || !u_2_b)
+    return einval(std::string(name) + ": null array");
+  if (u_2_b == u_b || u_2_b == u_1_b || u_2_b == c_b)
+    return einval(std::string(name) + ": u_2_b must not alias the other arrays");
+  cudaStream_t s = as_stream(stream);
+  if (star3_tma_supported<3, float>(n) && !std::getenv("SGB_STEP_UNFUSED"))
+    return star3_v7_gather<3>(Slab3{n, 0, n}, 4, n - 5, 0, n, (float)D, c, c_b, u_1, u_1_b,
+                              u_2_b, u_b, s, name);
+  // other shapes: the two launches it fuses
+  const int rc = wave3d_r4_b_f32(n, D, c, c_b, u_1, u_1_b, u_b, stream);
+  if (rc != 0) return rc;
+  return sgb_box_set_f32(u_2_b, u_b, -1.0, n, 4, n - 5, 0, n, stream);
+}
+
 int wave3d_r4_b_slab_peer_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
                               float* u_b, int i_base, int nplanes, int out_i0, int out_i1,
                               const float* lo_c, const float* lo_u_1, const float* lo_u_b,

@@ -21,10 +21,14 @@ namespace sgb {
 // MODE 0: wave3d_c  (c linear; u_2 active)
 // MODE 1: wave3d_c2 (c^2;      u_2 active)
 // MODE 2: wave3d_r4 (c^2;      u_2 passive; radius 4)
+// MODE 3: wave3d_r4 gather that also writes the u_2 partial of a time loop,
+//         u_2_b = -u_b on B and 0 elsewhere (drivers.time_loop_adjoint; the
+//         fused form of gather + sgb_box_set, fp32 streaming kernel only)
 template <int MODE>
 struct Star3 {
-  static constexpr int R = MODE == 2 ? 4 : 1;
-  static constexpr bool kU2 = MODE != 2;
+  static constexpr int R = MODE >= 2 ? 4 : 1;
+  static constexpr bool kU2 = MODE < 2;
+  static constexpr bool kU2Set = MODE == 3;
   static constexpr bool kC2 = MODE != 0;
   static constexpr bool kIncrement = MODE != 2;  // primal mode of the spec
   // weight of offset |r| along one axis; r == 0 gives the folded 3-axis centre

@@ -510,6 +510,26 @@ __device__ __forceinline__ void star3_v7_body(
             }
           }
         }
+        // ---- time-loop u_2 partial (MODE 3): u_2_b[p] = -u_b[p] on B, 0
+        // elsewhere, for every owned plane p of this chunk (sgb_box_set's
+        // values bit for bit: 0 - u is 0 + (-1) u for every u)
+        if (S3::kU2Set && q_role && p >= o_begin && p < o_end) {
+          float* u2_plane = u_2_b + (long long)(p - i_base) * plane;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            if (!INT && !((fm >> (22 + h)) & 1)) continue;  // row outside the grid
+            float4 ubm = lds4(UBs + (r0 + h) * BW + col);
+            bool m[4] = {pin, pin, pin, pin};
+            if (!INT) {
+              const bool jin = (fm >> (20 + h)) & 1;
+#pragma unroll
+              for (int x = 0; x < 4; x++) m[x] = pin && jin && ((fm >> (16 + x)) & 1);
+            }
+            __stcs(reinterpret_cast<float4*>(u2_plane + coff + h * n),
+                   make_float4(m[0] ? 0.f - ubm.x : 0.f, m[1] ? 0.f - ubm.y : 0.f,
+                               m[2] ? 0.f - ubm.z : 0.f, m[3] ? 0.f - ubm.w : 0.f));
+          }
+        }
         __syncthreads();
         if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
 

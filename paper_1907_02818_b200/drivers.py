@@ -229,7 +229,7 @@ def time_loop_forward(n, T, D, c, u0, u1, store=None):
     return cur
 
 
-def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None):
+def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None, fused=True):
     """Gradient of J = <w, u^T> w.r.t. (u^0, u^1, c) through T-1 primal steps.
     Returns (u0_b, u1_b, c_b, stats)."""
     import math
@@ -283,10 +283,15 @@ def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None):
             states[t + 1] = nxt
             recomputed += 1
         for t in reversed(range(s, t_end)):
-            api.adjoint(fam, n, {"D": D}, {"c": c, "c_b": c_b, "u_1": states[t],
-                                           "u_1_b": ub_cur, "u_b": ub_next})
-            # u-bar^{t-1} = -u-bar^{t+1} on B (the u_2 partial), 0 elsewhere
-            api.box_set(ub_prev, ub_next, -1.0, n, lo, hi)
+            # gather adjoint of step t, and u-bar^{t-1} = -u-bar^{t+1} on B
+            # (the u_2 partial), 0 elsewhere -- one fused pass unless `fused`
+            # is off (then the gather and sgb_box_set, bitwise the same)
+            arrs = {"c": c, "c_b": c_b, "u_1": states[t], "u_1_b": ub_cur, "u_b": ub_next}
+            if fused and c.dtype == torch.float32:
+                api.adjoint_time_step(n, {"D": D}, arrs, ub_prev)
+            else:
+                api.adjoint(fam, n, {"D": D}, arrs)
+                api.box_set(ub_prev, ub_next, -1.0, n, lo, hi)
             ub_next, ub_cur, ub_prev = ub_cur, ub_prev, ub_next
         for t, st in states.items():
             release(st, keep)

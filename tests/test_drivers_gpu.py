@@ -231,6 +231,36 @@ def test_time_loop_adjoint_checkpointing_and_gradient(mods):
     assert abs(fd - ad) / (1 + abs(ad)) < 1e-6, (fd, ad)
 
 
+@pytest.mark.parametrize("n", [40, 68, 37])
+def test_time_loop_fused_step_bitwise(mods, n, monkeypatch):
+    """fp32 time loop: the fused reverse step (gather adjoint + u_2 partial in
+    one radius-4 streaming pass, sgb_wave3d_r4_b_step_f32) equals the gather
+    followed by sgb_box_set bit for bit -- the whole gradient after T steps,
+    incl. the zeros outside the box; n = 37 takes the entry's two-launch path."""
+    torch, api, drivers = mods
+    T, D = 6, 0.01
+    g = torch.Generator(device="cpu").manual_seed(n)
+    c = (torch.rand((n, n, n), generator=g) * 3 + 1.5).cuda()
+    u0, u1, w = (torch.randn((n, n, n), generator=g).cuda() for _ in range(3))
+    a = drivers.time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=2, fused=True)
+    b = drivers.time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=2, fused=False)
+    for x, y in zip(a[:3], b[:3]):
+        assert torch.equal(x, y)
+    # one step against the two-launch form, with a poisoned u_2_b buffer
+    arrs = {"c": c, "c_b": torch.randn_like(c), "u_1": u1, "u_1_b": torch.randn_like(c),
+            "u_b": w}
+    ref = {k: v.clone() for k, v in arrs.items()}
+    u2 = torch.full_like(c, float("nan"))
+    api.adjoint_time_step(n, {"D": D}, arrs, u2)
+    api.adjoint("wave3d_r4", n, {"D": D}, ref)
+    u2_ref = torch.empty_like(c)
+    api.box_set(u2_ref, w, -1.0, n, 4, n - 5)
+    for k in ("c_b", "u_1_b"):
+        assert torch.equal(arrs[k], ref[k]), k
+    assert torch.equal(u2, u2_ref)
+    assert torch.equal(u2.view(torch.int32), u2_ref.view(torch.int32))  # zero signs too
+
+
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("n,lo,hi,base,npl", [(40, 4, 35, 0, 40), (37, 1, 35, 0, 37),
                                               (64, 4, 59, 10, 30), (33, 3, 30, 5, 9)])
