@@ -332,6 +332,8 @@ __global__ void __launch_bounds__(BurgRing<T, S_>::THREADS, 8)
   const bool jin[2] = {inB(j), inB(j + 1)};
   const bool jl_[2] = {inB(j - 1), jin[0]}, jr_[2] = {jin[1], inB(j + 2)};
   const bool jreach[2] = {j >= lo - 1 && j <= hi + 1, j + 1 >= lo - 1 && j + 1 <= hi + 1};
+  // columns j, j+1 and their k-neighbours all inside [lo, hi]
+  const bool inner = jl_[0] && jin[0] && jin[1] && jr_[1];
   T* orow = u1b + (size_t)i0 * n + j;
   tma::mbar_wait(&bars[0], 0);
   // stages of rows r-1, r, r+1 (row r is ring row k = r - r_first) and the
@@ -361,28 +363,50 @@ __global__ void __launch_bounds__(BurgRing<T, S_>::THREADS, 8)
               bP[2] = {bp.x, bp.y};
       T acc[2];
       bool reach[2];
-#pragma unroll
-      for (int m = 0; m < 2; m++) {
+      auto terms = [&](int m, T& t1, T& t2, T& tc, T& t4, T& t5) {
         const T u = ucv[m];
         const T ge = u >= T(0) ? T(1) : T(0), le = -u >= T(0) ? T(1) : T(0);
         const T cen = -C * ((u - uM[m]) * ge + (u - uL[m]) * ge + (uR[m] - u) * le +
                             (uP[m] - u) * le + T(2) * pos0(u) - T(2) * neg0(u)) -
                       T(4) * D + T(1);
-        const T t1 = (C * pos0(uP[m]) + D) * bP[m];
-        const T t2 = (C * pos0(uR[m]) + D) * bR[m];
-        const T t4 = (-C * neg0(uL[m]) + D) * bL[m];
-        const T t5 = (-C * neg0(uM[m]) + D) * bM[m];
-        T a = T(0);
-        a += jin[m] && iin_p ? t1 : T(0);
-        a += iin && jr_[m] ? t2 : T(0);
-        a += iin && jin[m] ? cen * bcv[m] : T(0);
-        a += iin && jl_[m] ? t4 : T(0);
-        a += jin[m] && iin_m ? t5 : T(0);
-        acc[m] = a;
-        reach[m] = (iin && jreach[m]) || (jin[m] && ireach);
+        t1 = (C * pos0(uP[m]) + D) * bP[m];
+        t2 = (C * pos0(uR[m]) + D) * bR[m];
+        tc = cen * bcv[m];
+        t4 = (-C * neg0(uL[m]) + D) * bL[m];
+        t5 = (-C * neg0(uM[m]) + D) * bM[m];
+      };
+      if (iin && iin_m && iin_p && inner) {
+        // both points and all five terms inside the box (all but a 2-point
+        // frame): the same sums without the per-term masks
+#pragma unroll
+        for (int m = 0; m < 2; m++) {
+          T t1, t2, tc, t4, t5;
+          terms(m, t1, t2, tc, t4, t5);
+          T a = T(0) + t1;
+          a += t2;
+          a += tc;
+          a += t4;
+          a += t5;
+          acc[m] = a;
+        }
+        st2cs(orow, oc.x + acc[0], oc.y + acc[1]);
+      } else {
+#pragma unroll
+        for (int m = 0; m < 2; m++) {
+          T t1, t2, tc, t4, t5;
+          terms(m, t1, t2, tc, t4, t5);
+          T a = T(0);
+          a += jin[m] && iin_p ? t1 : T(0);
+          a += iin && jr_[m] ? t2 : T(0);
+          a += iin && jin[m] ? tc : T(0);
+          a += iin && jl_[m] ? t4 : T(0);
+          a += jin[m] && iin_m ? t5 : T(0);
+          acc[m] = a;
+          reach[m] = (iin && jreach[m]) || (jin[m] && ireach);
+        }
+        if (reach[0] || reach[1])
+          st2cs(orow, reach[0] ? oc.x + acc[0] : oc.x, reach[1] ? oc.y + acc[1] : oc.y);
       }
-      if (reach[0] || reach[1])
-        st2cs(orow, reach[0] ? oc.x + acc[0] : oc.x, reach[1] ? oc.y + acc[1] : oc.y);
     }
     __syncthreads();  // row r-1's stage is free
     if (tid == 0 && k - 1 + S < nrows) issue(k - 1 + S);
