@@ -411,18 +411,21 @@ inline int choose_chunks(long long tiles, long long nout, int R, int per_sm) {
     int c = std::atoi(e);
     if (c > 0) return c;
   }
-  // Measured on B200 (768^3 / 1024^3, radius 4, profiles/): chunks of ~96
-  // planes keep the resident CTAs in near lock-step, so the halo rows a tile
-  // shares with its neighbours are still in L2 when the neighbour reads them,
-  // while the 2R re-read i-halo planes per chunk stay ~8% of a chunk.
-  (void)tiles;
-  (void)per_sm;
-  // radius 1 (v1 kernel, far less work per plane): ~192-plane chunks
-  const long long len = R >= 4 ? 96 : 192;
-  long long c = (nout + len / 2) / len;
-  if (c < 1) c = 1;
-  if (c > 64) c = 64;
-  return (int)c;
+  // Wave model (as star3d_r4.cuh): CTAs are equal-length column tiles over
+  // chunk + 2R planes, per_sm resident per SM, so a launch costs
+  // ceil(tiles * c / slots) * (ceil(nout / c) + 2R) plane-times; take the c
+  // minimising it.  At 512^3 radius 1 (256 tiles, 296 slots) it picks 8
+  // chunks, the measured optimum (0.77 ms; 3 chunks of the earlier fixed
+  // ~192-plane rule: 0.81 ms; 7 chunks, one CTA past 6 full waves: 0.81 ms).
+  const long long slots = (long long)per_sm * num_sms();
+  int best_c = 1;
+  long long best = -1;
+  for (int c = 1; c <= 64 && c <= nout; c++) {
+    const long long len = (nout + c - 1) / c;
+    const long long cost = ((tiles * c + slots - 1) / slots) * (len + 2 * R);
+    if (best < 0 || cost < best) best = cost, best_c = c;
+  }
+  return best_c;
 }
 
 template <int MODE>
