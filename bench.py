@@ -119,7 +119,9 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples),
-                "power_w": statistics.median(self.power_w) if self.power_w else None,
+                # NVML's board power is a ~1 s running average: over a short
+                # timed region it lags the load (scripts/sustain_probe.py)
+                "power_w_nvml_avg": statistics.median(self.power_w) if self.power_w else None,
                 "power_limit_w": self.power_limit_w}
 
 
