@@ -24,15 +24,33 @@ __device__ __forceinline__ uint64_t hash3(uint64_t seed, uint64_t stream, uint64
   return mix64(hash_key(seed, stream) + ctr);
 }
 
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {  // murmur3 finaliser
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
 // One Box-Muller pair from the hash of pair index m: (cos branch, sin branch)
-// = the values of flat indices 2m and 2m+1.
+// = the values of flat indices 2m and 2m+1.  32-bit hashing (two chained
+// murmur3 finalisers keyed by the 64-bit stream key) and the MUFU
+// approximations (flush-to-zero lg2 / sqrt / sin / cos; the angle taken in
+// [-pi, pi), where sin.approx / cos.approx are accurate): the generator runs
+// inside cfg 5's timed step, where the 64-bit splitmix + IEEE form was
+// issue-bound (profiles/).
 __device__ __forceinline__ float2 normal_pair(uint64_t key, uint64_t m) {
-  const uint64_t h = mix64(key + m);
-  const float u1 = ((float)(uint32_t)(h >> 40) + 1.0f) * 0x1.0p-24f;  // (0, 1]
-  const float u2 = (float)(uint32_t)(h & 0xFFFFFFu) * 0x1.0p-24f;     // [0, 1)
-  const float rad = sqrtf(-2.0f * __logf(u1));
-  float sn, cs;
-  __sincosf(6.283185307179586f * u2, &sn, &cs);
+  const uint32_t a = fmix32((uint32_t)m ^ (uint32_t)key ^ ((uint32_t)(m >> 32) * 0x9E3779B9u));
+  const uint32_t b = fmix32(a ^ (uint32_t)(key >> 32));
+  const float u1 = ((float)(a >> 8) + 1.0f) * 0x1.0p-24f;                      // (0, 1]
+  const float th = fmaf((float)(b >> 8), 6.283185307179586f * 0x1.0p-24f,
+                        -3.141592653589793f);                                  // [-pi, pi)
+  float l2, rad, sn, cs;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u1));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rad) : "f"(-1.3862943611198906f * l2));  // -2 ln u1
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(sn) : "f"(th));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(cs) : "f"(th));
   return make_float2(rad * cs, rad * sn);
 }
 
@@ -58,39 +76,51 @@ __global__ void fill_random_kernel(T* dst, long long count, long long base, uint
 // 3D fill with a fused zero halo: planes [i_base, i_base+nplanes) of an n^3
 // grid, h-point zero shell, N(mean, scale^2) elsewhere; 4 points per thread.
 // With n even the 4 points are two whole Box-Muller pairs, each computed once
-// (same values as draw()).
-__global__ void fill_normal3d_f32_kernel(float* dst, long long n, long long i_base,
-                                         long long nplanes, int h, uint64_t seed,
-                                         uint64_t stream, float mean, float scale) {
-  const long long k = 4 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
-  const long long j = blockIdx.y;
+// (same values as draw()).  32-bit coordinates (n <= 2^20), a 64-bit flat
+// index advanced per plane.
+__global__ void fill_normal3d_f32_kernel(float* dst, int n, int i_base, int nplanes, int h,
+                                         uint64_t seed, uint64_t stream, float mean,
+                                         float scale) {
+  const int k = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int j = blockIdx.y;
   if (k >= n) return;
   const uint64_t key = hash_key(seed, stream);
   const bool jh = j < h || j >= n - h;
-  for (long long li = blockIdx.z; li < nplanes; li += gridDim.z) {
-    const long long i = i_base + li;
-    const long long g = (i * n + j) * n + k;
+  const bool kin = k >= h && k + 3 < n - h;  // no k halo point among the 4
+  const long long plane = (long long)n * n;
+  const long long dg = (long long)gridDim.z * plane;
+  long long g = ((long long)(i_base + (int)blockIdx.z) * n + j) * n + k;  // global flat index
+  float* p = dst + ((long long)blockIdx.z * n + j) * n + k;
+  const long long dp = dg;
+  for (int li = blockIdx.z; li < nplanes; li += gridDim.z, g += dg, p += dp) {
+    const int i = i_base + li;
     const bool rowh = jh || i < h || i >= n - h;
     float v[4];
-    if ((g & 1) == 0 && k + 3 < n) {
+    if (!rowh && kin && (g & 1) == 0) {  // no halo point: plain draws
+      const float2 a = normal_pair(key, (uint64_t)g >> 1);
+      const float2 b = normal_pair(key, ((uint64_t)g >> 1) + 1);
+      v[0] = mean + scale * a.x;
+      v[1] = mean + scale * a.y;
+      v[2] = mean + scale * b.x;
+      v[3] = mean + scale * b.y;
+    } else if ((g & 1) == 0 && k + 3 < n) {
       const float2 a = normal_pair(key, (uint64_t)g >> 1);
       const float2 b = normal_pair(key, ((uint64_t)g >> 1) + 1);
       const float z[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
       for (int m = 0; m < 4; m++) {
-        const long long kk = k + m;
+        const int kk = k + m;
         v[m] = (rowh || kk < h || kk >= n - h) ? 0.f : mean + scale * z[m];
       }
     } else {
 #pragma unroll
       for (int m = 0; m < 4; m++) {
-        const long long kk = k + m;
+        const int kk = k + m;
         const bool halo = rowh || kk < h || kk >= n - h;
         v[m] = (halo || kk >= n) ? 0.f
                                  : mean + scale * (float)draw(seed, stream, (uint64_t)(g + m), 0);
       }
     }
-    float* p = dst + (li * n + j) * n + k;
     if (n % 4 == 0) {
       *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
     } else {
@@ -257,6 +287,7 @@ int sgb_fill_normal3d_f32(float* dst, int n, int i_base, int nplanes, int halo, 
   if (!dst || n <= 0 || nplanes <= 0 || halo < 0) return SGB_EINVAL;
   dim3 b(64), g((unsigned)((n / 4 + 63) / 64 + ((n % 4) ? 1 : 0)), (unsigned)n,
                 (unsigned)(nplanes < 64 ? nplanes : 64));
+  if (n > (1 << 20)) return SGB_EINVAL;
   fill_normal3d_f32_kernel<<<g, b, 0, as_stream(stream)>>>(dst, n, i_base, nplanes, halo, seed,
                                                            stream_id, (float)mean, (float)scale);
   return launch_status("sgb_fill_normal3d_f32");
