@@ -204,6 +204,16 @@ int sgb_box_set_f64(double* y, const double* x, double alpha, int n, int lo, int
  * (bitwise = wave3d_r4_b_f32 followed by sgb_box_set_f32(u_2_b, u_b, -1)). */
 int sgb_wave3d_r4_b_step_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
                              float* u_b, float* u_2_b, sgb_stream_t stream);
+/* wave3d_r4_b with u_1_b = this call's adjoint alone (c_b accumulated as
+ * usual): the fused form of zeroing u_1_b and calling wave3d_r4_b_f32 --
+ * bitwise equal -- for independent reverse steps (BASELINE cfg 5; no
+ * reference counterpart).  The slab form works on local planes like
+ * wave3d_r4_b_slab_f32 and writes the output planes [out_i0, out_i1). */
+int wave3d_r4_b_fresh_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                              float* u_b, sgb_stream_t stream);
+int wave3d_r4_b_fresh_slab_f32(int n, double D, float* c, float* c_b, float* u_1,
+                                   float* u_1_b, float* u_b, int i_base, int nplanes,
+                                   int out_i0, int out_i1, sgb_stream_t stream);
 /* one interior pass of the 5-point average u <- (u + 4 neighbours)/5 (2D) */
 int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream);
 

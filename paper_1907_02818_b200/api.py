@@ -26,7 +26,8 @@ from . import _lib
 FAMILIES = {"wave1d": 1, "wave3d_c": 3, "wave3d_c2": 3, "burgers2d": 2, "wave3d_r4": 3}
 SCALARS = {"wave1d": ["D"], "wave3d_c": ["D"], "wave3d_c2": ["D"], "burgers2d": ["C", "D"],
            "wave3d_r4": ["D"]}
-_SUFFIX = {"primal": "", "adjoint": "_b", "scatter": "_scatter_b", "slab": "_b_slab"}
+_SUFFIX = {"primal": "", "adjoint": "_b", "scatter": "_scatter_b", "slab": "_b_slab",
+           "fresh": "_b_fresh", "fresh_slab": "_b_fresh_slab"}
 
 
 def _sfx(dtype) -> str:
@@ -62,7 +63,7 @@ def _call(family, kind, n, scalars, arrays, stream=None, extra=()):
     # every array holds the full n^d grid (a slab: nplanes whole planes); a
     # short buffer would be read out of bounds, so it is rejected here like
     # the reference's bounds error (interp.cpp:30-35)
-    want = int(extra[1]) * int(n) ** (d - 1) if kind == "slab" else int(n) ** d
+    want = int(extra[1]) * int(n) ** (d - 1) if kind.endswith("slab") else int(n) ** d
     dtype = None
     ptrs = []
     for nm in names:
@@ -103,6 +104,19 @@ def scatter_adjoint(family, n, scalars, arrays, stream=None):
 def adjoint_slab(family, n, scalars, arrays, i_base, nplanes, out_i0, out_i1, stream=None):
     """z-slab gather adjoint over global output planes [out_i0, out_i1)."""
     _call(family, "slab", n, scalars, arrays, stream,
+          extra=(int(i_base), int(nplanes), int(out_i0), int(out_i1)))
+
+
+def adjoint_fresh(family, n, scalars, arrays, stream=None):
+    """wave3d_r4_b_fresh_f32: the gather adjoint with u_1_b = this call's
+    adjoint alone (c_b accumulated) -- zeroing u_1_b and accumulating, fused."""
+    _call(family, "fresh", n, scalars, arrays, stream)
+
+
+def adjoint_slab_fresh(family, n, scalars, arrays, i_base, nplanes, out_i0, out_i1,
+                       stream=None):
+    """z-slab form of adjoint_fresh over global output planes [out_i0, out_i1)."""
+    _call(family, "fresh_slab", n, scalars, arrays, stream,
           extra=(int(i_base), int(nplanes), int(out_i0), int(out_i1)))
 
 

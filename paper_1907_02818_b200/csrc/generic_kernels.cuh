@@ -24,11 +24,15 @@ namespace sgb {
 // MODE 3: wave3d_r4 gather that also writes the u_2 partial of a time loop,
 //         u_2_b = -u_b on B and 0 elsewhere (drivers.time_loop_adjoint; the
 //         fused form of gather + sgb_box_set, fp32 streaming kernel only)
+// MODE 4: wave3d_r4 gather whose u_1_b is this step's adjoint alone (u_1_b =
+//         0 + sum where reached, 0 elsewhere: the fused form of zeroing u_1_b
+//         and accumulating, cfg 5's independent steps; fp32 streaming only)
 template <int MODE>
 struct Star3 {
   static constexpr int R = MODE >= 2 ? 4 : 1;
   static constexpr bool kU2 = MODE < 2;
   static constexpr bool kU2Set = MODE == 3;
+  static constexpr bool kU1bFresh = MODE == 4;
   static constexpr bool kC2 = MODE != 0;
   static constexpr bool kIncrement = MODE != 2;  // primal mode of the spec
   // weight of offset |r| along one axis; r == 0 gives the folded 3-axis centre

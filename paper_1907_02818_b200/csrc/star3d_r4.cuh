@@ -280,8 +280,10 @@ __device__ __noinline__ void v7_issue(float* dst, uint64_t* bar, const CUtensorM
                                       const CUtensorMap* tm_cb, const CUtensorMap* tm_u1b,
                                       const CUtensorMap* tm_u2b, const PeerHalo* peer, int p,
                                       int pl, int k0, int j0, int HK, int HJ, int ulo, int R,
-                                      int BF, int TILE, int box_bytes, bool emit, bool u2) {
-  tma::mbar_arrive_expect_tx(bar, 3 * box_bytes + ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE * 4);
+                                      int BF, int TILE, int box_bytes, bool emit, bool u2,
+                                      bool u1b) {
+  tma::mbar_arrive_expect_tx(
+      bar, 3 * box_bytes + ((emit ? (u1b ? 2 : 1) : 0) + (u2 ? 1 : 0)) * TILE * 4);
   const CUtensorMap *mc = tm_c, *mub = tm_ub, *mu1 = tm_u1;
   int pin = pl;
   if (peer) {  // uniform per plane: which array holds input plane p
@@ -298,7 +300,7 @@ __device__ __noinline__ void v7_issue(float* dst, uint64_t* bar, const CUtensorM
   tma::load_3d(dst + 2 * BF, mu1, bar, k0 - HK, j0 - HJ, pin);
   if (emit) {
     tma::load_3d(dst + 3 * BF, tm_cb, bar, k0, j0, pl - R);
-    tma::load_3d(dst + 3 * BF + TILE, tm_u1b, bar, k0, j0, pl - R);
+    if (u1b) tma::load_3d(dst + 3 * BF + TILE, tm_u1b, bar, k0, j0, pl - R);
   }
   if (u2) tma::load_3d(dst + 3 * BF + 2 * TILE, tm_u2b, bar, k0, j0, pl);
 }
@@ -355,17 +357,19 @@ __device__ __forceinline__ void star3_v7_body(
     const bool u2 = S3::kU2 && p >= o_begin && p < o_end;
     if (peer) {  // fused-halo launches only (out of line: I-cache, see v7_issue)
       v7_issue(dst, &bars[s], &tm_c, &tm_ub, &tm_u1, &tm_cb, &tm_u1b, &tm_u2b, peer, p, pl, k0,
-               j0, HK, HJ, ulo, R, BF, TILE, Tl::BOX_BYTES, emit, u2);
+               j0, HK, HJ, ulo, R, BF, TILE, Tl::BOX_BYTES, emit, u2, !S3::kU1bFresh);
       return;
     }
-    tma::mbar_arrive_expect_tx(&bars[s], 3 * Tl::BOX_BYTES +
-                                             ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE * 4);
+    // fresh u_1_b (MODE 4): its old tile is not needed
+    tma::mbar_arrive_expect_tx(
+        &bars[s], 3 * Tl::BOX_BYTES +
+                      ((emit ? (S3::kU1bFresh ? 1 : 2) : 0) + (u2 ? 1 : 0)) * TILE * 4);
     tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
     tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK - ulo, j0 - HJ - ulo, pl);
     tma::load_3d(dst + 2 * BF, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
     if (emit) {
       tma::load_3d(dst + 3 * BF, &tm_cb, &bars[s], k0, j0, pl - R);
-      tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
+      if (!S3::kU1bFresh) tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
     }
     if (u2) tma::load_3d(dst + 3 * BF + 2 * TILE, &tm_u2b, &bars[s], k0, j0, pl);
   };
@@ -457,8 +461,12 @@ __device__ __forceinline__ void star3_v7_body(
         float4 old[2];
         {
           const float* OLD = Cs + 3 * BF + (q_role ? TILE : 0) + trow;
-          old[0] = lds4(OLD);
-          old[1] = lds4(OLD + TK);
+          if (S3::kU1bFresh && q_role) {  // u_1_b starts from zero this step
+            old[0] = old[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            old[0] = lds4(OLD);
+            old[1] = lds4(OLD + TK);
+          }
         }
 
         // ---- q over the halo box; g for the centre elements
@@ -564,6 +572,11 @@ __device__ __forceinline__ void star3_v7_body(
                 for (int h = 0; h < 2; h++)
                   __stcs(reinterpret_cast<float4*>(u1b_plane + coff + h * n),
                          add4(old[h], acc[es][h]));
+              } else if (S3::kU1bFresh) {  // not reached: zero
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                  __stcs(reinterpret_cast<float4*>(u1b_plane + coff + h * n),
+                         make_float4(0.f, 0.f, 0.f, 0.f));
               }
             } else {
               // reached iff at most one coordinate is outside [lo, hi], by <= R
@@ -572,7 +585,7 @@ __device__ __forceinline__ void star3_v7_body(
 #pragma unroll
               for (int h = 0; h < 2; h++) {
                 const uint32_t mk = reach >> (4 * h);
-                if (!((fm >> (22 + h)) & 1) || !(mk & 0xf)) continue;
+                if (!((fm >> (22 + h)) & 1) || (!S3::kU1bFresh && !(mk & 0xf))) continue;
                 const float4 a = acc[es][h];
                 const float4 nv = make_float4(mk & 1 ? old[h].x + a.x : old[h].x,
                                               mk & 2 ? old[h].y + a.y : old[h].y,

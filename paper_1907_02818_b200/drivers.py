@@ -44,14 +44,17 @@ def regen_seed(u_b, n, t, seed, sl=None):
 
 
 def adjoint_step(family, n, scalars, arrays, sl=None, exchange=("u_1", "u_b"), overlap=True,
-                 link=None):
+                 link=None, fresh=False):
     """One gather-adjoint step; with a slab, halos of `exchange` are refreshed
     first -- overlapped with the interior planes when `overlap` -- or, with a
     peer `link` (peer.try_connect), read by the kernel straight from the
     neighbours' arrays after a stream-ordered cross-rank sync."""
+    if fresh and link is not None:
+        raise ValueError("fresh u_1_b is not available on the peer-halo path")
     if sl is None:
-        api.adjoint(family, n, scalars, arrays)
+        (api.adjoint_fresh if fresh else api.adjoint)(family, n, scalars, arrays)
         return 1
+    slab_call = api.adjoint_slab_fresh if fresh else api.adjoint_slab
     if link is not None:
         from . import peer
         peer.step_sync()
@@ -62,21 +65,21 @@ def adjoint_step(family, n, scalars, arrays, sl=None, exchange=("u_1", "u_b"), o
     fields = [arrays[k] for k in exchange]
     if not overlap or hi_in <= lo_in or sl.world == 1:
         slabmod.exchange_halos(sl, fields)
-        api.adjoint_slab(family, n, scalars, arrays, sl.base, sl.nplanes, sl.own0, sl.own1)
+        slab_call(family, n, scalars, arrays, sl.base, sl.nplanes, sl.own0, sl.own1)
         return 1
     import torch.distributed as dist
     ops = slabmod.halo_ops(sl, fields)
     reqs = dist.batch_isend_irecv(ops)
     # interior planes: their stencils only read owned planes
-    api.adjoint_slab(family, n, scalars, arrays, sl.base, sl.nplanes, lo_in, hi_in)
+    slab_call(family, n, scalars, arrays, sl.base, sl.nplanes, lo_in, hi_in)
     for r in reqs:
         r.wait()
     launches = 1
     if lo_in > sl.own0:
-        api.adjoint_slab(family, n, scalars, arrays, sl.base, sl.nplanes, sl.own0, lo_in)
+        slab_call(family, n, scalars, arrays, sl.base, sl.nplanes, sl.own0, lo_in)
         launches += 1
     if hi_in < sl.own1:
-        api.adjoint_slab(family, n, scalars, arrays, sl.base, sl.nplanes, hi_in, sl.own1)
+        slab_call(family, n, scalars, arrays, sl.base, sl.nplanes, hi_in, sl.own1)
         launches += 1
     return launches
 
@@ -101,8 +104,9 @@ class HaloPrefetch:
     the side stream."""
 
     def __init__(self, family, n, scalars, arrays, sl, fields=("u_1", "u_b"), regen=None,
-                 exchange=None):
+                 exchange=None, fresh=False):
         self.family, self.n, self.scalars, self.arrays, self.sl = family, n, scalars, arrays, sl
+        self.fresh = fresh  # u_1_b = this step's adjoint alone (cfg 5)
         self.fields = tuple(fields)
         self.regen = regen
         self.exchange = exchange or (lambda ts: slabmod.exchange_halos(sl, ts))
@@ -143,8 +147,9 @@ class HaloPrefetch:
         cur = torch.cuda.current_stream()
         cur.wait_event(self.ready[s])
         sl = self.sl
-        api.adjoint_slab(self.family, self.n, self.scalars, self.inputs(t), sl.base, sl.nplanes,
-                         sl.own0, sl.own1)
+        call = api.adjoint_slab_fresh if self.fresh else api.adjoint_slab
+        call(self.family, self.n, self.scalars, self.inputs(t), sl.base, sl.nplanes, sl.own0,
+             sl.own1)
         self.free[s].record(cur)
         self._t = t + 1
         self._prepare(t + 2)
@@ -170,7 +175,7 @@ def init_static(family, arrays, n, seed=0, sl=None):
         api.fill_random(arrays["c"], base * n * n, seed, 0, "uniform", 1.5, 3.0)
 
 
-def run_independent(n, steps, seed=0, D=0.01, sl=None, arrays=None, overlap=True):
+def run_independent(n, steps, seed=0, D=0.01, sl=None, arrays=None, overlap=True, fresh=True):
     """cfg 5: independent reverse steps of wave3d_r4, c_b accumulated."""
     fam = "wave3d_r4"
     if arrays is None:
@@ -179,8 +184,11 @@ def run_independent(n, steps, seed=0, D=0.01, sl=None, arrays=None, overlap=True
     for t in range(steps):
         regen_state(arrays["u_1"], n, t, seed, 4, sl)
         regen_seed(arrays["u_b"], n, t, seed, sl)
-        arrays["u_1_b"].zero_()
-        adjoint_step(fam, n, {"D": D}, arrays, sl, overlap=overlap)
+        if fresh:  # u_1_b = this step's adjoint: zeroing fused into the gather
+            adjoint_step(fam, n, {"D": D}, arrays, sl, overlap=overlap, fresh=True)
+        else:
+            arrays["u_1_b"].zero_()
+            adjoint_step(fam, n, {"D": D}, arrays, sl, overlap=overlap)
     return arrays
 
 

@@ -99,9 +99,10 @@ def test_interior_edge_split_equals_single_launch(mods, family, n, world):
             assert torch.equal(loc[k], one[k]), (family, r, k)
 
 
-@pytest.mark.parametrize("n,world,regen", [(40, 2, True), (52, 3, True), (40, 2, False),
-                                           (44, 4, False)])
-def test_halo_prefetch_pipeline_bitwise(mods, n, world, regen):
+@pytest.mark.parametrize("n,world,regen,fresh", [(40, 2, True, False), (52, 3, True, True),
+                                                 (40, 2, False, False), (44, 4, False, False),
+                                                 (48, 2, True, True)])
+def test_halo_prefetch_pipeline_bitwise(mods, n, world, regen, fresh):
     """HaloPrefetch (exchange of step t+1's halos on a side stream behind step
     t's compute, double-buffered u_1 / u_b) on emulated ranks of one GPU:
     every rank's owned planes of c_b / u_1_b after T steps are bitwise the
@@ -161,15 +162,56 @@ def test_halo_prefetch_pipeline_bitwise(mods, n, world, regen):
                 dst[top:].copy_(g[sl.own1:sl.base + sl.nplanes])
 
         pf = drivers.HaloPrefetch(fam, n, sc, loc, sl, regen=regen_fn if regen else None,
-                                  exchange=exchange_fn)
+                                  exchange=exchange_fn, fresh=fresh)
         for t in range(T):
-            if regen:
+            if regen and not fresh:
                 loc["u_1_b"].zero_()
             pf.step(t)
         torch.cuda.synchronize()
         own = slice(sl.halo_lo, top)
         for k in ("c_b", "u_1_b"):
             assert torch.equal(loc[k][own], full[k][sl.own0:sl.own1]), (r, k)
+
+
+@pytest.mark.parametrize("n,world", [(40, 1), (68, 1), (37, 1), (48, 2), (68, 3), (36, 4)])
+def test_fresh_gather_equals_zero_then_accumulate(mods, n, world):
+    """wave3d_r4_b_fresh(_slab)_f32 (u_1_b = this call's adjoint; the zeroing
+    fused into the streaming kernel) is bitwise the zeroed u_1_b followed by
+    the accumulating gather, c_b accumulated as usual -- full grid (n = 37:
+    the entry's memset + gather path) and every rank of z-slab
+    decompositions, incl. the overlapped interior / edge-band split."""
+    torch, api, drivers = mods
+    from paper_1907_02818_b200 import slab as slabmod
+    fam, sc = "wave3d_r4", {"D": 0.01}
+    g = torch.Generator(device="cpu").manual_seed(n + world)
+    full = {k: torch.randn((n, n, n), generator=g).cuda()
+            for k in ("c", "c_b", "u_1", "u_1_b", "u_b")}
+    for r in range(world):
+        sl = slabmod.decompose(n, 4, world, r) if world > 1 else None
+        if sl is None:
+            a = {k: v.clone() for k, v in full.items()}
+        else:
+            a = {k: v[sl.base:sl.base + sl.nplanes].clone() for k, v in full.items()}
+        b = {k: v.clone() for k, v in a.items()}
+        a["u_1_b"].fill_(float("nan"))  # every output plane must be written
+        if sl is None:
+            api.adjoint_fresh(fam, n, sc, a)
+            b["u_1_b"].zero_()
+            api.adjoint(fam, n, sc, b)
+            own = slice(0, n)
+        else:
+            R = 4
+            lo_in = sl.own0 + (R if r > 0 else 0)
+            hi_in = sl.own1 - (R if r < world - 1 else 0)
+            for (o0, o1) in ((lo_in, hi_in), (sl.own0, lo_in), (hi_in, sl.own1)):
+                if o1 > o0:
+                    api.adjoint_slab_fresh(fam, n, sc, a, sl.base, sl.nplanes, o0, o1)
+            b["u_1_b"][sl.own0 - sl.base:sl.own1 - sl.base].zero_()
+            api.adjoint_slab(fam, n, sc, b, sl.base, sl.nplanes, sl.own0, sl.own1)
+            own = slice(sl.own0 - sl.base, sl.own1 - sl.base)
+        torch.cuda.synchronize()
+        for k in ("c_b", "u_1_b"):
+            assert torch.equal(a[k][own].view(torch.int32), b[k][own].view(torch.int32)), (r, k)
 
 
 def test_generators_are_decomposition_invariant(mods):
