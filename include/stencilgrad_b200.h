@@ -65,6 +65,15 @@ int wave1d_b_f32(int n, double D, float* c, float* c_b, float* u, float* u_b, fl
                  float* u_next_b, sgb_stream_t stream);
 int wave1d_scatter_b_f32(int n, double D, float* c, float* c_b, float* u, float* u_b,
                          float* u_prev_b, float* u_next_b, sgb_stream_t stream);
+/* wave1d_b restricted to the outputs j in [j0, j1) (n, j0, j1 even, 16-byte
+ * aligned arrays): inputs [j0-1, j1] must be resident.  The chunk unit of the
+ * pipelined host-buffer plan. */
+int wave1d_b_range_f64(int n, double D, double* c, double* c_b, double* u, double* u_b,
+                       double* u_prev_b, double* u_next_b, long long j0, long long j1,
+                       sgb_stream_t stream);
+int wave1d_b_range_f32(int n, double D, float* c, float* c_b, float* u, float* u_b,
+                       float* u_prev_b, float* u_next_b, long long j0, long long j1,
+                       sgb_stream_t stream);
 
 /* ---- cfg 2: wave3d_c, 7-point star, linear c (oracle/specs/wave3d_c.json) ---
  * u[i][j][k] += 2u_1 - u_2 + c D Lap7(u_1), box [1, n-2]^3.
@@ -109,6 +118,12 @@ int burgers2d_b_f32(int n, double C, double D, float* u_1, float* u_1_b, float* 
                     sgb_stream_t stream);
 int burgers2d_scatter_b_f32(int n, double C, double D, float* u_1, float* u_1_b, float* u_b,
                             sgb_stream_t stream);
+/* burgers2d_b restricted to output rows [row0, row1) (rows a 16-byte
+ * multiple, aligned arrays): rows row0-1 .. row1 must be resident. */
+int burgers2d_b_rows_f64(int n, double C, double D, double* u_1, double* u_1_b, double* u_b,
+                         int row0, int row1, sgb_stream_t stream);
+int burgers2d_b_rows_f32(int n, double C, double D, float* u_1, float* u_1_b, float* u_b,
+                         int row0, int row1, sgb_stream_t stream);
 
 /* ---- cfg 4/5: wave3d_r4, 8th-order 25-point star (oracle/specs/wave3d_r4.json)
  * u = 2u_1 - u_2 + c^2 D Lap25(u_1), box [4, n-5]^3; u_2 passive.

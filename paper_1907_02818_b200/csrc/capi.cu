@@ -155,17 +155,32 @@ static int star3_scatter(const char* name, long long n, double D, const T* c, T*
 }
 
 // ------------------------------------------------------------------ wave1d
+// Output range [j0, j1) of the streaming kernel (the range entries and the
+// pipelined host plan); needs n, j0, j1 even and 16-byte aligned arrays.
+template <typename T>
+static bool wave1d_range_ok(long long n, long long j0, long long j1, const void* c,
+                            const void* c_b, const void* u, const void* u_b, const void* u_prev_b,
+                            const void* u_next_b) {
+  return n % 2 == 0 && j0 % 2 == 0 && j1 % 2 == 0 && 0 <= j0 && j0 <= j1 && j1 <= n &&
+         aligned16(c, c_b, u, u_b) && aligned16(u_prev_b, u_next_b);
+}
+
 template <typename T>
 static int wave1d_gather(long long n, double D, const T* c, T* c_b, const T* u, T* u_b,
-                         T* u_prev_b, const T* u_next_b, cudaStream_t s) {
+                         T* u_prev_b, const T* u_next_b, cudaStream_t s, long long j0 = 0,
+                         long long j1 = -1) {
   if (n <= 0) return einval("wave1d_b: n must be positive");
   if (!guard_ok(WAVE1D, n)) return SGB_GUARD;
   if (!c || !c_b || !u || !u_b || !u_prev_b || !u_next_b) return einval("wave1d_b: null array");
-  if (n % 2 == 0 && aligned16(c, c_b, u, u_b) && aligned16(u_prev_b, u_next_b)) {
-    wave1d_stream_kernel<T>
-        <<<grid_1d(n / 2, 256), 256, 0, s>>>(n, (T)D, c, c_b, u, u_b, u_prev_b, u_next_b);
+  const bool range = j1 >= 0;
+  if (!range) j1 = n;
+  if (wave1d_range_ok<T>(n, j0, j1, c, c_b, u, u_b, u_prev_b, u_next_b)) {
+    if (j1 == j0) return 0;
+    wave1d_stream_kernel<T><<<grid_1d((j1 - j0) / 2, 256), 256, 0, s>>>(
+        n, (T)D, c, c_b, u, u_b, u_prev_b, u_next_b, j0, j1);
     return launch_status("wave1d_b");
   }
+  if (range) return einval("wave1d_b_range: needs even n, j0, j1 and 16-byte aligned arrays");
   wave1d_gather_kernel<T>
       <<<grid_1d(n, 256), 256, 0, s>>>(n, (T)D, c, c_b, u, u_b, u_prev_b, u_next_b);
   return launch_status("wave1d_b");
@@ -174,12 +189,17 @@ static int wave1d_gather(long long n, double D, const T* c, T* c_b, const T* u, 
 // ------------------------------------------------------------------ burgers2d
 template <typename T>
 static int burgers2d_gather(long long n, double C, double D, const T* u_1, T* u_1_b,
-                            const T* u_b, cudaStream_t s) {
+                            const T* u_b, cudaStream_t s, int row_lo = 0, int row_hi = -1) {
   if (n <= 0) return einval("burgers2d_b: n must be positive");
   if (!guard_ok(BURGERS2D, n)) return SGB_GUARD;
   if (!u_1 || !u_1_b || !u_b) return einval("burgers2d_b: null array");
+  const bool range = row_hi >= 0;
+  if (!range) row_hi = (int)n;
+  if (range && (row_lo < 0 || row_lo > row_hi || row_hi > n))
+    return einval("burgers2d_b_rows: bad row range");
   if ((n * (long long)sizeof(T)) % 16 == 0 && n <= (1 << 30) && aligned16(u_1, u_1_b, u_b, u_b) &&
-      !std::getenv("SGB_BURGERS_NORING")) {
+      (range || !std::getenv("SGB_BURGERS_NORING"))) {
+    if (row_hi == row_lo) return 0;
     // rows per CTA / ring stages: measured defaults, env overrides (read per call)
     int rb = 32, stages = 5;
     if (const char* e = std::getenv("SGB_BURGERS_RING_RB")) rb = std::max(1, std::atoi(e));
@@ -197,21 +217,22 @@ static int burgers2d_gather(long long n, double C, double D, const T* u_1, T* u_
       attr = true;
     }
     constexpr int W = BurgRing<T>::W, TH = BurgRing<T>::THREADS;
-    dim3 g((unsigned)((n + W - 1) / W), (unsigned)((n + rb - 1) / rb));
+    dim3 g((unsigned)((n + W - 1) / W), (unsigned)((row_hi - row_lo + rb - 1) / rb));
     if (stages == 4)
-      burgers2d_ring_kernel<T, 4><<<g, TH, BurgRing<T, 4>::SMEM, s>>>((int)n, (T)C, (T)D, u_1,
-                                                                      u_1_b, u_b, rb);
+      burgers2d_ring_kernel<T, 4><<<g, TH, BurgRing<T, 4>::SMEM, s>>>(
+          (int)n, (T)C, (T)D, u_1, u_1_b, u_b, rb, row_lo, row_hi);
     else if (stages == 5)
-      burgers2d_ring_kernel<T, 5><<<g, TH, BurgRing<T, 5>::SMEM, s>>>((int)n, (T)C, (T)D, u_1,
-                                                                      u_1_b, u_b, rb);
+      burgers2d_ring_kernel<T, 5><<<g, TH, BurgRing<T, 5>::SMEM, s>>>(
+          (int)n, (T)C, (T)D, u_1, u_1_b, u_b, rb, row_lo, row_hi);
     else if (stages == 6)
-      burgers2d_ring_kernel<T, 6><<<g, TH, BurgRing<T, 6>::SMEM, s>>>((int)n, (T)C, (T)D, u_1,
-                                                                      u_1_b, u_b, rb);
+      burgers2d_ring_kernel<T, 6><<<g, TH, BurgRing<T, 6>::SMEM, s>>>(
+          (int)n, (T)C, (T)D, u_1, u_1_b, u_b, rb, row_lo, row_hi);
     else
-      burgers2d_ring_kernel<T, 8><<<g, TH, BurgRing<T, 8>::SMEM, s>>>((int)n, (T)C, (T)D, u_1,
-                                                                      u_1_b, u_b, rb);
+      burgers2d_ring_kernel<T, 8><<<g, TH, BurgRing<T, 8>::SMEM, s>>>(
+          (int)n, (T)C, (T)D, u_1, u_1_b, u_b, rb, row_lo, row_hi);
     return launch_status("burgers2d_b");
   }
+  if (range) return einval("burgers2d_b_rows: needs 16-byte rows and aligned arrays");
   if (n % 2 == 0 && aligned16(u_1, u_1_b, u_b, u_b)) {
     static int rb = -1;  // rows per block (SGB_BURGERS_RB), measured default
     if (rb < 0) {
@@ -288,6 +309,12 @@ unsigned long long sgb_launch_count(void) { return g_launches.load(); }
   int wave1d_b_##SFX(int n, double D, T* c, T* c_b, T* u, T* u_b, T* u_prev_b, T* u_next_b,    \
                      sgb_stream_t stream) {                                                    \
     return wave1d_gather<T>(n, D, c, c_b, u, u_b, u_prev_b, u_next_b, as_stream(stream));      \
+  }                                                                                            \
+  int wave1d_b_range_##SFX(int n, double D, T* c, T* c_b, T* u, T* u_b, T* u_prev_b,             \
+                           T* u_next_b, long long j0, long long j1, sgb_stream_t stream) {      \
+    if (j1 < 0) return einval("wave1d_b_range: bad range");                                    \
+    return wave1d_gather<T>(n, D, c, c_b, u, u_b, u_prev_b, u_next_b, as_stream(stream), j0,   \
+                            j1);                                                               \
   }                                                                                            \
   int wave1d_scatter_b_##SFX(int n, double D, T* c, T* c_b, T* u, T* u_b, T* u_prev_b,         \
                              T* u_next_b, sgb_stream_t stream) {                               \
@@ -498,6 +525,10 @@ int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float
   int burgers2d_b_##SFX(int n, double C, double D, T* u_1, T* u_1_b, T* u_b,                   \
                         sgb_stream_t stream) {                                                 \
     return burgers2d_gather<T>(n, C, D, u_1, u_1_b, u_b, as_stream(stream));                   \
+  }                                                                                            \
+  int burgers2d_b_rows_##SFX(int n, double C, double D, T* u_1, T* u_1_b, T* u_b, int row0,    \
+                             int row1, sgb_stream_t stream) {                                  \
+    return burgers2d_gather<T>(n, C, D, u_1, u_1_b, u_b, as_stream(stream), row0, row1);       \
   }                                                                                            \
   int burgers2d_scatter_b_##SFX(int n, double C, double D, T* u_1, T* u_1_b, T* u_b,           \
                                 sgb_stream_t stream) {                                         \

@@ -64,24 +64,30 @@ __global__ void __launch_bounds__(256) wave1d_stream_kernel(long long n, T D,
                                                             const T* __restrict__ u,
                                                             T* __restrict__ u_b,
                                                             T* __restrict__ u_prev_b,
-                                                            const T* __restrict__ s) {
+                                                            const T* __restrict__ s,
+                                                            long long j0, long long j1) {
+  // outputs j in [j0, j1) (j0 even; the full grid: 0, n); inputs are read at
+  // j-1 .. j+2, so [j0-1, j1] must be resident
   const int lane = threadIdx.x & 31;
-  const long long j = 2 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
-  const bool active = j < n;  // n even: both points or none
+  const long long j = j0 + 2 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+  const bool active = j < j1;   // n, j0, j1 even: both points or none
+  const bool inside = j < n;    // lanes past j1 still feed their neighbours' shuffles
   const long long lo = 1, hi = n - 2;
   typename Vec2<T>::type cv{}, uv{}, sv{}, ob{}, op{}, ou{};
-  if (active) {  // every load of this thread issued up front
+  if (inside) {  // every input load of this thread issued up front
     cv = ld2(c + j);
     uv = ld2(u + j);
     sv = ld2(s + j);
+  }
+  if (active) {
     ob = ld2(c_b + j);
     op = ld2(u_prev_b + j);
     ou = ld2(u_b + j);
   }
   // neighbours j-1 and j+2 of c, u, s (all warps participate in the shuffles)
-  const T cl = left_of(cv.y, c, j, n, lane, active), cr = right_of(cv.x, c, j, n, lane, active);
-  const T ul = left_of(uv.y, u, j, n, lane, active), ur = right_of(uv.x, u, j, n, lane, active);
-  const T sl = left_of(sv.y, s, j, n, lane, active), sr = right_of(sv.x, s, j, n, lane, active);
+  const T cl = left_of(cv.y, c, j, n, lane, inside), cr = right_of(cv.x, c, j, n, lane, inside);
+  const T ul = left_of(uv.y, u, j, n, lane, inside), ur = right_of(uv.x, u, j, n, lane, inside);
+  const T sl = left_of(sv.y, s, j, n, lane, inside), sr = right_of(sv.x, s, j, n, lane, inside);
   if (!active) return;
   // q = D c^2 s masked to the primal box at each of j-1 .. j+2
   auto q = [&](long long x, T cx, T sx) { return (x >= lo && x <= hi) ? D * cx * cx * sx : T(0); };
@@ -285,7 +291,10 @@ __device__ __forceinline__ T neg0(T u) { return u < T(0) ? u : T(0); }
 template <typename T, int S_>
 __global__ void __launch_bounds__(BurgRing<T, S_>::THREADS, 8)
     burgers2d_ring_kernel(int n, T C, T D, const T* __restrict__ u1, T* __restrict__ u1b,
-                          const T* __restrict__ ub, int rows_per_block) {
+                          const T* __restrict__ ub, int rows_per_block, int row_lo,
+                          int row_hi) {
+  // output rows [row_lo, row_hi) (the full grid: 0, n); rows row_lo-1 ..
+  // row_hi of u_1 / u_b must be resident
   using Rg = BurgRing<T, S_>;
   using V = typename Vec2<T>::type;
   constexpr int W = Rg::W, H = Rg::H, UW = Rg::UW, S = Rg::S, ST = Rg::STAGE;
@@ -294,8 +303,8 @@ __global__ void __launch_bounds__(BurgRing<T, S_>::THREADS, 8)
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + S * ST);
   const int tid = threadIdx.x;
   const int j0 = blockIdx.x * W;
-  const int i0 = blockIdx.y * rows_per_block;
-  const int i1 = min(i0 + rows_per_block, n);
+  const int i0 = row_lo + blockIdx.y * rows_per_block;
+  const int i1 = min(i0 + rows_per_block, row_hi);
   const int lo = 1, hi = n - 2;
   const int ca = max(j0 - H, 0), cb = min(j0 + W + H, n), oa = j0, ob = min(j0 + W, n);
   const uint32_t ubytes = (uint32_t)(cb - ca) * sizeof(T), obytes = (uint32_t)(ob - oa) * sizeof(T);

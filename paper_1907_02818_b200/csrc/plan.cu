@@ -100,13 +100,18 @@ sgb_plan* sgb_plan_create_slab(const char* family, int n, int dtype_bytes, int i
     p->dev.push_back(d);
     p->rmw.push_back(fs->rmw[a]);
   }
-  if (fs->dims == 3 && p->dtype == 4) {
-    // pipelined host path: C chunks of the local planes (at least 2R planes
-    // each); the call costs ~ H2D(all) + D2H(one chunk), so more chunks
-    // shorten the tail
-    int c = nplanes >= 128 ? 32 : 1;
+  // pipelined host path (3D fp32 slabs / grids, burgers2d rows, wave1d index
+  // ranges, on the shapes the range kernels take): C chunks of the outermost
+  // dimension; the call costs ~ H2D(all) + D2H(one chunk), so more chunks
+  // shorten the tail
+  const long long units = fs->dims == 3 ? nplanes : n;  // planes / rows / elements
+  const bool pipelined = (fs->dims == 3 && p->dtype == 4) ||
+                         (fs->dims == 2 && ((long long)n * dtype_bytes) % 16 == 0) ||
+                         (fs->dims == 1 && n % 2 == 0);
+  if (pipelined) {
+    int c = units >= 128 ? 32 : 1;
     if (const char* e = std::getenv("SGB_PLAN_CHUNKS")) c = std::max(1, std::atoi(e));
-    p->chunks = std::min(c, std::max(1, nplanes / 16));
+    p->chunks = (int)std::min<long long>(c, std::max<long long>(1, units / 16));
     cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p->s_cmp, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
@@ -135,14 +140,21 @@ void sgb_plan_destroy(sgb_plan* plan) {
   delete plan;
 }
 
-// 3D fp32 families: H2D of chunk c+1 (copy engine), the slab adjoint of
-// chunk c (SMs) and D2H of chunk c-1 (other copy engine) overlap.  Local
-// planes are split into C chunks; the outputs inside chunk c need input planes
-// up to R beyond it, so chunk c's kernel waits for the H2D of chunks c and c+1.
+// Chunked families: H2D of chunk c+1 (copy engine), the adjoint of chunk c's
+// outputs (SMs) and D2H of chunk c-1 (other copy engine) overlap.  The
+// outermost dimension (3D: local planes, 2D: rows, 1D: elements) is split
+// into C chunks; the outputs inside chunk c need inputs up to R = 1..4 units
+// beyond it, so chunk c's kernel waits for the H2D of chunks c and c+1.
 static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
-  const int n = p->n, C = p->chunks, L = p->nplanes, base = p->i_base;
-  const size_t plane = (size_t)n * n * 4;
-  auto bound = [&](int c) { return (int)((long long)L * c / C); };  // local plane
+  const int n = p->n, C = p->chunks, base = p->i_base;
+  const int L = p->dims == 3 ? p->nplanes : n;
+  // bytes of one unit of the outermost dimension
+  const size_t plane = (size_t)(p->dims == 3 ? (long long)n * n : (p->dims == 2 ? n : 1)) *
+                       p->dtype;
+  auto bound = [&](int c) {  // local unit; 1D chunk bounds even (2-point threads)
+    const long long b = (long long)L * c / C;
+    return (int)(p->dims == 1 ? b & ~1LL : b);
+  };
   const size_t na = p->dev.size();
   for (int c = 0; c < C; c++) {
     const int a = bound(c), b = bound(c + 1);
@@ -162,16 +174,30 @@ static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
     cudaStreamWaitEvent(p->s_cmp, p->ev_in[c], 0);
     if (c + 1 < C) cudaStreamWaitEvent(p->s_cmp, p->ev_in[c + 1], 0);
     if (a < b) {
-      float** d = reinterpret_cast<float**>(p->dev.data());
-      int rc;
-      if (p->family == "wave3d_r4")
-        rc = wave3d_r4_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L, a, b,
+      int rc = SGB_EINVAL;
+      if (p->dims == 3) {
+        float** d = reinterpret_cast<float**>(p->dev.data());
+        if (p->family == "wave3d_r4")
+          rc = wave3d_r4_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L, a, b,
+                                    p->s_cmp);
+        else if (p->family == "wave3d_c")
+          rc = wave3d_c_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], base, L,
+                                   a, b, p->s_cmp);
+      } else if (p->dtype == 8) {
+        double** d = reinterpret_cast<double**>(p->dev.data());
+        if (p->family == "burgers2d")
+          rc = burgers2d_b_rows_f64(n, scalars[0], scalars[1], d[0], d[1], d[2], a, b, p->s_cmp);
+        else if (p->family == "wave1d")
+          rc = wave1d_b_range_f64(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], a, b,
                                   p->s_cmp);
-      else if (p->family == "wave3d_c")
-        rc = wave3d_c_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], base, L, a,
-                                 b, p->s_cmp);
-      else
-        return SGB_EINVAL;
+      } else {
+        float** d = reinterpret_cast<float**>(p->dev.data());
+        if (p->family == "burgers2d")
+          rc = burgers2d_b_rows_f32(n, scalars[0], scalars[1], d[0], d[1], d[2], a, b, p->s_cmp);
+        else if (p->family == "wave1d")
+          rc = wave1d_b_range_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], a, b,
+                                  p->s_cmp);
+      }
       if (rc != 0) return rc;
     }
     cudaEventRecord(p->ev_out[c], p->s_cmp);
@@ -200,7 +226,7 @@ int sgb_plan_run_adjoint_host(sgb_plan* p, const double* scalars, void** arrays,
     sgb::set_error("sgb_plan_run_adjoint_host: null argument");
     return SGB_EINVAL;
   }
-  if (p->s_cmp && (p->family == "wave3d_r4" || p->family == "wave3d_c")) {
+  if (p->s_cmp) {
     for (size_t a = 0; a < p->dev.size(); a++)
       if (!arrays[a]) {
         sgb::set_error("sgb_plan_run_adjoint_host: null host array");

@@ -211,10 +211,14 @@ def test_dot_product_test_on_gpu(api):
 
 @pytest.mark.parametrize("name,n,dtype", [("wave3d_r4", 136, "f32"), ("wave3d_c", 128, "f32"),
                                           ("wave3d_r4", 40, "f64"), ("burgers2d", 64, "f64"),
-                                          ("wave1d", 300, "f64")])
+                                          ("burgers2d", 1000, "f64"), ("burgers2d", 516, "f32"),
+                                          ("wave1d", 300, "f64"), ("wave1d", 100002, "f64"),
+                                          ("wave1d", 4099, "f64"), ("wave1d", 5000, "f32")])
 def test_host_buffer_plan_entry(api, name, n, dtype):
     """sgb_plan_run_adjoint_host (host arrays in, accumulated adjoints out;
-    pipelined over i-chunks for 3D fp32) equals the device-pointer entry."""
+    pipelined over chunks of the outermost dimension for 3D fp32, burgers2d
+    rows and wave1d index ranges; one shot otherwise) equals the
+    device-pointer entry bit for bit."""
     import torch
     scalars, grids, adjs = gen.family_inputs(name, n, seed=4, accumulate=True)
     np_dt = np.float32 if dtype == "f32" else np.float64
