@@ -174,6 +174,14 @@ int sgb_ipc_close(void* ptr, long long offset);
 int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
                         float* u_2_b, float* u_b, int i_base, int nplanes, int out_i0,
                         int out_i1, sgb_stream_t stream);
+/* fp64 forms of the z-slab entries (the reference's precision; host-buffer
+ * plan chunks, multi-GPU slabs) */
+int wave3d_r4_b_slab_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                         double* u_b, int i_base, int nplanes, int out_i0, int out_i1,
+                         sgb_stream_t stream);
+int wave3d_c_b_slab_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                        double* u_2_b, double* u_b, int i_base, int nplanes, int out_i0,
+                        int out_i1, sgb_stream_t stream);
 
 /* ---- device input generation (synthetic BASELINE distributions) -------------
  * Counter-based: value(index) depends only on (seed, stream, global index), so

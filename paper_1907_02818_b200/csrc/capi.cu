@@ -506,6 +506,20 @@ int wave3d_c_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, float
                                 nplanes, out_i0, out_i1, as_stream(stream));
 }
 
+int wave3d_r4_b_slab_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                         double* u_b, int i_base, int nplanes, int out_i0, int out_i1,
+                         sgb_stream_t stream) {
+  return star3_gather<2, double>("wave3d_r4_b_slab", n, D, c, c_b, u_1, u_1_b, nullptr, u_b,
+                                 i_base, nplanes, out_i0, out_i1, as_stream(stream));
+}
+
+int wave3d_c_b_slab_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                        double* u_2_b, double* u_b, int i_base, int nplanes, int out_i0,
+                        int out_i1, sgb_stream_t stream) {
+  return star3_gather<0, double>("wave3d_c_b_slab", n, D, c, c_b, u_1, u_1_b, u_2_b, u_b,
+                                 i_base, nplanes, out_i0, out_i1, as_stream(stream));
+}
+
 // ---- burgers2d
 #define SGB_BURGERS(T, SFX)                                                                    \
   int burgers2d_##SFX(int n, double C, double D, T* u_1, T* u, sgb_stream_t stream) {          \

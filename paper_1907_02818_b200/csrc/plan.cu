@@ -69,10 +69,10 @@ sgb_plan* sgb_plan_create_slab(const char* family, int n, int dtype_bytes, int i
   }
   const bool full = i_base == 0 && nplanes == n && out_i0 == 0 && out_i1 == n;
   const bool has_slab = std::string(family) == "wave3d_r4" || std::string(family) == "wave3d_c";
-  if (!full && (!has_slab || dtype_bytes != 4 || i_base < 0 || nplanes <= 0 ||
+  if (!full && (!has_slab || i_base < 0 || nplanes <= 0 ||
                 i_base + nplanes > n || out_i0 < i_base || out_i1 > i_base + nplanes ||
                 out_i0 >= out_i1)) {
-    sgb::set_error("sgb_plan_create_slab: slabs need wave3d_r4 / wave3d_c in fp32 and "
+    sgb::set_error("sgb_plan_create_slab: slabs need wave3d_r4 / wave3d_c and "
                    "i_base <= out_i0 < out_i1 <= i_base + nplanes <= n");
     return nullptr;
   }
@@ -105,7 +105,7 @@ sgb_plan* sgb_plan_create_slab(const char* family, int n, int dtype_bytes, int i
   // dimension; the call costs ~ H2D(all) + D2H(one chunk), so more chunks
   // shorten the tail
   const long long units = fs->dims == 3 ? nplanes : n;  // planes / rows / elements
-  const bool pipelined = (fs->dims == 3 && p->dtype == 4) ||
+  const bool pipelined = (fs->dims == 3 && p->family != "wave3d_c2") ||
                          (fs->dims == 2 && ((long long)n * dtype_bytes) % 16 == 0) ||
                          (fs->dims == 1 && n % 2 == 0);
   if (pipelined) {
@@ -175,13 +175,21 @@ static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
     if (c + 1 < C) cudaStreamWaitEvent(p->s_cmp, p->ev_in[c + 1], 0);
     if (a < b) {
       int rc = SGB_EINVAL;
-      if (p->dims == 3) {
+      if (p->dims == 3 && p->dtype == 4) {
         float** d = reinterpret_cast<float**>(p->dev.data());
         if (p->family == "wave3d_r4")
           rc = wave3d_r4_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L, a, b,
                                     p->s_cmp);
         else if (p->family == "wave3d_c")
           rc = wave3d_c_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], base, L,
+                                   a, b, p->s_cmp);
+      } else if (p->dims == 3) {
+        double** d = reinterpret_cast<double**>(p->dev.data());
+        if (p->family == "wave3d_r4")
+          rc = wave3d_r4_b_slab_f64(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L, a, b,
+                                    p->s_cmp);
+        else if (p->family == "wave3d_c")
+          rc = wave3d_c_b_slab_f64(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], base, L,
                                    a, b, p->s_cmp);
       } else if (p->dtype == 8) {
         double** d = reinterpret_cast<double**>(p->dev.data());

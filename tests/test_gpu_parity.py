@@ -210,7 +210,8 @@ def test_dot_product_test_on_gpu(api):
 
 
 @pytest.mark.parametrize("name,n,dtype", [("wave3d_r4", 136, "f32"), ("wave3d_c", 128, "f32"),
-                                          ("wave3d_r4", 40, "f64"), ("burgers2d", 64, "f64"),
+                                          ("wave3d_r4", 40, "f64"), ("wave3d_r4", 136, "f64"),
+                                          ("wave3d_c", 130, "f64"), ("burgers2d", 64, "f64"),
                                           ("burgers2d", 1000, "f64"), ("burgers2d", 516, "f32"),
                                           ("wave1d", 300, "f64"), ("wave1d", 100002, "f64"),
                                           ("wave1d", 4099, "f64"), ("wave1d", 5000, "f32")])
