@@ -130,6 +130,14 @@ static int star3_primal(const char* name, long long n, double D, const T* c, con
                                           (const float*)u_2, (float*)u, s, name);
     if (rc != 1) return rc;  // 1: TMA path not applicable (alignment / size)
   }
+  if constexpr (std::is_same<T, double>::value && MODE == 2) {
+    // radius 4 (the radius-1 fp64 primal is already at the copy bandwidth on
+    // the per-point kernel)
+    if (!std::getenv("SGB_PRIMAL_GENERIC")) {
+      const int rc = star3_primal_f64_stream<MODE>(n, D, c, u_1, u_2, u, s, name);
+      if (rc != 1) return rc;
+    }
+  }
   const long long lo = R, hi = n - 1 - R;
   dim3 b(32, 4), gr((unsigned)((n + 31) / 32), (unsigned)((n + 3) / 4), (unsigned)n);
   star3_primal_kernel<MODE, T><<<gr, b, 0, s>>>(Slab3{n, 0, n}, lo, hi, 0, n, (T)D, c, u_1,

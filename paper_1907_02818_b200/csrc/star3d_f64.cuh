@@ -431,4 +431,194 @@ inline int star3_f64_stream_gather(const Slab3& g, long long lo, long long hi, l
   return launch_status(name);
 }
 
+// ---------------------------------------------------------------------------
+// fp64 streaming primal (run_nest semantics, interp.cpp:153-173; emitted form
+// codegen.cpp:311-330): u = 2 u_1 - u_2 + c^(1|2) D Lap(u_1) on B (or += for
+// the '+=' specs), points outside B untouched.  The fp32 streaming primal's
+// scheme (star3d_primal.cuh) with the fp64 gather's 2 x 2 register blocking:
+// 32x32 column tiles, 256 threads, per plane p the u_1 halo box and the c /
+// u_2 / u_1 (/ u) tiles of the output plane o = p - R through a 3-stage TMA
+// ring, ~110 KB: two CTAs per SM; ~48-plane i-chunks (the lock-step that
+// made the fp32 primal reach the copy bandwidth).
+template <int MODE>
+struct PrimalTileD {
+  static constexpr int R = Star3<MODE>::R;
+  static constexpr int TK = StarTileD<MODE>::TK, TJ = StarTileD<MODE>::TJ;
+  static constexpr int HK = StarTileD<MODE>::HK, HJ = R;
+  static constexpr int BW = StarTileD<MODE>::BW, BJ = StarTileD<MODE>::BJ;
+  static constexpr int RING = 2 * R + 1, NS = 3;
+  static constexpr int THREADS = (TK / 2) * (TJ / 2);
+  static constexpr int BOX = BW * BJ, BP = StarTileD<MODE>::BP, TILE = TK * TJ;
+  static constexpr int NT = Star3<MODE>::kIncrement ? 4 : 3;  // c, u_2, u_1 (, u)
+  static constexpr int SF = BP + NT * TILE;
+  static constexpr int SMEM = NS * SF * 8 + NS * 8;
+  static_assert(RING % NS == 0, "static stage index");
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(PrimalTileD<MODE>::THREADS, 2)
+    star3_primal_f64_kernel(const __grid_constant__ CUtensorMap tm_box,
+                            const __grid_constant__ CUtensorMap tm_c,
+                            const __grid_constant__ CUtensorMap tm_u2,
+                            const __grid_constant__ CUtensorMap tm_u1,
+                            const __grid_constant__ CUtensorMap tm_u, double* __restrict__ u,
+                            int n, int lo, int hi, int chunk, int tiles_k, double D) {
+  using Tl = PrimalTileD<MODE>;
+  using S3 = Star3<MODE>;
+  constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, TK = Tl::TK, RING = Tl::RING;
+  constexpr int NS = Tl::NS, BOX = Tl::BOX, BP = Tl::BP, TILE = Tl::TILE, SF = Tl::SF;
+  constexpr int NT = Tl::NT;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stage = reinterpret_cast<double*>(smem_raw);  // [NS][box | c | u_2 | u_1 (| u)]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + NS * SF);
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int tk = blockIdx.x % tiles_k, tj = blockIdx.x / tiles_k;
+  const int k0 = tk * TK, j0 = tj * Tl::TJ;
+  const int o_begin = lo + blockIdx.y * chunk;
+  const int o_end = min(o_begin + chunk, hi + 1);
+  if (o_begin >= o_end) return;
+  const int pstart = o_begin - R;
+  const int P = (o_end - o_begin) + 2 * R;
+
+  const double w0 = S3::template w<double>(0);
+  double wr[R + 1];
+  wr[0] = w0;
+#pragma unroll
+  for (int r = 1; r <= R; r++) wr[r] = S3::template w<double>(r);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int it) {
+    const int s = it % NS;
+    double* dst = stage + s * SF;
+    const int p = pstart + it;
+    const bool emit = it >= 2 * R;
+    tma::mbar_arrive_expect_tx(&bars[s], (BOX + (emit ? NT * TILE : 0)) * 8);
+    tma::load_3d(dst, &tm_box, &bars[s], k0 - HK, j0 - HJ, p);
+    if (emit) {
+      const int o = p - R;
+      tma::load_3d(dst + BP, &tm_c, &bars[s], k0, j0, o);
+      tma::load_3d(dst + BP + TILE, &tm_u2, &bars[s], k0, j0, o);
+      tma::load_3d(dst + BP + 2 * TILE, &tm_u1, &bars[s], k0, j0, o);
+      if (NT == 4) tma::load_3d(dst + BP + 3 * TILE, &tm_u, &bars[s], k0, j0, o);
+    }
+  };
+  if (tid == 0)
+    for (int it = 0; it < NS && it < P; it++) issue(it);
+
+  const int jr0 = j0 + 2 * ty, kc = k0 + 2 * tx;
+  const int r0 = 2 * ty + HJ, col = HK + 2 * tx;
+  const int trow = 2 * ty * TK + 2 * tx;
+  const long long plane = (long long)n * n;
+  const long long coff = (long long)jr0 * n + kc;
+  bool jin[2], kin[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) jin[h] = jr0 + h >= lo && jr0 + h <= hi;
+#pragma unroll
+  for (int x = 0; x < 2; x++) kin[x] = kc + x >= lo && kc + x <= hi;
+
+  double2 acc[RING][2];
+#pragma unroll
+  for (int s = 0; s < RING; s++) acc[s][0] = acc[s][1] = make_double2(0.0, 0.0);
+
+  for (int base = 0; base < P; base += RING) {
+    const int par0 = base / NS;
+#pragma unroll
+    for (int ph = 0; ph < RING; ph++) {
+      const int it = base + ph;
+      if (it < P) {
+        const int s = ph % NS;
+        const double* F = stage + s * SF;
+        tma::mbar_wait(&bars[s], (par0 + ph / NS) & 1);
+        field2x2_d<MODE>(F, r0, col, w0, wr, acc, ph);
+        if (it >= 2 * R) {
+          const int es = (ph + R + 1) % RING;
+          const int o = pstart + it - R;
+          double* urow = u + (long long)o * plane + coff;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            if (!jin[h] || !(kin[0] || kin[1])) continue;
+            const double* T0 = F + BP + trow + h * TK;
+            const double2 cv = ldd2(T0), u2 = ldd2(T0 + TILE), u1 = ldd2(T0 + 2 * TILE);
+            const double cc[2] = {S3::kC2 ? cv.x * cv.x : cv.x, S3::kC2 ? cv.y * cv.y : cv.y};
+            const double a[2] = {acc[es][h].x, acc[es][h].y};
+            const double v1[2] = {u1.x, u1.y}, v2[2] = {u2.x, u2.y};
+            double v[2];
+#pragma unroll
+            for (int x = 0; x < 2; x++) v[x] = (2.0 * v1[x] - v2[x]) + (D * cc[x]) * a[x];
+            if (NT == 4) {
+              const double2 uo = ldd2(T0 + 3 * TILE);
+              v[0] = uo.x + v[0];
+              v[1] = uo.y + v[1];
+            }
+            if (kin[0] && kin[1]) {
+              *reinterpret_cast<double2*>(urow + h * n) = make_double2(v[0], v[1]);
+            } else {
+#pragma unroll
+              for (int x = 0; x < 2; x++)
+                if (kin[x]) urow[h * n + x] = v[x];
+            }
+          }
+        }
+        __syncthreads();  // stage s consumed by every thread
+        if (tid == 0 && it + NS < P) issue(it + NS);
+      }
+    }
+  }
+}
+
+// Host launcher; returns 1 when the shape does not fit (caller uses the
+// per-point kernel), 0 / negative like the other entries.
+template <int MODE>
+inline int star3_primal_f64_stream(long long n, double D, const double* c, const double* u_1,
+                                   const double* u_2, double* u, cudaStream_t s,
+                                   const char* name) {
+  using Tl = PrimalTileD<MODE>;
+  constexpr int R = Tl::R;
+  const long long lo = R, hi = n - 1 - R;
+  if (n % 2 != 0 || n < 2 * R + 2 || n > (1 << 20)) return 1;
+  for (const void* p : {(const void*)c, (const void*)u_1, (const void*)u_2, (const void*)u})
+    if (reinterpret_cast<uintptr_t>(p) & 15) return 1;
+  CUtensorMap maps[5];
+  int rc = 0;
+  rc |= encode_3d_t(&maps[0], u_1, n, n, Tl::BW, Tl::BJ, name);
+  rc |= encode_3d_t(&maps[1], c, n, n, Tl::TK, Tl::TJ, name);
+  rc |= encode_3d_t(&maps[2], u_2, n, n, Tl::TK, Tl::TJ, name);
+  rc |= encode_3d_t(&maps[3], u_1, n, n, Tl::TK, Tl::TJ, name);
+  rc |= encode_3d_t(&maps[4], (const double*)u, n, n, Tl::TK, Tl::TJ, name);
+  if (rc) return SGB_EINVAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(star3_primal_f64_kernel<MODE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Tl::SMEM);
+    attr = true;
+  }
+  const int tiles_k = (int)((n + Tl::TK - 1) / Tl::TK);
+  const long long tiles = (long long)tiles_k * ((n + Tl::TJ - 1) / Tl::TJ);
+  const long long nout = hi - lo + 1;
+  // wave model (two CTAs per SM) with ~48-plane chunks as the fp32 primal
+  const long long slots = 2LL * num_sms();
+  int nch = 1;
+  long long best = -1;
+  for (int cc = 1; cc <= 64 && cc <= nout; cc++) {
+    const long long len = (nout + cc - 1) / cc;
+    const long long cost = ((tiles * cc + slots - 1) / slots) * (len + 2 * R);
+    if (best < 0 || cost < best) best = cost, nch = cc;
+  }
+  if (R >= 2) nch = (int)std::max<long long>(nch, (nout + 47) / 48);
+  if (const char* e = std::getenv("SGB_PRIMAL_CHUNKS")) nch = std::max(1, std::atoi(e));
+  const int chunk = (int)((nout + nch - 1) / nch);
+  const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
+  star3_primal_f64_kernel<MODE><<<dim3((unsigned)tiles, gy), Tl::THREADS, Tl::SMEM, s>>>(
+      maps[0], maps[1], maps[2], maps[3], maps[4], u, (int)n, (int)lo, (int)hi, chunk, tiles_k,
+      D);
+  return launch_status(name);
+}
+
 }  // namespace sgb

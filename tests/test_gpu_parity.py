@@ -338,6 +338,28 @@ def test_primal_f32_matches_oracle(api, name, n):
     check_close(got[out], want[out], "f32", f"{name} n={n} primal")
 
 
+@pytest.mark.parametrize("n", [20, 24, 40, 66, 98, 136])
+def test_primal_f64_r4_streaming(api, n, monkeypatch):
+    """fp64 radius-4 streaming primal (even n): matches the oracle's run_nest
+    at 1e-12 (the output starts non-zero, so points outside the box are
+    checked to be untouched); i-chunking changes nothing (bitwise)."""
+    name = "wave3d_r4"
+    scalars, grids, _ = gen.family_inputs(name, n, seed=n + 17)
+    f = oracle.family(name)
+    out = f.arrays[f.output]
+    grids[out] = np.random.default_rng(n + 3).standard_normal(grids[out].shape)
+    got = api.run_nest(name, n, scalars, grids, dtype="f64")
+    want = {k: v.copy() for k, v in grids.items()}
+    assert oracle.run_primal(name, n, scalars, want) == 0
+    check_close(got[out], want[out], "f64", f"{name} n={n} primal")
+    assert np.array_equal(got[out][:4], grids[out][:4])  # planes outside the box untouched
+    for chunks in ("1", "5"):
+        with monkeypatch.context() as m:
+            m.setenv("SGB_PRIMAL_CHUNKS", chunks)
+            again = api.run_nest(name, n, scalars, grids, dtype="f64")
+        assert np.array_equal(again[out], got[out]), chunks
+
+
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("n", [64, 300, 1032])
 def test_burgers_primal_ring_variants_bitwise_equal(api, n, dtype, monkeypatch):
