@@ -4,6 +4,12 @@
 // Appendix C; reference adjoint.cpp:73-163 / interp.cpp:189-198).  Design,
 // measurements and the path from the earlier versions: DESIGN.md ("Radius-4
 // streaming kernel") and profiles/.
+//
+// Instantiated for MODE 2 (wave3d_r4: the reference's wave3d_r4_b), MODE 3
+// (the same plus the time-loop u_2 partial written from the u_b box the
+// q-role threads already hold) and MODE 4 (u_1_b = this call's adjoint:
+// zeroing fused, the u_1_b tile not loaded); MODE 0 / 1 (radius 1) compile
+// too but the v1 kernel is faster there (star3d_tma.cuh).
 #pragma once
 #include <cstring>
 #include <mutex>
