@@ -1,0 +1,40 @@
+"""bench.py contract on the B200 (our arm): one JSON line with the keys the
+driver reads -- metric / value / unit / timing, the roofline object, the
+end-to-end (host-buffer) figure with its copy byte counts, clocks, the
+launch count and the CPU baseline -- on a reduced grid so the test is fast."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("config,n", [("4", 128), ("5", 96), ("3", 1024), ("1", 1 << 16)])
+def test_bench_line_contract(config, n):
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", config, "--n", str(n),
+           "--steps", "4", "--warmup", "3", "--no-ablation", "--no-configs", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+              "gpu_launches", "roofline", "clocks", "cpu_baseline"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 4 and d["warmup"] == 3
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["higher_is_better"] is True
+    assert d["gpu_launches"] >= 4
+    assert "workload" in d["config"]
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["peak"] > 0
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("reference", "port")
+    assert d["clocks"]["samples"] >= 0
