@@ -408,11 +408,21 @@ class EmittedProblem:
                          + ", ".join(f"I z_{s}" for s in self.sizes) + f") {{ return {body}; }}")
         return lines, fns, szv
 
+    def _written(self):
+        """Arrays the current kernel writes (the gather / nest forms: the
+        adjoint targets; the primal: its output); the rest are passed as
+        const __restrict__, so their loads may take the read-only path."""
+        if self._which == "primal":
+            return {self.out}
+        return {t.adjoint for t in self.terms}
+
     def _signature(self, kname, index="long long"):
         ps = [f"{index} z_{s}" for s in self.sizes]
         ps += [f"T s_{s}" for s in self.scalars]
+        written = self._written()
         for arr in self.param_arrays(self._which):
-            ps.append(f"T* __restrict__ a_{arr}")
+            q = "" if arr in written else "const "
+            ps.append(f"{q}T* __restrict__ a_{arr}")
         return f'extern "C" __global__ void {kname}(' + ", ".join(ps) + ")"
 
     def _box_checks(self, xs, szv):
