@@ -237,9 +237,13 @@ def time_loop_forward(n, T, D, c, u0, u1, store=None):
     return cur
 
 
-def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None, fused=True):
+def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None, fused=True,
+                      workspace=None):
     """Gradient of J = <w, u^T> w.r.t. (u^0, u^1, c) through T-1 primal steps.
-    Returns (u0_b, u1_b, c_b, stats)."""
+    Returns (u0_b, u1_b, c_b, stats).  `workspace`: an optional caller-owned
+    list of state buffers kept across calls (a solver evaluating gradients
+    repeatedly keeps its state memory; the buffers are zero outside the box
+    and need no re-zeroing)."""
     import math
     fam = "wave3d_r4"
     K = checkpoint_every or max(1, int(math.isqrt(T)))
@@ -247,14 +251,17 @@ def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None, fused=True):
     # state buffers: the primal writes only the box, so a buffer this driver
     # allocated (zero outside the box) can be reused without re-zeroing; the
     # caller's u0 / u1 are read, never written or recycled
-    pool = []
-    owned = set()
+    pool = [t for t in (workspace or []) if t.shape == u1.shape and t.dtype == u1.dtype
+            and t.device == u1.device]
+    if workspace is not None:
+        workspace.clear()
+    owned = {id(t): t for t in pool}
 
     def fresh():
         if pool:
             return pool.pop()
         t = torch.zeros_like(u1)
-        owned.add(id(t))
+        owned[id(t)] = t
         return t
 
     def release(t, keep):
@@ -304,6 +311,8 @@ def time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=None, fused=True):
         for t, st in states.items():
             release(st, keep)
     # after the loop: ub_next = u-bar^1, ub_cur = u-bar^0
+    if workspace is not None:  # every state buffer back to the caller's workspace
+        workspace.extend(owned.values())
     stats = {"checkpoint_every": K, "checkpoints": len(starts), "recomputed_steps": recomputed,
              "adjoint_steps": T - 1}
     return ub_cur, ub_next, c_b, stats

@@ -288,6 +288,13 @@ def test_time_loop_fused_step_bitwise(mods, n, monkeypatch):
     b = drivers.time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=2, fused=False)
     for x, y in zip(a[:3], b[:3]):
         assert torch.equal(x, y)
+    # a workspace kept across calls (reused state buffers) changes nothing
+    ws = []
+    for _ in range(2):
+        r = drivers.time_loop_adjoint(n, T, D, c, u0, u1, w, checkpoint_every=2, workspace=ws)
+        for x, y in zip(a[:3], r[:3]):
+            assert torch.equal(x, y)
+    assert ws
     # one step against the two-launch form, with a poisoned u_2_b buffer
     arrs = {"c": c, "c_b": torch.randn_like(c), "u_1": u1, "u_1_b": torch.randn_like(c),
             "u_b": w}
