@@ -104,25 +104,36 @@ class HaloPrefetch:
     the side stream."""
 
     def __init__(self, family, n, scalars, arrays, sl, fields=("u_1", "u_b"), regen=None,
-                 exchange=None, fresh=False):
+                 exchange=None, fresh=False, compute=None):
         self.family, self.n, self.scalars, self.arrays, self.sl = family, n, scalars, arrays, sl
         self.fresh = fresh  # u_1_b = this step's adjoint alone (cfg 5)
         self.fields = tuple(fields)
         self.regen = regen
         self.exchange = exchange or (lambda ts: slabmod.exchange_halos(sl, ts))
+        # compute(inputs, t): the step's kernel (default: the slab gather);
+        # CPU tensors (the gloo tests of the exchange schedule) run it and
+        # the preparation in program order, without streams or events
+        self.compute = compute
         # both sets are private copies (initialised from `arrays`), so the
         # side stream never writes a tensor the caller may still use
         self.sets = [{f: arrays[f].clone() for f in self.fields} for _ in range(2)]
-        self.side = torch.cuda.Stream(priority=-1)
-        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
-        self.free = [torch.cuda.Event(), torch.cuda.Event()]
-        self.side.wait_stream(torch.cuda.current_stream())  # arrays initialised
+        self.cuda = arrays[self.fields[0]].is_cuda
+        if self.cuda:
+            self.side = torch.cuda.Stream(priority=-1)
+            self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+            self.free = [torch.cuda.Event(), torch.cuda.Event()]
+            self.side.wait_stream(torch.cuda.current_stream())  # arrays initialised
         self._t = 0
         self._prepare(0)
         self._prepare(1)
 
     def _prepare(self, t):
         s = t % 2
+        if not self.cuda:
+            if self.regen is not None:
+                self.regen(self.sets[s], t)
+            self.exchange([self.sets[s][f] for f in self.fields])
+            return
         with torch.cuda.stream(self.side):
             if t >= 2:  # step t-2 finished reading this set
                 self.side.wait_event(self.free[s])
@@ -144,20 +155,26 @@ class HaloPrefetch:
         if t != self._t:
             raise ValueError(f"HaloPrefetch steps run in order: expected {self._t}, got {t}")
         s = t % 2
-        cur = torch.cuda.current_stream()
-        cur.wait_event(self.ready[s])
         sl = self.sl
-        call = api.adjoint_slab_fresh if self.fresh else api.adjoint_slab
-        call(self.family, self.n, self.scalars, self.inputs(t), sl.base, sl.nplanes, sl.own0,
-             sl.own1)
-        self.free[s].record(cur)
+        if self.cuda:
+            cur = torch.cuda.current_stream()
+            cur.wait_event(self.ready[s])
+        if self.compute is not None:
+            self.compute(self.inputs(t), t)
+        else:
+            call = api.adjoint_slab_fresh if self.fresh else api.adjoint_slab
+            call(self.family, self.n, self.scalars, self.inputs(t), sl.base, sl.nplanes,
+                 sl.own0, sl.own1)
+        if self.cuda:
+            self.free[s].record(cur)
         self._t = t + 1
         self._prepare(t + 2)
         return 1
 
     def close(self):
-        torch.cuda.current_stream().wait_stream(self.side)
-        self.side.synchronize()
+        if self.cuda:
+            torch.cuda.current_stream().wait_stream(self.side)
+            self.side.synchronize()
 
 
 def alloc(family, n, sl=None, dtype=torch.float32):

@@ -72,3 +72,59 @@ def test_halo_exchange_gloo(world, n, radius):
     for p in procs:
         p.join(timeout=60)
     assert all(res.values()), res
+
+
+def _prefetch_worker(rank, world, port, n, radius, steps, q):
+    """drivers.HaloPrefetch's schedule with the real exchange (gloo, CPU
+    tensors): each step's compute must see its own step's owned planes and the
+    neighbours' edge planes of the SAME step in its halos, from the set the
+    double buffering assigns it -- the data routing of the pipelined exchange
+    in a true multi-process run (the CUDA stream / event ordering on top of it
+    is covered on the B200, tests/test_drivers_gpu.py)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1907_02818_b200 import drivers
+        sl = slabmod.decompose(n, radius, world, rank)
+        shape = (sl.nplanes, 6, 5)
+
+        def glob(t, field):  # the step-t global field, planes [base, base + nplanes)
+            g = torch.arange(n * 6 * 5, dtype=torch.float64).reshape(n, 6, 5)
+            return g + 1e6 * t + (0.5 if field == "u_b" else 0.0)
+
+        def regen(fs, t):  # owned planes only; halo planes poisoned
+            for f, tens in fs.items():
+                tens.fill_(float("nan"))
+                tens[sl.halo_lo:sl.halo_lo + sl.owned] = glob(t, f)[sl.own0:sl.own1]
+
+        seen = []
+
+        def compute(inputs, t):
+            ok = all(torch.equal(inputs[f], glob(t, f)[sl.base:sl.base + sl.nplanes])
+                     for f in ("u_1", "u_b"))
+            seen.append(ok)
+
+        arrays = {f: torch.zeros(shape, dtype=torch.float64) for f in ("c", "u_1", "u_b")}
+        pf = drivers.HaloPrefetch("wave3d_r4", n, {"D": 0.01}, arrays, sl, regen=regen,
+                                  compute=compute)
+        for _ in range(steps):
+            pf.step()
+        pf.close()
+        q.put((rank, len(seen) == steps and all(seen)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,radius", [(2, 20, 4), (3, 17, 4)])
+def test_halo_prefetch_schedule_gloo(world, n, radius):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_prefetch_worker, args=(r, world, port, n, radius, 5, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res.values()), res
