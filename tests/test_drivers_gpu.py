@@ -173,8 +173,9 @@ def test_halo_prefetch_pipeline_bitwise(mods, n, world, regen, fresh):
             assert torch.equal(loc[k][own], full[k][sl.own0:sl.own1]), (r, k)
 
 
+@pytest.mark.parametrize("noubwin", ["", "1"])
 @pytest.mark.parametrize("n,world", [(40, 1), (68, 1), (37, 1), (48, 2), (68, 3), (36, 4)])
-def test_fresh_gather_equals_zero_then_accumulate(mods, n, world):
+def test_fresh_gather_equals_zero_then_accumulate(mods, n, world, noubwin, monkeypatch):
     """wave3d_r4_b_fresh(_slab)_f32 (u_1_b = this call's adjoint; the zeroing
     fused into the streaming kernel) is bitwise the zeroed u_1_b followed by
     the accumulating gather, c_b accumulated as usual -- full grid (n = 37:
@@ -182,6 +183,8 @@ def test_fresh_gather_equals_zero_then_accumulate(mods, n, world):
     decompositions, incl. the overlapped interior / edge-band split."""
     torch, api, drivers = mods
     from paper_1907_02818_b200 import slab as slabmod
+    if noubwin:  # the in-kernel seed mask instead of the windowed seed map
+        monkeypatch.setenv("SGB_NO_UBWIN", "1")
     fam, sc = "wave3d_r4", {"D": 0.01}
     g = torch.Generator(device="cpu").manual_seed(n + world)
     full = {k: torch.randn((n, n, n), generator=g).cuda()
