@@ -276,13 +276,16 @@ def test_time_loop_adjoint_checkpointing_and_gradient(mods):
     assert abs(fd - ad) / (1 + abs(ad)) < 1e-6, (fd, ad)
 
 
+@pytest.mark.parametrize("noubwin", ["", "1"])
 @pytest.mark.parametrize("n", [40, 68, 37])
-def test_time_loop_fused_step_bitwise(mods, n, monkeypatch):
+def test_time_loop_fused_step_bitwise(mods, n, noubwin, monkeypatch):
     """fp32 time loop: the fused reverse step (gather adjoint + u_2 partial in
     one radius-4 streaming pass, sgb_wave3d_r4_b_step_f32) equals the gather
     followed by sgb_box_set bit for bit -- the whole gradient after T steps,
     incl. the zeros outside the box; n = 37 takes the entry's two-launch path."""
     torch, api, drivers = mods
+    if noubwin:  # the in-kernel seed mask instead of the windowed seed map
+        monkeypatch.setenv("SGB_NO_UBWIN", "1")
     T, D = 6, 0.01
     g = torch.Generator(device="cpu").manual_seed(n)
     c = (torch.rand((n, n, n), generator=g) * 3 + 1.5).cuda()
