@@ -386,6 +386,10 @@ def run_ours(args, cfg):
 
     from paper_1907_02818_b200 import drivers
     regen = args.config == "5"  # cfg 5: forward state and seed regenerated per step
+    # cfg 2: carried reverse steps (drivers.run_carried), in runs of 10 as the
+    # BASELINE config states: state u_1 regenerated per step, seed <- u_1_b,
+    # u_1_b <- u_2_b, u_2_b <- 0 after each; every 10th step starts a new run
+    carried = args.config == "2"
     tstep = [0]
     halo_mode = "serial" if args.no_overlap else args.halo
     overlap_sel = [halo_mode != "serial"]
@@ -397,7 +401,7 @@ def run_ours(args, cfg):
 
     pf_sel = [False]     # cross-step pipelined exchange (drivers.HaloPrefetch)
     pf = [None]
-    if sl is not None and world > 1 and halo_mode in ("auto", "prefetch"):
+    if sl is not None and world > 1 and halo_mode in ("auto", "prefetch") and not carried:
         def pf_regen(fs, t):
             drivers.regen_state(fs["u_1"], n, t, 0, R, sl)
             drivers.regen_seed(fs["u_b"], n, t, 0, sl)
@@ -414,6 +418,15 @@ def run_ours(args, cfg):
                 b.record(stream)
                 kev.append((a, b, nl))
             return
+        if carried:
+            t = tstep[0]
+            tstep[0] += 1
+            k = t % 10
+            if k == 0:  # a new 10-step run: seed u-bar^{T+1}, accumulators zero
+                drivers.regen_seed(arrays["u_b"], n, 10, 0, sl)
+                arrays["u_1_b"].zero_()
+                arrays["u_2_b"].zero_()
+            drivers.regen_state(arrays["u_1"], n, 9 - k, 0, R, sl)
         if regen:
             if peer_sel[0]:  # neighbours finished reading the planes regen overwrites
                 peermod.step_sync()
@@ -433,6 +446,10 @@ def run_ours(args, cfg):
         if record:
             b.record(stream)
             kev.append((a, b, nl))
+        if carried:  # rotate: seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- 0
+            arrays["u_b"], arrays["u_1_b"], arrays["u_2_b"] = (arrays["u_1_b"], arrays["u_2_b"],
+                                                               arrays["u_b"])
+            arrays["u_2_b"].zero_()
 
     def barrier():
         torch.cuda.synchronize()
@@ -615,7 +632,10 @@ def run_ours(args, cfg):
                    "regenerated_per_step": "u_1, u_b (regen kernels inside the timed step); "
                                            "u_1_b = the step's adjoint (zeroing fused into "
                                            "the gather)"
-                   if args.config == "5" else None},
+                   if args.config == "5" else
+                   ("carried runs of 10 reverse steps: u_1 regenerated per step, adjoints "
+                    "rotated (seed <- u_1_b <- u_2_b <- 0) inside the timed step"
+                    if carried else None)},
         "achieved_hbm_gbs": achieved,
         "clocks": clk.summary(),
         "e2e": e2e,

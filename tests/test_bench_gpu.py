@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("config,n", [("4", 128), ("5", 96), ("3", 1024), ("1", 1 << 16)])
+@pytest.mark.parametrize("config,n", [("4", 128), ("5", 96), ("2", 96), ("3", 1024), ("1", 1 << 16)])
 def test_bench_line_contract(config, n):
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", config, "--n", str(n),
            "--steps", "4", "--warmup", "3", "--no-ablation", "--no-configs", "--e2e-steps", "1"]
