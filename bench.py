@@ -439,17 +439,22 @@ def run_ours(args, cfg):
         if record:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        # cfg 5: u_1_b = this step's adjoint, zeroing fused into the gather
-        nl = drivers.adjoint_step(family, n, scalars, arrays, sl, overlap=overlap_sel[0],
-                                  link=link if peer_sel[0] else None,
-                                  fresh=regen and not peer_sel[0])
+        if carried and sl is None:  # u_2_b's zeroing after the rotation, fused
+            api.adjoint_fresh_u2(family, n, scalars, arrays)
+            nl = 1
+        else:
+            # cfg 5: u_1_b = this step's adjoint, zeroing fused into the gather
+            nl = drivers.adjoint_step(family, n, scalars, arrays, sl, overlap=overlap_sel[0],
+                                      link=link if peer_sel[0] else None,
+                                      fresh=regen and not peer_sel[0])
         if record:
             b.record(stream)
             kev.append((a, b, nl))
         if carried:  # rotate: seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- 0
             arrays["u_b"], arrays["u_1_b"], arrays["u_2_b"] = (arrays["u_1_b"], arrays["u_2_b"],
                                                                arrays["u_b"])
-            arrays["u_2_b"].zero_()
+            if sl is not None:  # N > 1: the slab gather accumulates u_2_b
+                arrays["u_2_b"].zero_()
 
     def barrier():
         torch.cuda.synchronize()
@@ -564,8 +569,8 @@ def run_ours(args, cfg):
     value = pts * args.steps / (ms / 1e3) / 1e9
     # roofline of the dominant kernel (per launch, this rank's share)
     local_pts = pts if sl is None else float(sl.owned) * n * n
-    if regen and not peer_sel[0]:
-        bpp -= 4  # fresh u_1_b: written, not read (24 B/pt instead of 28)
+    if (regen and not peer_sel[0]) or (carried and sl is None):
+        bpp -= 4  # fresh u_1_b / u_2_b: written, not read (24 / 32 B/pt instead of 28 / 36)
     achieved = bpp * local_pts / (kms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     traffic, tsrc = committed_traffic(family, n) if sl is None else (None, None)

@@ -237,6 +237,14 @@ int wave3d_r4_b_fresh_f32(int n, double D, float* c, float* c_b, float* u_1, flo
 int wave3d_r4_b_fresh_slab_f32(int n, double D, float* c, float* c_b, float* u_1,
                                    float* u_1_b, float* u_b, int i_base, int nplanes,
                                    int out_i0, int out_i1, sgb_stream_t stream);
+/* wave3d_c_b / wave3d_c2_b with u_2_b = this call's u_2 partial alone (-u_b
+ * on [1, n-2]^3, 0 elsewhere; c_b, u_1_b accumulated): the zeroing of u_2_b
+ * a carried reverse sweep does after rotating its adjoints, fused -- bitwise
+ * equal to zeroing u_2_b and calling the accumulating entry. */
+int wave3d_c_b_fresh_u2_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                            float* u_2_b, float* u_b, sgb_stream_t stream);
+int wave3d_c2_b_fresh_u2_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                             float* u_2_b, float* u_b, sgb_stream_t stream);
 /* one interior pass of the 5-point average u <- (u + 4 neighbours)/5 (2D) */
 int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream);
 

@@ -27,7 +27,7 @@ FAMILIES = {"wave1d": 1, "wave3d_c": 3, "wave3d_c2": 3, "burgers2d": 2, "wave3d_
 SCALARS = {"wave1d": ["D"], "wave3d_c": ["D"], "wave3d_c2": ["D"], "burgers2d": ["C", "D"],
            "wave3d_r4": ["D"]}
 _SUFFIX = {"primal": "", "adjoint": "_b", "scatter": "_scatter_b", "slab": "_b_slab",
-           "fresh": "_b_fresh", "fresh_slab": "_b_fresh_slab"}
+           "fresh": "_b_fresh", "fresh_slab": "_b_fresh_slab", "fresh_u2": "_b_fresh_u2"}
 
 
 def _sfx(dtype) -> str:
@@ -118,6 +118,12 @@ def adjoint_slab_fresh(family, n, scalars, arrays, i_base, nplanes, out_i0, out_
     """z-slab form of adjoint_fresh over global output planes [out_i0, out_i1)."""
     _call(family, "fresh_slab", n, scalars, arrays, stream,
           extra=(int(i_base), int(nplanes), int(out_i0), int(out_i1)))
+
+
+def adjoint_fresh_u2(family, n, scalars, arrays, stream=None):
+    """wave3d_c(2)_b_fresh_u2_f32: the radius-1 gather with u_2_b = this call's
+    u_2 partial alone (a carried sweep's zeroing of u_2_b, fused)."""
+    _call(family, "fresh_u2", n, scalars, arrays, stream)
 
 
 # ------------------------------------------------------------ device inputs

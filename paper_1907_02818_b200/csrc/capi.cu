@@ -296,6 +296,26 @@ static bool burgers2d_primal_ring(long long n, double C, double D, const T* u_1,
   return true;
 }
 
+// wave3d_c / wave3d_c2 gather whose u_2_b is this call's u_2 partial alone
+// (0 - u_b on the box, 0 elsewhere): the carried reverse sweep's zeroing of
+// u_2_b after its rotation, fused (v1 streaming kernel, U2SET).
+template <int MODE>
+static int star3_c_fresh_u2(const char* name, int n, double D, float* c, float* c_b,
+                            float* u_1, float* u_1_b, float* u_2_b, float* u_b,
+                            cudaStream_t s) {
+  if (n <= 0) return einval(std::string(name) + ": n must be positive");
+  if (!guard_ok(MODE == 0 ? WAVE3D_C : WAVE3D_C2, n)) return SGB_GUARD;
+  if (!c || !c_b || !u_1 || !u_1_b || !u_2_b || !u_b)
+    return einval(std::string(name) + ": null array");
+  if (star3_tma_supported<MODE, float>(n) && !std::getenv("SGB_FRESH_UNFUSED"))
+    return star3_tma_gather<MODE, true>(Slab3{n, 0, n}, 1, n - 2, 0, n, (float)D, c, c_b, u_1,
+                                        u_1_b, u_2_b, u_b, s, name);
+  // other shapes: zero u_2_b, then the accumulating gather
+  if (cudaMemsetAsync(u_2_b, 0, (size_t)n * n * n * sizeof(float), s) != cudaSuccess)
+    return launch_status(name);
+  return star3_gather<MODE, float>(name, n, D, c, c_b, u_1, u_1_b, u_2_b, u_b, 0, n, 0, n, s);
+}
+
 }  // namespace sgb
 
 using namespace sgb;
@@ -421,6 +441,18 @@ int wave3d_r4_b_fresh_slab_f32(int n, double D, float* c, float* c_b, float* u_1
                                    int out_i0, int out_i1, sgb_stream_t stream) {
   return r4_fresh("sgb_wave3d_r4_b_fresh_slab", n, D, c, c_b, u_1, u_1_b, u_b, i_base, nplanes,
                   out_i0, out_i1, as_stream(stream));
+}
+
+int wave3d_c_b_fresh_u2_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                            float* u_2_b, float* u_b, sgb_stream_t stream) {
+  return star3_c_fresh_u2<0>("wave3d_c_b_fresh_u2", n, D, c, c_b, u_1, u_1_b, u_2_b, u_b,
+                             as_stream(stream));
+}
+
+int wave3d_c2_b_fresh_u2_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
+                             float* u_2_b, float* u_b, sgb_stream_t stream) {
+  return star3_c_fresh_u2<1>("wave3d_c2_b_fresh_u2", n, D, c, c_b, u_1, u_1_b, u_2_b, u_b,
+                             as_stream(stream));
 }
 
 int sgb_wave3d_r4_b_step_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,

@@ -154,7 +154,10 @@ __device__ __forceinline__ void star_field_plane(const float* F, int crow, int t
   }
 }
 
-template <int MODE>
+// U2SET (radius-1 specs): u_2_b is written as this call's u_2 partial alone
+// (0 - u_b on B, 0 elsewhere) instead of accumulated -- the zeroing a carried
+// reverse sweep does after its rotation, fused (bitwise equal).
+template <int MODE, bool U2SET = false>
 __global__ void __launch_bounds__(256, 2)
     star3_tma_kernel(const __grid_constant__ CUtensorMap tm_c,
                      const __grid_constant__ CUtensorMap tm_ub,
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(256, 2)
           u1b_old = *reinterpret_cast<const float4*>(u_1_b + gidx);
           if (o >= lo && o <= hi && jin) {
             cb_old = *reinterpret_cast<const float4*>(c_b + gidx);
-            if (S3::kU2) u2b_old = *reinterpret_cast<const float4*>(u_2_b + gidx);
+            if (S3::kU2 && !U2SET) u2b_old = *reinterpret_cast<const float4*>(u_2_b + gidx);
           }
         }
 
@@ -336,13 +339,15 @@ __global__ void __launch_bounds__(256, 2)
               *reinterpret_cast<float4*>(c_b + gidx) = cb;
               if (S3::kU2) {
                 const float4 um = uq[qs];
-                float4 u2 = u2b_old;
+                float4 u2 = u2b_old;  // zero in U2SET mode
                 if (kin[0]) u2.x = u2.x + -um.x;
                 if (kin[1]) u2.y = u2.y + -um.y;
                 if (kin[2]) u2.z = u2.z + -um.z;
                 if (kin[3]) u2.w = u2.w + -um.w;
                 *reinterpret_cast<float4*>(u_2_b + gidx) = u2;
               }
+            } else if (S3::kU2 && U2SET) {  // not on the box: u_2_b = 0
+              *reinterpret_cast<float4*>(u_2_b + gidx) = make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
         }
@@ -428,7 +433,7 @@ inline int choose_chunks(long long tiles, long long nout, int R, int per_sm) {
   return best_c;
 }
 
-template <int MODE>
+template <int MODE, bool U2SET = false>
 inline int star3_tma_gather(const Slab3& g, long long lo, long long hi, long long out_i0,
                             long long out_i1, float D, const float* c, float* c_b,
                             const float* u_1, float* u_1_b, float* u_2_b, const float* u_b,
@@ -458,7 +463,7 @@ inline int star3_tma_gather(const Slab3& g, long long lo, long long hi, long lon
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(star3_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(star3_tma_kernel<MODE, U2SET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Tl::SMEM);
     attr_set = true;
   }
@@ -468,7 +473,7 @@ inline int star3_tma_gather(const Slab3& g, long long lo, long long hi, long lon
   const int chunks = choose_chunks((long long)tiles_k * tiles_j, nout, Tl::R, Tl::MIN_BLOCKS);
   const int chunk = (int)((nout + chunks - 1) / chunks);
   dim3 grid((unsigned)(tiles_k * tiles_j), (unsigned)((nout + chunk - 1) / chunk));
-  star3_tma_kernel<MODE><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
+  star3_tma_kernel<MODE, U2SET><<<grid, Tl::THREADS, Tl::SMEM, s>>>(
       maps[0], maps[1], maps[2], c_b, u_1_b, u_2_b, (int)g.n, (int)g.i_base, (int)lo, (int)hi,
       (int)out_i0, (int)out_i1, chunk, tiles_k, D);
   return launch_status(name);

@@ -215,13 +215,18 @@ def run_carried(n, steps, seed=0, D=0.1, family="wave3d_c", arrays=None):
         arrays = alloc(family, n)
         init_static(family, arrays, n, seed)
         regen_seed(arrays["u_b"], n, steps, seed)  # u-bar^{T+1}
+    fused = arrays["u_1"].dtype == torch.float32
     for t in reversed(range(steps)):
         regen_state(arrays["u_1"], n, t, seed, 1)
-        api.adjoint(family, n, {"D": D}, arrays)
+        if fused:  # u_2_b written as this step's partial: the zeroing below, fused
+            api.adjoint_fresh_u2(family, n, {"D": D}, arrays)
+        else:
+            api.adjoint(family, n, {"D": D}, arrays)
         # rotate: seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- 0
         arrays["u_b"], arrays["u_1_b"], arrays["u_2_b"] = (arrays["u_1_b"], arrays["u_2_b"],
                                                            arrays["u_b"])
-        arrays["u_2_b"].zero_()
+        if not fused:
+            arrays["u_2_b"].zero_()
     return arrays
 
 

@@ -217,6 +217,28 @@ def test_fresh_gather_equals_zero_then_accumulate(mods, n, world, noubwin, monke
             assert torch.equal(a[k][own].view(torch.int32), b[k][own].view(torch.int32)), (r, k)
 
 
+@pytest.mark.parametrize("family", ["wave3d_c", "wave3d_c2"])
+@pytest.mark.parametrize("n", [40, 68, 37])
+def test_fresh_u2_gather_equals_zero_then_accumulate(mods, family, n):
+    """wave3d_c(2)_b_fresh_u2_f32 (u_2_b written as the call's u_2 partial;
+    the carried sweep's zeroing fused into the radius-1 streaming kernel) is
+    bitwise the zeroed u_2_b followed by the accumulating gather, on every
+    point incl. zero signs; n = 37 takes the entry's memset + gather path."""
+    torch, api, drivers = mods
+    sc = {"D": 0.1}
+    g = torch.Generator(device="cpu").manual_seed(n + 7)
+    a = {k: torch.randn((n, n, n), generator=g).cuda()
+         for k in ("c", "c_b", "u_1", "u_1_b", "u_2_b", "u_b")}
+    b = {k: v.clone() for k, v in a.items()}
+    a["u_2_b"].fill_(float("nan"))
+    api.adjoint_fresh_u2(family, n, sc, a)
+    b["u_2_b"].zero_()
+    api.adjoint(family, n, sc, b)
+    torch.cuda.synchronize()
+    for k in ("c_b", "u_1_b", "u_2_b"):
+        assert torch.equal(a[k].view(torch.int32), b[k].view(torch.int32)), k
+
+
 def test_generators_are_decomposition_invariant(mods):
     """fill_normal3d / fill_random / fill_layered values depend only on the
     global index: a slab regenerates exactly the single-GPU planes."""
