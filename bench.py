@@ -706,12 +706,9 @@ def boundary_ab(torch, family, n, scalars, arrays, dtype, kms):
         from paper_1907_02818_b200 import api
         zero_ms = _time_launch(torch, lambda: api.adjoint(family, n, scalars, arrays), iters=5,
                                warm=2)
-        os.environ["SGB_NO_UBWIN"] = "1"
-        try:
+        with api.options(NO_UBWIN=1):
             guard_ms = _time_launch(torch, lambda: api.adjoint(family, n, scalars, arrays),
                                     iters=5, warm=2)
-        finally:
-            del os.environ["SGB_NO_UBWIN"]
         out["hand_tuned_zero_padded_seed_ms"] = zero_ms
         out["hand_tuned_guarded_seed_ms"] = guard_ms
     return out

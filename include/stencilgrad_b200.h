@@ -48,6 +48,43 @@ const char* sgb_version(void);
 /* number of kernel launches issued by this library since load (all threads) */
 unsigned long long sgb_launch_count(void);
 
+/* ---- run-time options ---------------------------------------------------------
+ * Scheduling / A-B knobs (kernel variant, i-chunking, ...) whose defaults are
+ * the measured best; none selects a CPU path.  The environment (SGB_<NAME>)
+ * is read once, at the first call that needs an option; afterwards options
+ * change only through these calls (thread-safe, process-wide).  Names are
+ * listed by sgb_option_name(0 .. ) (NULL past the end); an "SGB_" prefix is
+ * accepted.  Unknown names return SGB_EINVAL. */
+int sgb_set_option(const char* name, long long value);
+int sgb_clear_option(const char* name);
+int sgb_get_option(const char* name, long long* value, int* is_set);
+const char* sgb_option_name(int index);
+
+/* ---- program-keyed dispatch ---------------------------------------------------
+ * The hand-tuned kernels of a family compute ONE AdjointProgram: the
+ * reference front end's assemble_adjoint (adjoint.cpp:152-163, adjoint.hpp:37-45)
+ * of oracle/specs/<family>.json.  sgb_program_family(text) returns the family
+ * whose kernels compute exactly the program whose canonical text is given, or
+ * NULL (sgb_last_error names the closest family and the first differing
+ * line) -- callers holding an AdjointProgram dispatch through this instead of
+ * a name, and lower any other program with the NVRTC emitter.  Canonical text
+ * (one item per line, as printed by b200_program_text in
+ * oracle/ref/b200_binding.cpp):
+ *   sgb-program 1
+ *   counters <c0> <c1> ...
+ *   guard <hi - lo (AffineExpr::str)> >= <needed>          per dimension
+ *   term <t> read <array> offset <o..> adjoint <a_b> seed <seed>[<c>].. partial <to_input_string>
+ *   valid <t> <lo>:<hi>,...                                 per shifted statement
+ *   nest <lo>:<hi>,... terms <t..>[ core]                   per nest, program order
+ *   core <core_index>
+ * sgb_program_text(family): the embedded text; sgb_family_signature(family):
+ * "<sizes>;<scalars>;<arrays>" of the generated <family>_b prototype
+ * (codegen.cpp:198-230), comma-separated, e.g. "n;D;c,c_b,u_1,u_1_b,u_b".
+ * None of these needs a GPU. */
+const char* sgb_program_family(const char* canonical_text);
+const char* sgb_program_text(const char* family);
+const char* sgb_family_signature(const char* family);
+
 /* ---- cfg 1: wave1d (oracle/specs/wave1d.json) -------------------------------
  * u_next[i] = 2u[i] - u_prev[i] + c[i]^2 D (u[i-1] - 2u[i] + u[i+1]), i in [1, n-2]
  * Reference prototypes: wave1d(int n, double D, double *c, double *u,
@@ -247,6 +284,23 @@ int wave3d_c2_b_fresh_u2_f32(int n, double D, float* c, float* c_b, float* u_1, 
                              float* u_2_b, float* u_b, sgb_stream_t stream);
 /* one interior pass of the 5-point average u <- (u + 4 neighbours)/5 (2D) */
 int sgb_smooth5_f64(const double* src, double* dst, int n, sgb_stream_t stream);
+
+/* ---- device-side parity reductions (verification entries; synchronous) -----
+ * compare_grids of the reference (interp.cpp:290-298) on DEVICE arrays, a in
+ * the kernel's precision, b the fp64 oracle grid uploaded to the device:
+ * out4[0] = max_i |a_i - b_i| / (1 + |b_i|) over finite terms, out4[1] =
+ * sum (a - b)^2, out4[2] = sum b^2 (the norm metric), out4[3] = number of
+ * non-finite terms (a pass needs 0).  fp64 accumulation, deterministic.
+ * sgb_dot_*: <a, b> in fp64, the inner products of dot_product_test
+ * (interp.cpp:354-375). */
+int sgb_compare_f32(const float* a, const double* b, long long count, double* out4,
+                    sgb_stream_t stream);
+int sgb_compare_f64(const double* a, const double* b, long long count, double* out4,
+                    sgb_stream_t stream);
+int sgb_dot_f32(const float* a, const float* b, long long count, double* out,
+                sgb_stream_t stream);
+int sgb_dot_f64(const double* a, const double* b, long long count, double* out,
+                sgb_stream_t stream);
 
 /* ---- host-buffer entry (end-to-end path) ------------------------------------
  * Same arguments as <name>_b but HOST pointers; copies inputs and accumulated

@@ -61,6 +61,23 @@ struct Env {
 
 enum class Precision { f64, f32 };
 
+// An AdjointProgram (adjoint.hpp:37-45) in the canonical text form of
+// sgb_program_family (stencilgrad_b200.h): what run_program executes.
+// Program::of(family) is the program the family's kernels compute (the
+// reference front end's assemble_adjoint of oracle/specs/<family>.json).
+struct Program {
+  std::string text;
+  static Program of(const std::string& family);
+  // the family whose hand-tuned kernels compute exactly this program; throws
+  // Error (naming the first differing line) when there is none
+  std::string family() const;
+};
+
+// Gather adjoint of `program` (run_program(const AdjointProgram&, const Env&),
+// interp.hpp:59): dispatched on the program itself -- a program no hand-tuned
+// family computes throws Error instead of running a hard-coded stencil.
+Env run_program(const Program& program, const Env& env, Precision p = Precision::f64);
+
 // Primal (run_nest semantics): the output grid updated on the primal box.
 Env run_nest(const std::string& family, const Env& env, Precision p = Precision::f64);
 // Gather adjoint (run_program semantics): guards first, then every input

@@ -268,3 +268,70 @@ def ref_available() -> bool:
 def spec_path(name: str) -> str:
     p = os.path.join(SPEC_DIR, name + ".json")
     return p if os.path.exists(p) else "example:" + name
+
+
+# ---------------------------------------------------------------- reference emitted C
+def ref_emitted_path(name: str) -> str:
+    return os.path.join(REF_DIR, f"libref_{name}.so")
+
+
+def ref_emitted_available(name: str) -> bool:
+    return os.path.exists(ref_emitted_path(name))
+
+
+def ref_emitted_opt(name: str) -> str:
+    p = os.path.join(REF_DIR, f"libref_{name}.opt")
+    return open(p).read().strip() if os.path.exists(p) else "-O2"
+
+
+def _ref_params(name: str, fn: str):
+    """Parameter names of <fn> from the prototypes the reference emitted
+    itself (oracle/_ref/gen/<name>_protos.h; codegen.cpp:198-230)."""
+    import re
+    text = open(os.path.join(REF_DIR, "gen", f"{name}_protos.h")).read()
+    m = re.search(r"int\s+" + re.escape(fn) + r"\(([^)]*)\);", text)
+    if not m:
+        raise KeyError(fn)
+    out = []
+    for a in m.group(1).split(","):
+        a = a.strip()
+        out.append(("ptr" if "*" in a else a.split()[0], a.replace("*", " ").split()[-1]))
+    return out
+
+
+_ref_libs = {}
+
+
+def ref_emitted(name: str, kind: str = "adjoint"):
+    """The reference's OWN generated OpenMP function (emit_primal /
+    emit_adjoint / emit_scatter_adjoint, codegen.cpp:311-434, compiled by
+    oracle/ref/Makefile into oracle/_ref/libref_<name>.so).  Returns
+    call(n, scalars, arrays) -> return code, arrays = name -> C-contiguous
+    fp64 buffer (numpy array or CPU torch tensor), updated in place."""
+    fn_name = name + {"primal": "", "adjoint": "_b", "scatter": "_scatter_b"}[kind]
+    if name not in _ref_libs:
+        _ref_libs[name] = ctypes.CDLL(ref_emitted_path(name))
+    fn = getattr(_ref_libs[name], fn_name)
+    fn.restype = ctypes.c_int
+    params = _ref_params(name, fn_name)
+
+    def ptr(a):
+        if hasattr(a, "data_ptr"):
+            import torch
+            assert a.dtype == torch.float64 and a.is_contiguous() and not a.is_cuda
+            return ctypes.c_void_p(a.data_ptr())
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+        return ctypes.c_void_p(a.ctypes.data)
+
+    def call(n, scalars, arrays):
+        args = []
+        for typ, pn in params:
+            if typ == "int":
+                args.append(ctypes.c_int(int(n) if pn == "n" else int(scalars[pn])))
+            elif typ == "double":
+                args.append(ctypes.c_double(float(scalars[pn])))
+            else:
+                args.append(ptr(arrays[pn]))
+        return fn(*args)
+    call.params = [pn for typ, pn in params if typ == "ptr"]
+    return call

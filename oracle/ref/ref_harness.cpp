@@ -14,7 +14,15 @@
 //   b200   <spec> <n> <in_dir> S=v            run_program vs run_program_b200 (the
 //                                             INTEGRATION.md binding, b200_binding.cpp)
 //                                             on the same Env; prints the max
-//                                             compare_grids error as JSON
+//                                             compare_grids error as JSON, or
+//                                             {"error": ...} (exit 3) when the
+//                                             binding refuses the program
+//   canon  <spec>                             the program's canonical text
+//                                             (b200_program_text), exported as
+//                                             paper_1907_02818_b200/programs/<name>.canon
+//   match  <spec>                             the family the B200 library's
+//                                             sgb_program_family() assigns to the
+//                                             program (no GPU needed), JSON
 //   spec   <spec>                             serialize_spec (specfile.cpp:208-240)
 //   emit   <spec> <out_dir>                   emit_primal / emit_adjoint /
 //                                             emit_scatter_adjoint with restrict,
@@ -45,8 +53,10 @@
 
 namespace sg = stencilgrad;
 
-namespace stencilgrad {
-Env run_program_b200(const Problem& p, const Env& env);  // b200_binding.cpp
+namespace stencilgrad {  // b200_binding.cpp
+Env run_program_b200(const AdjointProgram& prog, const Env& env);
+std::string b200_program_text(const AdjointProgram& prog);
+std::string b200_program_family(const AdjointProgram& prog, std::string* why);
 }
 
 static std::string slurp(const std::string& path) {
@@ -202,8 +212,18 @@ static sg::Env load_env(const sg::Problem& p, long long n, const std::string& in
 static int cmd_b200(const sg::Problem& p, long long n, const std::string& in_dir, int argc,
                     char** argv) {
   sg::Env env = load_env(p, n, in_dir, argc, argv);
-  sg::Env ref = sg::run_program(sg::assemble_adjoint(p), env);
-  sg::Env gpu = sg::run_program_b200(p, env);
+  const auto prog = sg::assemble_adjoint(p);
+  sg::Env ref = sg::run_program(prog, env);
+  sg::Env gpu;
+  try {
+    gpu = sg::run_program_b200(prog, env);
+  } catch (const sg::Error& e) {
+    std::string msg = e.what();
+    for (auto& ch : msg)
+      if (ch == '"' || ch == '\\' || ch == '\n') ch = ' ';
+    std::cout << "{\"name\":\"" << p.name << "\",\"error\":\"" << msg << "\"}\n";
+    return 3;
+  }
   const sg::ArrayDecl& out = sg::output_array(p);
   double worst = 0.0;
   std::ostringstream os;
@@ -298,6 +318,20 @@ int main(int argc, char** argv) {
       return 0;
     }
     if (cmd == "b200" && argc >= 5) return cmd_b200(p, std::atoll(argv[3]), argv[4], argc - 5, argv + 5);
+    if (cmd == "canon") {
+      std::cout << sg::b200_program_text(sg::assemble_adjoint(p));
+      return 0;
+    }
+    if (cmd == "match") {
+      std::string why;
+      const std::string fam = sg::b200_program_family(sg::assemble_adjoint(p), &why);
+      for (auto& ch : why)
+        if (ch == '"' || ch == '\\' || ch == '\n') ch = ' ';
+      std::cout << "{\"name\":\"" << p.name << "\",\"family\":"
+                << (fam.empty() ? std::string("null") : "\"" + fam + "\"")
+                << ",\"why\":\"" << why << "\"}\n";
+      return 0;
+    }
     std::cerr << "bad arguments\n";
     return 2;
   } catch (const std::exception& e) {

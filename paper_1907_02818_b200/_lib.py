@@ -33,6 +33,7 @@ _CTYPES = {
     "void*": ctypes.c_void_p,
     "const void*": ctypes.c_void_p,
     "long long*": ctypes.c_void_p,
+    "int*": ctypes.c_void_p,
     "const char*": ctypes.c_char_p,
     "sgb_plan*": ctypes.c_void_p,
     "sgb_jit_kernel*": ctypes.c_void_p,

@@ -283,3 +283,147 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------ device parity reductions
+def compare(a, b):
+    """compare_grids (interp.cpp:290-298) on the device: a (fp32 / fp64 CUDA
+    tensor) against the fp64 CUDA tensor b.  Returns {"max_rel": max |a-b| /
+    (1+|b|), "norm_rel": ||a-b|| / ||b||, "nonfinite": count}."""
+    import math
+    import torch
+    if not (a.is_cuda and b.is_cuda and a.is_contiguous() and b.is_contiguous()):
+        raise _lib.StencilError("compare: contiguous CUDA tensors required")
+    if b.dtype != torch.float64 or a.numel() != b.numel():
+        raise _lib.StencilError("compare: b must be fp64 with a's element count")
+    fn = {torch.float32: _lib.lib().sgb_compare_f32,
+          torch.float64: _lib.lib().sgb_compare_f64}.get(a.dtype)
+    if fn is None:
+        raise _lib.StencilError(f"compare: unsupported dtype {a.dtype}")
+    out = (ctypes.c_double * 4)()
+    _lib.check(fn(ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()), a.numel(), out,
+                  _stream_ptr()), "compare")
+    nb = math.sqrt(out[2])
+    return {"max_rel": out[0], "norm_rel": math.sqrt(out[1]) / (nb if nb > 0 else 1.0),
+            "nonfinite": int(out[3])}
+
+
+def dot(a, b):
+    """<a, b> accumulated in fp64 on the device (dot_product_test's inner
+    products, interp.cpp:354-375)."""
+    import torch
+    if a.dtype != b.dtype or a.numel() != b.numel() or not (a.is_cuda and b.is_cuda):
+        raise _lib.StencilError("dot: CUDA tensors of one dtype and size required")
+    fn = {torch.float32: _lib.lib().sgb_dot_f32, torch.float64: _lib.lib().sgb_dot_f64}.get(
+        a.dtype)
+    if fn is None:
+        raise _lib.StencilError(f"dot: unsupported dtype {a.dtype}")
+    out = ctypes.c_double()
+    _lib.check(fn(ctypes.c_void_p(a.contiguous().data_ptr()),
+                  ctypes.c_void_p(b.contiguous().data_ptr()), a.numel(), ctypes.byref(out),
+                  _stream_ptr()), "dot")
+    return out.value
+
+
+# ------------------------------------------------------------ run-time options
+def option_names():
+    out, i = [], 0
+    while True:
+        nm = _lib.lib().sgb_option_name(i)
+        if nm is None:
+            return out
+        out.append(nm.decode())
+        i += 1
+
+
+def get_option(name: str):
+    """(value, is_set) of a run-time option (sgb_get_option)."""
+    v, s = ctypes.c_longlong(), ctypes.c_int()
+    _lib.check(_lib.lib().sgb_get_option(name.encode(), ctypes.byref(v), ctypes.byref(s)),
+               "sgb_get_option")
+    return v.value, bool(s.value)
+
+
+def set_option(name: str, value=None):
+    """Sets (value not None) or clears a run-time option (sgb_set_option)."""
+    L = _lib.lib()
+    if value is None:
+        _lib.check(L.sgb_clear_option(name.encode()), "sgb_clear_option")
+    else:
+        _lib.check(L.sgb_set_option(name.encode(), int(value)), "sgb_set_option")
+
+
+class options:
+    """Context manager: ``with api.options(NO_UBWIN=1, ICHUNKS=3): ...``
+    restores the previous settings on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.saved = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.saved[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, (v, was_set) in self.saved.items():
+            set_option(k, v if was_set else None)
+
+
+# ------------------------------------------------------------ program-keyed entry
+_PROG_DIR = __import__("os").path.join(__import__("os").path.dirname(
+    __import__("os").path.abspath(__file__)), "programs")
+
+
+def load_program(name: str) -> dict:
+    """A reference front-end output committed under programs/<name>.json:
+    {"spec": serialize_spec (specfile.cpp:208-240), "terms": the
+    AdjointProgram's terms in active_reads order with to_input_string
+    partials (adjoint.hpp:13-19)}."""
+    import json
+    import os
+    with open(os.path.join(_PROG_DIR, name + ".json")) as fh:
+        d = json.load(fh)
+    return {"spec": d["spec"], "terms": d["terms"]}
+
+
+def _norm_program(p: dict):
+    import json
+    terms = [{"array": t["array"], "adjoint": t["adjoint"], "offset": list(t["offset"]),
+              "partial": " ".join(str(t["partial"]).split())} for t in p["terms"]]
+    return json.dumps(p["spec"], sort_keys=True), json.dumps(terms)
+
+
+def program_family(program: dict):
+    """The family whose hand-tuned kernels compute exactly `program` (same
+    spec -- counters, bounds, arrays, lhs, mode, rhs -- and the same terms:
+    arrays, offsets, partials), or None."""
+    key = _norm_program(program)
+    for fam in FAMILIES:
+        if _norm_program(load_program(fam)) == key:
+            return fam
+    return None
+
+
+def run_program_from(program: dict, sizes: dict, scalars: dict, grids: dict, adjs: dict,
+                     dtype="f64", return_route=False):
+    """run_program(const AdjointProgram&, const Env&) (interp.hpp:59) keyed on
+    the PROGRAM: a program one of the hand-tuned families computes runs those
+    kernels; any other program is lowered through the NVRTC emitter
+    (emitter.py), which consumes its terms and bounds.  Host grids in, new
+    host adjoint arrays out (the inputs are untouched)."""
+    fam = program_family(program)
+    if fam is not None:
+        out = run_program(fam, int(sizes["n"]), scalars, grids, adjs, dtype=dtype)
+        return (out, "hand-tuned") if return_route else out
+    import torch
+    from . import emitter
+    ep = emitter.EmittedProblem(program["spec"], program["terms"], _sfx(dtype))
+    td = torch.float32 if _sfx(dtype) == "f32" else torch.float64
+    arrays = {k: _to_dev(v, td) for k, v in {**grids, **adjs}.items()}
+    ep.adjoint(sizes, scalars, arrays)
+    torch.cuda.synchronize()
+    out = {k: arrays[k].to("cpu", torch.float64).numpy() for k in adjs}
+    return (out, "emitter") if return_route else out

@@ -55,10 +55,8 @@ static bool guard_ok(int fam, long long n) {
 // radius-4 streaming kernel (v7) for radius 4, the v1 streaming kernel for
 // radius 1 (measured faster there); SGB_STAR_KERNEL=1|7 forces one of them.
 static int star_kernel_version(int mode) {
-  if (const char* e = std::getenv("SGB_STAR_KERNEL")) {
-    const int v = std::atoi(e);
-    if (v == 1 || v == 7) return v;
-  }
+  const long long v = opt(OPT_STAR_KERNEL, 0);
+  if (v == 1 || v == 7) return (int)v;
   return mode == 2 ? 7 : 1;
 }
 
@@ -83,12 +81,19 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
   if (out_i1 == out_i0) return 0;
   const long long lo = R, hi = n - 1 - R;
   Slab3 g{n, i_base, nplanes};
-  if (star3_tma_supported<MODE, T>(n)) {
+  if (star3_tma_ok<MODE, T>(n, {c, c_b, u_1, u_1_b, u_2_b, u_b})) {
     if (star_kernel_version(MODE) == 7)
       return star3_v7_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
                                    (float*)c_b, (const float*)u_1, (float*)u_1_b, (float*)u_2_b,
                                    (const float*)u_b, s, name);
-    return star3_tma_gather<MODE>(g, lo, hi, out_i0, out_i1, (float)D, (const float*)c,
+    if constexpr (MODE < 2) {
+      if (opt(OPT_R1_FP64ACC, 1))  // radius-1 specs: fp64 accumulation
+        return star3_tma_gather<MODE, false, true>(g, lo, hi, out_i0, out_i1, D,
+                                                   (const float*)c, (float*)c_b,
+                                                   (const float*)u_1, (float*)u_1_b,
+                                                   (float*)u_2_b, (const float*)u_b, s, name);
+    }
+    return star3_tma_gather<MODE>(g, lo, hi, out_i0, out_i1, D, (const float*)c,
                                   (float*)c_b, (const float*)u_1, (float*)u_1_b,
                                   (float*)u_2_b, (const float*)u_b, s, name);
   }
@@ -96,14 +101,14 @@ static int star3_gather(const char* name, long long n, double D, const T* c, T* 
   // radius 1 keeps the per-point kernel (measured faster there)
   if constexpr (std::is_same<T, double>::value) {
     // fp64: the register-blocked streaming kernel (star3d_f64.cuh)
-    if (!std::getenv("SGB_F64_PLANE") && !std::getenv("SGB_GENERIC_POINT") && n <= 46340) {
+    if (!opt_flag(OPT_F64_PLANE) && !opt_flag(OPT_GENERIC_POINT) && n <= 46340) {
       const int rc = star3_f64_stream_gather<MODE>(g, lo, hi, out_i0, out_i1, D, c, c_b, u_1,
                                                    u_1_b, u_2_b, u_b, s, name);
       if (rc != 1) return rc;
     }
   }
-  if (MODE == 2 && !std::getenv("SGB_GENERIC_POINT") && n <= 46340) {
-    if (!std::getenv("SGB_PLANE_NO_TMA")) {
+  if (MODE == 2 && !opt_flag(OPT_GENERIC_POINT) && n <= 46340) {
+    if (!opt_flag(OPT_PLANE_NO_TMA)) {
       const int rc = star3_plane_tma_gather<MODE, T>(g, lo, hi, out_i0, out_i1, (T)D, c, c_b,
                                                      u_1, u_1_b, u_2_b, u_b, s, name);
       if (rc != 1) return rc;
@@ -125,7 +130,7 @@ static int star3_primal(const char* name, long long n, double D, const T* c, con
   if (n <= 0) return einval(std::string(name) + ": n must be positive");
   if (!c || !u_1 || !u_2 || !u) return einval(std::string(name) + ": null array");
   if (n < 2 * R + 1) return 0;  // empty primal box
-  if (std::is_same<T, float>::value && !std::getenv("SGB_PRIMAL_GENERIC")) {
+  if (std::is_same<T, float>::value && !opt_flag(OPT_PRIMAL_GENERIC)) {
     const int rc = star3_primal_tma<MODE>(n, (float)D, (const float*)c, (const float*)u_1,
                                           (const float*)u_2, (float*)u, s, name);
     if (rc != 1) return rc;  // 1: TMA path not applicable (alignment / size)
@@ -133,7 +138,7 @@ static int star3_primal(const char* name, long long n, double D, const T* c, con
   if constexpr (std::is_same<T, double>::value && MODE == 2) {
     // radius 4 (the radius-1 fp64 primal is already at the copy bandwidth on
     // the per-point kernel)
-    if (!std::getenv("SGB_PRIMAL_GENERIC")) {
+    if (!opt_flag(OPT_PRIMAL_GENERIC)) {
       const int rc = star3_primal_f64_stream<MODE>(n, D, c, u_1, u_2, u, s, name);
       if (rc != 1) return rc;
     }
@@ -206,24 +211,21 @@ static int burgers2d_gather(long long n, double C, double D, const T* u_1, T* u_
   if (range && (row_lo < 0 || row_lo > row_hi || row_hi > n))
     return einval("burgers2d_b_rows: bad row range");
   if ((n * (long long)sizeof(T)) % 16 == 0 && n <= (1 << 30) && aligned16(u_1, u_1_b, u_b, u_b) &&
-      (range || !std::getenv("SGB_BURGERS_NORING"))) {
+      (range || !opt_flag(OPT_BURGERS_NORING))) {
     if (row_hi == row_lo) return 0;
-    // rows per CTA / ring stages: measured defaults, env overrides (read per call)
-    int rb = 32, stages = 5;
-    if (const char* e = std::getenv("SGB_BURGERS_RING_RB")) rb = std::max(1, std::atoi(e));
-    if (const char* f = std::getenv("SGB_BURGERS_RING_S")) stages = std::atoi(f);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(burgers2d_ring_kernel<T, 4>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, BurgRing<T, 4>::SMEM);
-      cudaFuncSetAttribute(burgers2d_ring_kernel<T, 5>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, BurgRing<T, 5>::SMEM);
-      cudaFuncSetAttribute(burgers2d_ring_kernel<T, 6>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, BurgRing<T, 6>::SMEM);
-      cudaFuncSetAttribute(burgers2d_ring_kernel<T, 8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, BurgRing<T, 8>::SMEM);
-      attr = true;
-    }
+    // rows per CTA / ring stages: measured defaults (options override)
+    const int rb = (int)std::max<long long>(1, opt(OPT_BURGERS_RING_RB, 32));
+    const int stages = (int)opt(OPT_BURGERS_RING_S, 5);
+    int rc = 0;
+    if (stages == 4)
+      rc = ensure_smem((const void*)burgers2d_ring_kernel<T, 4>, BurgRing<T, 4>::SMEM, "burgers2d_b");
+    else if (stages == 5)
+      rc = ensure_smem((const void*)burgers2d_ring_kernel<T, 5>, BurgRing<T, 5>::SMEM, "burgers2d_b");
+    else if (stages == 6)
+      rc = ensure_smem((const void*)burgers2d_ring_kernel<T, 6>, BurgRing<T, 6>::SMEM, "burgers2d_b");
+    else
+      rc = ensure_smem((const void*)burgers2d_ring_kernel<T, 8>, BurgRing<T, 8>::SMEM, "burgers2d_b");
+    if (rc) return rc;
     constexpr int W = BurgRing<T>::W, TH = BurgRing<T>::THREADS;
     dim3 g((unsigned)((n + W - 1) / W), (unsigned)((row_hi - row_lo + rb - 1) / rb));
     if (stages == 4)
@@ -242,12 +244,8 @@ static int burgers2d_gather(long long n, double C, double D, const T* u_1, T* u_
   }
   if (range) return einval("burgers2d_b_rows: needs 16-byte rows and aligned arrays");
   if (n % 2 == 0 && aligned16(u_1, u_1_b, u_b, u_b)) {
-    static int rb = -1;  // rows per block (SGB_BURGERS_RB), measured default
-    if (rb < 0) {
-      const char* e = std::getenv("SGB_BURGERS_RB");
-      rb = e ? std::atoi(e) : 32;
-      if (rb <= 0) rb = 32;
-    }
+    long long rb = opt(OPT_BURGERS_RB, 32);  // rows per block, measured default
+    if (rb <= 0) rb = 32;
     dim3 g((unsigned)((n / 2 + 127) / 128), (unsigned)((n + rb - 1) / rb));
     burgers2d_stream_kernel<T><<<g, 128, 0, s>>>(n, (T)C, (T)D, u_1, u_1_b, u_b, rb);
     return launch_status("burgers2d_b");
@@ -264,24 +262,19 @@ template <typename T>
 static bool burgers2d_primal_ring(long long n, double C, double D, const T* u_1, T* u,
                                   cudaStream_t s) {
   if ((n * (long long)sizeof(T)) % 16 != 0 || n > (1 << 30) || !aligned16(u_1, u, u_1, u) ||
-      std::getenv("SGB_BURGERS_NORING"))
+      opt_flag(OPT_BURGERS_NORING))
     return false;
-  int rb = 16, stages = 6;  // measured at 8192^2; env overrides per call
-  if (const char* e = std::getenv("SGB_BURGERS_PRIMAL_RB")) rb = std::max(1, std::atoi(e));
-  if (const char* f = std::getenv("SGB_BURGERS_PRIMAL_S")) {
-    const int v = std::atoi(f);
-    stages = v <= 4 ? 4 : (v >= 8 ? 8 : 6);
-  }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(burgers2d_primal_ring_kernel<T, 4>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, BurgPrimalRing<T, 4>::SMEM);
-    cudaFuncSetAttribute(burgers2d_primal_ring_kernel<T, 6>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, BurgPrimalRing<T, 6>::SMEM);
-    cudaFuncSetAttribute(burgers2d_primal_ring_kernel<T, 8>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, BurgPrimalRing<T, 8>::SMEM);
-    attr = true;
-  }
+  // measured at 8192^2; options override
+  const int rb = (int)std::max<long long>(1, opt(OPT_BURGERS_PRIMAL_RB, 16));
+  const long long sv = opt(OPT_BURGERS_PRIMAL_S, 6);
+  const int stages = sv <= 4 ? 4 : (sv >= 8 ? 8 : 6);
+  const int rc = stages == 4 ? ensure_smem((const void*)burgers2d_primal_ring_kernel<T, 4>,
+                                           BurgPrimalRing<T, 4>::SMEM, "burgers2d")
+                 : stages == 6 ? ensure_smem((const void*)burgers2d_primal_ring_kernel<T, 6>,
+                                             BurgPrimalRing<T, 6>::SMEM, "burgers2d")
+                               : ensure_smem((const void*)burgers2d_primal_ring_kernel<T, 8>,
+                                             BurgPrimalRing<T, 8>::SMEM, "burgers2d");
+  if (rc) return false;
   constexpr int W = BurgPrimalRing<T, 4>::W, TH = BurgPrimalRing<T, 4>::THREADS;
   dim3 g((unsigned)((n + W - 1) / W), (unsigned)((n + rb - 1) / rb));
   if (stages == 4)
@@ -307,9 +300,15 @@ static int star3_c_fresh_u2(const char* name, int n, double D, float* c, float* 
   if (!guard_ok(MODE == 0 ? WAVE3D_C : WAVE3D_C2, n)) return SGB_GUARD;
   if (!c || !c_b || !u_1 || !u_1_b || !u_2_b || !u_b)
     return einval(std::string(name) + ": null array");
-  if (star3_tma_supported<MODE, float>(n) && !std::getenv("SGB_FRESH_UNFUSED"))
-    return star3_tma_gather<MODE, true>(Slab3{n, 0, n}, 1, n - 2, 0, n, (float)D, c, c_b, u_1,
+  if (star3_tma_ok<MODE, float>(n, {c, c_b, u_1, u_1_b, u_2_b, u_b}) &&
+      !opt_flag(OPT_FRESH_UNFUSED))
+  {
+    if (opt(OPT_R1_FP64ACC, 1))
+      return star3_tma_gather<MODE, true, true>(Slab3{n, 0, n}, 1, n - 2, 0, n, D, c, c_b,
+                                                u_1, u_1_b, u_2_b, u_b, s, name);
+    return star3_tma_gather<MODE, true>(Slab3{n, 0, n}, 1, n - 2, 0, n, D, c, c_b, u_1,
                                         u_1_b, u_2_b, u_b, s, name);
+  }
   // other shapes: zero u_2_b, then the accumulating gather
   if (cudaMemsetAsync(u_2_b, 0, (size_t)n * n * n * sizeof(float), s) != cudaSuccess)
     return launch_status(name);
@@ -418,7 +417,7 @@ static int r4_fresh(const char* name, int n, double D, float* c, float* c_b, flo
   if (out_i1 > out_i0 && (need_lo < i_base || need_hi >= i_base + nplanes))
     return einval(std::string(name) + ": slab does not hold the radius-R halo of the outputs");
   if (out_i1 == out_i0) return 0;
-  if (star3_tma_supported<4, float>(n) && !std::getenv("SGB_FRESH_UNFUSED"))
+  if (star3_tma_ok<4, float>(n, {c, c_b, u_1, u_1_b, u_b}) && !opt_flag(OPT_FRESH_UNFUSED))
     return star3_v7_gather<4>(Slab3{n, i_base, nplanes}, R, n - 1 - R, out_i0, out_i1, (float)D,
                               c, c_b, u_1, u_1_b, nullptr, u_b, s, name);
   // other shapes: zero the output planes of u_1_b, then the accumulating gather
@@ -465,7 +464,8 @@ int sgb_wave3d_r4_b_step_f32(int n, double D, float* c, float* c_b, float* u_1, 
   if (u_2_b == u_b || u_2_b == u_1_b || u_2_b == c_b)
     return einval(std::string(name) + ": u_2_b must not alias the other arrays");
   cudaStream_t s = as_stream(stream);
-  if (star3_tma_supported<3, float>(n) && !std::getenv("SGB_STEP_UNFUSED"))
+  if (star3_tma_ok<3, float>(n, {c, c_b, u_1, u_1_b, u_b, u_2_b}) &&
+      !opt_flag(OPT_STEP_UNFUSED))
     return star3_v7_gather<3>(Slab3{n, 0, n}, 4, n - 5, 0, n, (float)D, c, c_b, u_1, u_1_b,
                               u_2_b, u_b, s, name);
   // other shapes: the two launches it fuses

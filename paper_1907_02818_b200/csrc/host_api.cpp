@@ -197,6 +197,22 @@ Env run_scatter_adjoint(const std::string& family, const Env& env, Precision p) 
   return dispatch(family, env, p, 2);
 }
 
+Program Program::of(const std::string& family) {
+  const char* t = sgb_program_text(family.c_str());
+  if (!t) throw Error(sgb_last_error());
+  return Program{t};
+}
+
+std::string Program::family() const {
+  const char* f = sgb_program_family(text.c_str());
+  if (!f) throw Error(std::string("no B200 kernel computes this program: ") + sgb_last_error());
+  return f;
+}
+
+Env run_program(const Program& program, const Env& env, Precision p) {
+  return dispatch(program.family(), env, p, 1);
+}
+
 std::vector<std::string> array_params(const std::string& family, const std::string& kind) {
   const Family& f = find_family(family);
   if (kind == "primal") return f.primal;

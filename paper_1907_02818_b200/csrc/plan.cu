@@ -110,7 +110,7 @@ sgb_plan* sgb_plan_create_slab(const char* family, int n, int dtype_bytes, int i
                          (fs->dims == 1 && n % 2 == 0);
   if (pipelined) {
     int c = units >= 128 ? 32 : 1;
-    if (const char* e = std::getenv("SGB_PLAN_CHUNKS")) c = std::max(1, std::atoi(e));
+    if (sgb::opt(sgb::OPT_PLAN_CHUNKS, 0) > 0) c = (int)sgb::opt(sgb::OPT_PLAN_CHUNKS, 0);
     p->chunks = (int)std::min<long long>(c, std::max<long long>(1, units / 16));
     cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p->s_cmp, cudaStreamNonBlocking);

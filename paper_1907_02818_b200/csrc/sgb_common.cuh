@@ -56,6 +56,53 @@ __device__ __forceinline__ bool star_reached(long long i, long long j, long long
   return nout == 0 || (nout == 1 && oi <= R && oj <= R && ok <= R);
 }
 
+// ---- launcher state (runtime.cu) --------------------------------------------
+// Run-time options: scheduling / A-B knobs whose defaults are the measured
+// best.  Read from the environment (SGB_<NAME>) once per process, changed
+// afterwards only through sgb_set_option; no launcher calls getenv.
+#define SGB_OPTIONS(X)                                                                     \
+  X(STAR_KERNEL)      /* 1 | 7: force the radius-1 or radius-4 streaming design */       \
+  X(F64_PLANE)        /* fp64 radius 4 on the plane kernels */                          \
+  X(GENERIC_POINT)    /* per-point 3D gather kernels */                                 \
+  X(PLANE_NO_TMA)     /* plane kernel without TMA */                                    \
+  X(PRIMAL_GENERIC)   /* per-point primal kernels */                                    \
+  X(BURGERS_NORING)   /* burgers2d register-streaming kernels */                        \
+  X(BURGERS_RING_RB)  /* rows per CTA of the burgers2d ring gather */                   \
+  X(BURGERS_RING_S)   /* ring stages of the burgers2d gather */                         \
+  X(BURGERS_RB)       /* rows per CTA of the burgers2d streaming gather */              \
+  X(BURGERS_PRIMAL_RB)                                                                   \
+  X(BURGERS_PRIMAL_S)                                                                    \
+  X(FRESH_UNFUSED)    /* fresh entries as memset + accumulating gather */               \
+  X(STEP_UNFUSED)     /* time-loop step as gather + box set */                          \
+  X(PLAN_CHUNKS)      /* i-chunks of the host-buffer pipeline */                        \
+  X(F64_ICHUNKS)      /* i-chunks of the fp64 streaming gather */                       \
+  X(PRIMAL_CHUNKS)    /* i-chunks of the 3D primals */                                  \
+  X(PLANE_CHUNK)      /* planes per CTA of the plane kernels */                         \
+  X(NO_UBWIN)         /* in-kernel seed mask instead of the windowed TMA map */         \
+  X(ICHUNKS)          /* i-chunks of the radius-4 interior (or unified) launch */       \
+  X(ICHUNKS_F)        /* i-chunks of the radius-4 frame launch */                       \
+  X(V7_UNIFIED)       /* radius 4: one launch for frame + interior */                   \
+  X(V7_SPLIT)         /* radius 4: two launches even for partial plane ranges */        \
+  X(FORK)             /* radius 4: frame launch on a side stream */                     \
+  X(DISABLE_TMA)      /* no TMA kernels */                                              \
+  X(L2PROMO)          /* TMA L2 promotion bytes (0, 64, 128, 256) */                    \
+  X(V7_BALANCED)      /* radius 4: balanced frame/interior work list (0 = off) */       \
+  X(R1_FP64ACC)       /* radius-1 fp32 gathers accumulate in fp64 (default 1) */
+
+#define SGB_OPT_ENUM(n) OPT_##n,
+enum Opt : int { SGB_OPTIONS(SGB_OPT_ENUM) kNumOpts };
+#undef SGB_OPT_ENUM
+#define SGB_OPT_NAME(n) #n,
+static constexpr const char* kOptNames[] = {SGB_OPTIONS(SGB_OPT_NAME)};
+#undef SGB_OPT_NAME
+
+long long opt(Opt o, long long dflt);  // the set value, else dflt
+bool opt_flag(Opt o);                  // set and non-zero
+int num_sms();                         // SMs of the current device (cached per device)
+// dynamic shared-memory attribute of `fn` on the current device, set once per
+// (device, kernel); 0 or a negative error (sgb_last_error set)
+int ensure_smem(const void* fn, size_t bytes, const char* what);
+
 inline unsigned grid_1d(long long work, int block) {
   long long g = (work + block - 1) / block;
   return (unsigned)(g < 1 ? 1 : g);

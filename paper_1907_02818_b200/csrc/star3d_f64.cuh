@@ -398,20 +398,16 @@ inline int star3_f64_stream_gather(const Slab3& g, long long lo, long long hi, l
   rc |= encode_3d_t(&maps[5], (const double*)(kU2 ? u_2_b : u_1_b), g.n, g.nplanes, Tl::TK,
                     Tl::TJ, name);
   if (rc) return SGB_EINVAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(star3_f64_stream_kernel<MODE, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
-    cudaFuncSetAttribute(star3_f64_stream_kernel<MODE, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
-    attr = true;
-  }
+  if (int rc = ensure_smem((const void*)star3_f64_stream_kernel<MODE, true>, Tl::SMEM, name))
+    return rc;
+  if (int rc = ensure_smem((const void*)star3_f64_stream_kernel<MODE, false>, Tl::SMEM, name))
+    return rc;
   const int tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
   const long long tiles = (long long)tiles_k * ((g.n + Tl::TJ - 1) / Tl::TJ);
   const long long nout = out_i1 - out_i0;
   // i-chunks: the wave model of star3d_r4.cuh (one CTA per SM, equal-length CTAs)
   int nch = 0;
-  if (const char* e = std::getenv("SGB_F64_ICHUNKS")) nch = std::max(1, std::atoi(e));
+  if (opt(OPT_F64_ICHUNKS, 0) > 0) nch = (int)opt(OPT_F64_ICHUNKS, 0);
   if (nch == 0) {
     const int sms = num_sms();
     long long best = -1;
@@ -593,12 +589,8 @@ inline int star3_primal_f64_stream(long long n, double D, const double* c, const
   rc |= encode_3d_t(&maps[3], u_1, n, n, Tl::TK, Tl::TJ, name);
   rc |= encode_3d_t(&maps[4], (const double*)u, n, n, Tl::TK, Tl::TJ, name);
   if (rc) return SGB_EINVAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(star3_primal_f64_kernel<MODE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, Tl::SMEM);
-    attr = true;
-  }
+  if (int rc = ensure_smem((const void*)star3_primal_f64_kernel<MODE>, Tl::SMEM, name))
+    return rc;
   const int tiles_k = (int)((n + Tl::TK - 1) / Tl::TK);
   const long long tiles = (long long)tiles_k * ((n + Tl::TJ - 1) / Tl::TJ);
   const long long nout = hi - lo + 1;
@@ -612,7 +604,7 @@ inline int star3_primal_f64_stream(long long n, double D, const double* c, const
     if (best < 0 || cost < best) best = cost, nch = cc;
   }
   if (R >= 2) nch = (int)std::max<long long>(nch, (nout + 47) / 48);
-  if (const char* e = std::getenv("SGB_PRIMAL_CHUNKS")) nch = std::max(1, std::atoi(e));
+  if (opt(OPT_PRIMAL_CHUNKS, 0) > 0) nch = (int)opt(OPT_PRIMAL_CHUNKS, 0);
   const int chunk = (int)((nout + nch - 1) / nch);
   const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
   star3_primal_f64_kernel<MODE><<<dim3((unsigned)tiles, gy), Tl::THREADS, Tl::SMEM, s>>>(

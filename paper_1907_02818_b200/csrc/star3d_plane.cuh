@@ -163,7 +163,7 @@ inline int star3_plane_gather(const Slab3& g, long long lo, long long hi, long l
   // ~256 output planes per CTA (measured insensitive: 64..768 within 4%); 2R halo planes
   // re-read per chunk (L2 hits for the most part)
   long long len = 256;
-  if (const char* e = std::getenv("SGB_PLANE_CHUNK")) len = std::max(1, std::atoi(e));
+  if (opt(OPT_PLANE_CHUNK, 0) > 0) len = (int)opt(OPT_PLANE_CHUNK, 0);
   const int chunk = (int)std::min<long long>(nout, len);
   dim3 grid((unsigned)((g.n + Tl::TK - 1) / Tl::TK), (unsigned)((g.n + Tl::TJ - 1) / Tl::TJ),
             (unsigned)((nout + chunk - 1) / chunk));
@@ -404,15 +404,11 @@ inline int star3_plane_tma_gather(const Slab3& g, long long lo, long long hi, lo
   rc |= encode_3d_t(&maps[5], (const T*)c_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
   rc |= encode_3d_t(&maps[6], (const T*)u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ, name);
   if (rc) return SGB_EINVAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(star3_plane_tma_kernel<MODE, T>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, Tl::SMEM);
-    attr = true;
-  }
+  if (int rc = ensure_smem((const void*)star3_plane_tma_kernel<MODE, T>, Tl::SMEM, name))
+    return rc;
   const long long nout = out_i1 - out_i0;
   long long len = 256;
-  if (const char* e = std::getenv("SGB_PLANE_CHUNK")) len = std::max(1, std::atoi(e));
+  if (opt(OPT_PLANE_CHUNK, 0) > 0) len = (int)opt(OPT_PLANE_CHUNK, 0);
   const int chunk = (int)std::min<long long>(nout, len);
   dim3 grid((unsigned)((g.n + Tl::TK - 1) / Tl::TK), (unsigned)((g.n + Tl::TJ - 1) / Tl::TJ),
             (unsigned)((nout + chunk - 1) / chunk));

@@ -169,12 +169,8 @@ inline int star3_primal_tma(long long n, float D, const float* c, const float* u
   rc |= encode_3d(&maps[3], u_1, n, n, Tl::TK, Tl::TJ, name);
   rc |= encode_3d(&maps[4], u, n, n, Tl::TK, Tl::TJ, name);
   if (rc) return SGB_EINVAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(star3_primal_tma_kernel<MODE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, Tl::SMEM);
-    attr = true;
-  }
+  if (int rc = ensure_smem((const void*)star3_primal_tma_kernel<MODE>, Tl::SMEM, name))
+    return rc;
   const int tiles_k = (int)((n + Tl::TK - 1) / Tl::TK);
   const long long tiles = (long long)tiles_k * ((n + Tl::TJ - 1) / Tl::TJ);
   const long long nout = hi - lo + 1;
@@ -193,7 +189,7 @@ inline int star3_primal_tma(long long n, float D, const float* c, const float* u
   // still in L2: 768^3 1.34 -> 1.11 ms although every chunk re-reads 2R halo
   // planes.  Radius 1 keeps the wave model (measured best there).
   if (R >= 2) nch = (int)std::max<long long>(nch, (nout + 47) / 48);
-  if (const char* e = std::getenv("SGB_PRIMAL_CHUNKS")) nch = std::max(1, std::atoi(e));
+  if (opt(OPT_PRIMAL_CHUNKS, 0) > 0) nch = (int)opt(OPT_PRIMAL_CHUNKS, 0);
   const int chunk = (int)((nout + nch - 1) / nch);
   const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
   star3_primal_tma_kernel<MODE><<<dim3((unsigned)tiles, gy), Tl::THREADS, Tl::SMEM, s>>>(

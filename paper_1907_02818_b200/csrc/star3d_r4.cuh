@@ -666,7 +666,7 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   int rc = 0;
   rc |= encode_3d(&maps[0], c, g.n, g.nplanes, Tl::BW, Tl::BJ, name);
   int ubwin = 0;
-  if (!std::getenv("SGB_NO_UBWIN")) {
+  if (!opt_flag(OPT_NO_UBWIN)) {
     const int w = encode_3d_window(&maps[1], u_b, g.n, g.nplanes, lo, hi - lo + 1, Tl::BW, Tl::BJ,
                                    name);
     if (w < 0) return w;
@@ -679,19 +679,15 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   rc |= encode_3d(&maps[5], Star3<MODE>::kU2 ? u_2_b : u_1_b, g.n, g.nplanes, Tl::TK, Tl::TJ,
                   name);
   if (rc) return SGB_EINVAL;
-  static bool attr_set = false;
-  if (!attr_set) {
+  {
     const void* ks[] = {(const void*)star3_v7_kernel<MODE, true, true>,
                         (const void*)star3_v7_kernel<MODE, true, false>,
                         (const void*)star3_v7_kernel<MODE, false, true>,
-                        (const void*)star3_v7_kernel<MODE, false, false>};
+                        (const void*)star3_v7_kernel<MODE, false, false>,
+                        (const void*)star3_v7_unified<MODE, true>,
+                        (const void*)star3_v7_unified_peer<MODE, true>};
     for (const void* k : ks)
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
-    cudaFuncSetAttribute((const void*)star3_v7_unified<MODE, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
-    cudaFuncSetAttribute((const void*)star3_v7_unified_peer<MODE, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tl::SMEM);
-    attr_set = true;
+      if (int r = ensure_smem(k, Tl::SMEM, name)) return r;
   }
   TileMap tm;
   tm.tiles_k = (int)((g.n + Tl::TK - 1) / Tl::TK);
@@ -716,9 +712,8 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   // takes ceil(tiles*c / SMs) * (ceil(nout/c) + 2R) plane-times.  Minimising it
   // reproduced the measured best chunking at 768^3 and 1024^3.
   const int sms = num_sms();
-  auto chunking = [&](const char* env, long long tiles) {
-    int c = 0;
-    if (const char* e = std::getenv(env)) c = std::max(1, std::atoi(e));
+  auto chunking = [&](Opt knob, long long tiles) {
+    int c = (int)std::max<long long>(0, opt(knob, 0));
     if (c == 0) {
       long long best = -1;
       for (int cc = 1; cc <= 64 && cc <= nout; cc++) {
@@ -731,8 +726,8 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     const int len = (int)((nout + c - 1) / c);
     return std::make_pair(len, (unsigned)((nout + len - 1) / len));
   };
-  const auto ci = chunking("SGB_ICHUNKS", tm.n_interior());
-  const auto cf = chunking("SGB_ICHUNKS_F", tm.n_frame());
+  const auto ci = chunking(OPT_ICHUNKS, tm.n_interior());
+  const auto cf = chunking(OPT_ICHUNKS_F, tm.n_frame());
   // one launch for partial plane ranges (z-slabs, edge bands: measured 5-12%
   // faster there, fewer CTA waves); two launches for the full grid (faster in
   // the sustained single-GPU run); SGB_V7_UNIFIED / SGB_V7_SPLIT force either
@@ -741,7 +736,7 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
       set_error(std::string(name) + ": peer halo path needs 16-byte aligned arrays");
       return SGB_EINVAL;
     }
-    const auto cu = chunking("SGB_ICHUNKS", (long long)tm.tiles_k * tm.tiles_j);
+    const auto cu = chunking(OPT_ICHUNKS, (long long)tm.tiles_k * tm.tiles_j);
     star3_v7_unified_peer<MODE, true>
         <<<dim3((unsigned)(tm.tiles_k * tm.tiles_j), cu.second), Tl::THREADS, Tl::SMEM, s>>>(
             maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
@@ -749,17 +744,16 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     return launch_status(name);
   }
   const bool partial = out_i0 != 0 || out_i1 != g.n;
-  const bool unified = std::getenv("SGB_V7_UNIFIED") ||
-                       (partial && !std::getenv("SGB_V7_SPLIT"));
+  const bool unified = opt_flag(OPT_V7_UNIFIED) || (partial && !opt_flag(OPT_V7_SPLIT));
   if (ubwin && unified) {
-    const auto cu = chunking("SGB_ICHUNKS", (long long)tm.tiles_k * tm.tiles_j);
+    const auto cu = chunking(OPT_ICHUNKS, (long long)tm.tiles_k * tm.tiles_j);
     star3_v7_unified<MODE, true>
         <<<dim3((unsigned)(tm.tiles_k * tm.tiles_j), cu.second), Tl::THREADS, Tl::SMEM, s>>>(
             maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
             (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cu.first, tm, D);
     return launch_status(name);
   }
-  const bool fork = tm.n_interior() > 0 && tm.n_frame() > 0 && std::getenv("SGB_FORK");
+  const bool fork = tm.n_interior() > 0 && tm.n_frame() > 0 && opt_flag(OPT_FORK);
   SideStream* ss = fork ? side_stream() : nullptr;
   if (ss) {
     if (cudaEventRecord(ss->fork, s) != cudaSuccess ||

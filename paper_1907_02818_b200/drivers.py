@@ -210,22 +210,30 @@ def run_independent(n, steps, seed=0, D=0.01, sl=None, arrays=None, overlap=True
 
 
 def run_carried(n, steps, seed=0, D=0.1, family="wave3d_c", arrays=None):
-    """cfg 2: carried reverse steps of the 7-point wave (single GPU)."""
+    """cfg 2: carried reverse steps of the 7-point wave (single GPU).  On
+    return u_b = u-bar^0 (the last step's u_1_b), u_1_b = u-bar^{-1} (its u_2
+    partial) and u_2_b = 0, whichever path ran.  Caller-supplied `arrays`
+    keep their u_1_b / u_2_b / c_b contents as the initial accumulators."""
+    caller = arrays is not None
     if arrays is None:
         arrays = alloc(family, n)
         init_static(family, arrays, n, seed)
         regen_seed(arrays["u_b"], n, steps, seed)  # u-bar^{T+1}
     fused = arrays["u_1"].dtype == torch.float32
-    for t in reversed(range(steps)):
+    for k, t in enumerate(reversed(range(steps))):
         regen_state(arrays["u_1"], n, t, seed, 1)
-        if fused:  # u_2_b written as this step's partial: the zeroing below, fused
+        # u_2_b written as this step's partial (the zeroing below, fused); a
+        # caller's first step accumulates into whatever u_2_b it passed
+        if fused and not (caller and k == 0):
             api.adjoint_fresh_u2(family, n, {"D": D}, arrays)
         else:
             api.adjoint(family, n, {"D": D}, arrays)
-        # rotate: seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- 0
+        # rotate: seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- 0 (on the fused path
+        # the zeroing is folded into the next step's gather, and done once
+        # after the sweep)
         arrays["u_b"], arrays["u_1_b"], arrays["u_2_b"] = (arrays["u_1_b"], arrays["u_2_b"],
                                                            arrays["u_b"])
-        if not fused:
+        if not fused or k == steps - 1:
             arrays["u_2_b"].zero_()
     return arrays
 

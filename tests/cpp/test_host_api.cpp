@@ -143,6 +143,28 @@ int main() {
   CHECK(throws([&] { sgb::run_program("lap1d", small); }));
   CHECK(throws([&] { sgb::DenseGrid({4, 4}).flat({4, 0}); }));
 
+  // program-keyed dispatch: the family's own program runs its kernels (same
+  // result as the name-keyed call); an edited program is refused
+  {
+    const sgb::Env env = make_env(SG_WAVE3D_R4, 36, 11);
+    const sgb::Program prog = sgb::Program::of("wave3d_r4");
+    CHECK(prog.family() == "wave3d_r4");
+    const sgb::Env a = sgb::run_program(prog, env), b = sgb::run_program("wave3d_r4", env);
+    CHECK(a.grids.at("c_b").data() == b.grids.at("c_b").data());
+    CHECK(a.grids.at("u_1_b").data() == b.grids.at("u_1_b").data());
+    sgb::Program edited = prog;  // one partial's weight changed
+    const auto at = edited.text.find("partial ");
+    CHECK(at != std::string::npos);
+    edited.text.insert(at + 8, "1.01*");
+    CHECK(throws([&] { sgb::run_program(edited, env); }));
+    sgb::Program bounds = prog;  // another primal box
+    const auto g = bounds.text.find("guard n - 9");
+    CHECK(g != std::string::npos);
+    bounds.text.replace(g, 11, "guard n - 8");
+    CHECK(throws([&] { (void)bounds.family(); }));
+    CHECK(throws([&] { (void)sgb::Program::of("lap1d"); }));
+  }
+
   std::printf("host_api: %d checks, %d failures\n", g_checks, g_failures);
   return g_failures ? 1 : 0;
 }

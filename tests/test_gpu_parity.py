@@ -236,7 +236,7 @@ def test_host_buffer_plan_entry(api, name, n, dtype):
 
 
 @pytest.mark.parametrize("n", [68, 97, 136])
-def test_r4_launch_variants_bitwise_equal(api, n, monkeypatch):
+def test_r4_launch_variants_bitwise_equal(api, n, sgbopt):
     """The radius-4 launch knobs (windowed seed map vs in-kernel mask, one
     launch vs interior/frame launches, wave-model vs forced i-chunking, frame
     on a side stream) change only scheduling: every
@@ -253,7 +253,7 @@ def test_r4_launch_variants_bitwise_equal(api, n, monkeypatch):
                 {"SGB_ICHUNKS": "1", "SGB_ICHUNKS_F": "1"}, {"SGB_FORK": "1"},
                 {"SGB_V7_UNIFIED": "1"}, {"SGB_V7_UNIFIED": "1", "SGB_ICHUNKS": "3"},
                 {"SGB_V7_SPLIT": "1"}):
-        with monkeypatch.context() as m:
+        with sgbopt.context() as m:
             for k, v in env.items():
                 m.setenv(k, v)
             got = api.run_program(name, n, scalars, g, a, dtype="f32")
@@ -263,7 +263,7 @@ def test_r4_launch_variants_bitwise_equal(api, n, monkeypatch):
 
 @pytest.mark.parametrize("name,n", [("wave3d_r4", 68), ("wave3d_r4", 136), ("wave3d_r4", 200),
                                     ("wave3d_c", 136)])
-def test_primal_chunking_bitwise_equal(api, name, n, monkeypatch):
+def test_primal_chunking_bitwise_equal(api, name, n, sgbopt):
     """The streaming primal's i-chunk count (default: ~48-plane chunks at
     radius 4, wave model at radius 1) changes only which CTA streams which
     planes: results are bitwise identical for any count, incl. one chunk per
@@ -275,14 +275,14 @@ def test_primal_chunking_bitwise_equal(api, name, n, monkeypatch):
     g = _round(grids, "f32")
     base = api.run_nest(name, n, scalars, g, dtype="f32")[out]
     for chunks in ("1", "2", "5", "64"):
-        with monkeypatch.context() as m:
+        with sgbopt.context() as m:
             m.setenv("SGB_PRIMAL_CHUNKS", chunks)
             got = api.run_nest(name, n, scalars, g, dtype="f32")[out]
         assert np.array_equal(got, base), chunks
 
 
 @pytest.mark.parametrize("n", [64, 300, 1030])
-def test_burgers_ring_variants_bitwise_equal(api, n, monkeypatch):
+def test_burgers_ring_variants_bitwise_equal(api, n, sgbopt):
     """burgers2d ring kernel: stage count and rows per CTA change only the
     schedule, so results are bitwise identical; the register-streaming kernel
     it replaced agrees to fp64 rounding."""
@@ -293,12 +293,12 @@ def test_burgers_ring_variants_bitwise_equal(api, n, monkeypatch):
     check_close(base["u_1_b"], want["u_1_b"], "f64", f"{name} n={n}")
     for env in ({"SGB_BURGERS_RING_S": "4"}, {"SGB_BURGERS_RING_S": "8"},
                 {"SGB_BURGERS_RING_RB": "7"}, {"SGB_BURGERS_RING_RB": "256"}):
-        with monkeypatch.context() as m:
+        with sgbopt.context() as m:
             for k, v in env.items():
                 m.setenv(k, v)
             got = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
         assert np.array_equal(got["u_1_b"], base["u_1_b"]), env
-    with monkeypatch.context() as m:
+    with sgbopt.context() as m:
         m.setenv("SGB_BURGERS_NORING", "1")
         old = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
     assert oracle.max_rel_err(old["u_1_b"], base["u_1_b"]) <= 1e-14
@@ -339,7 +339,7 @@ def test_primal_f32_matches_oracle(api, name, n):
 
 
 @pytest.mark.parametrize("n", [20, 24, 40, 66, 98, 136])
-def test_primal_f64_r4_streaming(api, n, monkeypatch):
+def test_primal_f64_r4_streaming(api, n, sgbopt):
     """fp64 radius-4 streaming primal (even n): matches the oracle's run_nest
     at 1e-12 (the output starts non-zero, so points outside the box are
     checked to be untouched); i-chunking changes nothing (bitwise)."""
@@ -354,7 +354,7 @@ def test_primal_f64_r4_streaming(api, n, monkeypatch):
     check_close(got[out], want[out], "f64", f"{name} n={n} primal")
     assert np.array_equal(got[out][:4], grids[out][:4])  # planes outside the box untouched
     for chunks in ("1", "5"):
-        with monkeypatch.context() as m:
+        with sgbopt.context() as m:
             m.setenv("SGB_PRIMAL_CHUNKS", chunks)
             again = api.run_nest(name, n, scalars, grids, dtype="f64")
         assert np.array_equal(again[out], got[out]), chunks
@@ -362,7 +362,7 @@ def test_primal_f64_r4_streaming(api, n, monkeypatch):
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("n", [64, 300, 1032])
-def test_burgers_primal_ring_variants_bitwise_equal(api, n, dtype, monkeypatch):
+def test_burgers_primal_ring_variants_bitwise_equal(api, n, dtype, sgbopt):
     """The ring primal evaluates the register-streaming kernel's expression
     with the same grouping: bitwise equal to it, for every stage count and
     rows-per-CTA (incl. a strip taller than the grid)."""
@@ -374,7 +374,7 @@ def test_burgers_primal_ring_variants_bitwise_equal(api, n, dtype, monkeypatch):
     for env in ({"SGB_BURGERS_NORING": "1"}, {"SGB_BURGERS_PRIMAL_S": "4"},
                 {"SGB_BURGERS_PRIMAL_S": "8"}, {"SGB_BURGERS_PRIMAL_RB": "7"},
                 {"SGB_BURGERS_PRIMAL_RB": "5000"}):
-        with monkeypatch.context() as m:
+        with sgbopt.context() as m:
             for k, v in env.items():
                 m.setenv(k, v)
             got = api.run_nest(name, n, scalars, g, dtype=dtype)["u"]
@@ -441,7 +441,7 @@ def test_slab_plans_reassemble_full_plan(api, name, n, nslabs):
 
 
 @pytest.mark.parametrize("n", [24, 40, 68, 97])
-def test_plane_kernels_tma_equals_plain_fp64(api, n, monkeypatch):
+def test_plane_kernels_tma_equals_plain_fp64(api, n, sgbopt):
     """fp64 radius-4 plane kernels (the general-shape path behind the
     register-blocked kernel): the TMA-fed plane kernel (even n) and the
     plain-load plane kernel apply the same arithmetic per point (bitwise
@@ -449,7 +449,7 @@ def test_plane_kernels_tma_equals_plain_fp64(api, n, monkeypatch):
     name = "wave3d_r4"
     scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 9, accumulate=True)
     want = oracle_gather(name, n, scalars, grids, adjs)
-    with monkeypatch.context() as m:
+    with sgbopt.context() as m:
         m.setenv("SGB_F64_PLANE", "1")
         base = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
         m.setenv("SGB_PLANE_NO_TMA", "1")
@@ -462,7 +462,7 @@ def test_plane_kernels_tma_equals_plain_fp64(api, n, monkeypatch):
 @pytest.mark.parametrize("name,n", [("wave3d_r4", n) for n in (20, 24, 40, 66, 98, 136)] +
                          [("wave3d_c", n) for n in (6, 16, 34, 66, 100)] +
                          [("wave3d_c2", n) for n in (12, 64)])
-def test_f64_streaming_kernel(api, name, n, monkeypatch):
+def test_f64_streaming_kernel(api, name, n, sgbopt):
     """fp64 register-blocked streaming kernel (even n; radius 4 and the
     radius-1 specs with their u_2 partial): matches the oracle at 1e-12 per
     point on the accumulated adjoints (partial tiles, frame tiles, one-tile
@@ -475,8 +475,40 @@ def test_f64_streaming_kernel(api, name, n, monkeypatch):
     for adj in outs:
         check_close(base[adj], want[adj], "f64", f"{name} n={n} {adj}")
     for chunks in ("1", "3", "7"):
-        with monkeypatch.context() as m:
+        with sgbopt.context() as m:
             m.setenv("SGB_F64_ICHUNKS", chunks)
             got = api.run_program(name, n, scalars, grids, adjs, dtype="f64")
         for adj in outs:
             assert np.array_equal(got[adj], base[adj]), (chunks, adj)
+
+
+@pytest.mark.parametrize("name,kind", [("wave3d_c", "adjoint"), ("wave3d_c", "fresh_u2"),
+                                       ("wave3d_r4", "adjoint"), ("wave3d_r4", "fresh")])
+def test_misaligned_arrays_take_a_safe_path(api, name, kind):
+    """Arrays at a 4-byte offset (a contiguous view of a larger buffer, or an
+    offset pointer from a C caller) cannot use the TMA / 16-byte vector
+    kernels: the entry takes the per-point path instead of faulting, and the
+    result still matches the aligned call."""
+    import torch
+    from paper_1907_02818_b200 import api as A
+    n = 40
+    sc = {"D": 0.1 if name == "wave3d_c" else 0.01}
+    g = torch.Generator(device="cpu").manual_seed(5)
+    names = A.array_params(name, "adjoint")
+    aligned = {k: torch.randn((n, n, n), generator=g).cuda() for k in names}
+    off = {}
+    for k, v in aligned.items():
+        buf = torch.empty(n ** 3 + 1, device="cuda")
+        t = buf[1:].view(n, n, n)
+        t.copy_(v)
+        assert t.data_ptr() % 16 != 0
+        off[k] = t
+    call = {"adjoint": A.adjoint, "fresh_u2": A.adjoint_fresh_u2, "fresh": A.adjoint_fresh}[kind]
+    call(name, n, sc, aligned)
+    call(name, n, sc, off)
+    torch.cuda.synchronize()
+    for k in names:
+        a, b = aligned[k].double().cpu().numpy(), off[k].double().cpu().numpy()
+        assert oracle.max_rel_err(b, a) <= 1e-5, k
+    # the context is healthy afterwards
+    assert float(torch.ones(4, device="cuda").sum()) == 4.0

@@ -1,0 +1,209 @@
+"""Multi-step parity protocol at the BASELINE
+sizes, against the reference's OWN compiled emitted adjoint.
+
+The oracle here is not the C restatement but the reference itself: the OpenMP
+C that `emit_adjoint` (/root/reference/proj/src/codegen.cpp:332-382) generates
+for the config's spec, compiled by oracle/ref/Makefile into
+oracle/_ref/libref_<family>.so (fp64, the reference's only precision).  Both
+sides see the same fp32 inputs (generated on the device by the counter-based
+generators, widened exactly to fp64 for the reference).  Comparisons run on the
+device (sgb_compare_*: the reference's compare_grids metric, interp.cpp:290-298,
+plus the norm) so a 1024^3 check never downloads a kernel output.
+
+* cfg 2 -- wave3d_c (7-point, linear c, D = 0.1), 512^3, 10 CARRIED reverse
+  steps (drivers.run_carried's recursion: seed <- u_1_b <- u_2_b <- 0, u_1 = u^t
+  regenerated per step), compared after every step.  Alongside the pure fp64
+  reference chain runs the "fp32-storage floor": the same reference arithmetic
+  (fp64) with the carried adjoints rounded to fp32 after every step, i.e. the
+  error any kernel storing its adjoints in fp32 (the BASELINE dtype) incurs
+  even with exact arithmetic.  Gates: norm <= 1e-5 after every step; per
+  point <= 1e-5, or -- where the fp32-storage floor itself exceeds 1e-5 (the
+  carried seed grows to |a| ~ 1e2, and rounding it to fp32 leaves ~1e-5
+  absolute error at the zero crossings of later steps) -- within 1.5x of
+  that floor.  The measured numbers are written to $SGB_PROTOCOL_OUT.
+* cfg 5 -- wave3d_r4 (D = 0.01), independent reverse steps with u_1 and u_b
+  regenerated from (seed, step), u_1_b = the step's adjoint, c_b accumulated
+  over all steps: per point and norm <= 1e-5 for u_1_b at every step and for
+  c_b at the end.  Default: 1024^3 x 8 steps and 256^3 x 100 steps (the
+  driver's test budget); SGB_FULL_PROTOCOL=1 runs the full 1024^3 x 100
+  (~10 min, log committed under profiles/).
+"""
+import json
+import os
+import time
+
+import pytest
+
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+OUT = os.environ.get("SGB_PROTOCOL_OUT")
+
+
+def _host_ram_gb():
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 2 ** 30
+    except Exception:
+        return 1e9
+
+
+def _dump(name, rec):
+    if OUT:
+        os.makedirs(OUT, exist_ok=True)
+        with open(os.path.join(OUT, name), "w") as fh:
+            json.dump(rec, fh, indent=1)
+    print(json.dumps(rec)[:2000])
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1907_02818_b200 import api, drivers
+    return torch, api, drivers
+
+
+def _need_ref(name):
+    if not oracle.ref_emitted_available(name):
+        pytest.fail(f"oracle/_ref/libref_{name}.so missing (build it: make -C oracle/ref)")
+
+
+def test_cfg2_carried_512(env):
+    torch, api, drivers = env
+    fam = "wave3d_c"
+    _need_ref(fam)
+    n = int(os.environ.get("SGB_CFG2_N", "512"))
+    steps, seed, D = 10, 0, 0.1
+    if _host_ram_gb() < 14 * n ** 3 * 8 / 2 ** 30:
+        pytest.skip("host RAM")
+    ref = oracle.ref_emitted(fam)
+    f64 = dict(dtype=torch.float64)
+    # device (fp32, the BASELINE dtype) state: drivers.run_carried's recursion
+    g = drivers.alloc(fam, n)
+    drivers.init_static(fam, g, n, seed)
+    drivers.regen_seed(g["u_b"], n, steps, seed)
+    torch.cuda.synchronize()
+    c = g["c"].double().cpu()
+    chains = {}
+    for label in ("ref", "floor"):
+        chains[label] = {"c": c, "u_1": torch.empty((n, n, n), **f64),
+                         "u_b": g["u_b"].double().cpu(), "c_b": torch.zeros((n, n, n), **f64),
+                         "u_1_b": torch.zeros((n, n, n), **f64),
+                         "u_2_b": torch.zeros((n, n, n), **f64)}
+    dev64 = torch.empty((n, n, n), device="cuda", **f64)
+    dev64b = torch.empty((n, n, n), device="cuda", **f64)
+
+    def cmp(gpu_t, host_t):
+        dev64.copy_(host_t)
+        return api.compare(gpu_t, dev64)
+
+    def cmp_host(a, b):  # floor chain vs reference chain (both fp64)
+        dev64.copy_(b)
+        dev64b.copy_(a)
+        return api.compare(dev64b, dev64)
+
+    rec = {"config": f"cfg2 {fam} {n}^3 fp32, D={D}, {steps} carried reverse steps",
+           "oracle": "reference emitted wave3d_c_b (codegen.cpp:332-382), gcc "
+                     f"{oracle.ref_emitted_opt(fam)} -fopenmp, fp64", "steps": []}
+    t0 = time.time()
+    for k, t in enumerate(reversed(range(steps))):
+        drivers.regen_state(g["u_1"], n, t, seed, 1)
+        u1 = g["u_1"].double().cpu()
+        # the fused form writes u_2_b as this step's partial (u_2_b is zero at
+        # the start of every step of the recursion)
+        api.adjoint_fresh_u2(fam, n, {"D": D}, g)
+        for label, ch in chains.items():
+            ch["u_1"] = u1
+            assert ref(n, {"D": D}, ch) == 0
+            if label == "floor":  # fp32 storage of the carried adjoints
+                for nm in ("c_b", "u_1_b", "u_2_b"):
+                    ch[nm].copy_(ch[nm].float())
+        r, fl = chains["ref"], chains["floor"]
+        step = {"t": t, "max_abs_seed": float(r["u_1_b"].abs().max())}
+        for nm in ("u_1_b", "c_b"):
+            e = cmp(g[nm], r[nm])
+            ef = cmp_host(fl[nm], r[nm])
+            assert e["nonfinite"] == 0, (t, nm)
+            step[nm] = {"gpu_max_rel": e["max_rel"], "gpu_norm_rel": e["norm_rel"],
+                        "fp32_storage_floor_max_rel": ef["max_rel"],
+                        "fp32_storage_floor_norm_rel": ef["norm_rel"]}
+        rec["steps"].append(step)
+        # rotate (seed <- u_1_b <- u_2_b <- 0) on both sides
+        g["u_b"], g["u_1_b"], g["u_2_b"] = g["u_1_b"], g["u_2_b"], g["u_b"]
+        for ch in chains.values():
+            ch["u_b"], ch["u_1_b"], ch["u_2_b"] = ch["u_1_b"], ch["u_2_b"], ch["u_b"]
+            ch["u_2_b"].zero_()
+    rec["seconds"] = time.time() - t0
+    worst = {}
+    for nm in ("u_1_b", "c_b"):
+        worst[nm] = {k: max(s[nm][k] for s in rec["steps"])
+                     for k in rec["steps"][0][nm]}
+    rec["worst"] = worst
+    _dump(f"protocol_cfg2_{n}.json", rec)
+    for nm, w in worst.items():
+        assert w["gpu_norm_rel"] <= 1e-5, (nm, w)
+        gate = max(1e-5, 1.5 * w["fp32_storage_floor_max_rel"])
+        assert w["gpu_max_rel"] <= gate, (nm, w)
+
+
+def _cfg5(env, n, steps):
+    torch, api, drivers = env
+    fam = "wave3d_r4"
+    _need_ref(fam)
+    seed, D = 0, 0.01
+    if _host_ram_gb() < 6 * n ** 3 * 8 / 2 ** 30:
+        pytest.skip(f"host RAM < {6 * n ** 3 * 8 / 2 ** 30:.0f} GB for the fp64 reference")
+    ref = oracle.ref_emitted(fam)
+    f64 = dict(dtype=torch.float64)
+    g = drivers.alloc(fam, n)
+    drivers.init_static(fam, g, n, seed)
+    torch.cuda.synchronize()
+    pin = dict(pin_memory=True, **f64)
+    h = {"c": g["c"].double().cpu(), "c_b": torch.zeros((n, n, n), **f64),
+         "u_1": torch.empty((n, n, n), **pin), "u_b": torch.empty((n, n, n), **pin),
+         "u_1_b": torch.empty((n, n, n), **pin)}
+    dev64 = torch.empty((n, n, n), device="cuda", **f64)
+    rec = {"config": f"cfg5 {fam} {n}^3 fp32, D={D}, {steps} independent reverse steps "
+                     "(u_1, u_b regenerated per step; u_1_b = the step's adjoint; c_b "
+                     "accumulated)",
+           "oracle": "reference emitted wave3d_r4_b (codegen.cpp:332-382), gcc "
+                     f"{oracle.ref_emitted_opt(fam)} -fopenmp, fp64", "steps": []}
+    t0 = time.time()
+    worst = {"max_rel": 0.0, "norm_rel": 0.0}
+    for t in range(steps):
+        drivers.regen_state(g["u_1"], n, t, seed, 4)
+        drivers.regen_seed(g["u_b"], n, t, seed)
+        for nm in ("u_1", "u_b"):
+            dev64.copy_(g[nm])
+            h[nm].copy_(dev64)
+        api.adjoint_fresh(fam, n, {"D": D}, g)   # async: runs beside the CPU reference
+        h["u_1_b"].zero_()
+        assert ref(n, {"D": D}, h) == 0
+        dev64.copy_(h["u_1_b"])
+        e = api.compare(g["u_1_b"], dev64)
+        assert e["nonfinite"] == 0
+        worst = {k: max(worst[k], e[k]) for k in worst}
+        if t % 10 == 0 or t == steps - 1:
+            rec["steps"].append({"t": t, "u_1_b": e, "elapsed_s": time.time() - t0})
+    dev64.copy_(h["c_b"])
+    ec = api.compare(g["c_b"], dev64)
+    rec.update({"u_1_b_worst_over_steps": worst, "c_b_after_all_steps": ec,
+                "max_abs_c_b": float(h["c_b"].abs().max()), "seconds": time.time() - t0})
+    _dump(f"protocol_cfg5_{n}_{steps}.json", rec)
+    assert worst["max_rel"] <= 1e-5 and worst["norm_rel"] <= 1e-5, worst
+    assert ec["nonfinite"] == 0
+    assert ec["max_rel"] <= 1e-5 and ec["norm_rel"] <= 1e-5, ec
+
+
+def test_cfg5_full_size_steps(env):
+    """1024^3 (the BASELINE size): 8 steps by default, the full 100 with
+    SGB_FULL_PROTOCOL=1."""
+    full = os.environ.get("SGB_FULL_PROTOCOL") == "1"
+    _cfg5(env, int(os.environ.get("SGB_CFG5_N", "1024")), 100 if full else 8)
+
+
+def test_cfg5_hundred_steps(env):
+    """All 100 steps of the protocol at 256^3 (the c_b accumulation depth)."""
+    _cfg5(env, 256, 100)
