@@ -209,67 +209,104 @@ def _omp_env():
     return int(os.environ["OMP_NUM_THREADS"])
 
 
+def _host_ram_free_gb():
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 2 ** 30
+    except Exception:  # pragma: no cover
+        return float("inf")
+
+
 def cpu_reference_runner(family: str):
-    """Returns (kind, call(n, scalars, arrays), label).  kind 'reference' = the
-    reference's own emitted OpenMP adjoint (oracle/_ref), else 'port' = the
-    repo's C restatement (oracle/sg_oracle.c, OpenMP predicate form)."""
-    import numpy as np
-    lib_path = os.path.join(ROOT, "oracle", "_ref", f"libref_{family}.so")
-    if os.path.exists(lib_path):
-        L = ctypes.CDLL(lib_path)
-        fn = getattr(L, f"{family}_b")
-        fn.restype = ctypes.c_int
-        opt = "-O2"
-        optf = os.path.join(ROOT, "oracle", "_ref", f"libref_{family}.opt")
-        if os.path.exists(optf):
-            opt = open(optf).read().strip()
-        from paper_1907_02818_b200 import api
-        names = api.array_params(family, "adjoint")
-        scal = api.SCALARS[family]
+    """Returns (kind, call(n, scalars, arrays), label, set_threads).  kind
+    'reference' = the reference's own emitted OpenMP adjoint (oracle/_ref,
+    emit_adjoint codegen.cpp:332-382 compiled by oracle/ref/Makefile), else
+    'port' = the repo's C restatement (oracle/sg_oracle.c, OpenMP predicate
+    form).  set_threads(k) sets the OpenMP thread count of that library."""
+    from oracle import oracle
+    if oracle.ref_emitted_available(family):
+        fn = oracle.ref_emitted(family, "adjoint")
+        opt = oracle.ref_emitted_opt(family)
 
         def call(n, scalars, arrays):
-            args = [ctypes.c_int(n)] + [ctypes.c_double(scalars[s]) for s in scal] + \
-                   [arrays[nm].ctypes.data_as(ctypes.c_void_p) for nm in names]
-            rc = fn(*args)
+            rc = fn(n, scalars, arrays)
             if rc != 0:
                 raise RuntimeError(f"reference {family}_b returned {rc}")
-        return "reference", call, f"reference emitted {family}_b, gcc {opt} -fopenmp, fp64"
-    from oracle import oracle
+        label = f"reference emitted {family}_b, gcc {opt} -fopenmp, fp64"
+        lib = ctypes.CDLL(oracle.ref_emitted_path(family))
+    else:
+        def call(n, scalars, arrays):
+            f = oracle.family(family)
+            grids = {a: arrays[a] for a in f.arrays if a in arrays}
+            adjs = {a: arrays[a] for a in f.adjoints if a and a in arrays}
+            oracle.run_program_omp(family, n, scalars, grids, adjs)
+        label = f"oracle port (sg_run_program_omp) {family}, fp64"
+        lib = oracle.lib()
 
-    def call(n, scalars, arrays):
-        f = oracle.family(family)
-        grids = {a: arrays[a] for a in f.arrays if a in arrays}
-        adjs = {a: arrays[a] for a in f.adjoints if a and a in arrays}
-        oracle.run_program_omp(family, n, scalars, grids, adjs)
-    return "port", call, f"oracle port (sg_run_program_omp) {family}, fp64"
+    def set_threads(k):
+        try:
+            lib.omp_set_num_threads(ctypes.c_int(int(k)))
+        except AttributeError:  # pragma: no cover
+            ctypes.CDLL("libgomp.so.1").omp_set_num_threads(ctypes.c_int(int(k)))
+    kind = "reference" if oracle.ref_emitted_available(family) else "port"
+    return kind, call, label, set_threads
 
 
 def cpu_arrays(family, n):
+    """fp64 host arrays of the reference prototype, filled IN PARALLEL (first
+    touch by the OpenMP-sized torch thread pool, pages spread over the cores
+    that will stream them; the reference's own bench fills serially,
+    stencilgrad.cpp:309-360 -- a stated deviation): c in [1.5, 4.5), the rest
+    in [-1, 1), from a counter hash (the timing does not depend on the values:
+    wave / burgers adjoints have no data-dependent control flow beyond the
+    Burgers max/min selects, which see both signs)."""
     import numpy as np
+    import torch
     from paper_1907_02818_b200 import api
-    rng = np.random.default_rng(0)
     shape = (n,) * DIMS[family]
     out = {}
-    for nm in api.array_params(family, "adjoint"):
-        if nm == "c":
-            out[nm] = rng.uniform(1.5, 4.5, shape)
-        else:
-            out[nm] = rng.standard_normal(shape)
+    for k, nm in enumerate(api.array_params(family, "adjoint")):
+        t = torch.empty(shape, dtype=torch.float64)
+        flat = t.view(-1)
+        chunk = 1 << 24
+        for a in range(0, flat.numel(), chunk):  # bounded temporaries
+            idx = torch.arange(a, min(a + chunk, flat.numel()), dtype=torch.float64)
+            v = torch.frac(torch.sin(idx * 12.9898 + 78.233 * (k + 1)) * 43758.5453).abs_()
+            flat[a:a + idx.numel()] = 1.5 + 3.0 * v if nm == "c" else 2.0 * v - 1.0
+        out[nm] = t.numpy()
     return out
 
 
-def time_cpu(family, scalars, n_full, target_s=4.0, calls=3):
-    """Best-of-`calls` time of one reference adjoint call on the full workload
-    grid (or, if one call there exceeds target_s, the largest cube that fits;
-    see run_reference_arm for why the sample must not be small)."""
-    threads = _omp_env()
-    kind, call, label = cpu_reference_runner(family)
+def _ref_fit_n(family, n_full, arrays_wanted=None):
+    """Largest grid extent <= n_full whose fp64 reference state (every array of
+    the prototype) fits in 70% of the free host RAM."""
+    from paper_1907_02818_b200 import api
     d = DIMS[family]
+    na = len(api.array_params(family, "adjoint")) if arrays_wanted is None else arrays_wanted
+    free = _host_ram_free_gb() * 0.7 * 2 ** 30
     n = n_full
+    while n > 8 and na * 8.0 * n ** d > free:
+        n = int(n * 0.9)
+        if d == 3:
+            n -= n % 4
+    return n
+
+
+def time_cpu(family, scalars, n_full, target_s=4.0, calls=3, one_thread_s=3.0):
+    """Best-of-`calls` time of one reference adjoint call on the full workload
+    grid (or, if one call there exceeds target_s / the host RAM, the largest
+    cube that fits; see run_reference_arm for why the sample must not be
+    small), plus the same on ONE thread over a bounded sample."""
+    threads = _omp_env()
+    kind, call, label, set_threads = cpu_reference_runner(family)
+    d = DIMS[family]
+    n = _ref_fit_n(family, n_full)
+    shrunk_ram = n != n_full
     if os.environ.get("SGB_REF_N"):
         n = int(os.environ["SGB_REF_N"])
+    set_threads(threads)
     a = cpu_arrays(family, n)
-    call(n, scalars, a)  # first touch
+    call(n, scalars, a)  # warm
     t0 = time.perf_counter()
     call(n, scalars, a)
     t = time.perf_counter() - t0
@@ -285,11 +322,27 @@ def time_cpu(family, scalars, n_full, target_s=4.0, calls=3):
         call(n, scalars, a)
         best = min(best, time.perf_counter() - t0)
     pts = n ** d
+    del a
+    # one thread, bounded sample (report OMP_NUM_THREADS=1 too)
+    n1 = {3: 192, 2: 4096, 1: 1 << 22}[d] if not os.environ.get("SGB_REF_N") else n
+    set_threads(1)
+    a1 = cpu_arrays(family, n1)
+    call(n1, scalars, a1)
+    t0 = time.perf_counter()
+    call(n1, scalars, a1)
+    t1 = time.perf_counter() - t0
+    set_threads(threads)
+    del a1
+    what = ("the full workload" if n == n_full else
+            f"bounded sample of the {n_full}^{d} workload" +
+            (" (host RAM)" if shrunk_ram else ""))
     return {"value": pts / best / 1e9, "unit": "GPts/s", "cores": threads, "kind": kind,
             "cpu_model": cpu_model(), "nproc": os.cpu_count(),
-            "sample": f"{label}; one call over a {n}^{d} grid "
-                      f"({'the full workload' if n == n_full else 'bounded sample of the ' + str(n_full) + '^' + str(d) + ' workload'}), best of {calls}",
-            "seconds_per_call": best, "n": n}
+            "sample": f"{label}; one call over a {n}^{d} grid ({what}), best of {calls}; "
+                      "arrays first-touched in parallel",
+            "seconds_per_call": best, "n": n,
+            "one_thread": {"value": n1 ** d / t1 / 1e9, "unit": "GPts/s", "n": n1,
+                           "seconds_per_call": t1}}
 
 
 def run_reference_arm(args, cfg):
@@ -298,30 +351,33 @@ def run_reference_arm(args, cfg):
     if rank != 0:
         return
     threads = _omp_env()
-    kind, call, label = cpu_reference_runner(family)
+    kind, call, label, set_threads = cpu_reference_runner(family)
+    set_threads(threads)
     d = DIMS[family]
     # size each step so that warmup + steps end within ~3 minutes
     budget = float(os.environ.get("SGB_REF_BUDGET_S", "180"))
     per_call = budget / max(1, args.steps + args.warmup)
-    # Calibrate at the FULL workload size: the reference's time per point falls
-    # with n (its boundary nests run serially and scale like n^(d-1); measured
-    # on the B200 host at radius 4: 0.17 GPts/s at 256^3, 0.37 at 748^3), so a
-    # small calibration cube would pick an unrepresentatively small sample.
-    # Shrink only as far as the budget requires (time ~ n^2.5 measured).
+    # Calibrate at the FULL workload size (or the largest cube the host RAM
+    # holds): the reference's time per point falls with n (its boundary nests
+    # run serially and scale like n^(d-1); measured on the B200 host at radius
+    # 4: 0.17 GPts/s at 256^3, 0.37 at 748^3), so a small calibration cube
+    # would pick an unrepresentatively small sample.  Shrink only as far as the
+    # budget requires (time ~ n^2.5 measured).
+    n_fit = _ref_fit_n(family, n_full)
     a = None
     if os.environ.get("SGB_REF_N"):  # fixed sample size (tests)
         n = int(os.environ["SGB_REF_N"])
     else:
-        a = cpu_arrays(family, n_full)
-        call(n_full, scalars, a)  # first touch
+        a = cpu_arrays(family, n_fit)
+        call(n_fit, scalars, a)  # warm
         t0 = time.perf_counter()
-        call(n_full, scalars, a)
-        t_full = max(time.perf_counter() - t0, 1e-4)
-        n = n_full if t_full <= per_call else int(n_full * (per_call / t_full) ** (1.0 / 2.5))
-        n = max(min(n, n_full), min(n_full, {3: 256, 2: 2048, 1: 1 << 20}[d]))
-    if n != n_full:
+        call(n_fit, scalars, a)
+        t_fit = max(time.perf_counter() - t0, 1e-4)
+        n = n_fit if t_fit <= per_call else int(n_fit * (per_call / t_fit) ** (1.0 / 2.5))
+        n = max(min(n, n_fit), min(n_fit, {3: 256, 2: 2048, 1: 1 << 20}[d]))
+    if a is not None and n != n_fit:
         a = None
-    if d == 3 and n != n_full:
+    if d == 3 and n != n_fit:
         n -= n % 4
     if a is None:
         a = cpu_arrays(family, n)
@@ -333,17 +389,20 @@ def run_reference_arm(args, cfg):
     sec = time.perf_counter() - t0
     pts = n ** d * args.steps
     value = pts / sec / 1e9
+    why = ("the full workload" if n == n_full else
+           f"a {n}^{d} sample of the {n_full}^{d} workload" +
+           (f" (host RAM fits {n_fit}^{d})" if n_fit != n_full else " (time budget)"))
     line = {
         "impl": "reference", "metric": "adjoint GPts/s", "value": value, "unit": "GPts/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "family": family, "n": n_full, "sample_n": n,
-                   "note": "reference CPU path on the host cores; each step is one call "
-                           f"over a {n}^{d} sample of the workload"},
+                   "note": f"reference CPU path on the host cores; each step is one call over "
+                           f"{why}; arrays first-touched in parallel"},
         "cpu_baseline": {"value": value, "unit": "GPts/s", "cores": threads, "kind": kind,
                          "cpu_model": cpu_model(), "nproc": os.cpu_count(),
-                         "sample": f"{label}; {n}^{d} grid per step"},
+                         "sample": f"{label}; {n}^{d} grid per step ({why})"},
         "e2e": {"value": value, "unit": "GPts/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

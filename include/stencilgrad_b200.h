@@ -220,6 +220,60 @@ int wave3d_c_b_slab_f64(int n, double D, double* c, double* c_b, double* u_1, do
                         double* u_2_b, double* u_b, int i_base, int nplanes, int out_i0,
                         int out_i1, sgb_stream_t stream);
 
+/* ---- multi-GPU z-slab plan ---------------------------------------
+ * One rank per GPU owns the global planes [own0, own1) of the outermost
+ * counter (sgb_slab_decompose: balanced contiguous split, R halo planes on
+ * interior sides; local arrays hold planes [base, base + nplanes)).  The plan
+ * owns the communication and a comm stream; the caller owns and binds every
+ * array of <family>_b (set 0; the inputs c / u_1 / u_b may get a second
+ * buffer set 1 for pipelining -- unbound set-1 arrays fall back to set 0).
+ * Transports (no reference counterpart: the reference is single-node CPU,
+ * SPEC.md:8):
+ *   SGB_TRANSPORT_NCCL  ncclSend / ncclRecv of the R edge planes to rank +- 1
+ *                       in one group on the comm stream; every rank passes the
+ *                       same 128-byte ncclUniqueId (sgb_nccl_unique_id on one
+ *                       rank, broadcast out of band); libnccl.so.2 dlopen'ed.
+ *   SGB_TRANSPORT_IPC   each rank maps its neighbours' arrays (CUDA IPC, peer
+ *                       memory over NVLink) and pushes its edge planes into
+ *                       their halos with copy engines; ordering by stream
+ *                       memory operations on epoch flags, no host round trip.
+ *                       Blobs are exchanged out of band: every rank calls
+ *                       sgb_slab_ipc_export after binding, then connects with
+ *                       its lower / upper neighbour's blob (NULL at grid ends).
+ * sgb_slab_halo_start(set, mask): refresh the halo planes of the fields in
+ * mask (1 = c, 2 = u_1, 4 = u_b) of `set`, ordered after the work queued on
+ * `stream`, asynchronously on the comm stream; every prior reader of those
+ * halos must be ordered before it on `stream`.  sgb_slab_halo_wait makes
+ * `stream` wait for it (incoming halos arrived, outgoing planes sent).
+ * sgb_slab_step: one reverse step over the owned planes -- exchange u_1 / u_b,
+ * then the gather (flags: SGB_STEP_OVERLAP = interior planes during the
+ * exchange, then the two edge bands; SGB_STEP_FRESH = u_1_b written as the
+ * step's adjoint alone (wave3d_r4 fp32); SGB_STEP_NO_EXCHANGE = the halos of
+ * `set` were refreshed by an earlier sgb_slab_halo_start (pipelined drivers):
+ * wait for it, then one launch).  All calls are collective in order: every
+ * rank issues the same sequence. */
+#define SGB_TRANSPORT_NCCL 1
+#define SGB_TRANSPORT_IPC 2
+#define SGB_STEP_FRESH 1
+#define SGB_STEP_OVERLAP 2
+#define SGB_STEP_NO_EXCHANGE 4
+typedef struct sgb_slab sgb_slab;
+int sgb_slab_decompose(int n, int radius, int world, int rank, int* own0, int* own1, int* base,
+                       int* nplanes);
+int sgb_nccl_unique_id(void* id128);
+sgb_slab* sgb_slab_create(const char* family, int n, int dtype_bytes, int rank, int world,
+                          int transport, const void* nccl_id128);
+int sgb_slab_geometry(const sgb_slab* plan, int* base, int* nplanes, int* own0, int* own1);
+int sgb_slab_bind(sgb_slab* plan, int set, const char* name, void* device_ptr);
+/* blob == NULL: *bytes = the blob size */
+int sgb_slab_ipc_export(const sgb_slab* plan, void* blob, long long* bytes);
+int sgb_slab_ipc_connect(sgb_slab* plan, const void* lower_blob, const void* upper_blob);
+int sgb_slab_halo_start(sgb_slab* plan, int set, unsigned fields_mask, sgb_stream_t stream);
+int sgb_slab_halo_wait(sgb_slab* plan, int set, sgb_stream_t stream);
+int sgb_slab_step(sgb_slab* plan, int set, const double* scalars, int flags,
+                  sgb_stream_t stream);
+void sgb_slab_destroy(sgb_slab* plan);
+
 /* ---- device input generation (synthetic BASELINE distributions) -------------
  * Counter-based: value(index) depends only on (seed, stream, global index), so
  * any slab of any decomposition sees identical inputs.  index = global flat
@@ -235,6 +289,10 @@ int sgb_fill_random_f64(double* dst, long long count, long long index_base, uint
  * h-point shell set to zero (one fused pass; same counter-based values as
  * sgb_fill_random_f32 at the same global indices) */
 int sgb_fill_normal3d_f32(float* dst, int n, int i_base, int nplanes, int halo, uint64_t seed,
+                          uint64_t stream_id, double mean, double scale, sgb_stream_t stream);
+/* the same values widened to fp64 (the fp64 forms of the 3D configurations
+ * see exactly the fp32 inputs) */
+int sgb_fill_normal3d_f64(double* dst, int n, int i_base, int nplanes, int halo, uint64_t seed,
                           uint64_t stream_id, double mean, double scale, sgb_stream_t stream);
 /* zero the h-point shell of planes [i_base, i_base+nplanes) of an n^d grid
  * (d = 1, 2 or 3; for d < 3 pass i_base = 0, nplanes = n) */

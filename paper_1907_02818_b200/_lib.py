@@ -36,6 +36,8 @@ _CTYPES = {
     "int*": ctypes.c_void_p,
     "const char*": ctypes.c_char_p,
     "sgb_plan*": ctypes.c_void_p,
+    "sgb_slab*": ctypes.c_void_p,
+    "const sgb_slab*": ctypes.c_void_p,
     "sgb_jit_kernel*": ctypes.c_void_p,
     "sgb_jit_kernel**": ctypes.c_void_p,
     "unsigned": ctypes.c_uint,

@@ -142,12 +142,15 @@ def fill_random(t, index_base: int, seed: int, stream_id: int, kind: str, a: flo
 def fill_normal3d(t, n: int, halo: int, seed: int, stream_id: int, i_base: int = 0,
                   nplanes: int | None = None, mean: float = 0.0, scale: float = 1.0,
                   stream=None):
-    """N(mean, scale^2) on planes [i_base, i_base+nplanes) of an n^3 fp32 grid
-    with a zero `halo`-point shell, in one pass (same values as fill_random)."""
-    _lib.check(_lib.lib().sgb_fill_normal3d_f32(
-        ctypes.c_void_p(t.data_ptr()), n, i_base, n if nplanes is None else nplanes, halo,
-        int(seed), int(stream_id), float(mean), float(scale), _stream_ptr(stream)),
-        "fill_normal3d")
+    """N(mean, scale^2) on planes [i_base, i_base+nplanes) of an n^3 grid
+    with a zero `halo`-point shell, in one pass (same values as fill_random;
+    an fp64 tensor gets the fp32 values widened)."""
+    import torch
+    fn = _lib.lib().sgb_fill_normal3d_f32 if t.dtype == torch.float32 else \
+        _lib.lib().sgb_fill_normal3d_f64
+    _lib.check(fn(ctypes.c_void_p(t.data_ptr()), n, i_base, n if nplanes is None else nplanes,
+                  halo, int(seed), int(stream_id), float(mean), float(scale),
+                  _stream_ptr(stream)), "fill_normal3d")
 
 
 def zero_halo(t, d: int, n: int, h: int, i_base: int = 0, nplanes: int | None = None,

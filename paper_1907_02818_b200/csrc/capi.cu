@@ -501,15 +501,7 @@ int sgb_ipc_handle(const void* ptr, void* handle64, long long* offset) {
   // allocation base of ptr (driver entry point, so the library keeps no hard
   // dependency on libcuda)
   using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
-  static GetRange get_range = nullptr;
-  if (!get_range) {
-    cudaDriverEntryPointQueryResult q;
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      get_range = reinterpret_cast<GetRange>(f);
-  }
+  const GetRange get_range = reinterpret_cast<GetRange>(driver_entry("cuMemGetAddressRange"));
   CUdeviceptr base = 0;
   size_t size = 0;
   if (!get_range || get_range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)

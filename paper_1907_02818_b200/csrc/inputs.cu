@@ -78,9 +78,11 @@ __global__ void fill_random_kernel(T* dst, long long count, long long base, uint
 // With n even the 4 points are two whole Box-Muller pairs, each computed once
 // (same values as draw()).  32-bit coordinates (n <= 2^20), a 64-bit flat
 // index advanced per plane.
-__global__ void fill_normal3d_f32_kernel(float* dst, int n, int i_base, int nplanes, int h,
-                                         uint64_t seed, uint64_t stream, float mean,
-                                         float scale) {
+// T = float, or double holding the SAME (fp32) values widened: the fp64
+// configurations regenerate exactly the inputs of the fp32 ones.
+template <typename T>
+__global__ void fill_normal3d_kernel(T* dst, int n, int i_base, int nplanes, int h,
+                                     uint64_t seed, uint64_t stream, float mean, float scale) {
   const int k = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int j = blockIdx.y;
   if (k >= n) return;
@@ -90,7 +92,7 @@ __global__ void fill_normal3d_f32_kernel(float* dst, int n, int i_base, int npla
   const long long plane = (long long)n * n;
   const long long dg = (long long)gridDim.z * plane;
   long long g = ((long long)(i_base + (int)blockIdx.z) * n + j) * n + k;  // global flat index
-  float* p = dst + ((long long)blockIdx.z * n + j) * n + k;
+  T* p = dst + ((long long)blockIdx.z * n + j) * n + k;
   const long long dp = dg;
   for (int li = blockIdx.z; li < nplanes; li += gridDim.z, g += dg, p += dp) {
     const int i = i_base + li;
@@ -122,7 +124,12 @@ __global__ void fill_normal3d_f32_kernel(float* dst, int n, int i_base, int npla
       }
     }
     if (n % 4 == 0) {
-      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+        *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+      }
     } else {
       for (int m = 0; m < 4 && k + m < n; m++) p[m] = v[m];
     }
@@ -288,9 +295,23 @@ int sgb_fill_normal3d_f32(float* dst, int n, int i_base, int nplanes, int halo, 
   dim3 b(64), g((unsigned)((n / 4 + 63) / 64 + ((n % 4) ? 1 : 0)), (unsigned)n,
                 (unsigned)(nplanes < 64 ? nplanes : 64));
   if (n > (1 << 20)) return SGB_EINVAL;
-  fill_normal3d_f32_kernel<<<g, b, 0, as_stream(stream)>>>(dst, n, i_base, nplanes, halo, seed,
-                                                           stream_id, (float)mean, (float)scale);
+  fill_normal3d_kernel<float><<<g, b, 0, as_stream(stream)>>>(dst, n, i_base, nplanes, halo,
+                                                              seed, stream_id, (float)mean,
+                                                              (float)scale);
   return launch_status("sgb_fill_normal3d_f32");
+}
+
+int sgb_fill_normal3d_f64(double* dst, int n, int i_base, int nplanes, int halo, uint64_t seed,
+                          uint64_t stream_id, double mean, double scale, sgb_stream_t stream) {
+  if (!dst || n <= 0 || nplanes <= 0 || halo < 0) return SGB_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) && n % 4 == 0) return SGB_EINVAL;
+  dim3 b(64), g((unsigned)((n / 4 + 63) / 64 + ((n % 4) ? 1 : 0)), (unsigned)n,
+                (unsigned)(nplanes < 64 ? nplanes : 64));
+  if (n > (1 << 20)) return SGB_EINVAL;
+  fill_normal3d_kernel<double><<<g, b, 0, as_stream(stream)>>>(dst, n, i_base, nplanes, halo,
+                                                               seed, stream_id, (float)mean,
+                                                               (float)scale);
+  return launch_status("sgb_fill_normal3d_f64");
 }
 
 int sgb_fill_layered_f32(float* c, int n, int layers, double lo, double hi, uint64_t seed,

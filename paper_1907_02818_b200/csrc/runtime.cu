@@ -14,6 +14,7 @@
 #include <set>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "sgb_common.cuh"
 
@@ -107,6 +108,21 @@ int ensure_smem(const void* fn, size_t bytes, const char* what) {
     return -static_cast<int>(e);
   }
   return 0;
+}
+
+void* driver_entry(const char* name) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::string, void*>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& kv : cache)
+    if (kv.first == name) return kv.second;
+  cudaDriverEntryPointQueryResult q;
+  void* f = nullptr;
+  if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    f = nullptr;
+  cache.emplace_back(name, f);
+  return f;
 }
 
 }  // namespace sgb

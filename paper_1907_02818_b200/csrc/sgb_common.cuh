@@ -102,6 +102,9 @@ int num_sms();                         // SMs of the current device (cached per 
 // dynamic shared-memory attribute of `fn` on the current device, set once per
 // (device, kernel); 0 or a negative error (sgb_last_error set)
 int ensure_smem(const void* fn, size_t bytes, const char* what);
+// a CUDA driver entry point by name (cudaGetDriverEntryPoint, cached; nullptr
+// if unavailable) -- the library keeps no link-time libcuda dependency for it
+void* driver_entry(const char* name);
 
 inline unsigned grid_1d(long long work, int block) {
   long long g = (work + block - 1) / block;

@@ -177,6 +177,55 @@ class HaloPrefetch:
             self.side.synchronize()
 
 
+class PlanPrefetch:
+    """HaloPrefetch on the library's own z-slab plan (slab.SlabPlan; the
+    exchange is the plan's NCCL or CUDA-IPC transport, sgb_slab_halo_start):
+    the u_1 / u_b inputs of step t live in buffer set t % 2 (both sets bound
+    to the plan); a high-priority side stream regenerates step t+1's owned
+    planes and starts that set's halo exchange while step t's single launch
+    over the owned planes reads the other set.  Same inputs per step as the
+    exchange-then-compute path, so the outputs are bitwise equal (tested).
+
+    plan: a connected SlabPlan whose set 0 / 1 are `sets[0]` / `sets[1]`
+    (dicts with "u_1", "u_b"); regen(fields, t) writes step t's OWNED planes
+    (None: static inputs, the halos are still refreshed every step)."""
+
+    def __init__(self, plan, scalars, sets, regen=None, fresh=False):
+        self.plan, self.scalars, self.sets = plan, scalars, sets
+        self.regen, self.fresh = regen, fresh
+        self.side = torch.cuda.Stream(priority=-1)
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+        self.side.wait_stream(torch.cuda.current_stream())
+        self._t = 0
+        self._prepare(0)
+        self._prepare(1)
+
+    def _prepare(self, t):
+        s = t % 2
+        with torch.cuda.stream(self.side):
+            if t >= 2:  # step t-2 finished reading this set on this rank
+                self.side.wait_event(self.free[s])
+            if self.regen is not None:
+                self.regen(self.sets[s], t)
+            self.plan.halo_start(("u_1", "u_b"), s, stream=self.side)
+
+    def step(self, t=None):
+        t = self._t if t is None else t
+        if t != self._t:
+            raise ValueError(f"PlanPrefetch steps run in order: expected {self._t}, got {t}")
+        s = t % 2
+        cur = torch.cuda.current_stream()
+        self.plan.step(self.scalars, set_=s, fresh=self.fresh, exchanged=True, stream=cur)
+        self.free[s].record(cur)
+        self._t = t + 1
+        self._prepare(t + 2)
+        return 1
+
+    def close(self):
+        torch.cuda.current_stream().wait_stream(self.side)
+        self.side.synchronize()
+
+
 def alloc(family, n, sl=None, dtype=torch.float32):
     shape = (sl.nplanes, n, n) if sl is not None else (n, n, n)
     return {nm: torch.zeros(shape, dtype=dtype, device="cuda")
