@@ -3,23 +3,28 @@
 
 Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
 JSON line on rank 0.  For N > 1 it runs under torchrun, one rank per GPU,
-z-slab decomposition with a per-step NCCL halo exchange.
+z-slab decomposition with a radius-4 halo exchange every step.
 
-Workload (default ``--config 4``; BASELINE.json configs[3]): wave3d_r4,
-8th-order 25-point star, fp32, 768^3 with a 4-point zero halo, adjoint w.r.t.
-u_1 and c, seeded synthetic inputs (c layered in z, u_1 and the seed u_b
-N(0,1)), D = 0.01.  One STEP = one reverse time step = the full gather adjoint
-(core + all 1456 boundary regions, one fused launch per rank) over the whole
-grid, plus the radius-4 halo exchange of u_1 and u_b when N > 1.
+Workload (default ``--config 5``; BASELINE.json configs[4], the largest 3D
+case the >= 80 %-at-8-GPUs target names): wave3d_r4, 8th-order 25-point
+star, fp32, 1024^3 with a 4-point zero halo, adjoint w.r.t. u_1 and c, D =
+0.01, c layered in z.  One STEP = one of the 100 independent reverse steps:
+u_1 and the seed u_b regenerated from (seed, step) on each rank's owned
+planes, their radius-4 halos exchanged (N > 1: the library's z-slab plan,
+sgb_slab_*), the fused gather adjoint (core + all 1456 boundary regions) with
+u_1_b = the step's adjoint and c_b accumulated.  cfg 4 (768^3, the same
+kernel, static inputs, exchange per step) is carried at the same N in
+other_configs; the other configs run with ``--config 4|2|1|3``.
 
 value  = grid-point updates / s over all ranks (GPts/s), device time with CUDA
-         events, max over ranks; inputs resident in HBM (12.7 GB touched per
-         step at 768^3 >> 126 MB L2, so no flush is needed).
-e2e    = the same metric through the host-buffer C-ABI entry
-         (sgb_plan_run_adjoint_host): pinned host arrays in, H2D + kernel +
-         D2H of the accumulated adjoints inside the timed region.
-roofline: algorithmic bytes per launch (28 B/pt: c, u_1, u_b read; c_b, u_1_b
-         read+write) / average launch time vs MEASURED_PEAKS.json hbm_gbs.
+         events, max over ranks; inputs resident in HBM (>= 3.7 GB touched per
+         rank and step >> 126 MB L2, so no flush is needed).
+e2e    = the same metric through the host-facing entry: pinned host arrays
+         in, H2D (+ the halo exchange at N > 1) + the gather + D2H of the
+         accumulated adjoints inside the timed region.
+roofline: algorithmic bytes of the step (24 B/pt gather with fresh u_1_b + 8
+         B/pt regenerated inputs) / step time vs MEASURED_PEAKS.json hbm_gbs.
+fp64   = the same workload at the reference's precision, device and e2e.
 cpu_baseline: the reference's own emitted OpenMP adjoint (oracle/_ref, built
          from /root/reference by oracle/ref/Makefile) on the host cores.
 
@@ -148,9 +153,10 @@ def committed_traffic(workload: str, n: int):
         return None, None
 
 
-def gen_inputs(api, torch, family, n, slab=None):
+def gen_inputs(api, torch, family, n, slab=None, dtype=None):
     """Seeded synthetic inputs on the device (counter-based in the global flat
-    index, so every decomposition holds the single-GPU values)."""
+    index, so every decomposition holds the single-GPU values).  dtype 'f64'
+    for a 3D family: the same (fp32-generated) values widened."""
     d = DIMS[family]
     seed = 0
     if d == 3:
@@ -161,11 +167,19 @@ def gen_inputs(api, torch, family, n, slab=None):
     else:
         base, npl, shape, ib = 0, n, (n,) * d, 0
     dt = torch.float32 if family in ("wave3d_r4", "wave3d_c") else torch.float64
+    if dtype is not None:
+        dt = torch.float32 if dtype == "f32" else torch.float64
     arrays = {nm: torch.zeros(shape, dtype=dt, device="cuda")
               for nm in api.array_params(family, "adjoint")}
     h = RADIUS[family]
     if family == "wave3d_r4":
-        api.fill_layered(arrays["c"], n, 8, 1.5, 4.5, seed, base, npl)
+        if dt == torch.float32:
+            api.fill_layered(arrays["c"], n, 8, 1.5, 4.5, seed, base, npl)
+        else:
+            c32 = torch.empty(shape, dtype=torch.float32, device="cuda")
+            api.fill_layered(c32, n, 8, 1.5, 4.5, seed, base, npl)
+            arrays["c"].copy_(c32)
+            del c32
         api.fill_normal3d(arrays["u_1"], n, 4, seed, 1, base, npl)
         api.fill_normal3d(arrays["u_b"], n, 0, seed, 3, base, npl)
     elif family == "wave3d_c":
@@ -410,312 +424,503 @@ def run_reference_arm(args, cfg):
 
 
 # ------------------------------------------------------------------ GPU arm
+class Dist:
+    """torch.distributed plumbing of the N-rank run: the max-over-ranks
+    reductions and the out-of-band channel of the slab plans.  The data path
+    (halo exchange) is the library's own sgb_slab plan."""
+
+    def __init__(self, torch, world, rank, local):
+        self.torch, self.world, self.rank, self.local = torch, world, rank, local
+        self.dist = None
+        self.backend = os.environ.get("SGB_BENCH_DIST_BACKEND", "nccl")
+        if world > 1:
+            import torch.distributed as dist
+            kw = {"device_id": torch.device("cuda", torch.cuda.current_device())} \
+                if self.backend == "nccl" else {}
+            dist.init_process_group(self.backend, **kw)
+            self.dist = dist
+
+    def _dev(self):
+        return "cuda" if self.backend == "nccl" else "cpu"
+
+    def max(self, *vals):
+        if self.dist is None:
+            return [float(v) for v in vals]
+        t = self.torch.tensor([float(v) for v in vals], dtype=self.torch.float64,
+                              device=self._dev())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return [float(x) for x in t.tolist()]
+
+    def all_ok(self, ok):
+        if self.dist is None:
+            return bool(ok)
+        t = self.torch.tensor([1 if ok else 0], dtype=self.torch.int32, device=self._dev())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        return bool(int(t[0]))
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.dist is not None:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+class Workload:
+    """One BASELINE configuration on this rank: its device state and its STEP
+    (DESIGN.md §8(d)):
+      cfg 5 -- regenerate u_1 / u_b from (seed, step) (owned planes), exchange
+               their radius-4 halos (N > 1), the fresh gather (u_1_b = the
+               step's adjoint, c_b accumulated);
+      cfg 4 -- the halo exchange of u_1 / u_b (N > 1) and the accumulating
+               gather over the whole grid (static inputs);
+      cfg 2 -- one carried reverse step (u_1 regenerated, adjoints rotated;
+               runs of 10 as the BASELINE config states);
+      cfg 1 / 3 -- the gather (single GPU; replicas only).
+    N > 1 strategies (--halo): 'ipc' / 'nccl' = the library's z-slab plan
+    (sgb_slab_*) with the CUDA-IPC copy-engine or NCCL transport, exchange of
+    step t+1 pipelined behind step t (drivers.PlanPrefetch; cfg 2: exchange,
+    interior overlapped); 'torch' = the same pipeline on torch.distributed
+    NCCL (drivers.HaloPrefetch); 'peer' = the fused peer-memory halo."""
+
+    def __init__(self, torch, api, cfg_id, n, dist, halo, dtype=None):
+        from paper_1907_02818_b200 import drivers, slab as slabmod
+        self.torch, self.api, self.drivers = torch, api, drivers
+        family, n_full, dt, bpp, scalars, desc = CONFIGS[cfg_id]
+        self.cfg_id, self.family, self.n = cfg_id, family, n or n_full
+        self.dtype = dtype or dt
+        self.scalars, self.desc = scalars, desc
+        self.d, self.R = DIMS[family], RADIUS[family]
+        self.dist = dist
+        self.world, self.rank = dist.world, dist.rank
+        self.regen = cfg_id == "5"
+        self.carried = cfg_id == "2"
+        self.fresh = self.regen and self.dtype == "f32"
+        self.bpp = bpp - (4 if (self.fresh or (self.carried and self.world == 1)) else 0)
+        if self.dtype == "f64":
+            self.bpp = (bpp - (4 if self.fresh else 0)) * 2
+        self.sl = None
+        if self.world > 1:
+            if self.d != 3:
+                raise SystemExit(f"{family} does not shard (replicas only); run with --gpus 1")
+            self.sl = slabmod.c_decompose(self.n, self.R, self.world, self.rank)
+        self.arrays = gen_inputs(api, torch, family, self.n, self.sl, self.dtype)
+        self.t = 0
+        self.record = False   # time the dominant kernel (the gather) per step
+        self.kev = []
+        self.pipe = None
+        self.plan = None
+        self.halo = halo if self.world > 1 else None
+        self.note = None
+        if self.world > 1:
+            self._setup_multi(halo)
+        torch.cuda.synchronize()
+
+    # ---- inputs of step t on this rank's owned planes
+    def _regen(self, arrs, t):
+        sl = self.sl
+        if sl is not None:
+            from paper_1907_02818_b200 import slab as slabmod
+            own = slice(sl.own0 - sl.base, sl.own1 - sl.base)
+            o = slabmod.Slab(self.n, self.R, sl.rank, sl.world, sl.own0, sl.own1, sl.own0,
+                             sl.owned)
+            self.drivers.regen_state(arrs["u_1"][own], self.n, t, 0, self.R, o)
+            self.drivers.regen_seed(arrs["u_b"][own], self.n, t, 0, o)
+        else:
+            self.drivers.regen_state(arrs["u_1"], self.n, t, 0, self.R)
+            self.drivers.regen_seed(arrs["u_b"], self.n, t, 0)
+
+    def _setup_multi(self, halo):
+        torch, drivers = self.torch, self.drivers
+        from paper_1907_02818_b200 import slab as slabmod
+        sl = self.sl
+        if self.carried or halo == "peer":
+            # c static: its halo once; cfg 2's rotating adjoints stay on the
+            # torch exchange (the carried seed buffer changes role every step)
+            slabmod.exchange_halos(sl, [self.arrays["c"]])
+            if halo == "peer":
+                from paper_1907_02818_b200 import peer as peermod
+                self.link = peermod.try_connect(sl, self.arrays)
+                if self.link is None:
+                    raise SystemExit("peer halo unavailable on this box")
+            return
+        if halo == "torch":
+            slabmod.exchange_halos(sl, [self.arrays["c"]])
+            self.pipe = drivers.HaloPrefetch(
+                self.family, self.n, self.scalars, self.arrays, sl,
+                regen=(lambda fs, t: self._regen(fs, t)) if self.regen else None,
+                fresh=self.fresh)
+            return
+        second = {k: self.arrays[k].clone() for k in ("u_1", "u_b")}
+        self.sets = [{k: self.arrays[k] for k in ("u_1", "u_b")}, second]
+        self.plan = slabmod.SlabPlan(self.family, self.n, self.arrays, self.rank, self.world,
+                                     halo, arrays1=second).connect()
+        self.plan.halo_start(("c",))  # c is static: exchanged once
+        self.pipe = drivers.PlanPrefetch(
+            self.plan, self.scalars, self.sets,
+            regen=(lambda fs, t: self._regen(fs, t)) if self.regen else None,
+            fresh=self.fresh)
+
+    def _gather(self, fn):
+        """Runs the step's gather launch(es), bracketed by CUDA events on the
+        launching stream when recording (roofline of the dominant kernel)."""
+        if not self.record:
+            return fn()
+        torch = self.torch
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = fn()
+        b.record()
+        self.kev.append((a, b))
+        return r
+
+    # ---- one step on the current stream; returns launches of our kernels
+    def step(self):
+        api, drivers = self.api, self.drivers
+        t = self.t
+        self.t += 1
+        if self.pipe is not None:  # the stream waits for the exchange, then one launch
+            return self._gather(self.pipe.step)
+        a = self.arrays
+        if self.carried:
+            k = t % 10
+            if k == 0:  # a new 10-step run: seed u-bar^{T+1}, accumulators zero
+                drivers.regen_seed(a["u_b"], self.n, 10, 0, self.sl)
+                a["u_1_b"].zero_()
+                a["u_2_b"].zero_()
+                a["c_b"].zero_()
+            drivers.regen_state(a["u_1"], self.n, 9 - k, 0, self.R, self.sl)
+            if self.sl is None:  # u_2_b's zeroing after the rotation, fused
+                self._gather(lambda: api.adjoint_fresh_u2(self.family, self.n, self.scalars, a))
+                nl = 3
+            else:
+                nl = 2 + self._gather(lambda: drivers.adjoint_step(self.family, self.n,
+                                                                   self.scalars, a, self.sl))
+            # rotate: seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- 0
+            a["u_b"], a["u_1_b"], a["u_2_b"] = a["u_1_b"], a["u_2_b"], a["u_b"]
+            if self.sl is not None:  # the slab gather accumulates u_2_b
+                a["u_2_b"].zero_()
+            return nl
+        if self.regen:
+            if self.halo == "peer":
+                from paper_1907_02818_b200 import peer as peermod
+                peermod.step_sync()
+            self._regen(a, t)
+            if self.halo == "peer":
+                a["u_1_b"].zero_()
+                return 3 + self._gather(lambda: drivers.adjoint_step(
+                    self.family, self.n, self.scalars, a, self.sl, link=self.link))
+            if self.dtype == "f64":  # no fused fresh form for fp64: zero, accumulate
+                a["u_1_b"].zero_()
+                self._gather(lambda: api.adjoint(self.family, self.n, self.scalars, a))
+                return 3
+            self._gather(lambda: api.adjoint_fresh(self.family, self.n, self.scalars, a))
+            return 3
+        if self.halo == "peer":
+            from paper_1907_02818_b200 import peer as peermod
+            peermod.step_sync()
+            return self._gather(lambda: drivers.adjoint_step(self.family, self.n, self.scalars,
+                                                             a, self.sl, link=self.link))
+        self._gather(lambda: api.adjoint(self.family, self.n, self.scalars, a))
+        return 1
+
+    def verify(self):
+        """N > 1: one step of the chosen strategy against the exchange-then-
+        compute path on torch.distributed (same inputs, regenerated / static),
+        owned planes bitwise; all ranks agree.  Returns True / False."""
+        if self.world == 1 or self.carried:
+            return True
+        torch, api, drivers = self.torch, self.api, self.drivers
+        from paper_1907_02818_b200 import slab as slabmod
+        sl = self.sl
+        probe = gen_inputs(api, torch, self.family, self.n, sl, self.dtype)
+        if self.regen:
+            self._regen(probe, 0)
+        for k in ("c", "u_1", "u_b"):
+            own = slice(sl.own0 - sl.base, sl.own1 - sl.base)
+            keep = probe[k][own].clone()
+            probe[k].fill_(float("nan"))
+            probe[k][own] = keep
+        if self.dist.backend == "nccl":
+            slabmod.exchange_halos(sl, [probe[k] for k in ("c", "u_1", "u_b")])
+        else:  # gloo (tests: ranks sharing one GPU): exchange through host copies
+            host = [probe[k].cpu() for k in ("c", "u_1", "u_b")]
+            slabmod.exchange_halos(sl, host)
+            for k, h in zip(("c", "u_1", "u_b"), host):
+                probe[k].copy_(h)
+        snap = {k: self.arrays[k].clone() for k in ("c_b", "u_1_b")}
+        for k in snap:
+            probe[k] = snap[k].clone()
+        call = api.adjoint_slab_fresh if self.fresh else api.adjoint_slab
+        call(self.family, self.n, self.scalars, probe, sl.base, sl.nplanes, sl.own0, sl.own1)
+        t0 = self.t
+        self.step()  # the pipeline's step t0 (its inputs: step t0's)
+        torch.cuda.synchronize()
+        if self.regen and t0 != 0:
+            raise RuntimeError("verify() must run before any other step")
+        a0, a1 = sl.own0 - sl.base, sl.own1 - sl.base
+        ok = all(torch.equal(self.arrays[k][a0:a1], probe[k][a0:a1]) for k in snap)
+        del probe
+        return self.dist.all_ok(ok)
+
+    def close(self):
+        if self.pipe is not None:
+            self.pipe.close()
+        if self.plan is not None:
+            self.plan.close()
+
+    def points(self):
+        return float(self.n) ** self.d
+
+    def local_points(self):
+        return self.points() if self.sl is None else float(self.sl.owned) * self.n * self.n
+
+    def halo_text(self):
+        return halo_text(self.halo, self.world, self.carried)
+
+
+def halo_text(halo, world, carried):
+    if world == 1:
+        return None
+    if carried:
+        return ("torch.distributed NCCL exchange of the carried seed / state, interior "
+                "overlapped (drivers.adjoint_step)")
+    return {"ipc": "library z-slab plan (sgb_slab_*), CUDA-IPC transport: copy-engine "
+                   "pushes of the radius-R edge planes of u_1, u_b into the neighbours' "
+                   "halos over NVLink, device-side epoch flags; step t+1's regeneration "
+                   "+ exchange pipelined behind step t (double-buffered inputs)",
+            "nccl": "library z-slab plan (sgb_slab_*), NCCL transport: ncclSend/ncclRecv "
+                    "of the radius-R edge planes of u_1, u_b on the plan's comm stream; "
+                    "step t+1's exchange pipelined behind step t (double-buffered inputs)",
+            "torch": "torch.distributed NCCL batch_isend_irecv of u_1, u_b per step, "
+                     "pipelined one step ahead (drivers.HaloPrefetch)",
+            "peer": "fused: the kernel's TMA loads read the radius-R halo planes from the "
+                    "neighbours' arrays over NVLink (CUDA IPC)"}[halo]
+
+
+def time_workload(torch, wl, steps, warmup, dist, clocks=True):
+    """Warm-up, then EXACTLY `steps` steps bracketed by barrier + synchronize,
+    CUDA events on the launching stream around the whole region and around
+    each step's gather launch (the dominant kernel); max over ranks.  Returns
+    (ms_total, ms of the gather per step, launches, clock summary)."""
+    from paper_1907_02818_b200 import _lib
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        wl.step()
+    dist.barrier()
+    wl.kev = []
+    wl.record = True
+    l0 = _lib.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(torch.cuda.current_device()) if clocks else None
+    if clk:
+        clk.__enter__()
+    try:
+        start.record(stream)
+        for _ in range(steps):
+            wl.step()
+        end.record(stream)
+        dist.barrier()
+    finally:
+        wl.record = False
+        if clk:
+            clk.__exit__(None, None, None)
+    launches = _lib.launch_count() - l0
+    ms = start.elapsed_time(end)
+    kms = sum(a.elapsed_time(b) for a, b in wl.kev) / max(1, len(wl.kev))
+    ms, kms = dist.max(ms, kms)
+    return ms, kms, launches, (clk.summary() if clk else None)
+
+
 def run_ours(args, cfg):
     import torch
-    family, n_full, dtype, bpp, scalars, desc = cfg
-    n = args.n or n_full
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}")
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1907_02818_b200 import api, _lib, slab as slabmod
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    dist = Dist(torch, world, rank, local)
+    from paper_1907_02818_b200 import api, _lib
     _lib.lib()
-    d = DIMS[family]
-    R = RADIUS[family]
-    sl = None
-    if world > 1:
-        if d != 3:
-            raise SystemExit(f"{family} does not shard (replicas only); run with --gpus 1")
-        sl = slabmod.decompose(n, R, world, rank)
-    arrays = gen_inputs(api, torch, family, n, sl)
-    if sl is not None:
-        # c is static: exchange its halo once at setup (it is regenerated from
-        # global indices anyway; the exchange keeps the data path honest)
-        slabmod.exchange_halos(sl, [arrays["c"]])
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-
-    kev = []
-
-    from paper_1907_02818_b200 import drivers
-    regen = args.config == "5"  # cfg 5: forward state and seed regenerated per step
-    # cfg 2: carried reverse steps (drivers.run_carried), in runs of 10 as the
-    # BASELINE config states: state u_1 regenerated per step, seed <- u_1_b,
-    # u_1_b <- u_2_b, u_2_b <- 0 after each; every 10th step starts a new run
-    carried = args.config == "2"
-    tstep = [0]
-    halo_mode = "serial" if args.no_overlap else args.halo
-    overlap_sel = [halo_mode != "serial"]
-    link = None          # fused peer-memory halo (peer.py), radius-4 slabs only
-    peer_sel = [False]
-    if sl is not None and world > 1 and family == "wave3d_r4" and halo_mode in ("auto", "peer"):
-        from paper_1907_02818_b200 import peer as peermod
-        link = peermod.try_connect(sl, arrays)
-
-    pf_sel = [False]     # cross-step pipelined exchange (drivers.HaloPrefetch)
-    pf = [None]
-    if sl is not None and world > 1 and halo_mode in ("auto", "prefetch") and not carried:
-        def pf_regen(fs, t):
-            drivers.regen_state(fs["u_1"], n, t, 0, R, sl)
-            drivers.regen_seed(fs["u_b"], n, t, 0, sl)
-        pf[0] = drivers.HaloPrefetch(family, n, scalars, arrays, sl,
-                                     regen=pf_regen if regen else None, fresh=regen)
-
-    def step(record):
-        if pf_sel[0]:  # cfg 5: u_1_b zeroing fused into the gather (fresh)
-            if record:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-            nl = pf[0].step()
-            if record:
-                b.record(stream)
-                kev.append((a, b, nl))
-            return
-        if carried:
-            t = tstep[0]
-            tstep[0] += 1
-            k = t % 10
-            if k == 0:  # a new 10-step run: seed u-bar^{T+1}, accumulators zero
-                drivers.regen_seed(arrays["u_b"], n, 10, 0, sl)
-                arrays["u_1_b"].zero_()
-                arrays["u_2_b"].zero_()
-            drivers.regen_state(arrays["u_1"], n, 9 - k, 0, R, sl)
-        if regen:
-            if peer_sel[0]:  # neighbours finished reading the planes regen overwrites
-                peermod.step_sync()
-            t = tstep[0]
-            tstep[0] += 1
-            drivers.regen_state(arrays["u_1"], n, t, 0, R, sl)
-            drivers.regen_seed(arrays["u_b"], n, t, 0, sl)
-            if peer_sel[0]:  # the peer kernel accumulates: zero u_1_b first
-                arrays["u_1_b"].zero_()
-        if record:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-        if carried and sl is None:  # u_2_b's zeroing after the rotation, fused
-            api.adjoint_fresh_u2(family, n, scalars, arrays)
-            nl = 1
-        else:
-            # cfg 5: u_1_b = this step's adjoint, zeroing fused into the gather
-            nl = drivers.adjoint_step(family, n, scalars, arrays, sl, overlap=overlap_sel[0],
-                                      link=link if peer_sel[0] else None,
-                                      fresh=regen and not peer_sel[0])
-        if record:
-            b.record(stream)
-            kev.append((a, b, nl))
-        if carried:  # rotate: seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- 0
-            arrays["u_b"], arrays["u_1_b"], arrays["u_2_b"] = (arrays["u_1_b"], arrays["u_2_b"],
-                                                               arrays["u_b"])
-            if sl is not None:  # N > 1: the slab gather accumulates u_2_b
-                arrays["u_2_b"].zero_()
-
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        step(False)
-    barrier()
-    halo_probe = None
-    if sl is not None and world > 1 and halo_mode == "auto":
-        # Two ways to hide / pay the per-step halo exchange:
-        # overlapped = interior planes during the exchange, then the two edge
-        # bands (re-reads 2R planes per band); serial = exchange, then one launch.
-        # Which wins depends on the link and the slab depth, so time both here
-        # (max over ranks) and keep the faster for the timed steps.
-        probe = {}
-        if link is not None:
-            # the fused path must reproduce the exchange path bit for bit
-            # (same kernel arithmetic, halo planes from the neighbours' arrays)
-            snap = {k: arrays[k].clone() for k in ("c_b", "u_1_b")}
-            drivers.adjoint_step(family, n, scalars, arrays, sl, overlap=False)
-            want = {k: arrays[k].clone() for k in snap}
-            for k in snap:
-                arrays[k].copy_(snap[k])
-            drivers.adjoint_step(family, n, scalars, arrays, sl, link=link)
-            a0, a1 = sl.own0 - sl.base, sl.own1 - sl.base
-            same = all(torch.equal(arrays[k][a0:a1], want[k][a0:a1]) for k in snap)
-            for k in snap:
-                arrays[k].copy_(snap[k])
-            flag = torch.tensor([1 if same else 0], device="cuda", dtype=torch.int32)
-            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if int(flag[0]) == 0:
-                link.close()
-                link = None
-                probe["peer"] = "disabled: result differed from the exchange path"
-        if pf[0] is not None:
-            # the pipelined exchange must reproduce the exchange path bit for
-            # bit: step 0 of the pipeline vs the exchange path on its inputs
-            stream.wait_event(pf[0].ready[0])
-            snap = {k: arrays[k].clone() for k in ("c_b", "u_1_b", "u_1", "u_b")}
-            for k in ("u_1", "u_b"):
-                arrays[k].copy_(pf[0].sets[0][k])
-            drivers.adjoint_step(family, n, scalars, arrays, sl, overlap=False, fresh=regen)
-            want = {k: arrays[k].clone() for k in ("c_b", "u_1_b")}
-            for k in snap:
-                arrays[k].copy_(snap[k])
-            pf[0].step(0)
-            a0, a1 = sl.own0 - sl.base, sl.own1 - sl.base
-            same = all(torch.equal(arrays[k][a0:a1], want[k][a0:a1]) for k in want)
-            for k in ("c_b", "u_1_b"):
-                arrays[k].copy_(snap[k])
-            flag = torch.tensor([1 if same else 0], device="cuda", dtype=torch.int32)
-            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if int(flag[0]) == 0:
-                pf[0].close()
-                pf[0] = None
-                probe["prefetch"] = "disabled: result differed from the exchange path"
-        modes = [("overlapped", True, False, False),
-                 ("exchange_then_compute", False, False, False)]
-        if link is not None:
-            modes.append(("peer", False, True, False))
-        if pf[0] is not None:
-            modes.append(("prefetch", False, False, True))
-        for label, mode, use_peer, use_pf in modes:
-            overlap_sel[0] = mode
-            peer_sel[0] = use_peer
-            pf_sel[0] = use_pf
-            step(False)
-            barrier()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(5):
-                step(False)
-            b.record(stream)
-            barrier()
-            tt = torch.tensor([a.elapsed_time(b) / 5], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            probe[label] = float(tt[0])
-        timed = {k: v for k, v in probe.items() if isinstance(v, float)}
-        best = min(timed, key=timed.get)
-        overlap_sel[0] = best == "overlapped"
-        peer_sel[0] = best == "peer"
-        pf_sel[0] = best == "prefetch"
-        halo_probe = probe
-    elif link is not None and halo_mode == "peer":
-        peer_sel[0] = True
-    elif pf[0] is not None and halo_mode == "prefetch":
-        pf_sel[0] = True
-    if pf[0] is not None and not pf_sel[0]:
-        pf[0].close()
-        pf[0] = None
-    l0 = _lib.launch_count()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        start.record(stream)
-        for _ in range(args.steps):
-            step(True)
-        end.record(stream)
-        barrier()
-    launches = _lib.launch_count() - l0
-    ms = start.elapsed_time(end)
-    # per launch of the dominant kernel (at N = 1 one launch per step; with a
-    # slab the interior + edge launches of a step, exchange overlapped)
-    kms = sum(a.elapsed_time(b) for a, b, _ in kev) / len(kev)
-    t = torch.tensor([ms, kms], device="cuda", dtype=torch.float64)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, kms = float(t[0]), float(t[1])
-    pts = float(n) ** d
+    family, n_full, dtype, bpp0, scalars, desc = cfg
+    halo = args.halo
+    wl = Workload(torch, api, args.config, args.n, dist, halo)
+    n = wl.n
+    verified = wl.verify()
+    if not verified:
+        # the chosen exchange disagreed with the reference exchange path:
+        # measure the torch.distributed pipeline instead, and say so
+        wl.close()
+        del wl
+        torch.cuda.empty_cache()
+        wl = Workload(torch, api, args.config, args.n, dist, "torch")
+        wl.note = f"--halo {halo} failed the bitwise check against the exchange path"
+        halo = "torch"
+    ms, kms, launches, clocks = time_workload(torch, wl, args.steps, args.warmup, dist)
+    pts = wl.points()
     value = pts * args.steps / (ms / 1e3) / 1e9
-    # roofline of the dominant kernel (per launch, this rank's share)
-    local_pts = pts if sl is None else float(sl.owned) * n * n
-    if (regen and not peer_sel[0]) or (carried and sl is None):
-        bpp -= 4  # fresh u_1_b / u_2_b: written, not read (24 / 32 B/pt instead of 28 / 36)
-    achieved = bpp * local_pts / (kms / 1e3) / 1e9
+    # roofline of the dominant kernel: the gather launch of each step (its
+    # CUDA events on the launching stream), its algorithmic bytes on this rank
+    # (24 B/pt with the fused fresh u_1_b, 28 accumulating); the whole step's
+    # bytes (+ 8 B/pt of regenerated u_1 / u_b at cfg 5) per step time beside it
+    bpp = wl.bpp
+    achieved = bpp * wl.local_points() / (kms / 1e3) / 1e9
+    step_bpp = bpp + (8 if wl.regen else 0)
+    step_gbs = step_bpp * wl.local_points() * args.steps / (ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
-    traffic, tsrc = committed_traffic(family, n) if sl is None else (None, None)
+    traffic, tsrc = committed_traffic(family, n) if wl.sl is None else (None, None)
 
-    # ---- e2e through the host-buffer C-ABI entry (N = 1) or per-rank copies
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d)
+        e2e = run_e2e(args, torch, api, wl, dist)
 
-    ablation = None
-    if world == 1 and not args.no_ablation:
-        # GPU scatter-with-atomics adjoint on the same inputs (BASELINE cfg 5
-        # ablation; same algorithmic bytes as the gather form)
-        ms_sc = _time_launch(torch, lambda: api.scatter_adjoint(family, n, scalars, arrays),
-                             iters=5, warm=2)
-        ablation = {"scatter_atomic_ms": ms_sc, "scatter_GPts_s": pts / ms_sc / 1e6,
-                    "gather_kernel_ms": kms, "gather_speedup_vs_scatter": ms_sc / kms}
-        try:
-            ablation["boundary_strategies"] = boundary_ab(torch, family, n, scalars, arrays,
-                                                          dtype, kms)
-        except Exception as ex:  # pragma: no cover - report, never fail the bench
-            ablation["boundary_strategies"] = {"error": str(ex)[:300]}
-        if family == "wave3d_r4":
-            try:
-                ablation["time_loop_adjoint"] = time_loop_bench(torch, api, n, scalars, arrays)
-            except Exception as ex:  # pragma: no cover
-                ablation["time_loop_adjoint"] = {"error": str(ex)[:300]}
+    # the other scored configuration at the same N (cfg 4 beside cfg 5)
+    other = None
+    if not args.no_configs:
+        other_id = "4" if args.config == "5" else ("5" if args.config == "4" else None)
+        if other_id and not args.n:
+            wl.close()
+            del wl
+            torch.cuda.empty_cache()
+            wl2 = Workload(torch, api, other_id, 0, dist, halo)
+            oms, okms, _, _ = time_workload(torch, wl2, max(5, min(args.steps, 50)), 3, dist,
+                                            clocks=False)
+            opts = wl2.points()
+            other = {f"cfg{other_id}_steps_same_n_gpus": {
+                "workload": wl2.desc, "n_gpus": world, "ms_per_step": oms / max(5, min(args.steps, 50)),
+                "GPts_s": opts * max(5, min(args.steps, 50)) / (oms / 1e3) / 1e9,
+                "gather_ms": okms,
+                "gather_alg_GB_s_per_rank": wl2.bpp * wl2.local_points() / (okms / 1e3) / 1e9,
+                "halo_exchange": wl2.halo_text()}}
+            wl2.close()
+            del wl2
+            torch.cuda.empty_cache()
+            wl = None
     table = None
-    if world == 1 and not args.no_configs:
-        table = config_table(torch, api, peak, args.config)
-
+    ablation = None
+    fp64 = None
+    if world == 1:
+        if wl is None:
+            wl = Workload(torch, api, args.config, args.n, dist, halo)
+        if not args.no_ablation:
+            ablation = run_ablation(torch, api, wl, kms)
+        if not args.no_configs:
+            table = config_table(torch, api, peak, args.config)
+            if other:
+                table.update(other)
+        if family == "wave3d_r4" and not args.no_fp64:
+            wl.close()
+            wl = None
+            torch.cuda.empty_cache()
+            fp64 = run_fp64_row(args, torch, api, dist)
+    elif other:
+        table = other
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             cpu = time_cpu(family, scalars, n)
         except Exception as ex:  # pragma: no cover
             log("cpu baseline failed:", ex)
-    if rank != 0:
-        return
-    line = {
-        "metric": "adjoint GPts/s", "value": value, "unit": "GPts/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
-        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-        "config": {"workload": desc, "family": family, "n": n, "points_per_step": int(pts),
-                   "parallelism": f"zslab{world}" if world > 1 else "single",
-                   "algorithmic_bytes_per_point": bpp,
-                   "l2": "no flush: every step streams >= 12.7 GB (inputs >> 126 MB L2)"
-                   if family == "wave3d_r4" else "inputs larger than L2",
-                   "halo_exchange": ("NCCL batch_isend_irecv u_1,u_b radius-R per step on a "
-                                     "side stream, pipelined one step ahead (double-buffered "
-                                     "inputs; step t's exchange behind step t-1's compute), "
-                                     "then one launch over the owned planes"
-                                     if pf_sel[0] else
-                                     ("fused: the kernel's TMA loads read the radius-R halo "
-                                      "planes from the neighbours' arrays over NVLink (CUDA "
-                                      "IPC), stream-ordered NCCL sync per step")
-                                     if peer_sel[0] else
-                                     ("NCCL batch_isend_irecv u_1,u_b radius-R per step, " +
-                                      ("overlapped with the interior planes" if overlap_sel[0]
-                                       else "then one launch over the owned planes")))
-                   if world > 1 else None,
-                   "halo_probe_ms_per_step": halo_probe,
-                   "regenerated_per_step": "u_1, u_b (regen kernels inside the timed step); "
-                                           "u_1_b = the step's adjoint (zeroing fused into "
-                                           "the gather)"
-                   if args.config == "5" else
-                   ("carried runs of 10 reverse steps: u_1 regenerated per step, adjoints "
-                    "rotated (seed <- u_1_b <- u_2_b <- 0) inside the timed step"
-                    if carried else None)},
-        "achieved_hbm_gbs": achieved,
-        "clocks": clk.summary(),
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel_ms": kms, "bytes_per_launch": bpp * local_pts,
-                     "peak_source": peak_src, "traffic_source": tsrc,
-                     "vs_nominal_8tbs": achieved / 8000.0},
-        "cpu_baseline": cpu,
-        "ablation": ablation,
-        "other_configs": table,
-    }
-    print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    if rank == 0:
+        line = {
+            "metric": "adjoint GPts/s", "value": value, "unit": "GPts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": desc, "family": family, "n": n, "points_per_step": int(pts),
+                       "parallelism": f"zslab{world}" if world > 1 else "single",
+                       "algorithmic_bytes_per_point": bpp,
+                       "l2": "no flush: every step streams >= 3.7 GB per rank (inputs >> "
+                             "126 MB L2)" if family == "wave3d_r4" else "inputs larger than L2",
+                       "halo_exchange": halo_text(halo, world, args.config == "2"),
+                       "halo_check": ("bitwise equal to the exchange-then-compute path on "
+                                      "torch.distributed, every rank" if verified else
+                                      f"FAILED for --halo {args.halo}; fell back to torch")
+                       if world > 1 else None,
+                       "step": step_text(args.config)},
+            "achieved_hbm_gbs": achieved,
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel_ms": kms, "bytes_per_launch": bpp * (pts if world == 1 else
+                                                                      pts / world),
+                         "peak_source": peak_src, "traffic_source": tsrc,
+                         "vs_nominal_8tbs": achieved / 8000.0,
+                         "kernel": "the step's gather launch (CUDA events on its stream)",
+                         "step_alg_bytes_per_point": step_bpp, "step_GB_s_per_rank": step_gbs,
+                         "step_frac": step_gbs / peak},
+            "cpu_baseline": cpu,
+            "fp64": fp64,
+            "ablation": ablation,
+            "other_configs": table,
+        }
+        print(json.dumps(line), flush=True)
+    if wl is not None:
+        wl.close()
+    dist.close()
+
+
+def step_text(cfg_id):
+    return {"5": "regenerate u_1, u_b from (seed, step) on the owned planes, exchange their "
+                 "radius-4 halos (N > 1), gather with u_1_b = the step's adjoint (zeroing fused) "
+                 "and c_b accumulated; 100-step protocol, independent steps",
+            "4": "exchange the radius-4 halos of u_1, u_b (N > 1), accumulating gather",
+            "2": "carried runs of 10 reverse steps: u_1 regenerated per step, adjoints rotated "
+                 "(seed <- u_1_b <- u_2_b <- 0) inside the timed step",
+            "1": "one gather-adjoint call", "3": "one gather-adjoint call"}[cfg_id]
+
+
+def run_ablation(torch, api, wl, kms):
+    """GPU scatter-with-atomics adjoint on the same inputs (BASELINE cfg 5
+    ablation; same algorithmic bytes as the gather form) and the paper's
+    boundary strategies; the time-loop gradient."""
+    family, n, scalars, arrays = wl.family, wl.n, wl.scalars, wl.arrays
+    out = {}
+    try:
+        kg = _time_launch(torch, lambda: api.adjoint(family, n, scalars, arrays), iters=5, warm=2)
+        ms_sc = _time_launch(torch, lambda: api.scatter_adjoint(family, n, scalars, arrays),
+                             iters=5, warm=2)
+        out = {"scatter_atomic_ms": ms_sc, "scatter_GPts_s": wl.points() / ms_sc / 1e6,
+               "gather_kernel_ms": kg, "gather_speedup_vs_scatter": ms_sc / kg}
+        out["boundary_strategies"] = boundary_ab(torch, family, n, scalars, arrays, wl.dtype, kg)
+    except Exception as ex:  # pragma: no cover - report, never fail the bench
+        out["error"] = str(ex)[:300]
+    if family == "wave3d_r4":
+        try:
+            out["time_loop_adjoint"] = time_loop_bench(torch, api, n, scalars, arrays)
+        except Exception as ex:  # pragma: no cover
+            out["time_loop_adjoint"] = {"error": str(ex)[:300]}
+    return out
+
+
+def run_fp64_row(args, torch, api, dist):
+    """The same workload at the reference's precision (fp64; the reference has
+    no fp32 path), beside the fp64 reference arm: device value and e2e."""
+    try:
+        wl = Workload(torch, api, args.config, args.n, dist, None, dtype="f64")
+        steps = max(3, min(args.steps, 20))
+        ms, kms, _, _ = time_workload(torch, wl, steps, 3, dist, clocks=False)
+        out = {"dtype": "f64", "value": wl.points() * steps / (ms / 1e3) / 1e9,
+               "unit": "GPts/s", "ms_per_step": ms / steps, "steps": steps,
+               "gather_ms": kms, "gather_alg_GB_s": wl.bpp * wl.points() / (kms / 1e3) / 1e9,
+               "gather_algorithmic_bytes_per_point": wl.bpp,
+               "note": "same step as the headline in fp64 (fp32 inputs widened); no fused "
+                       "fresh form: u_1_b zeroed, then the accumulating gather"}
+        if not args.no_e2e:
+            out["e2e"] = run_e2e(args, torch, api, wl, dist)
+        wl.close()
+        del wl
+        torch.cuda.empty_cache()
+        return out
+    except Exception as ex:  # pragma: no cover
+        return {"error": str(ex)[:300]}
 
 
 def _time_launch(torch, fn, iters=10, warm=3):
@@ -829,42 +1034,70 @@ def time_loop_bench(torch, api, n, scalars, arrays, T=16, K=4):
             "note": "alg bytes count the primal and fused reverse-step kernels only"}
 
 
-def run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d):
+def run_e2e(args, torch, api, wl, dist):
+    """The headline metric end to end through the host-facing entry: pinned
+    host arrays in, H2D + (N > 1: the halo exchange) + the accumulating gather
+    + D2H of the adjoints inside the timed region, every step.
+    N = 1: sgb_plan_run_adjoint_host (the host-buffer C-ABI call, H2D /
+    kernel / D2H pipelined over i-chunks).  N > 1: each rank copies its OWNED
+    planes in, the library's z-slab plan exchanges the c / u_1 / u_b halos
+    (sgb_slab_halo_start), one launch over the owned planes, the owned planes
+    of the adjoints come back."""
+    family, n, scalars, sl = wl.family, wl.n, wl.scalars, wl.sl
     names = api.array_params(family, "adjoint")
     rmw = [nm for nm in names if nm.endswith("_b") and nm != SEED[family]]
+    arrays = wl.arrays
     host = {nm: torch.empty(arrays[nm].shape, dtype=arrays[nm].dtype, pin_memory=True)
             for nm in names}
     for nm in names:
         host[nm].copy_(arrays[nm])
-    h2d = sum(host[nm].numel() * host[nm].element_size() for nm in names)
-    d2h = sum(host[nm].numel() * host[nm].element_size() for nm in rmw)
-    if sl is not None:  # only the owned planes of the adjoints come back
-        d2h = d2h * (sl.own1 - sl.own0) // sl.nplanes
+    esz = arrays[names[0]].element_size()
     torch.cuda.synchronize()
-    # the host-buffer plan: full grid at N = 1; per rank a z-slab plan whose
-    # host arrays hold the local planes incl. halos (a solver's host slab),
-    # H2D / kernel / D2H pipelined over i-chunks
-    plan = api.Plan(family, n, "f32" if host[names[0]].dtype == torch.float32 else "f64",
-                    slab=sl)
-
-    def step():
-        plan.run_adjoint_host(scalars, host)
-    step()
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
     k = max(1, args.e2e_steps)
+    plan = None
+    if sl is None:
+        h2d = sum(host[nm].numel() * esz for nm in names)
+        d2h = sum(host[nm].numel() * esz for nm in rmw)
+        hp = api.Plan(family, n, "f32" if esz == 4 else "f64")
+
+        def step():
+            hp.run_adjoint_host(scalars, host)
+        path = "sgb_plan_run_adjoint_host (pinned host buffers, H2D / kernel / D2H " \
+               "pipelined over i-chunks)"
+    else:
+        from paper_1907_02818_b200 import slab as slabmod
+        dev = {nm: torch.zeros_like(arrays[nm]) for nm in names}
+        transport = wl.halo if wl.halo in ("ipc", "nccl") else "ipc"
+        plan = slabmod.SlabPlan(family, n, dev, wl.rank, wl.world, transport).connect()
+        own = slice(sl.own0 - sl.base, sl.own1 - sl.base)
+        plane = n * n * esz
+        h2d = len(names) * sl.owned * plane
+        d2h = len(rmw) * sl.owned * plane
+
+        def step():
+            for nm in names:
+                dev[nm][own].copy_(host[nm][own], non_blocking=True)
+            plan.halo_start(("c", "u_1", "u_b"))
+            plan.step(scalars, exchanged=True)
+            for nm in rmw:
+                host[nm][own].copy_(dev[nm][own], non_blocking=True)
+        path = (f"per rank: H2D of the owned planes, library z-slab plan halo exchange of "
+                f"c, u_1, u_b ({transport}), one launch, D2H of the owned planes of "
+                + ", ".join(rmw))
+    step()
+    dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(k):
         step()
     e.record()
     torch.cuda.synchronize()
-    ms = torch.tensor([s.elapsed_time(e)], device="cuda", dtype=torch.float64)
-    if dist is not None:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms[0]) / k
-    plan.close()
+    ms = dist.max(s.elapsed_time(e))[0] / k
+    if plan is not None:
+        plan.close()
+        del dev
+    else:
+        hp.close()
     # the bound this path runs into: this box's pinned PCIe copy bandwidth
     nm0 = names[0]
     hb, db = host[nm0].view(-1), arrays[nm0].view(-1)
@@ -881,37 +1114,13 @@ def run_e2e(args, torch, api, family, n, scalars, arrays, sl, dist, pts, d):
     h2d_gbs = copy_gbs(db, hb)
     d2h_gbs = copy_gbs(hb, db)
     floor_ms = max(h2d / 1e9 / h2d_gbs, d2h / 1e9 / d2h_gbs) * 1e3
-    # the same step's copies with both directions in flight at once (no
-    # kernel): PCIe is full duplex, but the D2H traffic slows the H2D side
-    # (~7% here), so this -- not the one-way figure -- is what a pipelined
-    # step can reach
-    dev = {nm: torch.empty_like(arrays[nm]) for nm in names}
-    side = torch.cuda.Stream()
-
-    def copies():
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            for nm in rmw:
-                host[nm].copy_(dev[nm], non_blocking=True)
-        for nm in names:
-            dev[nm].copy_(host[nm], non_blocking=True)
-        torch.cuda.current_stream().wait_stream(side)
-    copies()
-    torch.cuda.synchronize()
-    s.record()
-    copies()
-    e.record()
-    torch.cuda.synchronize()
-    both_ms = s.elapsed_time(e)
-    del dev
-    return {"value": pts / (ms / 1e3) / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k,
-            "pcie_h2d_GBps": h2d_gbs, "pcie_d2h_GBps": d2h_gbs,
-            "copy_floor_ms": floor_ms, "frac_of_copy_floor": floor_ms / ms,
-            "copy_floor_concurrent_ms": both_ms, "frac_of_concurrent_copy_floor": both_ms / ms,
-            "path": "sgb_plan_run_adjoint_host (pinned host buffers)" if sl is None
-            else "per-rank sgb_plan_create_slab + run_adjoint_host (pinned local planes incl. "
-                 "halos; owned planes returned)"}
+    del host
+    return {"value": wl.points() / (ms / 1e3) / 1e9, "unit": "GPts/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "steps": k, "pcie_h2d_GBps": h2d_gbs, "pcie_d2h_GBps": d2h_gbs,
+            "copy_floor_ms": floor_ms, "frac_of_copy_floor": floor_ms / ms, "path": path,
+            "note": "e2e runs the accumulating gather of the reference ABI (<name>_b) on the "
+                    "host-held inputs; per-step regeneration is a device-side protocol detail"}
 
 
 def main():
@@ -920,16 +1129,19 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="4", choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=0, help="override grid extent")
+    ap.add_argument("--config", default="5", choices=sorted(CONFIGS))
+    ap.add_argument("--size", "--n", dest="n", type=int, default=0,
+                    help="override grid extent (--size under torchrun, whose own parser "
+                         "claims --n...)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-overlap", action="store_true", help="exchange, then compute")
-    ap.add_argument("--halo", default="auto",
-                    choices=["auto", "overlap", "serial", "peer", "prefetch"],
-                    help="N>1 halo strategy: auto = time each after warm-up, keep the fastest "
-                         "(peer only if it reproduces the exchange path bitwise)")
+    ap.add_argument("--halo", default="ipc", choices=["ipc", "nccl", "torch", "peer"],
+                    help="N>1 halo exchange: the library's z-slab plan with the CUDA-IPC "
+                         "copy-engine (default) or NCCL transport, torch.distributed NCCL, or "
+                         "the fused peer-memory halo; checked bitwise against the "
+                         "exchange-then-compute path before timing")
+    ap.add_argument("--no-fp64", action="store_true")
     ap.add_argument("--no-ablation", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
     args = ap.parse_args()

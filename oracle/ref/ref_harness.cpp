@@ -20,6 +20,15 @@
 //   canon  <spec>                             the program's canonical text
 //                                             (b200_program_text), exported as
 //                                             paper_1907_02818_b200/programs/<name>.canon
+//   timeloop <spec> <n> <T> <in_dir> <out_dir> S=v
+//                                             the adjoint of a whole time loop
+//                                             u^{t+1} = F(u^t, u^{t-1}), J = <w, u^T>,
+//                                             composed from the reference's own
+//                                             run_nest (forward) and run_program
+//                                             (reverse, interp.cpp:183-198); <spec>
+//                                             must have u_2 active (adjoint u_2_b);
+//                                             reads c, u0, u1, w; writes u0_b, u1_b,
+//                                             c_b (the pin of drivers.time_loop_adjoint)
 //   match  <spec>                             the family the B200 library's
 //                                             sgb_program_family() assigns to the
 //                                             program (no GPU needed), JSON
@@ -275,6 +284,68 @@ static int cmd_run(const sg::Problem& p, long long n, const std::string& in_dir,
   return 0;
 }
 
+static int cmd_timeloop(const sg::Problem& p, long long n, int T, const std::string& in_dir,
+                        const std::string& out_dir, int argc, char** argv) {
+  if (T < 2) throw sg::Error("timeloop needs T >= 2");
+  std::map<std::string, long long> sz{{"n", n}};
+  const sg::ArrayDecl& out = sg::output_array(p);
+  const std::string seed = out.adjoint;
+  const sg::ArrayDecl* u1d = sg::find_array(p, "u_1");
+  const sg::ArrayDecl* u2d = sg::find_array(p, "u_2");
+  const sg::ArrayDecl* cd = sg::find_array(p, "c");
+  if (!u1d || !u2d || !cd || !u2d->active || !u1d->active || !cd->active)
+    throw sg::Error("timeloop: c, u_1, u_2 must be active arrays");
+  const auto shape = shape_of(*u1d, sz);
+  sg::Env base;
+  base.sizes = sz;
+  for (const auto& s : p.scalars) base.scalars[s] = 0.0;
+  for (int a = 0; a < argc; a++) {
+    std::string kv = argv[a];
+    auto eq = kv.find('=');
+    base.scalars[kv.substr(0, eq)] = std::strtod(kv.c_str() + eq + 1, nullptr);
+  }
+  sg::DenseGrid c(shape), w(shape);
+  read_grid(in_dir + "/c.f64", c);
+  read_grid(in_dir + "/w.f64", w);
+  std::vector<sg::DenseGrid> u(T + 1, sg::DenseGrid(shape));
+  read_grid(in_dir + "/u0.f64", u[0]);
+  read_grid(in_dir + "/u1.f64", u[1]);
+  // forward: u^{t+1} = run_nest(primal)(c, u_1 = u^t, u_2 = u^{t-1}), u zero-initialised
+  for (int t = 1; t < T; t++) {
+    sg::Env e = base;
+    e.grids["c"] = c;
+    e.grids["u_1"] = u[t];
+    e.grids["u_2"] = u[t - 1];
+    e.grids[out.name] = sg::DenseGrid(shape);
+    u[t + 1] = sg::run_nest(p.nest, e).grids.at(out.name);
+  }
+  // reverse: seed u-bar^{t+1}; accumulate u-bar^t (u_1_b), u-bar^{t-1} (u_2_b), c_b
+  const auto prog = sg::assemble_adjoint(p);
+  std::vector<sg::DenseGrid> ub(T + 1, sg::DenseGrid(shape));
+  ub[T] = w;
+  sg::DenseGrid cb(shape);
+  for (int t = T - 1; t >= 1; t--) {
+    sg::Env e = base;
+    e.grids["c"] = c;
+    e.grids["u_1"] = u[t];
+    e.grids["u_2"] = u[t - 1];
+    e.grids[out.name] = sg::DenseGrid(shape);
+    e.grids[seed] = ub[t + 1];
+    e.grids[u1d->adjoint] = ub[t];
+    e.grids[u2d->adjoint] = ub[t - 1];
+    e.grids[cd->adjoint] = cb;
+    sg::Env r = sg::run_program(prog, e);
+    ub[t] = r.grids.at(u1d->adjoint);
+    ub[t - 1] = r.grids.at(u2d->adjoint);
+    cb = r.grids.at(cd->adjoint);
+  }
+  write_grid(out_dir + "/u0_b.f64", ub[0]);
+  write_grid(out_dir + "/u1_b.f64", ub[1]);
+  write_grid(out_dir + "/c_b.f64", cb);
+  write_grid(out_dir + "/uT.f64", u[T]);
+  return 0;
+}
+
 static int cmd_verify(const sg::Problem& p, long long n, unsigned long long seed, int trials) {
   auto rep = sg::verify_problem(p, {{"n", n}}, seed, trials, true);
   std::cout << rep.json_text();
@@ -318,6 +389,9 @@ int main(int argc, char** argv) {
       return 0;
     }
     if (cmd == "b200" && argc >= 5) return cmd_b200(p, std::atoll(argv[3]), argv[4], argc - 5, argv + 5);
+    if (cmd == "timeloop" && argc >= 7)
+      return cmd_timeloop(p, std::atoll(argv[3]), std::atoi(argv[4]), argv[5], argv[6], argc - 7,
+                          argv + 7);
     if (cmd == "canon") {
       std::cout << sg::b200_program_text(sg::assemble_adjoint(p));
       return 0;

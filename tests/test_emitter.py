@@ -17,7 +17,7 @@ from tests.fuzz_problems import random_spec
 
 NAMES = ["lap1d", "wave3d", "burgers1d", "wave1d", "wave3d_c", "wave3d_c2", "burgers2d",
          "wave3d_r4"]
-FUZZ = list(range(30))
+FUZZ = list(range(50))  # SPEC.md:475 asks for >= 50 fuzzed problems
 
 needs_ref = pytest.mark.skipif(not oracle.ref_available(),
                                reason="oracle/_ref/ref_harness not built")
