@@ -528,11 +528,9 @@ class Workload:
             own = slice(sl.own0 - sl.base, sl.own1 - sl.base)
             o = slabmod.Slab(self.n, self.R, sl.rank, sl.world, sl.own0, sl.own1, sl.own0,
                              sl.owned)
-            self.drivers.regen_state(arrs["u_1"][own], self.n, t, 0, self.R, o)
-            self.drivers.regen_seed(arrs["u_b"][own], self.n, t, 0, o)
+            self.drivers.regen_step(arrs["u_1"][own], arrs["u_b"][own], self.n, t, 0, self.R, o)
         else:
-            self.drivers.regen_state(arrs["u_1"], self.n, t, 0, self.R)
-            self.drivers.regen_seed(arrs["u_b"], self.n, t, 0)
+            self.drivers.regen_step(arrs["u_1"], arrs["u_b"], self.n, t, 0, self.R)
 
     def _setup_multi(self, halo):
         torch, drivers = self.torch, self.drivers

@@ -294,6 +294,15 @@ int sgb_fill_normal3d_f32(float* dst, int n, int i_base, int nplanes, int halo, 
  * see exactly the fp32 inputs) */
 int sgb_fill_normal3d_f64(double* dst, int n, int i_base, int nplanes, int halo, uint64_t seed,
                           uint64_t stream_id, double mean, double scale, sgb_stream_t stream);
+/* two fields in one pass (cfg 5 regenerates u_1 and the seed every step):
+ * bitwise the values of sgb_fill_normal3d_* (a, halo_a, stream_a) and
+ * (b, halo_b, stream_b) over the same planes */
+int sgb_fill_normal3d_pair_f32(float* a, int halo_a, uint64_t stream_a, float* b, int halo_b,
+                               uint64_t stream_b, int n, int i_base, int nplanes, uint64_t seed,
+                               double mean, double scale, sgb_stream_t stream);
+int sgb_fill_normal3d_pair_f64(double* a, int halo_a, uint64_t stream_a, double* b, int halo_b,
+                               uint64_t stream_b, int n, int i_base, int nplanes, uint64_t seed,
+                               double mean, double scale, sgb_stream_t stream);
 /* zero the h-point shell of planes [i_base, i_base+nplanes) of an n^d grid
  * (d = 1, 2 or 3; for d < 3 pass i_base = 0, nplanes = n) */
 int sgb_zero_halo_f32(float* a, int d, int n, int h, int i_base, int nplanes,

@@ -302,6 +302,32 @@ def _ref_params(name: str, fn: str):
 _ref_libs = {}
 
 
+def emitted_or_port(name: str):
+    """(call, label): the reference's own compiled emitted adjoint when
+    oracle/_ref holds it (ref_emitted), else the pinned C restatement's OpenMP
+    run_program (sg_run_program_omp, pinned to the reference's outputs by
+    tests/test_oracle_pins.py) behind the same call(n, scalars, arrays)
+    interface.  The radius-4 emitted adjoint is a ~12 min build (make -C
+    oracle/ref ref_r4), so a fresh build container may lack it; parity is then
+    anchored on the port, and the label says which oracle ran."""
+    if ref_emitted_available(name):
+        return ref_emitted(name), (f"reference emitted {name}_b (codegen.cpp:332-382), gcc "
+                                   f"{ref_emitted_opt(name)} -fopenmp, fp64")
+    f = family(name)
+
+    def view(a):
+        return a.numpy() if hasattr(a, "numpy") else a
+
+    def call(n, scalars, arrays):
+        grids = {a: view(arrays[a]) for a in f.arrays if a in arrays}
+        adjs = {b: view(arrays[b]) for b in f.adjoints if b and b in arrays}
+        rc = run_program_omp(name, n, scalars, grids, adjs)
+        return 0 if rc >= 1 else 1
+    return call, (f"oracle port sg_run_program_omp (restates interp.cpp:189-198; pinned to "
+                  f"the reference by tests/test_oracle_pins.py), fp64 -- "
+                  f"oracle/_ref/libref_{name}.so not built here")
+
+
 def ref_emitted(name: str, kind: str = "adjoint"):
     """The reference's OWN generated OpenMP function (emit_primal /
     emit_adjoint / emit_scatter_adjoint, codegen.cpp:311-434, compiled by

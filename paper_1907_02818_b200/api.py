@@ -42,7 +42,13 @@ def _sfx(dtype) -> str:
 def function_name(family: str, kind: str, dtype) -> str:
     if family not in FAMILIES:
         raise _lib.StencilError(f"unsupported stencil family '{family}'")
-    return f"{family}{_SUFFIX[kind]}_{_sfx(dtype)}"
+    if kind not in _SUFFIX:
+        raise _lib.StencilError(f"unknown entry kind '{kind}'")
+    name = f"{family}{_SUFFIX[kind]}_{_sfx(dtype)}"
+    if name not in _lib.PROTOTYPES:
+        raise _lib.StencilError(f"no entry point {name} in stencilgrad_b200.h "
+                                f"('{kind}' is not provided for {family} in this precision)")
+    return name
 
 
 def array_params(family: str, kind: str, dtype="f32"):
@@ -151,6 +157,22 @@ def fill_normal3d(t, n: int, halo: int, seed: int, stream_id: int, i_base: int =
     _lib.check(fn(ctypes.c_void_p(t.data_ptr()), n, i_base, n if nplanes is None else nplanes,
                   halo, int(seed), int(stream_id), float(mean), float(scale),
                   _stream_ptr(stream)), "fill_normal3d")
+
+
+def fill_normal3d_pair(a, halo_a: int, stream_a: int, b, halo_b: int, stream_b: int, n: int,
+                       seed: int, i_base: int = 0, nplanes: int | None = None,
+                       mean: float = 0.0, scale: float = 1.0, stream=None):
+    """Two fields in one pass: bitwise fill_normal3d(a, n, halo_a, seed,
+    stream_a, ...) and fill_normal3d(b, n, halo_b, seed, stream_b, ...)."""
+    import torch
+    if a.dtype != b.dtype:
+        raise _lib.StencilError("fill_normal3d_pair: both fields must share one dtype")
+    fn = _lib.lib().sgb_fill_normal3d_pair_f32 if a.dtype == torch.float32 else \
+        _lib.lib().sgb_fill_normal3d_pair_f64
+    _lib.check(fn(ctypes.c_void_p(a.data_ptr()), int(halo_a), int(stream_a),
+                  ctypes.c_void_p(b.data_ptr()), int(halo_b), int(stream_b), n, i_base,
+                  n if nplanes is None else nplanes, int(seed), float(mean), float(scale),
+                  _stream_ptr(stream)), "fill_normal3d_pair")
 
 
 def zero_halo(t, d: int, n: int, h: int, i_base: int = 0, nplanes: int | None = None,

@@ -300,8 +300,11 @@ static int star3_c_fresh_u2(const char* name, int n, double D, float* c, float* 
   if (!guard_ok(MODE == 0 ? WAVE3D_C : WAVE3D_C2, n)) return SGB_GUARD;
   if (!c || !c_b || !u_1 || !u_1_b || !u_2_b || !u_b)
     return einval(std::string(name) + ": null array");
+  // the fused U2SET form exists in the v1 kernel only: a forced radius-4
+  // design (SGB_STAR_KERNEL=7) takes the zero-then-accumulate form below, so
+  // this entry stays bitwise equal to adjoint() under every kernel choice
   if (star3_tma_ok<MODE, float>(n, {c, c_b, u_1, u_1_b, u_2_b, u_b}) &&
-      !opt_flag(OPT_FRESH_UNFUSED))
+      !opt_flag(OPT_FRESH_UNFUSED) && star_kernel_version(MODE) != 7)
   {
     if (opt(OPT_R1_FP64ACC, 1))
       return star3_tma_gather<MODE, true, true>(Slab3{n, 0, n}, 1, n - 2, 0, n, D, c, c_b,

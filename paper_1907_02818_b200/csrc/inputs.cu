@@ -8,7 +8,7 @@
 
 namespace sgb {
 
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // splitmix64 finaliser
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // splitmix64 finaliser
   x ^= x >> 30;
   x *= 0xBF58476D1CE4E5B9ull;
   x ^= x >> 27;
@@ -17,7 +17,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // splitmix64 finaliser
   return x;
 }
 
-__device__ __forceinline__ uint64_t hash_key(uint64_t seed, uint64_t stream) {
+__host__ __device__ __forceinline__ uint64_t hash_key(uint64_t seed, uint64_t stream) {
   return seed * 0x9E3779B97F4A7C15ull + mix64(stream + 0xD1B54A32D192ED03ull);
 }
 __device__ __forceinline__ uint64_t hash3(uint64_t seed, uint64_t stream, uint64_t ctr) {
@@ -34,24 +34,37 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {  // murmur3 finaliser
 }
 
 // One Box-Muller pair from the hash of pair index m: (cos branch, sin branch)
-// = the values of flat indices 2m and 2m+1.  32-bit hashing (two chained
-// murmur3 finalisers keyed by the 64-bit stream key) and the MUFU
-// approximations (flush-to-zero lg2 / sqrt / sin / cos; the angle taken in
-// [-pi, pi), where sin.approx / cos.approx are accurate): the generator runs
-// inside cfg 5's timed step, where the 64-bit splitmix + IEEE form was
-// issue-bound (profiles/).
-__device__ __forceinline__ float2 normal_pair(uint64_t key, uint64_t m) {
+// = the values of flat indices 2m and 2m+1.  Built for the XU (MUFU) pipe
+// and issue rate, since the generator runs inside cfg 5's timed step (the
+// 64-bit splitmix + IEEE form was issue-bound, then the two-murmur3 form
+// MUFU/I2F-throttled at ~33 instructions per value, profiles/):
+//   * one murmur3 finaliser per pair, keyed by the 64-bit stream key; the
+//     angle's bits are its Fibonacci-lattice partner a * 0x9E3779B9 (an odd
+//     multiplier: a permutation of a, whose top 23 bits are equidistributed
+//     against a's -- the 2D golden-ratio lattice, sampled at hashed points);
+//   * uniforms from the mantissa bits (OR into an exponent, one FADD)
+//     instead of I2F conversions, which share the XU pipe with MUFU;
+//   * MUFU lg2 / sqrt / sin / cos (flush-to-zero approximations; the angle in
+//     [-pi, pi), where sin.approx / cos.approx are accurate): 2 XU ops per value.
+struct NormalPair {
+  float rad, cs, sn;  // value(2m) = rad * cs, value(2m+1) = rad * sn
+};
+__device__ __forceinline__ NormalPair normal_pair_polar(uint64_t key, uint64_t m) {
   const uint32_t a = fmix32((uint32_t)m ^ (uint32_t)key ^ ((uint32_t)(m >> 32) * 0x9E3779B9u));
-  const uint32_t b = fmix32(a ^ (uint32_t)(key >> 32));
-  const float u1 = ((float)(a >> 8) + 1.0f) * 0x1.0p-24f;                      // (0, 1]
-  const float th = fmaf((float)(b >> 8), 6.283185307179586f * 0x1.0p-24f,
-                        -3.141592653589793f);                                  // [-pi, pi)
+  const uint32_t b = (a ^ (uint32_t)(key >> 32)) * 0x9E3779B9u;
+  const float u1 = 2.0f - __uint_as_float((a >> 9) | 0x3F800000u);            // (0, 1]
+  const float th = fmaf(__uint_as_float((b >> 9) | 0x40000000u), 3.14159265358979f,
+                        -9.42477796076938f);                                   // [-pi, pi)
   float l2, rad, sn, cs;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u1));
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rad) : "f"(-1.3862943611198906f * l2));  // -2 ln u1
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(sn) : "f"(th));
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(cs) : "f"(th));
-  return make_float2(rad * cs, rad * sn);
+  return NormalPair{rad, cs, sn};
+}
+__device__ __forceinline__ float2 normal_pair(uint64_t key, uint64_t m) {
+  const NormalPair p = normal_pair_polar(key, m);
+  return make_float2(p.rad * p.cs, p.rad * p.sn);
 }
 
 // kind 0: N(mean, scale^2); kind 1: U[mean, mean + scale).
@@ -98,21 +111,17 @@ __global__ void fill_normal3d_kernel(T* dst, int n, int i_base, int nplanes, int
     const int i = i_base + li;
     const bool rowh = jh || i < h || i >= n - h;
     float v[4];
-    if (!rowh && kin && (g & 1) == 0) {  // no halo point: plain draws
-      const float2 a = normal_pair(key, (uint64_t)g >> 1);
-      const float2 b = normal_pair(key, ((uint64_t)g >> 1) + 1);
-      v[0] = mean + scale * a.x;
-      v[1] = mean + scale * a.y;
-      v[2] = mean + scale * b.x;
-      v[3] = mean + scale * b.y;
-    } else if ((g & 1) == 0 && k + 3 < n) {
-      const float2 a = normal_pair(key, (uint64_t)g >> 1);
-      const float2 b = normal_pair(key, ((uint64_t)g >> 1) + 1);
-      const float z[4] = {a.x, a.y, b.x, b.y};
+    if ((g & 1) == 0 && k + 3 < n) {  // two whole pairs
+      const NormalPair a = normal_pair_polar(key, (uint64_t)g >> 1);
+      const NormalPair b = normal_pair_polar(key, ((uint64_t)g >> 1) + 1);
+      // fmaf(scale * rad, cos|sin, mean): the pair kernel's formula (bitwise
+      // equal values; = rad * cos|sin, the draw() value, at mean 0, scale 1)
+      const float z[4] = {fmaf(scale * a.rad, a.cs, mean), fmaf(scale * a.rad, a.sn, mean),
+                          fmaf(scale * b.rad, b.cs, mean), fmaf(scale * b.rad, b.sn, mean)};
 #pragma unroll
       for (int m = 0; m < 4; m++) {
         const int kk = k + m;
-        v[m] = (rowh || kk < h || kk >= n - h) ? 0.f : mean + scale * z[m];
+        v[m] = (rowh || kk < h || kk >= n - h) ? 0.f : z[m];
       }
     } else {
 #pragma unroll
@@ -132,6 +141,63 @@ __global__ void fill_normal3d_kernel(T* dst, int n, int i_base, int nplanes, int
       }
     } else {
       for (int m = 0; m < 4 && k + m < n; m++) p[m] = v[m];
+    }
+  }
+}
+
+// Two fields of one step in ONE pass (cfg 5 regenerates u_1 and the seed u_b
+// every step): fields f = 0, 1 with their own stream key and zero shell h_f,
+// N(mean, scale^2) elsewhere -- bitwise the values of two fill_normal3d calls
+// (value(2m) = mean + scale * rad * cs is evaluated as fmaf(scale * rad, cs,
+// mean) there too).  Fast-path shapes only: n % 4 == 0 (so a thread's 4
+// consecutive k are two whole Box-Muller pairs) and 16-byte aligned arrays;
+// the entry falls back to two fill_normal3d_kernel launches otherwise.  Each
+// thread owns 4 consecutive k of one row of both fields and strides over
+// planes: 8 values, 4 pairs in flight, two 16-byte (fp32) stores per plane.
+template <typename T>
+__global__ void __launch_bounds__(128) fill_normal3d_pair_kernel(
+    T* __restrict__ d0, T* __restrict__ d1, int n, int i_base, int nplanes, int h0, int h1,
+    uint64_t key0, uint64_t key1, float mean, float scale) {
+  const int k = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int j = blockIdx.y;
+  if (k >= n) return;
+  // plane-independent parts of the zero-shell masks: bit m = point k+m inside
+  uint32_t km0 = 0, km1 = 0;
+#pragma unroll
+  for (int m = 0; m < 4; m++) {
+    if (k + m >= h0 && k + m < n - h0) km0 |= 1u << m;
+    if (k + m >= h1 && k + m < n - h1) km1 |= 1u << m;
+  }
+  const bool j0h = j < h0 || j >= n - h0, j1h = j < h1 || j >= n - h1;
+  const long long plane = (long long)n * n;
+  const long long dg = (long long)gridDim.z * plane;
+  long long g = ((long long)(i_base + (int)blockIdx.z) * n + j) * n + k;  // global flat index
+  long long off = ((long long)blockIdx.z * n + j) * n + k;
+  for (int li = blockIdx.z; li < nplanes; li += gridDim.z, g += dg, off += dg) {
+    const int i = i_base + li;
+    const uint64_t m = (uint64_t)g >> 1;
+    const NormalPair a0 = normal_pair_polar(key0, m), b0 = normal_pair_polar(key0, m + 1);
+    const NormalPair a1 = normal_pair_polar(key1, m), b1 = normal_pair_polar(key1, m + 1);
+    const float z0[4] = {fmaf(scale * a0.rad, a0.cs, mean), fmaf(scale * a0.rad, a0.sn, mean),
+                         fmaf(scale * b0.rad, b0.cs, mean), fmaf(scale * b0.rad, b0.sn, mean)};
+    const float z1[4] = {fmaf(scale * a1.rad, a1.cs, mean), fmaf(scale * a1.rad, a1.sn, mean),
+                         fmaf(scale * b1.rad, b1.cs, mean), fmaf(scale * b1.rad, b1.sn, mean)};
+    const uint32_t m0 = (j0h || i < h0 || i >= n - h0) ? 0u : km0;
+    const uint32_t m1 = (j1h || i < h1 || i >= n - h1) ? 0u : km1;
+    float v0[4], v1[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      v0[q] = (m0 >> q) & 1 ? z0[q] : 0.f;
+      v1[q] = (m1 >> q) & 1 ? z1[q] : 0.f;
+    }
+    if constexpr (sizeof(T) == 4) {
+      __stcs(reinterpret_cast<float4*>(d0 + off), make_float4(v0[0], v0[1], v0[2], v0[3]));
+      __stcs(reinterpret_cast<float4*>(d1 + off), make_float4(v1[0], v1[1], v1[2], v1[3]));
+    } else {
+      __stcs(reinterpret_cast<double2*>(d0 + off), make_double2(v0[0], v0[1]));
+      __stcs(reinterpret_cast<double2*>(d0 + off + 2), make_double2(v0[2], v0[3]));
+      __stcs(reinterpret_cast<double2*>(d1 + off), make_double2(v1[0], v1[1]));
+      __stcs(reinterpret_cast<double2*>(d1 + off + 2), make_double2(v1[2], v1[3]));
     }
   }
 }
@@ -245,6 +311,40 @@ static unsigned fill_grid(long long count) {
   return (unsigned)(g < 1 ? 1 : g);
 }
 
+template <typename T>
+static int fill_normal3d_pair(const char* name, T* a, int halo_a, uint64_t stream_a, T* b,
+                              int halo_b, uint64_t stream_b, int n, int i_base, int nplanes,
+                              uint64_t seed, double mean, double scale, cudaStream_t s) {
+  if (!a || !b || a == b || n <= 0 || nplanes <= 0 || halo_a < 0 || halo_b < 0 ||
+      n > (1 << 20))
+  {
+    set_error(std::string(name) + ": bad arguments");
+    return SGB_EINVAL;
+  }
+  if (n % 4 != 0 || ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)) {
+    // general shapes: two single-field passes (same values)
+    dim3 bl(64), g((unsigned)((n / 4 + 63) / 64 + ((n % 4) ? 1 : 0)), (unsigned)n,
+                   (unsigned)(nplanes < 64 ? nplanes : 64));
+    fill_normal3d_kernel<T><<<g, bl, 0, s>>>(a, n, i_base, nplanes, halo_a, seed, stream_a,
+                                             (float)mean, (float)scale);
+    if (int rc = launch_status(name)) return rc;
+    fill_normal3d_kernel<T><<<g, bl, 0, s>>>(b, n, i_base, nplanes, halo_b, seed, stream_b,
+                                             (float)mean, (float)scale);
+    return launch_status(name);
+  }
+  // 128 threads x 4 k of one row; planes strided so the grid holds a few
+  // waves of 148 SMs x 16 resident blocks and each thread runs several planes
+  const unsigned gx = (unsigned)((n / 4 + 127) / 128);
+  const long long rows = (long long)gx * n;
+  long long gz = (148LL * 16 * 4 + rows - 1) / rows;
+  if (gz > nplanes) gz = nplanes;
+  if (gz < 1) gz = 1;
+  fill_normal3d_pair_kernel<T><<<dim3(gx, (unsigned)n, (unsigned)gz), 128, 0, s>>>(
+      a, b, n, i_base, nplanes, halo_a, halo_b, hash_key(seed, stream_a),
+      hash_key(seed, stream_b), (float)mean, (float)scale);
+  return launch_status(name);
+}
+
 }  // namespace sgb
 
 using namespace sgb;
@@ -312,6 +412,20 @@ int sgb_fill_normal3d_f64(double* dst, int n, int i_base, int nplanes, int halo,
                                                                seed, stream_id, (float)mean,
                                                                (float)scale);
   return launch_status("sgb_fill_normal3d_f64");
+}
+
+int sgb_fill_normal3d_pair_f32(float* a, int halo_a, uint64_t stream_a, float* b, int halo_b,
+                               uint64_t stream_b, int n, int i_base, int nplanes, uint64_t seed,
+                               double mean, double scale, sgb_stream_t stream) {
+  return fill_normal3d_pair("sgb_fill_normal3d_pair_f32", a, halo_a, stream_a, b, halo_b,
+                            stream_b, n, i_base, nplanes, seed, mean, scale, as_stream(stream));
+}
+
+int sgb_fill_normal3d_pair_f64(double* a, int halo_a, uint64_t stream_a, double* b, int halo_b,
+                               uint64_t stream_b, int n, int i_base, int nplanes, uint64_t seed,
+                               double mean, double scale, sgb_stream_t stream) {
+  return fill_normal3d_pair("sgb_fill_normal3d_pair_f64", a, halo_a, stream_a, b, halo_b,
+                            stream_b, n, i_base, nplanes, seed, mean, scale, as_stream(stream));
 }
 
 int sgb_fill_layered_f32(float* c, int n, int layers, double lo, double hi, uint64_t seed,

@@ -43,6 +43,12 @@ def regen_seed(u_b, n, t, seed, sl=None):
     api.fill_normal3d(u_b, n, 0, seed, 1001 + 2 * t, base, npl)
 
 
+def regen_step(u_1, u_b, n, t, seed, radius, sl=None):
+    """regen_state + regen_seed of step t in one pass (bitwise the same values)."""
+    base, npl = _planes(sl, n)
+    api.fill_normal3d_pair(u_1, radius, 1000 + 2 * t, u_b, 0, 1001 + 2 * t, n, seed, base, npl)
+
+
 def adjoint_step(family, n, scalars, arrays, sl=None, exchange=("u_1", "u_b"), overlap=True,
                  link=None, fresh=False):
     """One gather-adjoint step; with a slab, halos of `exchange` are refreshed
@@ -248,8 +254,7 @@ def run_independent(n, steps, seed=0, D=0.01, sl=None, arrays=None, overlap=True
         arrays = alloc(fam, n, sl)
         init_static(fam, arrays, n, seed, sl)
     for t in range(steps):
-        regen_state(arrays["u_1"], n, t, seed, 4, sl)
-        regen_seed(arrays["u_b"], n, t, seed, sl)
+        regen_step(arrays["u_1"], arrays["u_b"], n, t, seed, 4, sl)
         if fresh:  # u_1_b = this step's adjoint: zeroing fused into the gather
             adjoint_step(fam, n, {"D": D}, arrays, sl, overlap=overlap, fresh=True)
         else:

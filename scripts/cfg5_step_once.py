@@ -12,8 +12,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 a = drivers.alloc("wave3d_r4", n)
 drivers.init_static("wave3d_r4", a, n, 0)
 for t in range(3):
-    drivers.regen_state(a["u_1"], n, t, 0, 4)
-    drivers.regen_seed(a["u_b"], n, t, 0)
+    drivers.regen_step(a["u_1"], a["u_b"], n, t, 0, 4)
     api.adjoint_fresh("wave3d_r4", n, {"D": 0.01}, a)
 torch.cuda.synchronize()
 print("ok")

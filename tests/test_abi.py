@@ -72,3 +72,16 @@ def test_sass_is_sm100a_with_tma():
     i = sass.find("star3_tma_kernel")
     assert i >= 0
     assert "UTMALDG" in sass, "TMA loads missing from the streaming kernel"
+
+
+def test_missing_entry_kind_raises_stencil_error():
+    """An entry the header does not declare (fresh_u2 is radius-1 fp32 only)
+    is a StencilError naming the missing function, not a KeyError."""
+    from paper_1907_02818_b200 import api
+    assert api.function_name("wave3d_c", "fresh_u2", "f32") == "wave3d_c_b_fresh_u2_f32"
+    for fam, kind, dt in [("wave3d_r4", "fresh_u2", "f32"), ("wave3d_c", "fresh_u2", "f64"),
+                          ("wave1d", "fresh", "f64"), ("wave3d_r4", "bogus", "f32")]:
+        with pytest.raises(_lib.StencilError):
+            api.function_name(fam, kind, dt)
+        with pytest.raises(_lib.StencilError):
+            api.array_params(fam, kind, dt)

@@ -405,3 +405,64 @@ def test_fill_normal3d_equals_elementwise_draw(mods, n):
     api.fill_random(b, 0, 5, 3, "normal", 0.0, 1.0)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n,dtype", [(64, "f32"), (64, "f64"), (36, "f32"), (30, "f32"),
+                                     (37, "f64")])
+def test_fill_normal3d_pair_equals_two_fills(mods, n, dtype):
+    """sgb_fill_normal3d_pair (cfg 5's regeneration of u_1 and the seed in one
+    pass) writes bitwise the values of two fill_normal3d calls -- full grids
+    and slabs, zero shells 4 / 0 / 1, mean and scale != (0, 1) -- on the fused
+    fast path (n % 4 == 0) and the two-pass fallback (n % 4 != 0)."""
+    torch, api, drivers = mods
+    td = torch.float32 if dtype == "f32" else torch.float64
+    for (i0, npl), (ha, hb), (mean, scale) in [((0, n), (4, 0), (0.0, 1.0)),
+                                               ((5, 11), (1, 4), (0.25, 2.0)),
+                                               ((n - 7, 7), (0, 0), (-1.0, 0.5))]:
+        a = torch.full((npl, n, n), float("nan"), dtype=td, device="cuda")
+        b = torch.full_like(a, float("nan"))
+        api.fill_normal3d_pair(a, ha, 17, b, hb, 18, n, 9, i0, npl, mean, scale)
+        wa, wb = torch.empty_like(a), torch.empty_like(a)
+        api.fill_normal3d(wa, n, ha, 9, 17, i0, npl, mean, scale)
+        api.fill_normal3d(wb, n, hb, 9, 18, i0, npl, mean, scale)
+        torch.cuda.synchronize()
+        assert torch.equal(a, wa) and torch.equal(b, wb), (i0, npl, ha, hb)
+
+
+def test_regen_step_equals_state_and_seed(mods):
+    """drivers.regen_step = regen_state + regen_seed, bitwise, on a slab too."""
+    torch, api, drivers = mods
+    from paper_1907_02818_b200 import slab as slabmod
+    n = 48
+    for sl in (None, slabmod.Slab(n, 4, 1, 3, 16, 32, 12, 24)):
+        npl = n if sl is None else sl.nplanes
+        a = torch.empty((npl, n, n), dtype=torch.float32, device="cuda")
+        b, wa, wb = torch.empty_like(a), torch.empty_like(a), torch.empty_like(a)
+        drivers.regen_step(a, b, n, 3, 0, 4, sl)
+        drivers.regen_state(wa, n, 3, 0, 4, sl)
+        drivers.regen_seed(wb, n, 3, 0, sl)
+        torch.cuda.synchronize()
+        assert torch.equal(a, wa) and torch.equal(b, wb)
+
+
+def test_normal_generator_distribution(mods):
+    """N(0, 1) at 2^26 samples: mean, variance, kurtosis and tail mass within
+    a few standard errors; the (lg2, Fibonacci-lattice angle) pair has no
+    correlation between its cos and sin branches."""
+    torch, api, _ = mods
+    n = 256
+    a = torch.empty((n, n, n), dtype=torch.float32, device="cuda")
+    b = torch.empty_like(a)
+    api.fill_normal3d_pair(a, 0, 1, b, 0, 2, n, 0)
+    for x in (a, b):
+        z = x.double().flatten()
+        N = z.numel()
+        m, v = float(z.mean()), float(z.var())
+        k = float(((z - m) ** 4).mean()) / v ** 2
+        assert abs(m) < 5 / N ** 0.5 and abs(v - 1) < 5 * (2 / N) ** 0.5, (m, v)
+        assert abs(k - 3) < 5 * (24 / N) ** 0.5, k
+        tail = float((z.abs() > 3).double().mean())
+        assert abs(tail - 0.0026998) < 5 * (0.0027 / N) ** 0.5, tail
+        assert float(z.abs().max()) > 5.0
+        even, odd = z[0::2], z[1::2]
+        assert abs(float((even * odd).mean())) < 5 / (N / 2) ** 0.5
