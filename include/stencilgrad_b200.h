@@ -341,6 +341,12 @@ int wave3d_r4_b_fresh_f32(int n, double D, float* c, float* c_b, float* u_1, flo
 int wave3d_r4_b_fresh_slab_f32(int n, double D, float* c, float* c_b, float* u_1,
                                    float* u_1_b, float* u_b, int i_base, int nplanes,
                                    int out_i0, int out_i1, sgb_stream_t stream);
+/* the same at the reference's precision (fp64 streaming kernel, MODE 4) */
+int wave3d_r4_b_fresh_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                          double* u_b, sgb_stream_t stream);
+int wave3d_r4_b_fresh_slab_f64(int n, double D, double* c, double* c_b, double* u_1,
+                               double* u_1_b, double* u_b, int i_base, int nplanes, int out_i0,
+                               int out_i1, sgb_stream_t stream);
 /* wave3d_c_b / wave3d_c2_b with u_2_b = this call's u_2 partial alone (-u_b
  * on [1, n-2]^3, 0 elsewhere; c_b, u_1_b accumulated): the zeroing of u_2_b
  * a carried reverse sweep does after rotating its adjoints, fused -- bitwise

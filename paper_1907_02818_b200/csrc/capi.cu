@@ -318,6 +318,48 @@ static int star3_c_fresh_u2(const char* name, int n, double D, float* c, float* 
   return star3_gather<MODE, float>(name, n, D, c, c_b, u_1, u_1_b, u_2_b, u_b, 0, n, 0, n, s);
 }
 
+// wave3d_r4 gather with u_1_b = this call's adjoint alone (MODE 4 of the
+// radius-4 streaming kernels, fp32 and fp64), on local planes [i_base,
+// i_base + nplanes), outputs [out_i0, out_i1).
+template <typename T>
+static int r4_fresh(const char* name, int n, double D, T* c, T* c_b, T* u_1, T* u_1_b, T* u_b,
+                    long long i_base, long long nplanes, long long out_i0, long long out_i1,
+                    cudaStream_t s) {
+  constexpr int R = 4;
+  if (n <= 0 || nplanes <= 0) return einval(std::string(name) + ": bad sizes");
+  if (!guard_ok(WAVE3D_R4, n)) return SGB_GUARD;
+  if (!c || !c_b || !u_1 || !u_1_b || !u_b) return einval(std::string(name) + ": null array");
+  if (out_i0 < 0 || out_i1 > n || out_i0 > out_i1 || i_base < 0 || i_base + nplanes > n ||
+      out_i0 < i_base || out_i1 > i_base + nplanes)
+    return einval(std::string(name) + ": bad output plane range");
+  const long long need_lo = out_i0 - R < 0 ? 0 : out_i0 - R;
+  const long long need_hi = out_i1 - 1 + R > n - 1 ? n - 1 : out_i1 - 1 + R;
+  if (out_i1 > out_i0 && (need_lo < i_base || need_hi >= i_base + nplanes))
+    return einval(std::string(name) + ": slab does not hold the radius-R halo of the outputs");
+  if (out_i1 == out_i0) return 0;
+  if (!opt_flag(OPT_FRESH_UNFUSED)) {
+    if constexpr (std::is_same<T, float>::value) {
+      if (star3_tma_ok<4, float>(n, {c, c_b, u_1, u_1_b, u_b}))
+        return star3_v7_gather<4>(Slab3{n, i_base, nplanes}, R, n - 1 - R, out_i0, out_i1,
+                                  (float)D, c, c_b, u_1, u_1_b, nullptr, u_b, s, name);
+    } else {
+      if (!opt_flag(OPT_F64_PLANE) && !opt_flag(OPT_GENERIC_POINT)) {
+        const int rc = star3_f64_stream_gather<4>(Slab3{n, i_base, nplanes}, R, n - 1 - R,
+                                                  out_i0, out_i1, D, c, c_b, u_1, u_1_b,
+                                                  nullptr, u_b, s, name);
+        if (rc != 1) return rc;  // 1: shape / alignment not taken by the kernel
+      }
+    }
+  }
+  // other shapes: zero the output planes of u_1_b, then the accumulating gather
+  const size_t plane = (size_t)n * n;
+  if (cudaMemsetAsync(u_1_b + (out_i0 - i_base) * plane, 0,
+                      (size_t)(out_i1 - out_i0) * plane * sizeof(T), s) != cudaSuccess)
+    return launch_status(name);
+  return star3_gather<2, T>(name, n, D, c, c_b, u_1, u_1_b, nullptr, u_b, i_base, nplanes,
+                            out_i0, out_i1, s);
+}
+
 }  // namespace sgb
 
 using namespace sgb;
@@ -402,40 +444,23 @@ int wave3d_r4_b_slab_f32(int n, double D, float* c, float* c_b, float* u_1, floa
                                 i_base, nplanes, out_i0, out_i1, as_stream(stream));
 }
 
-// wave3d_r4 gather with u_1_b = this call's adjoint alone (MODE 4 of the
-// radius-4 streaming kernel), on local planes [i_base, i_base + nplanes),
-// outputs [out_i0, out_i1).
-static int r4_fresh(const char* name, int n, double D, float* c, float* c_b, float* u_1,
-                    float* u_1_b, float* u_b, long long i_base, long long nplanes,
-                    long long out_i0, long long out_i1, cudaStream_t s) {
-  constexpr int R = 4;
-  if (n <= 0 || nplanes <= 0) return einval(std::string(name) + ": bad sizes");
-  if (!guard_ok(WAVE3D_R4, n)) return SGB_GUARD;
-  if (!c || !c_b || !u_1 || !u_1_b || !u_b) return einval(std::string(name) + ": null array");
-  if (out_i0 < 0 || out_i1 > n || out_i0 > out_i1 || i_base < 0 || i_base + nplanes > n ||
-      out_i0 < i_base || out_i1 > i_base + nplanes)
-    return einval(std::string(name) + ": bad output plane range");
-  const long long need_lo = out_i0 - R < 0 ? 0 : out_i0 - R;
-  const long long need_hi = out_i1 - 1 + R > n - 1 ? n - 1 : out_i1 - 1 + R;
-  if (out_i1 > out_i0 && (need_lo < i_base || need_hi >= i_base + nplanes))
-    return einval(std::string(name) + ": slab does not hold the radius-R halo of the outputs");
-  if (out_i1 == out_i0) return 0;
-  if (star3_tma_ok<4, float>(n, {c, c_b, u_1, u_1_b, u_b}) && !opt_flag(OPT_FRESH_UNFUSED))
-    return star3_v7_gather<4>(Slab3{n, i_base, nplanes}, R, n - 1 - R, out_i0, out_i1, (float)D,
-                              c, c_b, u_1, u_1_b, nullptr, u_b, s, name);
-  // other shapes: zero the output planes of u_1_b, then the accumulating gather
-  const size_t plane = (size_t)n * n;
-  if (cudaMemsetAsync(u_1_b + (out_i0 - i_base) * plane, 0,
-                      (size_t)(out_i1 - out_i0) * plane * sizeof(float), s) != cudaSuccess)
-    return launch_status(name);
-  return star3_gather<2, float>(name, n, D, c, c_b, u_1, u_1_b, nullptr, u_b, i_base, nplanes,
-                                out_i0, out_i1, s);
-}
-
 int wave3d_r4_b_fresh_f32(int n, double D, float* c, float* c_b, float* u_1, float* u_1_b,
                               float* u_b, sgb_stream_t stream) {
   return r4_fresh("sgb_wave3d_r4_b_fresh", n, D, c, c_b, u_1, u_1_b, u_b, 0, n, 0, n,
                   as_stream(stream));
+}
+
+int wave3d_r4_b_fresh_f64(int n, double D, double* c, double* c_b, double* u_1, double* u_1_b,
+                          double* u_b, sgb_stream_t stream) {
+  return r4_fresh("sgb_wave3d_r4_b_fresh_f64", n, D, c, c_b, u_1, u_1_b, u_b, 0, n, 0, n,
+                  as_stream(stream));
+}
+
+int wave3d_r4_b_fresh_slab_f64(int n, double D, double* c, double* c_b, double* u_1,
+                               double* u_1_b, double* u_b, int i_base, int nplanes, int out_i0,
+                               int out_i1, sgb_stream_t stream) {
+  return r4_fresh("sgb_wave3d_r4_b_fresh_slab_f64", n, D, c, c_b, u_1, u_1_b, u_b, i_base,
+                  nplanes, out_i0, out_i1, as_stream(stream));
 }
 
 int wave3d_r4_b_fresh_slab_f32(int n, double D, float* c, float* c_b, float* u_1,

@@ -281,7 +281,9 @@ int gather(sgb_slab* p, int s, const double* sc, bool fresh, int o0, int o1, cud
       return wave3d_r4_b_slab_f32(n, sc[0], (float*)c, (float*)cb, (float*)u1, (float*)u1b,
                                   (float*)ub, b, np, o0, o1, ss);
     }
-    if (fresh) return fail("sgb_slab_step: SGB_STEP_FRESH needs fp32");
+    if (fresh)
+      return wave3d_r4_b_fresh_slab_f64(n, sc[0], (double*)c, (double*)cb, (double*)u1,
+                                        (double*)u1b, (double*)ub, b, np, o0, o1, ss);
     return wave3d_r4_b_slab_f64(n, sc[0], (double*)c, (double*)cb, (double*)u1, (double*)u1b,
                                 (double*)ub, b, np, o0, o1, ss);
   }

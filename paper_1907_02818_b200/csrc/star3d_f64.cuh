@@ -176,15 +176,17 @@ __global__ void __launch_bounds__(StarTileD<MODE>::THREADS, 1)
     const bool emit = it >= 2 * R;
     const int p = pstart + it;
     const bool u2 = S3::kU2 && p >= o_begin && p < o_end;  // u_2_b tile of plane p
-    tma::mbar_arrive_expect_tx(&bars[s],
-                               (3 * BOX + ((emit ? 2 : 0) + (u2 ? 1 : 0)) * TILE) * 8);
+    // fresh u_1_b (MODE 4): its old tile is not needed
+    tma::mbar_arrive_expect_tx(
+        &bars[s],
+        (3 * BOX + ((emit ? (S3::kU1bFresh ? 1 : 2) : 0) + (u2 ? 1 : 0)) * TILE) * 8);
     tma::load_3d(dst, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
     tma::load_3d(dst + BP, &tm_ub, &bars[s], k0 - HK - (UBW ? lo : 0), j0 - HJ - (UBW ? lo : 0),
                  pl);
     tma::load_3d(dst + 2 * BP, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
     if (emit) {
       tma::load_3d(dst + 3 * BP, &tm_cb, &bars[s], k0, j0, pl - R);
-      tma::load_3d(dst + 3 * BP + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
+      if (!S3::kU1bFresh) tma::load_3d(dst + 3 * BP + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
     }
     if (u2) tma::load_3d(dst + 3 * BP + 2 * TILE, &tm_u2b, &bars[s], k0, j0, pl);
   };
@@ -326,13 +328,15 @@ __global__ void __launch_bounds__(StarTileD<MODE>::THREADS, 1)
               }
             }
           } else {
-            // reached iff at most one coordinate is outside [lo, hi], by <= R
+            // reached iff at most one coordinate is outside [lo, hi], by <= R;
+            // MODE 4 writes every grid point (0 + sum where reached, else 0)
             const uint32_t reach = oout == 0 ? (inb | one) : (oout <= R ? inb : 0u);
 #pragma unroll
             for (int h = 0; h < 2; h++) {
               const uint32_t mk = reach >> (2 * h);
-              if (!((grid >> h) & 1) || !(mk & 3)) continue;
-              const double2 old = ldd2(OLD + h * TK);
+              if (!((grid >> h) & 1) || (!S3::kU1bFresh && !(mk & 3))) continue;
+              const double2 old =
+                  S3::kU1bFresh ? make_double2(0.0, 0.0) : ldd2(OLD + h * TK);
               const double2 a = acc[es][h];
               const double2 nv = make_double2((mk & 1) ? old.x + a.x : old.x,
                                               (mk & 2) ? old.y + a.y : old.y);

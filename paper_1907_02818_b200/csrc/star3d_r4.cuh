@@ -753,7 +753,19 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
             (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cu.first, tm, D);
     return launch_status(name);
   }
-  const bool fork = tm.n_interior() > 0 && tm.n_frame() > 0 && opt_flag(OPT_FORK);
+  // Frame launch on a side stream, concurrent with the interior launch, when
+  // the interior's last wave leaves more than 1/8 of the SMs idle (its frame
+  // CTAs fill them): 1024^3 (420 interior CTAs = 2.84 waves) 4.61 -> 4.51 ms
+  // burst, 4.94 -> 4.82 ms power-capped; at 768^3 (440 CTAs = 2.97 waves) it
+  // is neutral, so it stays off there (scripts/cfg5_ab.py).  SGB_FORK=0|1
+  // forces either.
+  long long fork_opt = opt(OPT_FORK, -1);
+  if (fork_opt < 0) {
+    const long long cta = (long long)tm.n_interior() * ci.second;
+    const long long waves = (cta + sms - 1) / sms;
+    fork_opt = (waves * sms - cta) * 8 > sms;
+  }
+  const bool fork = tm.n_interior() > 0 && tm.n_frame() > 0 && fork_opt > 0;
   SideStream* ss = fork ? side_stream() : nullptr;
   if (ss) {
     if (cudaEventRecord(ss->fork, s) != cudaSuccess ||

@@ -206,21 +206,23 @@ def test_halo_prefetch_pipeline_bitwise(mods, n, world, regen, fresh):
             assert torch.equal(loc[k][own], full[k][sl.own0:sl.own1]), (r, k)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("noubwin", ["", "1"])
 @pytest.mark.parametrize("n,world", [(40, 1), (68, 1), (37, 1), (48, 2), (68, 3), (36, 4)])
-def test_fresh_gather_equals_zero_then_accumulate(mods, n, world, noubwin, sgbopt):
-    """wave3d_r4_b_fresh(_slab)_f32 (u_1_b = this call's adjoint; the zeroing
-    fused into the streaming kernel) is bitwise the zeroed u_1_b followed by
-    the accumulating gather, c_b accumulated as usual -- full grid (n = 37:
-    the entry's memset + gather path) and every rank of z-slab
-    decompositions, incl. the overlapped interior / edge-band split."""
+def test_fresh_gather_equals_zero_then_accumulate(mods, n, world, noubwin, dtype, sgbopt):
+    """wave3d_r4_b_fresh(_slab)_{f32,f64} (u_1_b = this call's adjoint; the
+    zeroing fused into the streaming kernels' MODE 4) is bitwise the zeroed
+    u_1_b followed by the accumulating gather, c_b accumulated as usual --
+    full grid (n = 37: the entry's memset + gather path) and every rank of
+    z-slab decompositions, incl. the overlapped interior / edge-band split."""
     torch, api, drivers = mods
     from paper_1907_02818_b200 import slab as slabmod
     if noubwin:  # the in-kernel seed mask instead of the windowed seed map
         sgbopt.setenv("SGB_NO_UBWIN", "1")
     fam, sc = "wave3d_r4", {"D": 0.01}
+    td, ti = (torch.float32, torch.int32) if dtype == "f32" else (torch.float64, torch.int64)
     g = torch.Generator(device="cpu").manual_seed(n + world)
-    full = {k: torch.randn((n, n, n), generator=g).cuda()
+    full = {k: torch.randn((n, n, n), generator=g).to(td).cuda()
             for k in ("c", "c_b", "u_1", "u_1_b", "u_b")}
     for r in range(world):
         sl = slabmod.decompose(n, 4, world, r) if world > 1 else None
@@ -247,7 +249,7 @@ def test_fresh_gather_equals_zero_then_accumulate(mods, n, world, noubwin, sgbop
             own = slice(sl.own0 - sl.base, sl.own1 - sl.base)
         torch.cuda.synchronize()
         for k in ("c_b", "u_1_b"):
-            assert torch.equal(a[k][own].view(torch.int32), b[k][own].view(torch.int32)), (r, k)
+            assert torch.equal(a[k][own].view(ti), b[k][own].view(ti)), (r, k)
 
 
 @pytest.mark.parametrize("family", ["wave3d_c", "wave3d_c2"])
