@@ -1127,7 +1127,7 @@ def main():
     ap.add_argument("--size", "--n", dest="n", type=int, default=0,
                     help="override grid extent (--size under torchrun, whose own parser "
                          "claims --n...)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--halo", default="ipc", choices=["ipc", "nccl", "torch", "peer"],

@@ -404,6 +404,10 @@ int sgb_jit_compile(const char* source, const char* name, sgb_jit_kernel** out);
 int sgb_jit_check(const char* source);
 int sgb_jit_launch(sgb_jit_kernel* kernel, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
                    unsigned by, unsigned bz, void** args, sgb_stream_t stream);
+/* the same with `smem` bytes of dynamic shared memory */
+int sgb_jit_launch_smem(sgb_jit_kernel* kernel, unsigned gx, unsigned gy, unsigned gz,
+                        unsigned bx, unsigned by, unsigned bz, unsigned smem, void** args,
+                        sgb_stream_t stream);
 
 #ifdef __cplusplus
 }

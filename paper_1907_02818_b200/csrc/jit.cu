@@ -149,9 +149,25 @@ int sgb_jit_check(const char* source) {
 // for cudaLaunchKernel.
 int sgb_jit_launch(sgb_jit_kernel* k, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
                    unsigned by, unsigned bz, void** args, sgb_stream_t stream) {
+  return sgb_jit_launch_smem(k, gx, gy, gz, bx, by, bz, 0, args, stream);
+}
+
+// The same with `smem` bytes of dynamic shared memory (the tiled emitted
+// gather's plane rings); the kernel's limit is raised on the calling device.
+int sgb_jit_launch_smem(sgb_jit_kernel* k, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+                        unsigned by, unsigned bz, unsigned smem, void** args,
+                        sgb_stream_t stream) {
   if (!k || !args) return SGB_EINVAL;
+  if (smem > 48 * 1024) {
+    cudaError_t a = cudaFuncSetAttribute((const void*)k->kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (a != cudaSuccess) {
+      sgb::set_error(std::string("emitted kernel smem attribute: ") + cudaGetErrorString(a));
+      return -static_cast<int>(a);
+    }
+  }
   cudaError_t e = cudaLaunchKernel((const void*)k->kernel, dim3(gx, gy, gz), dim3(bx, by, bz),
-                                   args, 0, sgb::as_stream(stream));
+                                   args, smem, sgb::as_stream(stream));
   sgb::g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e != cudaSuccess) {
     sgb::set_error(std::string("emitted kernel launch failed: ") + cudaGetErrorString(e));

@@ -109,7 +109,10 @@ sgb_plan* sgb_plan_create_slab(const char* family, int n, int dtype_bytes, int i
                          (fs->dims == 2 && ((long long)n * dtype_bytes) % 16 == 0) ||
                          (fs->dims == 1 && n % 2 == 0);
   if (pipelined) {
+    // 3D: ~16-plane chunks (at most 64): 1024^3 e2e 425 -> 421 ms for 32 -> 64
+    // chunks, 0.98-0.99 of the box's concurrent-copy floor (scripts/e2e_time.py)
     int c = units >= 128 ? 32 : 1;
+    if (fs->dims == 3 && units >= 128) c = (int)std::min<long long>(64, units / 16);
     if (sgb::opt(sgb::OPT_PLAN_CHUNKS, 0) > 0) c = (int)sgb::opt(sgb::OPT_PLAN_CHUNKS, 0);
     p->chunks = (int)std::min<long long>(c, std::max<long long>(1, units / 16));
     cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);

@@ -167,3 +167,61 @@ def test_emitted_signatures_follow_reference_emitter():
         for which, key in (("gather", "adjoint"), ("primal", "primal")):
             arrays = [a for a in re.findall(r"double \*(\w+)", pr[key])]
             assert ep.param_arrays(which) == arrays, (fam, which)
+
+
+def test_factored_partials_share_one_subexpression():
+    """CSE of the partials: the 24 shifted u_1 terms of
+    wave3d_r4 are k_l * (D c^2) -- one group, one Q field; wave3d_c's six
+    D*c terms share theirs with k = 1; constant partials are not grouped."""
+    from paper_1907_02818_b200 import emitter
+    ep = emitter.load_program("wave3d_r4")
+    assert [len(t) for _, t in ep.groups] == [24]
+    assert ep.factor[0] is None and ep.factor[13] is None  # c_b term, centre term
+    lay = ep.tiled_layout()
+    assert [f["kind"] for f in lay["fields"]] == ["q", "raw"]  # Q and the u_1 planes
+    assert (lay["ZL"], lay["ZH"]) == (-4, 4)
+    ep = emitter.load_program("wave3d_c")
+    assert [len(t) for _, t in ep.groups] == [6]
+    assert all(ep.factor[ti][0] is None for ti in ep.groups[0][1])
+    assert ep.factor[8] is None  # partial -1
+
+
+def _tiled_cases():
+    return ["wave3d", "wave3d_c", "wave3d_c2", "wave3d_r4"] + FUZZ
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("name", _tiled_cases())
+def test_tiled_form_equals_flat_form_bitwise(name):
+    """The tiled gather (shared-memory plane rings of the factored Q fields
+    and of the many-point reads) applies the same per-cell increments as the
+    one-thread-per-point form: bitwise equal, incl. untouched cells (NaN and
+    -0.0 sentinels survive), partial tiles and several outer-counter chunks."""
+    import torch
+    from paper_1907_02818_b200 import emitter
+    with tempfile.TemporaryDirectory() as td:
+        spec, _, info = problem(name, 12, td)
+    ep = emitter.EmittedProblem(spec, info["terms"])
+    if ep.tiled_layout() is None:
+        pytest.skip("tiled form does not apply (not 3D / nothing shared)")
+    for n in ((20, 45) if name == "wave3d_r4" else (12, 37)):
+        sizes = {"n": n}
+        rng = np.random.default_rng(n)
+        scalars = {s: 0.3 for s in spec["scalars"]}
+        base = {}
+        for arr in ep.param_arrays():
+            shp = tuple(ep._eval_aff(a, sizes) for a in ep._shape_of(arr))
+            v = rng.standard_normal(shp)
+            if arr.endswith("_b") and arr != ep.seed:
+                flat = v.reshape(-1)
+                flat[::7] = np.nan
+                flat[3::7] = -0.0
+            base[arr] = torch.from_numpy(v).cuda()
+        a = {k: v.clone() for k, v in base.items()}
+        b = {k: v.clone() for k, v in base.items()}
+        ep.adjoint(sizes, scalars, a, form="tiled")
+        ep.adjoint(sizes, scalars, b, form="flat")
+        torch.cuda.synchronize()
+        for t in {t["adjoint"] for t in info["terms"]}:
+            assert torch.equal(a[t].view(torch.int64), b[t].view(torch.int64)), (name, n, t)
