@@ -133,6 +133,27 @@ __device__ __forceinline__ void ld4(const double* p, A* out) {
   const double2 b = *reinterpret_cast<const double2*>(p + 2);
   out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
 }
+// Row reads of the stencils: thread tx reads 4 elements at 4 tx + const.  For
+// doubles that is two 16-byte loads 32 bytes apart per lane, and the 8 lanes
+// of each 128-bit load phase then hit every other 16-byte bank group twice
+// (a 2-way conflict: 45 % of the PREC kernel's shared wavefronts, ncu).
+// Lanes with tx & 4 load their upper half first, so each phase covers all 32
+// banks once; the values land in the same registers (512^3 U2SET call 875 ->
+// 821 us, conflicts 82 M -> 53 M).  The same swap on the q-pass stores and
+// the g queue removed most of the rest (22 M) but cost more selects and
+// registers than it saved (939 us), so those stay plain.
+template <typename A>
+__device__ __forceinline__ void ld4r(const float* p, int tx, A* out) {
+  ld4(p, out);
+}
+template <typename A>
+__device__ __forceinline__ void ld4r(const double* p, int tx, A* out) {
+  const bool sw = (tx >> 2) & 1;
+  const double2 f = *reinterpret_cast<const double2*>(p + (sw ? 2 : 0));
+  const double2 g = *reinterpret_cast<const double2*>(p + (sw ? 0 : 2));
+  out[0] = sw ? g.x : f.x; out[1] = sw ? g.y : f.y;
+  out[2] = sw ? f.x : g.x; out[3] = sw ? f.y : g.y;
+}
 
 // One field's contribution from one plane: in-plane (k from a 12-element
 // register window, j from R rows above/below in smem) into the accumulator of
@@ -146,9 +167,9 @@ __device__ __forceinline__ void star_field_plane(const E* F, int crow, int tx, A
                                                  typename Vec4<A>::type (&acc)[RING], int ph) {
   constexpr int HK = 4, BW = 72;
   A win[12];
-  ld4(F + crow + 4 * tx, win);
-  ld4(F + crow + 4 * tx + 4, win + 4);
-  ld4(F + crow + 4 * tx + 8, win + 8);
+  ld4r(F + crow + 4 * tx, tx, win);
+  ld4r(F + crow + 4 * tx + 4, tx, win + 4);
+  ld4r(F + crow + 4 * tx + 8, tx, win + 8);
   A inp[4];
 #pragma unroll
   for (int m = 0; m < 4; m++) {
@@ -160,8 +181,8 @@ __device__ __forceinline__ void star_field_plane(const E* F, int crow, int tx, A
 #pragma unroll
   for (int r = 1; r <= R; r++) {
     A up[4], dn[4];
-    ld4(F + crow - r * BW + HK + 4 * tx, up);
-    ld4(F + crow + r * BW + HK + 4 * tx, dn);
+    ld4r(F + crow - r * BW + HK + 4 * tx, tx, up);
+    ld4r(F + crow + r * BW + HK + 4 * tx, tx, dn);
     inp[0] += wr[r] * (up[0] + dn[0]);
     inp[1] += wr[r] * (up[1] + dn[1]);
     inp[2] += wr[r] * (up[2] + dn[2]);
