@@ -2,7 +2,7 @@
 
 Used by the golden-fixture generator and the parity tests at oracle-sized n.
 (The benchmark generates its full-size inputs on the device with the product's
-counter-based generator; see paper_1907_02818_b200/runtime.py.)
+counter-based generators; see paper_1907_02818_b200/csrc/inputs.cu and drivers.py.)
 
 Distributions (BASELINE.json ``configs``):
   wave1d     u, u_prev, u_next_b ~ N(0,1), zero Dirichlet ends; c ~ U[1.5,4.5]; D=0.25
