@@ -743,7 +743,23 @@ def run_ours(args, cfg):
     _lib.lib()
     family, n_full, dtype, bpp0, scalars, desc = cfg
     halo = args.halo
-    wl = Workload(torch, api, args.config, args.n, dist, halo)
+    setup_error = None
+    try:
+        wl = Workload(torch, api, args.config, args.n, dist, halo)
+    except Exception as ex:  # e.g. no peer access for the IPC transport on this box
+        if world == 1:
+            raise
+        wl, setup_error = None, f"{type(ex).__name__}: {str(ex)[:200]}"
+    if world > 1 and not dist.all_ok(setup_error is None):
+        # every rank agrees to measure the torch.distributed exchange instead
+        if wl is not None:
+            wl.close()
+            del wl
+        torch.cuda.empty_cache()
+        log("halo setup failed, falling back to --halo torch:", setup_error)
+        wl = Workload(torch, api, args.config, args.n, dist, "torch")
+        wl.note = f"--halo {halo} setup failed ({setup_error or 'on another rank'})"
+        halo = "torch"
     n = wl.n
     verified = wl.verify()
     if not verified:
@@ -756,6 +772,7 @@ def run_ours(args, cfg):
         wl.note = f"--halo {halo} failed the bitwise check against the exchange path"
         halo = "torch"
     ms, kms, launches, clocks = time_workload(torch, wl, args.steps, args.warmup, dist)
+    halo_note = wl.note
     pts = wl.points()
     value = pts * args.steps / (ms / 1e3) / 1e9
     # roofline of the dominant kernel: the gather launch of each step (its
@@ -836,6 +853,7 @@ def run_ours(args, cfg):
                                       "torch.distributed, every rank" if verified else
                                       f"FAILED for --halo {args.halo}; fell back to torch")
                        if world > 1 else None,
+                       "halo_note": halo_note,
                        "step": step_text(args.config)},
             "achieved_hbm_gbs": achieved,
             "clocks": clocks,
