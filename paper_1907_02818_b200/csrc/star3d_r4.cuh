@@ -183,6 +183,9 @@ struct StarTile7 {
 #ifndef SGB_V7_QX
 #define SGB_V7_QX 2
 #endif
+#ifndef SGB_V7_PF_TILES
+#define SGB_V7_PF_TILES 1
+#endif
   static constexpr int NS = 3, NQB = SGB_V7_NQB;
   static constexpr int ROLE = 16 * (TJ / 2);  // 256 threads per field
   static constexpr int THREADS = 2 * ROLE;
@@ -317,7 +320,7 @@ __device__ __forceinline__ void star3_v7_body(
     const CUtensorMap& tm_cb, const CUtensorMap& tm_u1b, const CUtensorMap& tm_u2b,
     float* __restrict__ c_b, float* __restrict__ u_1_b, float* __restrict__ u_2_b, int n,
     int i_base, int lo, int hi, int out_i0, int out_i1, int chunk, int tk, int tj, float D,
-    const PeerHalo* peer = nullptr) {
+    const PeerHalo* peer = nullptr, int PF = 0) {
   using Tl = StarTile7<MODE>;
   using S3 = Star3<MODE>;
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
@@ -378,6 +381,18 @@ __device__ __forceinline__ void star3_v7_body(
       if (!S3::kU1bFresh) tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
     }
     if (u2) tma::load_3d(dst + 3 * BF + 2 * TILE, &tm_u2b, &bars[s], k0, j0, pl);
+    // L2 prefetch PF planes beyond the ring (the shared-memory ring holds
+    // NS planes; a plane's boxes then arrive from L2, not DRAM)
+    if (PF > 0 && it + PF < P) {
+      const int q = pl + PF;
+      tma::prefetch_3d(&tm_c, k0 - HK, j0 - HJ, q);
+      tma::prefetch_3d(&tm_ub, k0 - HK - ulo, j0 - HJ - ulo, q);
+      tma::prefetch_3d(&tm_u1, k0 - HK, j0 - HJ, q);
+      if (SGB_V7_PF_TILES && it + PF >= 2 * R) {
+        tma::prefetch_3d(&tm_cb, k0, j0, q - R);
+        if (!S3::kU1bFresh) tma::prefetch_3d(&tm_u1b, k0, j0, q - R);
+      }
+    }
   };
   if (tid == 0)
     for (int it = 0; it < NS && it < P; it++) issue(it);
@@ -613,7 +628,7 @@ __device__ __forceinline__ void star3_v7_body(
       const __grid_constant__ CUtensorMap tm_u1b,                                          \
       const __grid_constant__ CUtensorMap tm_u2b, float *__restrict__ c_b,                 \
       float *__restrict__ u_1_b, float *__restrict__ u_2_b, int n, int i_base, int lo,     \
-      int hi, int out_i0, int out_i1, int chunk, TileMap tm, float D
+      int hi, int out_i0, int out_i1, int chunk, TileMap tm, float D, int pf
 #define SGB_V7_ARGS                                                                    \
   tm_c, tm_ub, tm_u1, tm_cb, tm_u1b, tm_u2b, c_b, u_1_b, u_2_b, n, i_base, lo, hi, out_i0, \
       out_i1, chunk
@@ -627,7 +642,7 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_kernel(S
     tm.interior(blockIdx.x, tk, tj);
   else
     tm.frame(blockIdx.x, tk, tj);
-  star3_v7_body<MODE, INT, UBW>(SGB_V7_ARGS, tk, tj, D);
+  star3_v7_body<MODE, INT, UBW>(SGB_V7_ARGS, tk, tj, D, nullptr, pf);
 }
 
 // One launch over all tiles in row-major order, each CTA running the body
@@ -640,9 +655,9 @@ template <int MODE, bool UBW>
 __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1) star3_v7_unified(SGB_V7_PARAMS) {
   const int tk = blockIdx.x % tm.tiles_k, tj = blockIdx.x / tm.tiles_k;
   if (tk >= tm.ik0 && tk < tm.ik1 && tj >= tm.ij0 && tj < tm.ij1)
-    star3_v7_body<MODE, true, UBW>(SGB_V7_ARGS, tk, tj, D);
+    star3_v7_body<MODE, true, UBW>(SGB_V7_ARGS, tk, tj, D, nullptr, pf);
   else
-    star3_v7_body<MODE, false, UBW>(SGB_V7_ARGS, tk, tj, D);
+    star3_v7_body<MODE, false, UBW>(SGB_V7_ARGS, tk, tj, D, nullptr, pf);
 }
 
 // The same, with the halo planes read from the neighbours' arrays.
@@ -651,9 +666,9 @@ __global__ void __launch_bounds__(StarTile7<MODE>::THREADS, 1)
     star3_v7_unified_peer(SGB_V7_PARAMS, const __grid_constant__ PeerHalo peer) {
   const int tk = blockIdx.x % tm.tiles_k, tj = blockIdx.x / tm.tiles_k;
   if (tk >= tm.ik0 && tk < tm.ik1 && tj >= tm.ij0 && tj < tm.ij1)
-    star3_v7_body<MODE, true, UBW>(SGB_V7_ARGS, tk, tj, D, &peer);
+    star3_v7_body<MODE, true, UBW>(SGB_V7_ARGS, tk, tj, D, &peer, pf);
   else
-    star3_v7_body<MODE, false, UBW>(SGB_V7_ARGS, tk, tj, D, &peer);
+    star3_v7_body<MODE, false, UBW>(SGB_V7_ARGS, tk, tj, D, &peer, pf);
 }
 
 template <int MODE>
@@ -712,6 +727,15 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
   // takes ceil(tiles*c / SMs) * (ceil(nout/c) + 2R) plane-times.  Minimising it
   // reproduced the measured best chunking at 768^3 and 1024^3.
   const int sms = num_sms();
+  // L2 prefetch (cp.async.bulk.prefetch.tensor) of a plane's boxes and tiles
+  // `pf` planes beyond the shared-memory ring (SGB_V7_PREFETCH=pf; default off).
+  // Measured (scripts/pf_sweep.py, alternating order): the fresh (MODE 4)
+  // gather gains 1.6-3.7 % at n = 512..1088 (768^3: 1.918 -> 1.846 ms) but
+  // loses 9 % at n = 1024 (rows a multiple of 4 KiB: ncu DRAM reads +46 %,
+  // the prefetched lines are evicted before their TMA load); the
+  // accumulating gather (two tiles per plane) loses 19 % at 768^3 (boxes
+  // only: 4 %).  No BASELINE configuration gains, so the default stays off.
+  const int pf = (int)std::max<long long>(0, std::min<long long>(8, opt(OPT_V7_PREFETCH, 0)));
   auto chunking = [&](Opt knob, long long tiles) {
     int c = (int)std::max<long long>(0, opt(knob, 0));
     if (c == 0) {
@@ -740,7 +764,7 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     star3_v7_unified_peer<MODE, true>
         <<<dim3((unsigned)(tm.tiles_k * tm.tiles_j), cu.second), Tl::THREADS, Tl::SMEM, s>>>(
             maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cu.first, tm, D, *peer);
+            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cu.first, tm, D, pf, *peer);
     return launch_status(name);
   }
   const bool partial = out_i0 != 0 || out_i1 != g.n;
@@ -750,21 +774,14 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     star3_v7_unified<MODE, true>
         <<<dim3((unsigned)(tm.tiles_k * tm.tiles_j), cu.second), Tl::THREADS, Tl::SMEM, s>>>(
             maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cu.first, tm, D);
+            (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cu.first, tm, D, pf);
     return launch_status(name);
   }
-  // Frame launch on a side stream, concurrent with the interior launch, when
-  // the interior's last wave leaves more than 1/8 of the SMs idle (its frame
-  // CTAs fill them): 1024^3 (420 interior CTAs = 2.84 waves) 4.61 -> 4.51 ms
-  // burst, 4.94 -> 4.82 ms power-capped; at 768^3 (440 CTAs = 2.97 waves) it
-  // is neutral, so it stays off there (scripts/cfg5_ab.py).  SGB_FORK=0|1
-  // forces either.
-  long long fork_opt = opt(OPT_FORK, -1);
-  if (fork_opt < 0) {
-    const long long cta = (long long)tm.n_interior() * ci.second;
-    const long long waves = (cta + sms - 1) / sms;
-    fork_opt = (waves * sms - cta) * 8 > sms;
-  }
+  // Frame launch on a side stream, concurrent with the interior launch
+  // (SGB_FORK=1): an A/B with alternating order (scripts/cfg5_ab.py) measured
+  // it slower at 1024^3 (4.75 vs 4.67 ms) and 768^3 (1.99 vs 1.86 ms), so the
+  // default is one stream.
+  const long long fork_opt = opt(OPT_FORK, 0);
   const bool fork = tm.n_interior() > 0 && tm.n_frame() > 0 && fork_opt > 0;
   SideStream* ss = fork ? side_stream() : nullptr;
   if (ss) {
@@ -776,7 +793,7 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     auto k = ubwin ? star3_v7_kernel<MODE, false, true> : star3_v7_kernel<MODE, false, false>;
     k<<<dim3((unsigned)tm.n_frame(), cf.second), Tl::THREADS, Tl::SMEM, ss ? ss->s : s>>>(
         maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cf.first, tm, D);
+        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cf.first, tm, D, pf);
     const int st = launch_status(name);
     if (st) return st;
   }
@@ -784,7 +801,7 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     auto k = ubwin ? star3_v7_kernel<MODE, true, true> : star3_v7_kernel<MODE, true, false>;
     k<<<dim3((unsigned)tm.n_interior(), ci.second), Tl::THREADS, Tl::SMEM, s>>>(
         maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,
-        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, ci.first, tm, D);
+        (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, ci.first, tm, D, pf);
     const int st = launch_status(name);
     if (st) return st;
   }

@@ -77,6 +77,15 @@ __device__ __forceinline__ void load_3d(void* dst, const CUtensorMap* map, uint6
       : "memory");
 }
 
+// L2 prefetch of one box (no shared memory, no barrier): deepens a streaming
+// kernel's pipeline beyond its shared-memory ring.
+__device__ __forceinline__ void prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 }  // namespace tma
 
 template <int MODE, bool PREC = false>

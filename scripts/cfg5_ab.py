@@ -29,7 +29,7 @@ def parse(v):
 
 res = {v: ([], []) for v in variants}
 for r in range(rounds + 1):
-    for v in variants:
+    for v in (variants if r % 2 == 0 else variants[::-1]):  # no position bias
         with api.options(**parse(v)):
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
                    torch.cuda.Event(enable_timing=True)) for _ in range(steps)]

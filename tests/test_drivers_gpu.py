@@ -219,6 +219,8 @@ def test_fresh_gather_equals_zero_then_accumulate(mods, n, world, noubwin, dtype
     from paper_1907_02818_b200 import slab as slabmod
     if noubwin:  # the in-kernel seed mask instead of the windowed seed map
         sgbopt.setenv("SGB_NO_UBWIN", "1")
+    else:  # the L2-prefetching schedule gives the same bits
+        sgbopt.setenv("SGB_V7_PREFETCH", "1")
     fam, sc = "wave3d_r4", {"D": 0.01}
     td, ti = (torch.float32, torch.int32) if dtype == "f32" else (torch.float64, torch.int64)
     g = torch.Generator(device="cpu").manual_seed(n + world)

@@ -252,7 +252,7 @@ def test_r4_launch_variants_bitwise_equal(api, n, sgbopt):
     for env in ({"SGB_NO_UBWIN": "1"}, {"SGB_ICHUNKS": "3", "SGB_ICHUNKS_F": "5"},
                 {"SGB_ICHUNKS": "1", "SGB_ICHUNKS_F": "1"}, {"SGB_FORK": "1"},
                 {"SGB_V7_UNIFIED": "1"}, {"SGB_V7_UNIFIED": "1", "SGB_ICHUNKS": "3"},
-                {"SGB_V7_SPLIT": "1"}, {"SGB_FORK": "0"}):
+                {"SGB_V7_SPLIT": "1"}, {"SGB_FORK": "0"}, {"SGB_V7_PREFETCH": "2"}):
         with sgbopt.context() as m:
             for k, v in env.items():
                 m.setenv(k, v)
