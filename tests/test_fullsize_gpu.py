@@ -119,3 +119,35 @@ def test_cfg5_slabs_and_linearity(env):
         num = (a12[k].double() - a1[k].double() - a2[k].double()).norm()
         den = a12[k].double().norm()
         assert float(num / den) <= 1e-6, k
+
+
+@pytest.mark.parametrize("cfg,fresh", [("4", False), ("5", True)])
+def test_fullsize_fp64_3d_matches_reference(env, cfg, fresh):
+    """The bench line's fp64 row at its full size, against the reference's own
+    precision: cfg 4 (768^3, the accumulating gather on random initial
+    adjoints) and one cfg 5 step (1024^3, the fp64 MODE-4 fresh gather) vs the
+    reference's compiled emitted adjoint (oracle.emitted_or_port; the fresh
+    step's reference starts from u_1_b = 0) at the fp64 bound 1e-12, compared
+    on the device."""
+    torch, api, bench = env
+    family, n, _dt, _bpp, scalars, _desc = bench.CONFIGS[cfg]
+    if _host_ram_gb() < 8 * n ** 3 * 8 / 2 ** 30:
+        pytest.skip("host RAM for the fp64 reference")
+    ref, label = oracle.emitted_or_port(family)
+    arrays = bench.gen_inputs(api, torch, family, n, None, "f64")
+    for k, nm in enumerate(("c_b", "u_1_b")):
+        api.fill_random(arrays[nm], 0, 11, 40 + k, "normal", 0.0, 1.0)
+    torch.cuda.synchronize()
+    host = {k: v.cpu() for k, v in arrays.items()}
+    if fresh:
+        host["u_1_b"].zero_()
+        api.adjoint_fresh(family, n, scalars, arrays)   # runs beside the CPU reference
+    else:
+        api.adjoint(family, n, scalars, arrays)
+    assert ref(n, scalars, host) == 0, label
+    dev = torch.empty_like(arrays["c_b"])
+    for nm in ("c_b", "u_1_b"):
+        dev.copy_(host[nm])
+        e = api.compare(arrays[nm], dev)
+        assert e["nonfinite"] == 0, nm
+        assert e["max_rel"] <= 1e-12 and e["norm_rel"] <= 1e-12, (cfg, nm, e, label)
