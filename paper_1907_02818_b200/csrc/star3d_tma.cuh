@@ -150,7 +150,9 @@ __device__ __forceinline__ void ld4(const double* p, A* out) {
 // banks once; the values land in the same registers (512^3 U2SET call 875 ->
 // 821 us, conflicts 82 M -> 53 M).  The same swap on the q-pass stores and
 // the g queue removed most of the rest (22 M) but cost more selects and
-// registers than it saved (939 us), so those stay plain.
+// registers than it saved (939 us), and a 2-element-per-lane q pass (one
+// conflict-free double2 store per lane) cost more iterations than it saved
+// (accumulating call 855 -> 906 us), so those stay plain.
 template <typename A>
 __device__ __forceinline__ void ld4r(const float* p, int tx, A* out) {
   ld4(p, out);
