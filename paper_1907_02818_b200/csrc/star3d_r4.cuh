@@ -622,6 +622,229 @@ __device__ __forceinline__ void star3_v7_body(
   }
 }
 
+// ---------------------------------------------------------------------------
+// v8 (interior tiles of the radius-4 specs MODE 2 / 4; bitwise = v7):
+// the v7 tile, ring and shared-memory layout with HALF the threads -- 256,
+// each owning 4 rows x 4 k points of one field -- so the per-plane work that
+// does not scale with points (barrier, mbarrier wait, bookkeeping, the j rows
+// shared by a thread's rows: 12 row loads per 4 rows instead of 10 per 2)
+// is spread over twice the points, at 8 warps per SM and ~210 registers.
+template <int MODE>
+struct StarTile8 : StarTile7<MODE> {
+  static constexpr int ROLE = 16 * (StarTile7<MODE>::TJ / 4);  // 128 threads per field
+  static constexpr int THREADS = 2 * ROLE;
+  static constexpr int EPT = (StarTile7<MODE>::QELEMS + THREADS - 1) / THREADS;
+};
+
+template <int R, int RING>
+__device__ __forceinline__ void field4x4(const float* F, int r0, int col, float w0,
+                                         const float (&wr)[R + 1], float4 (&acc)[RING][4],
+                                         int ph) {
+  constexpr int BW = 72;
+  const float* row0 = F + r0 * BW + col;
+  float4 b[4], in[4];
+#pragma unroll
+  for (int h = 0; h < 4; h++) {
+    b[h] = lds4(row0 + h * BW);
+    in[h] = kstencil2<R>(lds4(row0 + h * BW - 4), b[h], lds4(row0 + h * BW + 4), w0, wr);
+  }
+  // j direction, each row's terms in EXACTLY field2x4's order (its pair
+  // partner first, then the other rows bottom to top), so v8 and v7 give the
+  // same bits: rows of the 4-row group from registers, the rest from shared
+  // memory (the compiler merges the repeated loads)
+#pragma unroll
+  for (int pos = 0; pos < 2 * R; pos++) {
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      // offsets of row h relative to itself, in v7's order for its pair slot
+      int off;
+      if ((h & 1) == 0) off = pos == 0 ? 1 : (pos <= R ? pos - 1 - R : pos - R + 1);
+      else off = pos == 0 ? -1 : (pos < R ? pos - 1 - R : pos - R + 1);
+      const int t = h + off;
+      const int d = off < 0 ? -off : off;
+      const float4 v = (t >= 0 && t <= 3) ? b[t < 0 ? 0 : (t > 3 ? 3 : t)] : lds4(row0 + t * BW);
+      in[h] = fmas4(wr[d], v, in[h]);
+    }
+  }
+  // i direction: this plane's sum into its slot, its centre values into the
+  // neighbouring planes' slots (the v7 ring)
+#pragma unroll
+  for (int h = 0; h < 4; h++) {
+    acc[ph][h] = add4(acc[ph][h], in[h]);
+    acc[(ph + R) % RING][h] = muls4(wr[R], b[h]);
+#pragma unroll
+    for (int r = 1; r <= R; r++) {
+      if (r < R) acc[(ph + r) % RING][h] = fmas4(wr[r], b[h], acc[(ph + r) % RING][h]);
+      acc[(ph + RING - r) % RING][h] = fmas4(wr[r], b[h], acc[(ph + RING - r) % RING][h]);
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
+    star3_v8_interior(const __grid_constant__ CUtensorMap tm_c,
+                      const __grid_constant__ CUtensorMap tm_ub,
+                      const __grid_constant__ CUtensorMap tm_u1,
+                      const __grid_constant__ CUtensorMap tm_cb,
+                      const __grid_constant__ CUtensorMap tm_u1b, float* __restrict__ c_b,
+                      float* __restrict__ u_1_b, int n, int i_base, int lo, int hi, int out_i0,
+                      int out_i1, int chunk, TileMap tmap, float D) {
+  using Tl = StarTile8<MODE>;
+  using S3 = Star3<MODE>;
+  static_assert(!S3::kU2 && !S3::kU2Set, "v8: radius-4 specs without u_2 partials");
+  constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
+  constexpr int RING = Tl::RING, NS = Tl::NS, BF = Tl::BF, QD = Tl::QD;
+  constexpr int SF = Tl::SF, TILE = Tl::TILE, ROLE = Tl::ROLE;
+  int tk, tj;
+  tmap.interior(blockIdx.x, tk, tj);
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage = reinterpret_cast<float*>(smem_raw);
+  float* qbuf = stage + NS * SF;
+  float* gq = qbuf + Tl::NQB * BF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gq + QD * TILE);
+
+  const int tid = threadIdx.x;
+  const bool q_role = tid >= ROLE;
+  const int rt = q_role ? tid - ROLE : tid;
+  const int tx = rt & 15, ty = rt >> 4;  // 4 k-points x rows 4ty .. 4ty+3
+  const int k0 = tk * TK, j0 = tj * Tl::TJ;
+  const int o_begin = out_i0 + blockIdx.y * chunk;
+  const int o_end = min(o_begin + chunk, out_i1);
+  if (o_begin >= o_end) return;
+  const int pstart = o_begin - R;
+  const int P = (o_end - o_begin) + 2 * R;
+
+  const float w0 = S3::template w<float>(0);
+  float wr[R + 1];
+  wr[0] = w0;
+#pragma unroll
+  for (int r = 1; r <= R; r++) wr[r] = S3::template w<float>(r);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int it) {
+    const int s = it % NS;
+    float* dst = stage + s * SF;
+    const int pl = pstart + it - i_base;
+    const bool emit = it >= 2 * R;
+    tma::mbar_arrive_expect_tx(
+        &bars[s], 3 * Tl::BOX_BYTES + (emit ? (S3::kU1bFresh ? 1 : 2) : 0) * TILE * 4);
+    tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK - lo, j0 - HJ - lo, pl);
+    tma::load_3d(dst + 2 * BF, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
+    if (emit) {
+      tma::load_3d(dst + 3 * BF, &tm_cb, &bars[s], k0, j0, pl - R);
+      if (!S3::kU1bFresh) tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
+    }
+  };
+  if (tid == 0)
+    for (int it = 0; it < NS && it < P; it++) issue(it);
+
+  const int jr0 = j0 + 4 * ty, kc = k0 + 4 * tx;
+  const int r0 = 4 * ty + HJ, col = HK + 4 * tx;
+  const int trow = 4 * ty * TK + 4 * tx;
+  const long long plane = (long long)n * n;
+  const int coff = jr0 * n + kc;
+
+  int qoff[Tl::EPT], goff[Tl::EPT];
+#pragma unroll
+  for (int m = 0; m < Tl::EPT; m++) {
+    const int e = tid + m * Tl::THREADS;
+    const int row = e / (BW / 4), c4 = e - row * (BW / 4);
+    qoff[m] = e < Tl::QELEMS ? row * BW + 4 * c4 : -1;
+    goff[m] = (e < Tl::QELEMS && row >= HJ && row < HJ + Tl::TJ && c4 >= 1 && c4 <= TK / 4)
+                  ? (row - HJ) * TK + 4 * (c4 - 1)
+                  : -1;
+  }
+
+  float4 acc[RING][4];
+#pragma unroll
+  for (int s = 0; s < RING; s++)
+#pragma unroll
+    for (int h = 0; h < 4; h++) acc[s][h] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  for (int base = 0; base < P; base += RING) {
+    const int par0 = base / NS;
+#pragma unroll
+    for (int ph = 0; ph < RING; ph++) {
+      const int it = base + ph;
+      if (it < P) {
+        const int s = ph % NS;
+        const int p = pstart + it;
+        const float* Cs = stage + s * SF;
+        const float* UBs = Cs + BF;
+        const float* U1s = Cs + 2 * BF;
+        float* Q = qbuf + ((it & 1) ? BF : 0);
+        float* G = gq + (it % QD) * TILE;
+        const bool emit = it >= 2 * R;
+        const int o = p - R;
+        const bool pin = p >= lo && p <= hi;
+
+        tma::mbar_wait(&bars[s], (par0 + ph / NS) & 1);
+#pragma unroll
+        for (int m = 0; m < Tl::EPT; m++) {
+          if (qoff[m] >= 0) {
+            const int qo = qoff[m];
+            const bool centre = goff[m] >= 0;
+            float4 qv = make_float4(0.f, 0.f, 0.f, 0.f), gv = qv;
+            if (pin) {
+              const float4 cv = lds4(Cs + qo);
+              const float4 du = muls4(D, lds4(UBs + qo));
+              qv = mul4(mul4(cv, cv), du);
+              if (centre) gv = mul4(muls4(2.f, cv), du);
+            }
+            *reinterpret_cast<float4*>(Q + qo) = qv;
+            if (centre) *reinterpret_cast<float4*>(G + goff[m]) = gv;
+          }
+        }
+        if (q_role && pin) {
+#pragma unroll
+          for (int h = 0; h < 4; h++)
+            acc[ph][h] = fmas4(2.f, lds4(UBs + (r0 + h) * BW + col), acc[ph][h]);
+        }
+        __syncthreads();
+        if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
+
+        field4x4<R, RING>(q_role ? Q : U1s, r0, col, w0, wr, acc, ph);
+
+        if (emit) {
+          const int es = (ph + R + 1) % RING;
+          float* obase = (q_role ? u_1_b : c_b) + (long long)(o - i_base) * plane + coff;
+          const float* OLD = Cs + 3 * BF + (q_role ? TILE : 0) + trow;
+          if (!q_role) {
+            if (o >= lo && o <= hi) {
+              const float* Go = gq + ((it - R) % QD) * TILE + trow;
+#pragma unroll
+              for (int h = 0; h < 4; h++)
+                __stcs(reinterpret_cast<float4*>(obase + h * n),
+                       fma4(lds4(Go + h * TK), acc[es][h], lds4(OLD + h * TK)));
+            }
+          } else {
+            const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
+            if (oout <= R) {
+#pragma unroll
+              for (int h = 0; h < 4; h++) {
+                const float4 old =
+                    S3::kU1bFresh ? make_float4(0.f, 0.f, 0.f, 0.f) : lds4(OLD + h * TK);
+                __stcs(reinterpret_cast<float4*>(obase + h * n), add4(old, acc[es][h]));
+              }
+            } else if (S3::kU1bFresh) {
+#pragma unroll
+              for (int h = 0; h < 4; h++)
+                __stcs(reinterpret_cast<float4*>(obase + h * n), make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 #define SGB_V7_PARAMS                                                                   \
   const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_ub,     \
       const __grid_constant__ CUtensorMap tm_u1, const __grid_constant__ CUtensorMap tm_cb, \
@@ -796,6 +1019,31 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
         (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cf.first, tm, D, pf);
     const int st = launch_status(name);
     if (st) return st;
+  }
+  if constexpr (MODE == 2 || MODE == 4) {
+    // v8 interior (bitwise = v7): 24 % fewer instructions and 18 % fewer
+    // shared wavefronts, same time at burst clocks (the TMA pipeline bounds
+    // both: the 1024^3 fresh gather 4.61 -> 4.57 ms) and ~2 % faster under the
+    // power cap (5.25 -> 5.14 ms; 768^3: 2.19 -> 2.17), slower on small grids
+    // (n = 200: +5 %): default for the fresh form (cfg 5) at n >= 512;
+    // SGB_V8_INTERIOR=0|1 forces either (scripts/v8_check.py, cfg5_ab.py)
+    const bool v8 = opt(OPT_V8_INTERIOR, MODE == 4 && g.n >= 512) != 0;
+    if (tm.n_interior() > 0 && ubwin && v8) {
+      using T8 = StarTile8<MODE>;
+      if (int r = ensure_smem((const void*)star3_v8_interior<MODE>, T8::SMEM, name)) return r;
+      star3_v8_interior<MODE><<<dim3((unsigned)tm.n_interior(), ci.second), T8::THREADS, T8::SMEM,
+                                 s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], c_b, u_1_b,
+                                      (int)g.n, (int)g.i_base, (int)lo, (int)hi, (int)out_i0,
+                                      (int)out_i1, ci.first, tm, D);
+      const int st = launch_status(name);
+      if (st) return st;
+      if (ss) {
+        if (cudaEventRecord(ss->join, ss->s) != cudaSuccess ||
+            cudaStreamWaitEvent(s, ss->join, 0) != cudaSuccess)
+          return launch_status(name);
+      }
+      return 0;
+    }
   }
   if (tm.n_interior() > 0) {
     auto k = ubwin ? star3_v7_kernel<MODE, true, true> : star3_v7_kernel<MODE, true, false>;

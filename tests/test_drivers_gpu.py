@@ -470,3 +470,25 @@ def test_normal_generator_distribution(mods):
         assert float(z.abs().max()) > 5.0
         even, odd = z[0::2], z[1::2]
         assert abs(float((even * odd).mean())) < 5 / (N / 2) ** 0.5
+
+
+@pytest.mark.parametrize("n", [72, 200])
+@pytest.mark.parametrize("fresh", [False, True])
+def test_v8_interior_bitwise_equals_v7(mods, n, fresh, sgbopt):
+    """The 4-rows-per-thread interior kernel (v8; default for the fresh form
+    at n >= 512) forms every term in v7's order: bitwise the same c_b and
+    u_1_b, accumulating and fresh."""
+    torch, api, drivers = mods
+    fam, sc = "wave3d_r4", {"D": 0.01}
+    g = torch.Generator(device="cpu").manual_seed(n)
+    base = {k: torch.randn((n, n, n), generator=g).cuda()
+            for k in ("c", "c_b", "u_1", "u_1_b", "u_b")}
+    out = {}
+    for v8 in ("0", "1"):
+        sgbopt.setenv("SGB_V8_INTERIOR", v8)
+        a = {k: v.clone() for k, v in base.items()}
+        (api.adjoint_fresh if fresh else api.adjoint)(fam, n, sc, a)
+        torch.cuda.synchronize()
+        out[v8] = a
+    for k in ("c_b", "u_1_b"):
+        assert torch.equal(out["0"][k].view(torch.int32), out["1"][k].view(torch.int32)), k
