@@ -634,6 +634,9 @@ struct StarTile8 : StarTile7<MODE> {
   static constexpr int ROLE = 16 * (StarTile7<MODE>::TJ / 4);  // 128 threads per field
   static constexpr int THREADS = 2 * ROLE;
   static constexpr int EPT = (StarTile7<MODE>::QELEMS + THREADS - 1) / THREADS;
+  // two mbarriers per stage: A (c, u_b boxes: dead after the q pass) and B
+  // (u_1 box, output tiles)
+  static constexpr size_t SMEM = StarTile7<MODE>::SMEM + StarTile7<MODE>::NS * 8;
 };
 
 template <int R, int RING>
@@ -721,29 +724,43 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
 #pragma unroll
   for (int r = 1; r <= R; r++) wr[r] = S3::template w<float>(r);
 
+  uint64_t* barsB = bars + NS;
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < NS; s++) tma::mbar_init(&bars[s], 1);
+    for (int s = 0; s < 2 * NS; s++) tma::mbar_init(&bars[s], 1);
     tma::fence_barrier_init();
   }
   __syncthreads();
-  auto issue = [&](int it) {
+  // A half of a stage: the c / u_b boxes, read only by the q pass (before the
+  // plane's barrier), so plane it + NS is requested right after plane it's
+  // barrier -- one plane earlier than the B half (u_1 box, output tiles),
+  // which is read after the barrier and freed at the next one
+  auto issueA = [&](int it) {
+    const int s = it % NS;
+    float* dst = stage + s * SF;
+    const int pl = pstart + it - i_base;
+    tma::mbar_arrive_expect_tx(&bars[s], 2 * Tl::BOX_BYTES);
+    tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK - lo, j0 - HJ - lo, pl);
+  };
+  auto issueB = [&](int it) {
     const int s = it % NS;
     float* dst = stage + s * SF;
     const int pl = pstart + it - i_base;
     const bool emit = it >= 2 * R;
     tma::mbar_arrive_expect_tx(
-        &bars[s], 3 * Tl::BOX_BYTES + (emit ? (S3::kU1bFresh ? 1 : 2) : 0) * TILE * 4);
-    tma::load_3d(dst + 0 * BF, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
-    tma::load_3d(dst + 1 * BF, &tm_ub, &bars[s], k0 - HK - lo, j0 - HJ - lo, pl);
-    tma::load_3d(dst + 2 * BF, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
+        &barsB[s], Tl::BOX_BYTES + (emit ? (S3::kU1bFresh ? 1 : 2) : 0) * TILE * 4);
+    tma::load_3d(dst + 2 * BF, &tm_u1, &barsB[s], k0 - HK, j0 - HJ, pl);
     if (emit) {
-      tma::load_3d(dst + 3 * BF, &tm_cb, &bars[s], k0, j0, pl - R);
-      if (!S3::kU1bFresh) tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &bars[s], k0, j0, pl - R);
+      tma::load_3d(dst + 3 * BF, &tm_cb, &barsB[s], k0, j0, pl - R);
+      if (!S3::kU1bFresh) tma::load_3d(dst + 3 * BF + TILE, &tm_u1b, &barsB[s], k0, j0, pl - R);
     }
   };
   if (tid == 0)
-    for (int it = 0; it < NS && it < P; it++) issue(it);
+    for (int it = 0; it < NS && it < P; it++) {
+      issueA(it);
+      issueB(it);
+    }
 
   const int jr0 = j0 + 4 * ty, kc = k0 + 4 * tx;
   const int r0 = 4 * ty + HJ, col = HK + 4 * tx;
@@ -785,7 +802,8 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
         const int o = p - R;
         const bool pin = p >= lo && p <= hi;
 
-        tma::mbar_wait(&bars[s], (par0 + ph / NS) & 1);
+        const uint32_t par = (par0 + ph / NS) & 1;
+        tma::mbar_wait(&bars[s], par);
 #pragma unroll
         for (int m = 0; m < Tl::EPT; m++) {
           if (qoff[m] >= 0) {
@@ -808,7 +826,11 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
             acc[ph][h] = fmas4(2.f, lds4(UBs + (r0 + h) * BW + col), acc[ph][h]);
         }
         __syncthreads();
-        if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
+        if (tid == 0) {
+          if (it + NS < P) issueA(it + NS);
+          if (it >= 1 && it - 1 + NS < P) issueB(it - 1 + NS);
+        }
+        tma::mbar_wait(&barsB[s], par);
 
         field4x4<R, RING>(q_role ? Q : U1s, r0, col, w0, wr, acc, ph);
 
@@ -1021,12 +1043,14 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     if (st) return st;
   }
   if constexpr (MODE == 2 || MODE == 4) {
-    // v8 interior (bitwise = v7): 24 % fewer instructions and 18 % fewer
-    // shared wavefronts, same time at burst clocks (the TMA pipeline bounds
-    // both: the 1024^3 fresh gather 4.61 -> 4.57 ms) and ~2 % faster under the
-    // power cap (5.25 -> 5.14 ms; 768^3: 2.19 -> 2.17), slower on small grids
-    // (n = 200: +5 %): default for the fresh form (cfg 5) at n >= 512;
-    // SGB_V8_INTERIOR=0|1 forces either (scripts/v8_check.py, cfg5_ab.py)
+    // v8 interior (bitwise = v7): 24 % fewer instructions, 18 % fewer shared
+    // wavefronts, and the c / u_b boxes requested a plane earlier (split
+    // stage barriers): the 1024^3 fresh gather 4.61 -> 4.44 ms at burst
+    // clocks, 5.26 -> 5.17 ms under the power cap, 768^3 1.93 -> 1.87 ms;
+    // slower for the accumulating form (the second output tile in the late
+    // half: +9 %) and on small grids (n = 200: +5 %), so the default is the
+    // fresh form (cfg 5) at n >= 512; SGB_V8_INTERIOR=0|1 forces either
+    // (scripts/v8_check.py, cfg5_ab.py)
     const bool v8 = opt(OPT_V8_INTERIOR, MODE == 4 && g.n >= 512) != 0;
     if (tm.n_interior() > 0 && ubwin && v8) {
       using T8 = StarTile8<MODE>;
