@@ -350,6 +350,263 @@ __global__ void __launch_bounds__(StarTileD<MODE>::THREADS, 1)
   }
 }
 
+// v8 form of the fp64 radius-4 gather (MODE 2 / 4, windowed seed map; opt-in,
+// SGB_F64_V8=1 -- measured no faster, see the launcher): 256
+// threads, each 4 rows x 2 k of one field -- the j rows shared by a thread's
+// 4 rows halve the shared-memory row loads per point (the kernel above is
+// bound by the shared-memory pipe) -- every term in field2x2_d's order
+// (bitwise equal to star3_f64_stream_kernel), and split stage barriers: the
+// c / u_b boxes (read only by the q pass) are requested right after the
+// plane's first barrier, a plane before the u_1 box and output tiles.
+template <int MODE>
+struct StarTileD8 : StarTileD<MODE> {
+  static constexpr int ROLE = (StarTileD<MODE>::TK / 2) * (StarTileD<MODE>::TJ / 4);  // 128
+  static constexpr int THREADS = 2 * ROLE;
+  static constexpr int EPT = (StarTileD<MODE>::QPAIRS + THREADS - 1) / THREADS;
+  static constexpr size_t SMEM = StarTileD<MODE>::SMEM + StarTileD<MODE>::NS * 8;
+};
+
+template <int MODE>
+__device__ __forceinline__ void field4x2_d(const double* F, int r0, int col, double w0,
+                                           const double (&wr)[StarTileD<MODE>::R + 1],
+                                           double2 (&acc)[StarTileD<MODE>::RING][4], int ph) {
+  constexpr int BW = StarTileD<MODE>::BW, HK = StarTileD<MODE>::HK;
+  constexpr int R = StarTileD<MODE>::R, RING = StarTileD<MODE>::RING;
+  const double* row0 = F + r0 * BW + col;
+  double2 b[4], in[4];
+#pragma unroll
+  for (int h = 0; h < 4; h++) {
+    b[h] = ldd2(row0 + h * BW);
+    in[h] = kstencil_d<R, HK>(row0 + h * BW, w0, wr);
+  }
+  // field2x2_d's per-row order: the pair partner, then the rows bottom to top
+#pragma unroll
+  for (int pos = 0; pos < 2 * R; pos++) {
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      int off;
+      if ((h & 1) == 0) off = pos == 0 ? 1 : (pos <= R ? pos - 1 - R : pos - R + 1);
+      else off = pos == 0 ? -1 : (pos < R ? pos - 1 - R : pos - R + 1);
+      const int t = h + off;
+      const int d = off < 0 ? -off : off;
+      const double2 v =
+          (t >= 0 && t <= 3) ? b[t < 0 ? 0 : (t > 3 ? 3 : t)] : ldd2(row0 + t * BW);
+      in[h] = fmad2(wr[d], v, in[h]);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 4; h++) {
+    acc[ph][h] = make_double2(acc[ph][h].x + in[h].x, acc[ph][h].y + in[h].y);
+    acc[(ph + R) % RING][h] = make_double2(wr[R] * b[h].x, wr[R] * b[h].y);
+#pragma unroll
+    for (int r = 1; r <= R; r++) {
+      if (r < R) acc[(ph + r) % RING][h] = fmad2(wr[r], b[h], acc[(ph + r) % RING][h]);
+      acc[(ph + RING - r) % RING][h] = fmad2(wr[r], b[h], acc[(ph + RING - r) % RING][h]);
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(StarTileD8<MODE>::THREADS, 1)
+    star3_f64_v8_kernel(const __grid_constant__ CUtensorMap tm_c,
+                        const __grid_constant__ CUtensorMap tm_ub,
+                        const __grid_constant__ CUtensorMap tm_u1,
+                        const __grid_constant__ CUtensorMap tm_cb,
+                        const __grid_constant__ CUtensorMap tm_u1b, double* __restrict__ c_b,
+                        double* __restrict__ u_1_b, int n, int i_base, int lo, int hi,
+                        int out_i0, int out_i1, int chunk, int tiles_k, double D) {
+  using Tl = StarTileD8<MODE>;
+  using S3 = Star3<MODE>;
+  static_assert(!S3::kU2 && !S3::kU2Set, "fp64 v8: radius-4 specs without u_2 partials");
+  constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
+  constexpr int RING = Tl::RING, NS = Tl::NS, BOX = Tl::BOX, BP = Tl::BP, QD = Tl::QD;
+  constexpr int SF = Tl::SF, TILE = Tl::TILE, ROLE = Tl::ROLE;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stage = reinterpret_cast<double*>(smem_raw);
+  double* Q = stage + NS * SF;
+  double* gq = Q + BP;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gq + QD * TILE);
+  uint64_t* barsB = bars + NS;
+
+  const int tid = threadIdx.x;
+  const bool q_role = tid >= ROLE;
+  const int rt = q_role ? tid - ROLE : tid;
+  const int tx = rt & 15, ty = rt >> 4;  // 2 k-points x rows 4ty .. 4ty+3
+  const int tk = blockIdx.x % tiles_k, tj = blockIdx.x / tiles_k;
+  const int k0 = tk * TK, j0 = tj * Tl::TJ;
+  const int o_begin = out_i0 + blockIdx.y * chunk;
+  const int o_end = min(o_begin + chunk, out_i1);
+  if (o_begin >= o_end) return;
+  const int pstart = o_begin - R;
+  const int P = (o_end - o_begin) + 2 * R;
+
+  const double w0 = S3::template w<double>(0);
+  double wr[R + 1];
+  wr[0] = w0;
+#pragma unroll
+  for (int r = 1; r <= R; r++) wr[r] = S3::template w<double>(r);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < 2 * NS; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issueA = [&](int it) {
+    const int s = it % NS;
+    double* dst = stage + s * SF;
+    const int pl = pstart + it - i_base;
+    tma::mbar_arrive_expect_tx(&bars[s], 2 * BOX * 8);
+    tma::load_3d(dst, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
+    tma::load_3d(dst + BP, &tm_ub, &bars[s], k0 - HK - lo, j0 - HJ - lo, pl);
+  };
+  auto issueB = [&](int it) {
+    const int s = it % NS;
+    double* dst = stage + s * SF;
+    const int pl = pstart + it - i_base;
+    const bool emit = it >= 2 * R;
+    tma::mbar_arrive_expect_tx(&barsB[s],
+                               (BOX + (emit ? (S3::kU1bFresh ? 1 : 2) : 0) * TILE) * 8);
+    tma::load_3d(dst + 2 * BP, &tm_u1, &barsB[s], k0 - HK, j0 - HJ, pl);
+    if (emit) {
+      tma::load_3d(dst + 3 * BP, &tm_cb, &barsB[s], k0, j0, pl - R);
+      if (!S3::kU1bFresh) tma::load_3d(dst + 3 * BP + TILE, &tm_u1b, &barsB[s], k0, j0, pl - R);
+    }
+  };
+  if (tid == 0)
+    for (int it = 0; it < NS && it < P; it++) {
+      issueA(it);
+      issueB(it);
+    }
+
+  const int jr0 = j0 + 4 * ty, kc = k0 + 2 * tx;
+  const int r0 = 4 * ty + HJ, col = HK + 2 * tx;
+  const int trow = 4 * ty * TK + 2 * tx;
+  const long long plane = (long long)n * n;
+  const long long coff = (long long)jr0 * n + kc;
+
+  int qoff[Tl::EPT], goff[Tl::EPT];
+#pragma unroll
+  for (int m = 0; m < Tl::EPT; m++) {
+    const int e = tid + m * Tl::THREADS;
+    const int row = e / (BW / 2), c2 = e - row * (BW / 2);
+    qoff[m] = e < Tl::QPAIRS ? row * BW + 2 * c2 : -1;
+    goff[m] = (e < Tl::QPAIRS && row >= HJ && row < HJ + Tl::TJ && c2 >= HK / 2 &&
+               c2 < HK / 2 + TK / 2)
+                  ? (row - HJ) * TK + 2 * (c2 - HK / 2)
+                  : -1;
+  }
+  // per-point masks: bit 2h+x for point (jr0+h, kc+x); grid bit h: row inside
+  uint32_t inb = 0, one = 0, grid = 0;
+#pragma unroll
+  for (int h = 0; h < 4; h++) {
+    const int j = jr0 + h;
+    if (j < n && kc < n) grid |= 1u << h;
+    const int jout = j < lo ? lo - j : (j > hi ? j - hi : 0);
+#pragma unroll
+    for (int x = 0; x < 2; x++) {
+      const int k = kc + x;
+      const int kout = k < lo ? lo - k : (k > hi ? k - hi : 0);
+      if (jout == 0 && kout == 0) inb |= 1u << (2 * h + x);
+      if ((jout > 0) + (kout > 0) == 1 && jout <= R && kout <= R) one |= 1u << (2 * h + x);
+    }
+  }
+
+  double2 acc[RING][4];
+#pragma unroll
+  for (int s = 0; s < RING; s++)
+#pragma unroll
+    for (int h = 0; h < 4; h++) acc[s][h] = make_double2(0.0, 0.0);
+
+  for (int base = 0; base < P; base += RING) {
+    const int par0 = base / NS;
+#pragma unroll
+    for (int ph = 0; ph < RING; ph++) {
+      const int it = base + ph;
+      if (it < P) {
+        const int s = ph % NS;
+        const int p = pstart + it;
+        const double* Cs = stage + s * SF;
+        const double* UBs = Cs + BP;
+        const double* U1s = Cs + 2 * BP;
+        double* G = gq + (it % QD) * TILE;
+        const int o = p - R;
+        const bool pin = p >= lo && p <= hi;
+        const uint32_t par = (par0 + ph / NS) & 1;
+
+        tma::mbar_wait(&bars[s], par);
+#pragma unroll
+        for (int m = 0; m < Tl::EPT; m++) {
+          if (qoff[m] >= 0) {
+            const int qo = qoff[m];
+            double2 qv = make_double2(0.0, 0.0), gv = qv;
+            if (pin) {
+              const double2 cv = ldd2(Cs + qo);
+              const double2 uv = ldd2(UBs + qo);
+              const double2 du = make_double2(D * uv.x, D * uv.y);
+              qv = make_double2(cv.x * cv.x * du.x, cv.y * cv.y * du.y);
+              gv = make_double2(2.0 * cv.x * du.x, 2.0 * cv.y * du.y);
+            }
+            *reinterpret_cast<double2*>(Q + qo) = qv;
+            if (goff[m] >= 0) *reinterpret_cast<double2*>(G + goff[m]) = gv;
+          }
+        }
+        if (q_role && pin) {
+#pragma unroll
+          for (int h = 0; h < 4; h++)
+            acc[ph][h] = fmad2(2.0, ldd2(UBs + (r0 + h) * BW + col), acc[ph][h]);
+        }
+        __syncthreads();  // Q / G of plane p complete; A half of stage s and the
+                          // B half of plane p-1's stage free
+        if (tid == 0) {
+          if (it + NS < P) issueA(it + NS);
+          if (it >= 1 && it - 1 + NS < P) issueB(it - 1 + NS);
+        }
+        tma::mbar_wait(&barsB[s], par);
+
+        field4x2_d<MODE>(q_role ? Q : U1s, r0, col, w0, wr, acc, ph);
+
+        if (it >= 2 * R) {
+          const int es = (ph + R + 1) % RING;
+          const long long obase = (long long)(o - i_base) * plane;
+          const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
+          const double* OLD = Cs + 3 * BP + (q_role ? TILE : 0) + trow;
+          if (!q_role) {
+            if (oout == 0) {
+              const double* Go = gq + ((it - R) % QD) * TILE + trow;
+#pragma unroll
+              for (int h = 0; h < 4; h++) {
+                const uint32_t mk = inb >> (2 * h);
+                if (!((grid >> h) & 1) || !(mk & 3)) continue;
+                const double2 old = ldd2(OLD + h * TK), g = ldd2(Go + h * TK);
+                const double2 a = acc[es][h];
+                const double2 nv = make_double2((mk & 1) ? fma(g.x, a.x, old.x) : old.x,
+                                                (mk & 2) ? fma(g.y, a.y, old.y) : old.y);
+                __stcs(reinterpret_cast<double2*>(c_b + obase + coff + h * n), nv);
+              }
+            }
+          } else {
+            const uint32_t reach = oout == 0 ? (inb | one) : (oout <= R ? inb : 0u);
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+              const uint32_t mk = reach >> (2 * h);
+              if (!((grid >> h) & 1) || (!S3::kU1bFresh && !(mk & 3))) continue;
+              const double2 old =
+                  S3::kU1bFresh ? make_double2(0.0, 0.0) : ldd2(OLD + h * TK);
+              const double2 a = acc[es][h];
+              const double2 nv = make_double2((mk & 1) ? old.x + a.x : old.x,
+                                              (mk & 2) ? old.y + a.y : old.y);
+              __stcs(reinterpret_cast<double2*>(u_1_b + obase + coff + h * n), nv);
+            }
+          }
+        }
+        __syncthreads();  // Q and the emitted g slot free for the next plane
+      }
+    }
+  }
+}
+
 // Same-shape TMA map restricted to the window [off, off+ext) in j and k
 // (TMA zero fill outside = the seed mask); needs a 16-byte aligned window base.
 inline int encode_3d_window_f64(CUtensorMap* map, const double* base, long long n,
@@ -424,6 +681,19 @@ inline int star3_f64_stream_gather(const Slab3& g, long long lo, long long hi, l
   }
   const int chunk = (int)((nout + nch - 1) / nch);
   const unsigned gy = (unsigned)((nout + chunk - 1) / chunk);
+  if constexpr (MODE == 2 || MODE == 4) {
+    // the v8 form (bitwise the same result): not faster here -- 768^3 4.48
+    // vs 4.52 ms accumulating, 4.27 vs 4.43 ms fresh; 1024^3 10.75 vs 10.70
+    // / 10.08 vs 10.31 ms (scripts/f64v8_check.py) -- so it is opt-in
+    if (ubw && opt(OPT_F64_V8, 0)) {
+      using T8 = StarTileD8<MODE>;
+      if (int rc = ensure_smem((const void*)star3_f64_v8_kernel<MODE>, T8::SMEM, name)) return rc;
+      star3_f64_v8_kernel<MODE><<<dim3((unsigned)tiles, gy), T8::THREADS, T8::SMEM, s>>>(
+          maps[0], maps[1], maps[2], maps[3], maps[4], c_b, u_1_b, (int)g.n, (int)g.i_base,
+          (int)lo, (int)hi, (int)out_i0, (int)out_i1, chunk, tiles_k, D);
+      return launch_status(name);
+    }
+  }
   auto kern = ubw ? star3_f64_stream_kernel<MODE, true> : star3_f64_stream_kernel<MODE, false>;
   kern<<<dim3((unsigned)tiles, gy), Tl::THREADS, Tl::SMEM, s>>>(
       maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b, (int)g.n,

@@ -492,3 +492,23 @@ def test_v8_interior_bitwise_equals_v7(mods, n, fresh, sgbopt):
         out[v8] = a
     for k in ("c_b", "u_1_b"):
         assert torch.equal(out["0"][k].view(torch.int32), out["1"][k].view(torch.int32)), k
+
+
+@pytest.mark.parametrize("fresh", [False, True])
+def test_f64_v8_bitwise_equals_two_row_form(mods, fresh, sgbopt):
+    """The opt-in 4-rows-per-thread fp64 radius-4 kernel (SGB_F64_V8=1) forms
+    every term in the 2-row kernel's order: bitwise the same result."""
+    torch, api, drivers = mods
+    n, fam, sc = 72, "wave3d_r4", {"D": 0.01}
+    g = torch.Generator(device="cpu").manual_seed(3)
+    base = {k: torch.randn((n, n, n), generator=g, dtype=torch.float64).cuda()
+            for k in ("c", "c_b", "u_1", "u_1_b", "u_b")}
+    out = {}
+    for v in ("0", "1"):
+        sgbopt.setenv("SGB_F64_V8", v)
+        a = {k: t.clone() for k, t in base.items()}
+        (api.adjoint_fresh if fresh else api.adjoint)(fam, n, sc, a)
+        torch.cuda.synchronize()
+        out[v] = a
+    for k in ("c_b", "u_1_b"):
+        assert torch.equal(out["0"][k].view(torch.int64), out["1"][k].view(torch.int64)), k
