@@ -826,9 +826,9 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
             acc[ph][h] = fmas4(2.f, lds4(UBs + (r0 + h) * BW + col), acc[ph][h]);
         }
         __syncthreads();
-        if (tid == 0) {
-          if (it + NS < P) issueA(it + NS);
+        if (tid == 0) {  // in the order they are needed: B of plane it+NS-1 first
           if (it >= 1 && it - 1 + NS < P) issueB(it - 1 + NS);
+          if (it + NS < P) issueA(it + NS);
         }
         tma::mbar_wait(&barsB[s], par);
 
