@@ -628,7 +628,7 @@ __device__ __forceinline__ void star3_v7_body(
 // each owning 4 rows x 4 k points of one field -- so the per-plane work that
 // does not scale with points (barrier, mbarrier wait, bookkeeping, the j rows
 // shared by a thread's rows: 12 row loads per 4 rows instead of 10 per 2)
-// is spread over twice the points, at 8 warps per SM and ~210 registers.
+// is spread over twice the points, at 8 warps per SM and 222 registers.
 template <int MODE>
 struct StarTile8 : StarTile7<MODE> {
   static constexpr int ROLE = 16 * (StarTile7<MODE>::TJ / 4);  // 128 threads per field
