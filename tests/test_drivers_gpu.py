@@ -472,7 +472,7 @@ def test_normal_generator_distribution(mods):
         assert abs(float((even * odd).mean())) < 5 / (N / 2) ** 0.5
 
 
-@pytest.mark.parametrize("n", [72, 200])
+@pytest.mark.parametrize("n", [72, 200, 520])
 @pytest.mark.parametrize("fresh", [False, True])
 def test_v8_interior_bitwise_equals_v7(mods, n, fresh, sgbopt):
     """The 4-rows-per-thread interior kernel (v8; default for the fresh form
