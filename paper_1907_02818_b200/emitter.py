@@ -1013,6 +1013,9 @@ class EmittedProblem:
         srcs = [self.gather_source(), self.primal_source()]
         if self.tiled_layout() is not None:
             srcs.append(self.tiled_source())
+        from . import emit_stream
+        if emit_stream.stream_layout(self) is not None:
+            srcs.append(emit_stream.stream_source(self))
         for src in srcs:
             if _lib.lib().sgb_jit_check(src.encode()) != 0:
                 raise _lib.StencilError(_lib.lib().sgb_jit_log().decode())
@@ -1024,6 +1027,9 @@ class EmittedProblem:
                 src = self.gather_source(index)
             elif which == "tiled":
                 src = self.tiled_source(index)
+            elif which == "stream":
+                from . import emit_stream
+                src = emit_stream.stream_source(self, index)
             else:
                 src = {"primal": self.primal_source, "nest": self.nest_source}[which]()
             h = ctypes.c_void_p()
@@ -1082,13 +1088,16 @@ class EmittedProblem:
                 return False
         return True
 
-    def adjoint(self, sizes, scalars, arrays, stream=None, form="flat"):
+    def adjoint(self, sizes, scalars, arrays, stream=None, form="auto"):
         """Gather adjoint (+= into every adjoint array) on the device.
-        form: "flat" (one thread per point, gather_source; the default:
-        measured faster), "tiled" (3D programs with shared subexpressions:
-        shared-memory plane rings, tiled_source; bitwise the same result).
-        At cfg 4 (768^3 wave3d_r4) flat 8.3 ms, tiled 8.5 ms fp32 and 14.7 /
-        16.6 ms fp64 (DESIGN.md, section 8(f) item 1)."""
+        form: "flat" (one thread per point, gather_source), "tiled" (3D
+        programs with shared subexpressions: shared-memory plane rings,
+        tiled_source; bitwise the flat result), "stream" (3D linear-stencil
+        programs: the hand-tuned kernels' structure generated,
+        emit_stream.py; the flat result to rounding), or "auto": stream in
+        fp32 where it applies, else flat.  At cfg 4 (768^3 wave3d_r4) fp32:
+        stream 6.0, flat 8.3, tiled 9.1 ms; fp64: flat 14.8, tiled 17.0,
+        stream 18.7 ms (DESIGN.md, section 8(f) item 1)."""
         if not self.terms:
             return
         if not self.guards_ok(sizes):
@@ -1099,8 +1108,38 @@ class EmittedProblem:
         big = max(int(np.prod([self._eval_aff(a, sizes) for a in self._shape_of(arr)]))
                   for arr in self.param_arrays("gather"))
         index = "int" if big < 2 ** 31 - 1 else "long long"
-        if form not in ("flat", "tiled"):
+        if form not in ("auto", "flat", "tiled", "stream"):
             raise _lib.StencilError(f"unknown emitted form {form!r}")
+        if form == "auto":
+            # the stream form where it applies in fp32 (cfg 4 768^3: 6.0 vs
+            # 8.3 ms flat); in fp64 the flat form is faster (14.8 vs 18.7 ms)
+            from . import emit_stream
+            form = "flat"
+            if self.T == "float" and W[2] % 4 == 0 and \
+                    not any(t.data_ptr() % 16 for t in arrays.values() if hasattr(t, "data_ptr")) \
+                    and emit_stream.stream_layout(self) is not None:
+                form = "stream"
+        if form == "stream":
+            from . import emit_stream
+            sl = emit_stream.stream_layout(self)
+            if sl is None:
+                raise _lib.StencilError(f"{self.name}: the stream form does not apply")
+            if W[2] % 4 != 0 or any(t.data_ptr() % 16 for t in arrays.values()):
+                raise _lib.StencilError(f"{self.name}: the stream form needs the innermost "
+                                        "extent a multiple of 4 and 16-byte aligned arrays")
+            gx = (W[2] + emit_stream.TK - 1) // emit_stream.TK
+            gy = (W[1] + emit_stream.TJ - 1) // emit_stream.TJ
+            nz = max(1, -(-W[0] // 256))
+            while nz < W[0] and gx * gy * nz < 2 * 148:
+                nz *= 2
+            zc = -(-W[0] // nz)
+            nz = -(-W[0] // zc)
+            if gy > 65535 or nz > 65535:
+                raise _lib.StencilError("grid too large")
+            zt = ctypes.c_int if index == "int" else ctypes.c_longlong
+            self._launch("stream", sizes, scalars, arrays, 0, stream, extra=(zt(zc),),
+                         grid=(gx, gy, nz, sl["threads"], 1, 1), index=index, smem=sl["smem"])
+            return
         lay = self.tiled_layout() if form == "tiled" else None
         if form == "tiled" and lay is None:
             raise _lib.StencilError(f"{self.name}: the tiled gather does not apply")

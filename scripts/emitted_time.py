@@ -17,7 +17,7 @@ for dt in ("f32", "f64"):
     ep = emitter.load_program("wave3d_r4", dt)
     hand = time_it(lambda: api.adjoint("wave3d_r4", n, {"D": 0.01}, arrays), iters=10, warm=2)
     out = [f"{dt} {n}^3: hand-tuned {hand:.3f} ms"]
-    for form in ("tiled", "flat"):
+    for form in ("stream", "tiled", "flat"):
         ms = time_it(lambda: ep.adjoint({"n": n}, {"D": 0.01}, arrays, form=form), iters=10,
                      warm=2)
         out.append(f"emitted {form} {ms:.3f} ms ({ms / hand:.2f}x)")

@@ -225,3 +225,90 @@ def test_tiled_form_equals_flat_form_bitwise(name):
         torch.cuda.synchronize()
         for t in {t["adjoint"] for t in info["terms"]}:
             assert torch.equal(a[t].view(torch.int64), b[t].view(torch.int64)), (name, n, t)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("name", ["wave3d", "wave3d_c", "wave3d_c2", "wave3d_r4"] + FUZZ)
+def test_stream_form_matches_flat(name):
+    """The stream form (emit_stream.py: staged planes, register rings, the
+    hand-tuned kernels' structure generated from the program) agrees with the
+    flat form to rounding -- fp64 1e-12, fp32 1e-5 in the compare_grids
+    metric -- and leaves the same cells untouched (NaN sentinels), on full
+    and partial tiles and several outer-counter chunks."""
+    import torch
+    from paper_1907_02818_b200 import emit_stream, emitter
+    with tempfile.TemporaryDirectory() as td:
+        spec, _, info = problem(name, 12, td)
+    for dt, tol in (("f64", 1e-12), ("f32", 1e-5)):
+        ep = emitter.EmittedProblem(spec, info["terms"], dt)
+        if emit_stream.stream_layout(ep) is None:
+            pytest.skip("stream form does not apply")
+        td_ = torch.float64 if dt == "f64" else torch.float32
+        for n in ((20, 68) if name == "wave3d_r4" else (12, 40)):
+            sizes = {"n": n}
+            rng = np.random.default_rng(n)
+            scalars = {s: 0.3 for s in spec["scalars"]}
+            base = {}
+            for arr in ep.param_arrays():
+                shp = tuple(ep._eval_aff(a, sizes) for a in ep._shape_of(arr))
+                v = rng.standard_normal(shp)
+                if arr.endswith("_b") and arr != ep.seed:
+                    v.reshape(-1)[::7] = np.nan
+                base[arr] = torch.from_numpy(v).to(td_).cuda()
+            a = {k: v.clone() for k, v in base.items()}
+            b = {k: v.clone() for k, v in base.items()}
+            ep.adjoint(sizes, scalars, a, form="stream")
+            ep.adjoint(sizes, scalars, b, form="flat")
+            torch.cuda.synchronize()
+            for t in {t["adjoint"] for t in info["terms"]}:
+                x, y = a[t].double(), b[t].double()
+                assert torch.equal(torch.isnan(x), torch.isnan(y)), (name, dt, n, t)
+                m = ~torch.isnan(y)
+                err = float(((x[m] - y[m]).abs() / (1 + y[m].abs())).max())
+                assert err <= tol, (name, dt, n, t, err)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("name", ["wave3d_c", "wave3d_c2", "wave3d_r4"])
+def test_stream_form_matches_reference(name):
+    """fp64 stream form vs the reference's own run_program at 1e-12."""
+    import torch
+    from paper_1907_02818_b200 import emitter
+    n = 20 if name == "wave3d_r4" else 12
+    rng = np.random.default_rng(7)
+    with tempfile.TemporaryDirectory() as td:
+        spec, path, info = problem(name, n, td)
+        ep = emitter.EmittedProblem(spec, info["terms"])
+        sizes = {"n": n}
+        scalars = {s: float(rng.uniform(0.1, 0.9)) for s in spec["scalars"]}
+        host = {}
+        for arr in ep.param_arrays():
+            shp = tuple(ep._eval_aff(a, sizes) for a in ep._shape_of(arr))
+            v = rng.uniform(1.5, 4.5, shp) if arr == "c" else rng.standard_normal(shp)
+            host[arr] = v
+            v.astype(np.float64).tofile(os.path.join(td, arr + ".f64"))
+        out = os.path.join(td, "out")
+        os.makedirs(out)
+        harness("run", path, n, td, out, *[f"{k}={v!r}" for k, v in scalars.items()])
+        dev = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
+        ep.adjoint(sizes, scalars, dev, form="stream")
+        torch.cuda.synchronize()
+        for t in {t["adjoint"] for t in info["terms"]}:
+            want = np.fromfile(os.path.join(out, f"gather_{t}.f64")).reshape(host[t].shape)
+            assert oracle.max_rel_err(dev[t].cpu().numpy(), want) <= 1e-12, (name, t)
+
+
+def test_stream_form_layouts():
+    """Which programs the stream form takes (CPU): the 3D config families
+    (two rings: the c_b term's Laplacian of u_1 and the shared q = D c^2 u_b
+    taps), not the 1D / 2D ones."""
+    from paper_1907_02818_b200 import emit_stream, emitter
+    lay = emit_stream.stream_layout(emitter.load_program("wave3d_r4", "f32"))
+    assert lay["roles"] == ["c_b", "u_1_b"] and lay["R"] == 4 and lay["HJ"] == 4
+    assert lay["rings"]["c_b"]["kind"] == "lin" and len(lay["rings"]["c_b"]["taps"]) == 25
+    assert lay["rings"]["u_1_b"]["kind"] == "fac" and len(lay["rings"]["u_1_b"]["taps"]) == 24
+    assert lay["points"]["u_1_b"] == [13]
+    for fam in ("wave1d", "burgers2d", "lap1d", "burgers1d"):
+        assert emit_stream.stream_layout(emitter.load_program(fam, "f32")) is None
