@@ -12,11 +12,12 @@ from scripts.quick_time import time_it  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 768
 for dt in ("f32", "f64"):
     arrays = bench.gen_inputs(api, torch, "wave3d_r4", n, None, dt)
-    for rpt, unroll in ((1, False), (1, True), (2, True)):
-        emit_stream.RPT, emit_stream.UNROLL = rpt, unroll
+    for tj, rpt, unroll in ((32, 1, False), (16, 1, False), (8, 1, False), (16, 2, False)):
+        emit_stream.TJ, emit_stream.RPT, emit_stream.UNROLL = tj, rpt, unroll
         ep = emitter.load_program("wave3d_r4", dt)
         ms = time_it(lambda: ep.adjoint({"n": n}, {"D": 0.01}, arrays, form="stream"),
                      iters=10, warm=2)
-        print(f"{dt} rows/thread {rpt} unrolled {unroll}: {ms:.3f} ms", flush=True)
+        print(f"{dt} tile rows {tj} rows/thread {rpt} unrolled {unroll}: {ms:.3f} ms",
+              flush=True)
     del arrays
     torch.cuda.empty_cache()
