@@ -828,7 +828,14 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
         __syncthreads();
         if (tid == 0) {  // in the order they are needed: B of plane it+NS-1 first
           if (it >= 1 && it - 1 + NS < P) issueB(it - 1 + NS);
-          if (it + NS < P) issueA(it + NS);
+          // the early A half pays for the fresh form only: with the second
+          // output tile (accumulating form) in the late half it loses 9-11 %,
+          // so there both halves of a plane are requested together
+          if (S3::kU1bFresh) {
+            if (it + NS < P) issueA(it + NS);
+          } else if (it >= 1 && it - 1 + NS < P) {
+            issueA(it - 1 + NS);
+          }
         }
         tma::mbar_wait(&barsB[s], par);
 
