@@ -1020,7 +1020,15 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     return launch_status(name);
   }
   const bool partial = out_i0 != 0 || out_i1 != g.n;
-  const bool unified = opt_flag(OPT_V7_UNIFIED) || (partial && !opt_flag(OPT_V7_SPLIT));
+  // v8 interior (below) for the fresh form at n >= 512
+  const bool v8 = (MODE == 2 || MODE == 4) && opt(OPT_V8_INTERIOR, MODE == 4 && g.n >= 512) != 0;
+  // partial plane ranges (z-slabs, edge bands) take one unified v7 launch
+  // (fewer CTA waves) -- except when the interior runs v8: the split launch
+  // then wins for slabs too (cfg 5 per-rank step at N = 2 / 4 / 8: 0.99 /
+  // 0.94 / 0.87 of single-GPU/N against 0.96 / 0.89 / 0.84 unified,
+  // scripts/cfg5_rank_time.py); both give the same bits
+  const bool unified =
+      opt_flag(OPT_V7_UNIFIED) || (partial && !opt_flag(OPT_V7_SPLIT) && !(v8 && ubwin));
   if (ubwin && unified) {
     const auto cu = chunking(OPT_ICHUNKS, (long long)tm.tiles_k * tm.tiles_j);
     star3_v7_unified<MODE, true>
@@ -1058,7 +1066,6 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
     // half: +9 %) and on small grids (n = 200: +5 %), so the default is the
     // fresh form (cfg 5) at n >= 512; SGB_V8_INTERIOR=0|1 forces either
     // (scripts/v8_check.py, cfg5_ab.py)
-    const bool v8 = opt(OPT_V8_INTERIOR, MODE == 4 && g.n >= 512) != 0;
     if (tm.n_interior() > 0 && ubwin && v8) {
       using T8 = StarTile8<MODE>;
       if (int r = ensure_smem((const void*)star3_v8_interior<MODE>, T8::SMEM, name)) return r;

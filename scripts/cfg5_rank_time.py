@@ -4,7 +4,7 @@ owned planes (one launch) and the fresh gather over its owned planes (one
 launch) -- while its halo exchange is emulated by copy-engine copies of the
 same volume on a side stream (R planes of u_1 and u_b in and out per interior
 side: what the library's IPC transport pushes), vs the single-GPU step / N.
-python scripts/cfg5_rank_time.py [n] [steps]"""
+python scripts/cfg5_rank_time.py [n] [steps] [OPT=V ...]  (options applied to every call)"""
 import sys
 
 import torch
@@ -14,6 +14,9 @@ from paper_1907_02818_b200 import api, drivers, slab  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+for kv in sys.argv[3:]:
+    k, v = kv.split("=")
+    api.set_option(k, int(v))
 R, fam, sc = 4, "wave3d_r4", {"D": 0.01}
 
 
