@@ -683,23 +683,18 @@ __device__ __forceinline__ void field4x4(const float* F, int r0, int col, float 
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
-    star3_v8_interior(const __grid_constant__ CUtensorMap tm_c,
-                      const __grid_constant__ CUtensorMap tm_ub,
-                      const __grid_constant__ CUtensorMap tm_u1,
-                      const __grid_constant__ CUtensorMap tm_cb,
-                      const __grid_constant__ CUtensorMap tm_u1b, float* __restrict__ c_b,
-                      float* __restrict__ u_1_b, int n, int i_base, int lo, int hi, int out_i0,
-                      int out_i1, int chunk, TileMap tmap, float D) {
+template <int MODE, bool INT>
+__device__ __forceinline__ void star3_v8_body(
+    const CUtensorMap& tm_c, const CUtensorMap& tm_ub, const CUtensorMap& tm_u1,
+    const CUtensorMap& tm_cb, const CUtensorMap& tm_u1b, float* __restrict__ c_b,
+    float* __restrict__ u_1_b, int n, int i_base, int lo, int hi, int out_i0, int out_i1,
+    int chunk, int tk, int tj, float D) {
   using Tl = StarTile8<MODE>;
   using S3 = Star3<MODE>;
   static_assert(!S3::kU2 && !S3::kU2Set, "v8: radius-4 specs without u_2 partials");
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, TK = Tl::TK;
   constexpr int RING = Tl::RING, NS = Tl::NS, BF = Tl::BF, QD = Tl::QD;
   constexpr int SF = Tl::SF, TILE = Tl::TILE, ROLE = Tl::ROLE;
-  int tk, tj;
-  tmap.interior(blockIdx.x, tk, tj);
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage = reinterpret_cast<float*>(smem_raw);
@@ -779,6 +774,33 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
                   : -1;
   }
 
+  // frame tiles: plane-independent per-point masks (v7's, for 4 rows):
+  //   fmA bit 4h+x: centre (h, x) with j, k in [lo, hi]
+  //   fmB bit 4h+x: exactly one of j, k outside [lo, hi], by <= R
+  //   fk  bit x: k = kc + x in [lo, hi]; fr bit h: row h in [lo, hi] and in
+  //   the grid; fg bit h: row h in the grid (kc < n: n % 4 == 0 on this path)
+  uint32_t fmA = 0, fmB = 0, fk = 0, fr = 0, fg = 0;
+  if (!INT) {
+#pragma unroll
+    for (int x = 0; x < 4; x++)
+      if (kc + x >= lo && kc + x <= hi) fk |= 1u << x;
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      const int j = jr0 + h;
+      const bool grid = j < n && kc < n;
+      const int jout = j < lo ? lo - j : (j > hi ? j - hi : 0);
+      if (grid) fg |= 1u << h;
+      if (grid && jout == 0) fr |= 1u << h;
+#pragma unroll
+      for (int x = 0; x < 4; x++) {
+        const int k = kc + x;
+        const int kout = k < lo ? lo - k : (k > hi ? k - hi : 0);
+        if (jout == 0 && kout == 0) fmA |= 1u << (4 * h + x);
+        if ((jout > 0) + (kout > 0) == 1 && jout <= R && kout <= R) fmB |= 1u << (4 * h + x);
+      }
+    }
+  }
+
   float4 acc[RING][4];
 #pragma unroll
   for (int s = 0; s < RING; s++)
@@ -849,9 +871,31 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
             if (o >= lo && o <= hi) {
               const float* Go = gq + ((it - R) % QD) * TILE + trow;
 #pragma unroll
-              for (int h = 0; h < 4; h++)
-                __stcs(reinterpret_cast<float4*>(obase + h * n),
-                       fma4(lds4(Go + h * TK), acc[es][h], lds4(OLD + h * TK)));
+              for (int h = 0; h < 4; h++) {
+                const float4 old = lds4(OLD + h * TK);
+                float4 nv = fma4(lds4(Go + h * TK), acc[es][h], old);
+                if (!INT) {
+                  if (!((fr >> h) & 1)) continue;
+                  nv = make_float4(fk & 1 ? nv.x : old.x, fk & 2 ? nv.y : old.y,
+                                   fk & 4 ? nv.z : old.z, fk & 8 ? nv.w : old.w);
+                }
+                __stcs(reinterpret_cast<float4*>(obase + h * n), nv);
+              }
+            }
+          } else if (!INT) {
+            // reached iff at most one coordinate is outside [lo, hi], by <= R
+            const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
+            const uint32_t reach = oout == 0 ? (fmA | fmB) : (oout <= R ? fmA : 0u);
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+              const uint32_t mk = (reach >> (4 * h)) & 0xf;
+              if (!((fg >> h) & 1) || (!S3::kU1bFresh && !mk)) continue;
+              const float4 old =
+                  S3::kU1bFresh ? make_float4(0.f, 0.f, 0.f, 0.f) : lds4(OLD + h * TK);
+              const float4 a = acc[es][h];
+              __stcs(reinterpret_cast<float4*>(obase + h * n),
+                     make_float4(mk & 1 ? old.x + a.x : old.x, mk & 2 ? old.y + a.y : old.y,
+                                 mk & 4 ? old.z + a.z : old.z, mk & 8 ? old.w + a.w : old.w));
             }
           } else {
             const int oout = o < lo ? lo - o : (o > hi ? o - hi : 0);
@@ -872,6 +916,31 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
       }
     }
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
+    star3_v8_kernel(const __grid_constant__ CUtensorMap tm_c,
+                    const __grid_constant__ CUtensorMap tm_ub,
+                    const __grid_constant__ CUtensorMap tm_u1,
+                    const __grid_constant__ CUtensorMap tm_cb,
+                    const __grid_constant__ CUtensorMap tm_u1b, float* __restrict__ c_b,
+                    float* __restrict__ u_1_b, int n, int i_base, int lo, int hi, int out_i0,
+                    int out_i1, int chunk, TileMap tmap, float D, int which) {
+  // which: 0 interior rectangle, 1 frame (a single launch over all tiles
+  // with a per-CTA body choice measured 1.75x slower: 8.1 vs 4.6 ms at 1024^3)
+  int tk, tj;
+  const bool interior = which == 0;
+  if (interior)
+    tmap.interior(blockIdx.x, tk, tj);
+  else
+    tmap.frame(blockIdx.x, tk, tj);
+  if (interior)
+    star3_v8_body<MODE, true>(tm_c, tm_ub, tm_u1, tm_cb, tm_u1b, c_b, u_1_b, n, i_base, lo, hi,
+                              out_i0, out_i1, chunk, tk, tj, D);
+  else
+    star3_v8_body<MODE, false>(tm_c, tm_ub, tm_u1, tm_cb, tm_u1b, c_b, u_1_b, n, i_base, lo,
+                               hi, out_i0, out_i1, chunk, tk, tj, D);
 }
 
 #define SGB_V7_PARAMS                                                                   \
@@ -1037,6 +1106,40 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
             (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cu.first, tm, D, pf);
     return launch_status(name);
   }
+  if constexpr (MODE == 2 || MODE == 4) {
+    // v8 (bitwise = v7): 24 % fewer instructions, 18 % fewer shared
+    // wavefronts, and for the fresh form the c / u_b boxes requested a plane
+    // earlier (split stage barriers): the 1024^3 fresh gather 4.61 -> 4.44 ms
+    // at burst clocks, 5.26 -> 5.17 ms under the power cap, 768^3 1.93 ->
+    // 1.87 ms; the accumulating form gains < 1 %, small grids lose (n = 200:
+    // +5 %), so the default is the fresh form (cfg 5) at n >= 512;
+    // SGB_V8_INTERIOR=0|1 forces either (scripts/v8_check.py, cfg5_ab.py).
+    // SGB_V8_FRAME=1: the frame tiles in v8 too (bitwise the same; 1024^3
+    // 4.62 -> 4.54 ms but 768^3 1.87 -> 1.92 ms, so off by default).
+    if (tm.n_interior() > 0 && ubwin && v8) {
+      using T8 = StarTile8<MODE>;
+      if (int r = ensure_smem((const void*)star3_v8_kernel<MODE>, T8::SMEM, name)) return r;
+      auto launch8 = [&](int which, unsigned ctas, std::pair<int, unsigned> c) {
+        star3_v8_kernel<MODE><<<dim3(ctas, c.second), T8::THREADS, T8::SMEM, s>>>(
+            maps[0], maps[1], maps[2], maps[3], maps[4], c_b, u_1_b, (int)g.n, (int)g.i_base,
+            (int)lo, (int)hi, (int)out_i0, (int)out_i1, c.first, tm, D, which);
+        return launch_status(name);
+      };
+      if (tm.n_frame() > 0) {
+        if (opt_flag(OPT_V8_FRAME)) {
+          if (int st = launch8(1, (unsigned)tm.n_frame(), cf)) return st;
+        } else {
+          star3_v7_kernel<MODE, false, true>
+              <<<dim3((unsigned)tm.n_frame(), cf.second), Tl::THREADS, Tl::SMEM, s>>>(
+                  maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], c_b, u_1_b, u_2_b,
+                  (int)g.n, (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1,
+                  cf.first, tm, D, pf);
+          if (int st = launch_status(name)) return st;
+        }
+      }
+      return launch8(0, (unsigned)tm.n_interior(), ci);
+    }
+  }
   // Frame launch on a side stream, concurrent with the interior launch
   // (SGB_FORK=1): an A/B with alternating order (scripts/cfg5_ab.py) measured
   // it slower at 1024^3 (4.75 vs 4.67 ms) and 768^3 (1.99 vs 1.86 ms), so the
@@ -1056,32 +1159,6 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
         (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1, cf.first, tm, D, pf);
     const int st = launch_status(name);
     if (st) return st;
-  }
-  if constexpr (MODE == 2 || MODE == 4) {
-    // v8 interior (bitwise = v7): 24 % fewer instructions, 18 % fewer shared
-    // wavefronts, and the c / u_b boxes requested a plane earlier (split
-    // stage barriers): the 1024^3 fresh gather 4.61 -> 4.44 ms at burst
-    // clocks, 5.26 -> 5.17 ms under the power cap, 768^3 1.93 -> 1.87 ms;
-    // slower for the accumulating form (the second output tile in the late
-    // half: +9 %) and on small grids (n = 200: +5 %), so the default is the
-    // fresh form (cfg 5) at n >= 512; SGB_V8_INTERIOR=0|1 forces either
-    // (scripts/v8_check.py, cfg5_ab.py)
-    if (tm.n_interior() > 0 && ubwin && v8) {
-      using T8 = StarTile8<MODE>;
-      if (int r = ensure_smem((const void*)star3_v8_interior<MODE>, T8::SMEM, name)) return r;
-      star3_v8_interior<MODE><<<dim3((unsigned)tm.n_interior(), ci.second), T8::THREADS, T8::SMEM,
-                                 s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], c_b, u_1_b,
-                                      (int)g.n, (int)g.i_base, (int)lo, (int)hi, (int)out_i0,
-                                      (int)out_i1, ci.first, tm, D);
-      const int st = launch_status(name);
-      if (st) return st;
-      if (ss) {
-        if (cudaEventRecord(ss->join, ss->s) != cudaSuccess ||
-            cudaStreamWaitEvent(s, ss->join, 0) != cudaSuccess)
-          return launch_status(name);
-      }
-      return 0;
-    }
   }
   if (tm.n_interior() > 0) {
     auto k = ubwin ? star3_v7_kernel<MODE, true, true> : star3_v7_kernel<MODE, true, false>;

@@ -512,3 +512,30 @@ def test_f64_v8_bitwise_equals_two_row_form(mods, fresh, sgbopt):
         out[v] = a
     for k in ("c_b", "u_1_b"):
         assert torch.equal(out["0"][k].view(torch.int64), out["1"][k].view(torch.int64)), k
+
+
+@pytest.mark.parametrize("n", [72, 200, 520])
+@pytest.mark.parametrize("fresh", [False, True])
+@pytest.mark.parametrize("opts", [{"SGB_V8_FRAME": "1"},
+                                  {"SGB_V8_FRAME": "1", "SGB_ICHUNKS": "3", "SGB_ICHUNKS_F": "5"}])
+def test_v8_frame_bitwise_equal_v7(mods, n, fresh, opts, sgbopt):
+    """v8's frame body (per-point masks for 4 rows) gives v7's bits, full
+    grids with partial tiles, any i-chunking."""
+    torch, api, drivers = mods
+    fam, sc = "wave3d_r4", {"D": 0.01}
+    g = torch.Generator(device="cpu").manual_seed(n + 7)
+    base = {k: torch.randn((n, n, n), generator=g).cuda()
+            for k in ("c", "c_b", "u_1", "u_1_b", "u_b")}
+    out = {}
+    for variant in ("v7", "v8"):
+        with sgbopt.context() as m:
+            m.setenv("SGB_V8_INTERIOR", "1" if variant == "v8" else "0")
+            if variant == "v8":
+                for k, v in opts.items():
+                    m.setenv(k, v)
+            a = {k: t.clone() for k, t in base.items()}
+            (api.adjoint_fresh if fresh else api.adjoint)(fam, n, sc, a)
+            torch.cuda.synchronize()
+        out[variant] = a
+    for k in ("c_b", "u_1_b"):
+        assert torch.equal(out["v7"][k].view(torch.int32), out["v8"][k].view(torch.int32)), k
