@@ -653,13 +653,33 @@ class Workload:
         call(self.family, self.n, self.scalars, probe, sl.base, sl.nplanes, sl.own0, sl.own1)
         t0 = self.t
         self.step()  # the pipeline's step t0 (its inputs: step t0's)
+        drained = self._watchdog(float(os.environ.get("SGB_BENCH_VERIFY_TIMEOUT", "120")))
         torch.cuda.synchronize()
         if self.regen and t0 != 0:
             raise RuntimeError("verify() must run before any other step")
         a0, a1 = sl.own0 - sl.base, sl.own1 - sl.base
-        ok = all(torch.equal(self.arrays[k][a0:a1], probe[k][a0:a1]) for k in snap)
+        ok = drained and all(torch.equal(self.arrays[k][a0:a1], probe[k][a0:a1]) for k in snap)
         del probe
         return self.dist.all_ok(ok)
+
+    def _watchdog(self, seconds):
+        """Waits for the queued step with a deadline.  An IPC exchange that
+        never completes (flags that never arrive) is drained by releasing this
+        rank's flags, so the rank can still agree to fall back instead of
+        hanging.  Returns False when the deadline passed."""
+        torch = self.torch
+        ev = torch.cuda.Event()
+        ev.record()
+        deadline = time.time() + seconds
+        while not ev.query():
+            if time.time() > deadline:
+                log(f"rank {self.rank}: --halo {self.halo} step did not complete in "
+                    f"{seconds:.0f} s; releasing the plan's flags")
+                if self.plan is not None:
+                    self.plan.release()
+                return False
+            time.sleep(0.01)
+        return True
 
     def close(self):
         if self.pipe is not None:

@@ -268,6 +268,17 @@ int sgb_slab_bind(sgb_slab* plan, int set, const char* name, void* device_ptr);
 /* blob == NULL: *bytes = the blob size */
 int sgb_slab_ipc_export(const sgb_slab* plan, void* blob, long long* bytes);
 int sgb_slab_ipc_connect(sgb_slab* plan, const void* lower_blob, const void* upper_blob);
+/* Connection probe (collective, after every rank connected): phase 0 writes
+ * this rank's token into each neighbour's probe words, once by a stream memory
+ * operation and once by a copy-engine copy (the two paths the exchange uses;
+ * neither can block); phase 1, after all ranks finished phase 0 (out-of-band
+ * barrier), checks that both neighbours' tokens arrived -- an error means the
+ * box has no usable peer path and the IPC transport must not be used. */
+int sgb_slab_ipc_probe(sgb_slab* plan, int phase);
+/* Watchdog's last resort for an IPC plan whose exchange never completed:
+ * satisfies every wait on this rank's epoch flags from a fresh stream so the
+ * queued work drains; the plan's results are void and it must be destroyed. */
+int sgb_slab_release(sgb_slab* plan);
 int sgb_slab_halo_start(sgb_slab* plan, int set, unsigned fields_mask, sgb_stream_t stream);
 int sgb_slab_halo_wait(sgb_slab* plan, int set, sgb_stream_t stream);
 int sgb_slab_step(sgb_slab* plan, int set, const double* scalars, int flags,

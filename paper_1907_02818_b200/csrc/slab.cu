@@ -108,6 +108,10 @@ constexpr int kSets = 2;
 // neighbour on `side`), 1 = "data arrived" (written by that neighbour)
 constexpr int kFlagWords = kSets * 2 * 2;
 inline int flag_index(int set, int kind, int side) { return (set * 2 + kind) * 2 + side; }
+// connection probe words after the epoch flags: [side] written by a stream
+// memory operation of the neighbour on `side`, [2 + side] by its copy engine
+constexpr int kProbeWords = 4;
+inline unsigned probe_token(int rank) { return 0x53500000u | (unsigned)(rank & 0xffff); }
 
 // IPC blob: geometry + handles of every set's exchanged arrays + the flags
 struct IpcEntry {
@@ -137,7 +141,8 @@ struct sgb_slab {
   // NCCL
   ncclComm_t nccl = nullptr;
   // IPC
-  unsigned* flags = nullptr;                    // kFlagWords, this rank's memory
+  unsigned* flags = nullptr;                    // kFlagWords + kProbeWords, this rank's memory
+  unsigned* token = nullptr;                    // device word holding probe_token(rank)
   struct Peer {
     bool present = false, connected = false;
     int own0 = 0, own1 = 0, base = 0, nplanes = 0;
@@ -386,8 +391,8 @@ sgb_slab* sgb_slab_create(const char* family, int n, int dtype_bytes, int rank, 
     }
   }
   if (transport == SGB_TRANSPORT_IPC) {
-    e = cudaMalloc(&p->flags, kFlagWords * sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMemset(p->flags, 0, kFlagWords * sizeof(unsigned));
+    e = cudaMalloc(&p->flags, (kFlagWords + kProbeWords) * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(p->flags, 0, (kFlagWords + kProbeWords) * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       cuda_fail("sgb_slab_create (flags)", e);
@@ -495,6 +500,66 @@ int sgb_slab_ipc_connect(sgb_slab* p, const void* lower_blob, const void* upper_
   return 0;
 }
 
+int sgb_slab_ipc_probe(sgb_slab* p, int phase) {
+  if (!p || p->transport != SGB_TRANSPORT_IPC) return fail("sgb_slab_ipc_probe: not an IPC plan");
+  if (phase == 0) {
+    // write our token into each neighbour's probe words: once by a stream
+    // memory operation (the epoch flags' path), once by a copy-engine copy
+    // (the halo planes' path); neither can block
+    const MemOps& M = memops();
+    if (!M.write32) return fail("stream memory operations unavailable");
+    if (!p->token) {
+      cudaError_t e = cudaMalloc(&p->token, sizeof(unsigned));
+      const unsigned t = probe_token(p->rank);
+      if (e == cudaSuccess) e = cudaMemcpy(p->token, &t, sizeof(t), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return cuda_fail("sgb_slab_ipc_probe", e);
+    }
+    CUstream cs = reinterpret_cast<CUstream>(p->comm);
+    for (int side = 0; side < 2; side++) {
+      const auto& nb = p->peer[side];
+      if (!nb.present) continue;
+      if (!nb.connected) return fail("sgb_slab_ipc_probe: neighbours not connected");
+      unsigned* w = nb.flags + kFlagWords;
+      if (M.write32(cs, (CUdeviceptr)(w + (1 - side)), probe_token(p->rank), 0) != CUDA_SUCCESS)
+        return fail("sgb_slab_ipc_probe: remote cuStreamWriteValue32 failed");
+      const cudaError_t e = cudaMemcpyAsync(w + 2 + (1 - side), p->token, sizeof(unsigned),
+                                            cudaMemcpyDeviceToDevice, p->comm);
+      if (e != cudaSuccess) return cuda_fail("sgb_slab_ipc_probe (peer copy)", e);
+    }
+    const cudaError_t e = cudaStreamSynchronize(p->comm);
+    return e == cudaSuccess ? 0 : cuda_fail("sgb_slab_ipc_probe", e);
+  }
+  // phase 1 (after every rank's phase 0): both tokens of each neighbour arrived
+  unsigned w[kProbeWords];
+  const cudaError_t e =
+      cudaMemcpy(w, p->flags + kFlagWords, sizeof(w), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail("sgb_slab_ipc_probe", e);
+  for (int side = 0; side < 2; side++) {
+    if (!p->peer[side].present) continue;
+    const unsigned want = probe_token(p->rank + (side == 0 ? -1 : 1));
+    if (w[side] != want || w[2 + side] != want)
+      return fail("sgb_slab_ipc_probe: the " + std::string(side == 0 ? "lower" : "upper") +
+                  " neighbour's remote writes did not arrive (no usable peer path)");
+  }
+  return 0;
+}
+
+int sgb_slab_release(sgb_slab* p) {
+  if (!p || p->transport != SGB_TRANSPORT_IPC) return fail("sgb_slab_release: not an IPC plan");
+  // watchdog's last resort: satisfy every wait on this rank's flags (cyclic
+  // GEQ compare) from a fresh stream, so a stuck exchange drains; the plan's
+  // results are void afterwards and it must be destroyed
+  unsigned v[kFlagWords];
+  for (int s = 0; s < kSets; s++)
+    for (int i = 0; i < 4; i++) v[s * 4 + i] = p->epoch[s] + (1u << 30);
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(p->flags, v, sizeof(v), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (st) cudaStreamDestroy(st);
+  return e == cudaSuccess ? 0 : cuda_fail("sgb_slab_release", e);
+}
+
 int sgb_slab_halo_start(sgb_slab* p, int set, unsigned fields_mask, sgb_stream_t stream) {
   if (!p || set < 0 || set >= kSets) return fail("sgb_slab_halo_start: bad arguments");
   cudaStream_t st = as_stream(stream);
@@ -561,6 +626,7 @@ void sgb_slab_destroy(sgb_slab* p) {
   for (auto& nb : p->peer)
     for (auto& o : nb.opened) sgb_ipc_close(o.first, o.second);
   if (p->flags) cudaFree(p->flags);
+  if (p->token) cudaFree(p->token);
   for (int s = 0; s < kSets; s++) {
     if (p->ev_done[s]) cudaEventDestroy(p->ev_done[s]);
   }

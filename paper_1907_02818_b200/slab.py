@@ -173,7 +173,28 @@ class SlabPlan:
         hi = ct.create_string_buffer(every[self.rank + 1]) if self.rank < self.world - 1 else None
         self._lib.check(L.sgb_slab_ipc_connect(ct.c_void_p(self._p), lo, hi),
                         "sgb_slab_ipc_connect")
+        # probe both peer paths (remote stream-memop write, peer copy) before
+        # any step can wait on them: a box without a usable peer path fails
+        # here instead of hanging in the first exchange
+        dist.barrier(group=self.group)
+        rc0 = L.sgb_slab_ipc_probe(ct.c_void_p(self._p), 0)
+        dist.barrier(group=self.group)
+        rc1 = L.sgb_slab_ipc_probe(ct.c_void_p(self._p), 1) if rc0 == 0 else rc0
+        msg = L.sgb_last_error().decode(errors="replace") if rc1 else ""
+        verdicts = [None] * self.world
+        dist.all_gather_object(verdicts, (rc1, msg), group=self.group)
+        bad = [(r, v) for r, v in enumerate(verdicts) if v[0] != 0]
+        if bad:  # every rank refuses the transport together
+            r, (rc, m) = bad[0]
+            raise self._lib.StencilError(f"sgb_slab_ipc_probe failed on rank {r} ({rc}): {m}")
         return self
+
+    def release(self):
+        """IPC watchdog: drain an exchange that never completed (the plan's
+        results are void afterwards; close it)."""
+        if self.transport == "ipc" and getattr(self, "_p", None):
+            self._lib.check(self._lib.lib().sgb_slab_release(self._ct.c_void_p(self._p)),
+                            "sgb_slab_release")
 
     def _stream(self, stream):
         import torch

@@ -128,6 +128,11 @@ static int run_rank(int rank, int world, int n, int T, int to_parent, int from_p
     return 4;
   CK(sgb_slab_ipc_connect(plan, rank > 0 ? &all[(rank - 1) * bytes] : nullptr,
                           rank < world - 1 ? &all[(rank + 1) * bytes] : nullptr));
+  // connection probe: every rank's phase 0 before anyone's phase 1
+  char sync = 1;
+  CK(sgb_slab_ipc_probe(plan, 0));
+  if (!write_all(to_parent, &sync, 1) || !read_all(from_parent, &sync, 1)) return 4;
+  CK(sgb_slab_ipc_probe(plan, 1));
   CK(sgb_slab_halo_start(plan, 0, 1u, s));  // c is static: its halo once
 
   const double sc[1] = {D};
@@ -197,7 +202,7 @@ int main(int argc, char** argv) {
     down[r] = b[1];
     pid[r] = p;
   }
-  // gather the blobs, hand every rank all of them; then one barrier round
+  // gather the blobs, hand every rank all of them; then two barrier rounds
   // (the parent never touches CUDA)
   std::vector<char> all;
   bool ok = true;
@@ -211,8 +216,10 @@ int main(int argc, char** argv) {
   }
   for (int r = 0; r < world && ok; r++) ok = write_all(down[r], all.data(), all.size());
   char tok;
-  for (int r = 0; r < world && ok; r++) ok = read_all(up[r], &tok, 1);
-  for (int r = 0; r < world && ok; r++) ok = write_all(down[r], &tok, 1);
+  for (int round = 0; round < 2; round++) {  // the probe barrier, then the final one
+    for (int r = 0; r < world && ok; r++) ok = read_all(up[r], &tok, 1);
+    for (int r = 0; r < world && ok; r++) ok = write_all(down[r], &tok, 1);
+  }
   int failures = ok ? 0 : 1;
   for (int r = 0; r < world; r++) {
     int st = 0;

@@ -127,6 +127,22 @@ def _py_rank(rank, world, port, n, steps, q):
             for k in ("c_b", "u_1_b"):
                 ok &= torch.equal(loc[k][own], want[k][sl.own0:sl.own1])
         dist.barrier()
+        if rank == 0:
+            # the bench watchdog's path: an exchange whose neighbour never
+            # joins stays queued; releasing this rank's flags drains it
+            import time
+            plan.halo_start(set_=1)
+            plan.halo_wait(set_=1)
+            ev = torch.cuda.Event()
+            ev.record()
+            time.sleep(1.0)
+            stuck = not ev.query()
+            plan.release()
+            t0 = time.time()
+            while not ev.query() and time.time() - t0 < 30:
+                time.sleep(0.01)
+            ok &= stuck and ev.query()
+        dist.barrier()
         plan.close()
         dist.barrier()
         dist.destroy_process_group()
