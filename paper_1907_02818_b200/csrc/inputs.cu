@@ -202,6 +202,43 @@ __global__ void __launch_bounds__(128) fill_normal3d_pair_kernel(
   }
 }
 
+// fp64 form of the pair kernel: each thread owns ONE Box-Muller pair (2
+// consecutive k) of both fields, so a warp's 16-byte stores cover 512
+// contiguous bytes per field.  (Four k per thread, as in the fp32 kernel,
+// left every double2 store instruction writing half of each 32-byte sector,
+// the other half by the next instruction: 3.7 TB/s at 1024^3.)  Same values.
+__global__ void __launch_bounds__(128) fill_normal3d_pair_f64_kernel(
+    double* __restrict__ d0, double* __restrict__ d1, int n, int i_base, int nplanes, int h0,
+    int h1, uint64_t key0, uint64_t key1, float mean, float scale) {
+  const int k = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int j = blockIdx.y;
+  if (k >= n) return;
+  uint32_t km0 = 0, km1 = 0;
+#pragma unroll
+  for (int m = 0; m < 2; m++) {
+    if (k + m >= h0 && k + m < n - h0) km0 |= 1u << m;
+    if (k + m >= h1 && k + m < n - h1) km1 |= 1u << m;
+  }
+  const bool j0h = j < h0 || j >= n - h0, j1h = j < h1 || j >= n - h1;
+  const long long plane = (long long)n * n;
+  const long long dg = (long long)gridDim.z * plane;
+  long long g = ((long long)(i_base + (int)blockIdx.z) * n + j) * n + k;  // global flat index
+  long long off = ((long long)blockIdx.z * n + j) * n + k;
+  for (int li = blockIdx.z; li < nplanes; li += gridDim.z, g += dg, off += dg) {
+    const int i = i_base + li;
+    const uint64_t m = (uint64_t)g >> 1;
+    const NormalPair a0 = normal_pair_polar(key0, m), a1 = normal_pair_polar(key1, m);
+    const float z0[2] = {fmaf(scale * a0.rad, a0.cs, mean), fmaf(scale * a0.rad, a0.sn, mean)};
+    const float z1[2] = {fmaf(scale * a1.rad, a1.cs, mean), fmaf(scale * a1.rad, a1.sn, mean)};
+    const uint32_t m0 = (j0h || i < h0 || i >= n - h0) ? 0u : km0;
+    const uint32_t m1 = (j1h || i < h1 || i >= n - h1) ? 0u : km1;
+    __stcs(reinterpret_cast<double2*>(d0 + off),
+           make_double2(m0 & 1 ? z0[0] : 0.f, m0 & 2 ? z0[1] : 0.f));
+    __stcs(reinterpret_cast<double2*>(d1 + off),
+           make_double2(m1 & 1 ? z1[0] : 0.f, m1 & 2 ? z1[1] : 0.f));
+  }
+}
+
 template <typename T>
 __global__ void zero_halo_kernel(T* a, int d, long long n, int h, long long i_base,
                                  long long nplanes) {
@@ -332,16 +369,23 @@ static int fill_normal3d_pair(const char* name, T* a, int halo_a, uint64_t strea
                                              (float)mean, (float)scale);
     return launch_status(name);
   }
-  // 128 threads x 4 k of one row; planes strided so the grid holds a few
-  // waves of 148 SMs x 16 resident blocks and each thread runs several planes
-  const unsigned gx = (unsigned)((n / 4 + 127) / 128);
+  // 128 threads x 4 k (fp64: 2 k) of one row; planes strided so the grid
+  // holds a few waves of 148 SMs x 16 resident blocks and each thread runs
+  // several planes
+  const int per = sizeof(T) == 8 ? 2 : 4;
+  const unsigned gx = (unsigned)((n / per + 127) / 128);
   const long long rows = (long long)gx * n;
   long long gz = (148LL * 16 * 4 + rows - 1) / rows;
   if (gz > nplanes) gz = nplanes;
   if (gz < 1) gz = 1;
-  fill_normal3d_pair_kernel<T><<<dim3(gx, (unsigned)n, (unsigned)gz), 128, 0, s>>>(
-      a, b, n, i_base, nplanes, halo_a, halo_b, hash_key(seed, stream_a),
-      hash_key(seed, stream_b), (float)mean, (float)scale);
+  if constexpr (sizeof(T) == 8)
+    fill_normal3d_pair_f64_kernel<<<dim3(gx, (unsigned)n, (unsigned)gz), 128, 0, s>>>(
+        a, b, n, i_base, nplanes, halo_a, halo_b, hash_key(seed, stream_a),
+        hash_key(seed, stream_b), (float)mean, (float)scale);
+  else
+    fill_normal3d_pair_kernel<T><<<dim3(gx, (unsigned)n, (unsigned)gz), 128, 0, s>>>(
+        a, b, n, i_base, nplanes, halo_a, halo_b, hash_key(seed, stream_a),
+        hash_key(seed, stream_b), (float)mean, (float)scale);
   return launch_status(name);
 }
 

@@ -411,7 +411,7 @@ def test_fill_normal3d_equals_elementwise_draw(mods, n):
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("n,dtype", [(64, "f32"), (64, "f64"), (36, "f32"), (30, "f32"),
+@pytest.mark.parametrize("n,dtype", [(64, "f32"), (64, "f64"), (72, "f64"), (36, "f32"), (30, "f32"),
                                      (37, "f64")])
 def test_fill_normal3d_pair_equals_two_fills(mods, n, dtype):
     """sgb_fill_normal3d_pair (cfg 5's regeneration of u_1 and the seed in one
