@@ -809,6 +809,11 @@ def run_ours(args, cfg):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, torch, api, wl, dist)
+        if e2e["mode"] == "sweep":  # the per-step call of the accumulating ABI beside it
+            abi = run_e2e(args, torch, api, wl, dist, mode="abi", steps=3)
+            e2e["accumulating_abi"] = {k: abi[k] for k in (
+                "value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step", "ms_per_step",
+                "steps", "frac_of_copy_floor", "path")}
 
     # the other scored configuration at the same N (cfg 4 beside cfg 5)
     other = None
@@ -1066,16 +1071,26 @@ def time_loop_bench(torch, api, n, scalars, arrays, T=16, K=4):
             "note": "alg bytes count the primal and fused reverse-step kernels only"}
 
 
-def run_e2e(args, torch, api, wl, dist):
+def run_e2e(args, torch, api, wl, dist, mode=None, steps=None):
     """The headline metric end to end through the host-facing entry: pinned
-    host arrays in, H2D + (N > 1: the halo exchange) + the accumulating gather
-    + D2H of the adjoints inside the timed region, every step.
-    N = 1: sgb_plan_run_adjoint_host (the host-buffer C-ABI call, H2D /
-    kernel / D2H pipelined over i-chunks).  N > 1: each rank copies its OWNED
-    planes in, the library's z-slab plan exchanges the c / u_1 / u_b halos
-    (sgb_slab_halo_start), one launch over the owned planes, the owned planes
-    of the adjoints come back."""
+    host arrays in, results back in host memory, every copy inside the timed
+    region.
+
+    mode "sweep" (cfg 5, the default there): the reverse sweep over HOST-held
+    forward states, sgb_plan_sweep_*: c and the accumulator c_b go to the
+    device when the sweep begins and c_b comes back when it ends (both inside
+    the timed region, amortised over its K steps -- the BASELINE sweep has 100);
+    each step moves u_1 and u_b in and its own adjoint u_1_b out.
+    mode "abi": one call of the accumulating reference ABI per step
+    (sgb_plan_run_adjoint_host): every array in, c_b and u_1_b back.
+    N > 1: each rank copies its OWNED planes, the library's z-slab plan
+    exchanges the halos (c once per sweep / every step in "abi" mode; u_1 and
+    u_b every step), one launch over the owned planes, the owned planes of the
+    adjoints come back."""
     family, n, scalars, sl = wl.family, wl.n, wl.scalars, wl.sl
+    if mode is None:
+        mode = "sweep" if (wl.fresh and family == "wave3d_r4") else "abi"
+    sweep = mode == "sweep"
     names = api.array_params(family, "adjoint")
     rmw = [nm for nm in names if nm.endswith("_b") and nm != SEED[family]]
     arrays = wl.arrays
@@ -1085,43 +1100,80 @@ def run_e2e(args, torch, api, wl, dist):
         host[nm].copy_(arrays[nm])
     esz = arrays[names[0]].element_size()
     torch.cuda.synchronize()
-    k = max(1, args.e2e_steps)
+    k = max(1, steps or args.e2e_steps)
     plan = None
+    once_in, once_out = (("c", "c_b"), ("c_b",)) if sweep else ((), ())
+    step_in = ("u_1", "u_b") if sweep else tuple(names)
+    step_out = ("u_1_b",) if sweep else tuple(rmw)
+    begin = end = lambda: None
     if sl is None:
-        h2d = sum(host[nm].numel() * esz for nm in names)
-        d2h = sum(host[nm].numel() * esz for nm in rmw)
+        per = host[names[0]].numel() * esz
         hp = api.Plan(family, n, "f32" if esz == 4 else "f64")
+        if sweep:
+            begin = lambda: hp.sweep_begin(host)
+            end = lambda: hp.sweep_end(host)
 
-        def step():
-            hp.run_adjoint_host(scalars, host)
-        path = "sgb_plan_run_adjoint_host (pinned host buffers, H2D / kernel / D2H " \
-               "pipelined over i-chunks)"
+            def step():
+                hp.sweep_step_host(scalars, host)
+            path = "sgb_plan_sweep_begin / _step_host x K / _end (pinned host buffers; c, " \
+                   "c_b resident over the sweep; per step H2D of u_1, u_b / the fresh " \
+                   "gather / D2H of u_1_b pipelined over i-chunks)"
+        else:
+            def step():
+                hp.run_adjoint_host(scalars, host)
+            path = "sgb_plan_run_adjoint_host (pinned host buffers, H2D / kernel / D2H " \
+                   "pipelined over i-chunks)"
     else:
         from paper_1907_02818_b200 import slab as slabmod
         dev = {nm: torch.zeros_like(arrays[nm]) for nm in names}
         transport = wl.halo if wl.halo in ("ipc", "nccl") else "ipc"
         plan = slabmod.SlabPlan(family, n, dev, wl.rank, wl.world, transport).connect()
         own = slice(sl.own0 - sl.base, sl.own1 - sl.base)
-        plane = n * n * esz
-        h2d = len(names) * sl.owned * plane
-        d2h = len(rmw) * sl.owned * plane
+        per = sl.owned * n * n * esz
 
-        def step():
-            for nm in names:
+        def up(nms):
+            for nm in nms:
                 dev[nm][own].copy_(host[nm][own], non_blocking=True)
-            plan.halo_start(("c", "u_1", "u_b"))
-            plan.step(scalars, exchanged=True)
-            for nm in rmw:
+
+        def down(nms):
+            for nm in nms:
                 host[nm][own].copy_(dev[nm][own], non_blocking=True)
-        path = (f"per rank: H2D of the owned planes, library z-slab plan halo exchange of "
-                f"c, u_1, u_b ({transport}), one launch, D2H of the owned planes of "
-                + ", ".join(rmw))
+        if sweep:
+            def begin():
+                up(once_in)
+                plan.halo_start(("c",))
+
+            def end():
+                down(once_out)
+
+            def step():
+                up(step_in)
+                plan.halo_start(("u_1", "u_b"))
+                plan.step(scalars, fresh=True, exchanged=True)
+                down(step_out)
+        else:
+            def step():
+                up(step_in)
+                plan.halo_start(("c", "u_1", "u_b"))
+                plan.step(scalars, exchanged=True)
+                down(step_out)
+        path = (f"per rank: H2D of the owned planes of {', '.join(step_in)}, library z-slab "
+                f"plan halo exchange ({transport}), one launch, D2H of the owned planes of "
+                + ", ".join(step_out)
+                + ("; c, c_b resident over the sweep (c's halo exchanged once)" if sweep else ""))
+    h2d = (len(step_in) + len(once_in) / k) * per
+    d2h = (len(step_out) + len(once_out) / k) * per
+    begin()
     step()
+    end()
+    torch.cuda.synchronize()
     dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
+    begin()
     for _ in range(k):
         step()
+    end()
     e.record()
     torch.cuda.synchronize()
     ms = dist.max(s.elapsed_time(e))[0] / k
@@ -1147,12 +1199,21 @@ def run_e2e(args, torch, api, wl, dist):
     d2h_gbs = copy_gbs(hb, db)
     floor_ms = max(h2d / 1e9 / h2d_gbs, d2h / 1e9 / d2h_gbs) * 1e3
     del host
-    return {"value": wl.points() / (ms / 1e3) / 1e9, "unit": "GPts/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "steps": k, "pcie_h2d_GBps": h2d_gbs, "pcie_d2h_GBps": d2h_gbs,
-            "copy_floor_ms": floor_ms, "frac_of_copy_floor": floor_ms / ms, "path": path,
-            "note": "e2e runs the accumulating gather of the reference ABI (<name>_b) on the "
-                    "host-held inputs; per-step regeneration is a device-side protocol detail"}
+    out = {"value": wl.points() / (ms / 1e3) / 1e9, "unit": "GPts/s",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
+           "steps": k, "pcie_h2d_GBps": h2d_gbs, "pcie_d2h_GBps": d2h_gbs,
+           "copy_floor_ms": floor_ms, "frac_of_copy_floor": floor_ms / ms, "mode": mode,
+           "path": path}
+    if sweep:
+        out["note"] = (f"host-held forward states instead of regenerated ones: per step u_1, u_b "
+                       f"H2D and u_1_b D2H; the sweep's one-off copies (c, c_b in, c_b out) are "
+                       f"inside the timed region and amortised over its {k} steps (the "
+                       f"BASELINE sweep has 100); bitwise = zeroing u_1_b and calling the "
+                       f"accumulating ABI per step (tests/test_gpu_parity.py)")
+    else:
+        out["note"] = ("one call of the accumulating reference ABI (<name>_b) on host-held "
+                       "arrays per step: every array in, the accumulated adjoints back")
+    return out
 
 
 def main():
@@ -1165,7 +1226,7 @@ def main():
     ap.add_argument("--size", "--n", dest="n", type=int, default=0,
                     help="override grid extent (--size under torchrun, whose own parser "
                          "claims --n...)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--halo", default="ipc", choices=["ipc", "nccl", "torch", "peer"],

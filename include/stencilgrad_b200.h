@@ -402,6 +402,21 @@ void sgb_plan_destroy(sgb_plan* plan);
 /* arrays[] in the reference prototype order of <family>_b (host pointers) */
 int sgb_plan_run_adjoint_host(sgb_plan* plan, const double* scalars, void** arrays,
                               sgb_stream_t stream);
+/* Reverse sweep over HOST-held forward states (BASELINE cfg 5 with the states
+ * checkpointed in host memory rather than regenerated; wave3d_r4 plans, fp32 /
+ * fp64, full grid or slab).  The reference's CPU sweep calls wave3d_r4_b
+ * (codegen.cpp:332-382) once per step with u_1_b zeroed by the caller and c,
+ * c_b staying where they are; here c and the accumulator c_b stay RESIDENT on
+ * the device between begin and end, and a step moves only u_1 and u_b in and
+ * the step's own adjoint u_1_b out -- 12 instead of 28 bytes per point over
+ * PCIe in fp32.  arrays[] in the prototype order c, c_b, u_1, u_1_b, u_b (host
+ * pointers; begin reads [0], [1]; step reads [2], [4], writes [3]; end writes
+ * [1]).  Every call returns with its copies complete.  The results are bitwise
+ * those of zeroing u_1_b and calling sgb_plan_run_adjoint_host per step. */
+int sgb_plan_sweep_begin(sgb_plan* plan, void** arrays, sgb_stream_t stream);
+int sgb_plan_sweep_step_host(sgb_plan* plan, const double* scalars, void** arrays,
+                             sgb_stream_t stream);
+int sgb_plan_sweep_end(sgb_plan* plan, void** arrays, sgb_stream_t stream);
 
 /* ---- emitted kernels (runtime compilation) ----------------
  * paper_1907_02818_b200/emitter.py generates CUDA source for the fused gather

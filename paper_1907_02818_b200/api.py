@@ -298,6 +298,41 @@ class Plan:
         _lib.check(_lib.lib().sgb_plan_run_adjoint_host(ctypes.c_void_p(self._p), sc, ptrs, s),
                    "sgb_plan_run_adjoint_host")
 
+    def _ptrs(self, host_arrays: dict, needed):
+        ptrs = (ctypes.c_void_p * len(self.names))()
+        for i, nm in enumerate(self.names):
+            a = host_arrays.get(nm)
+            if a is None:
+                if nm in needed:
+                    raise _lib.StencilError(f"Plan: host array {nm} missing")
+                continue
+            ptrs[i] = a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+        return ptrs
+
+    def sweep_begin(self, host_arrays: dict, stream=None):
+        """Start a reverse sweep over host-held states (sgb_plan_sweep_*): c and
+        the accumulator c_b go to the device once and stay there."""
+        s = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
+        _lib.check(_lib.lib().sgb_plan_sweep_begin(
+            ctypes.c_void_p(self._p), self._ptrs(host_arrays, ("c", "c_b")), s),
+            "sgb_plan_sweep_begin")
+
+    def sweep_step_host(self, scalars: dict, host_arrays: dict, stream=None):
+        """One reverse step: u_1, u_b in, u_1_b (this step's adjoint alone) out;
+        c_b accumulates on the device."""
+        sc = (ctypes.c_double * 2)(*[float(scalars[s]) for s in SCALARS[self.family]])
+        s = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
+        _lib.check(_lib.lib().sgb_plan_sweep_step_host(
+            ctypes.c_void_p(self._p), sc, self._ptrs(host_arrays, ("u_1", "u_1_b", "u_b")), s),
+            "sgb_plan_sweep_step_host")
+
+    def sweep_end(self, host_arrays: dict, stream=None):
+        """Finish the sweep: the accumulated c_b comes back to the host."""
+        s = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
+        _lib.check(_lib.lib().sgb_plan_sweep_end(
+            ctypes.c_void_p(self._p), self._ptrs(host_arrays, ("c_b",)), s),
+            "sgb_plan_sweep_end")
+
     def close(self):
         if self._p:
             _lib.lib().sgb_plan_destroy(ctypes.c_void_p(self._p))

@@ -27,6 +27,7 @@ struct sgb_plan {
   cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_out;
   int chunks = 1;
+  bool in_sweep = false;  // c, c_b resident (sgb_plan_sweep_*)
 };
 
 namespace {
@@ -148,7 +149,12 @@ void sgb_plan_destroy(sgb_plan* plan) {
 // outermost dimension (3D: local planes, 2D: rows, 1D: elements) is split
 // into C chunks; the outputs inside chunk c need inputs up to R = 1..4 units
 // beyond it, so chunk c's kernel waits for the H2D of chunks c and c+1.
-static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
+// `up` / `down`: which arrays are copied in / out (a reverse sweep keeps c and
+// c_b resident and moves only the step's states and adjoint); `fresh`: the
+// radius-4 gather writes u_1_b as the step's adjoint alone.
+static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays,
+                         const std::vector<bool>& up, const std::vector<bool>& down,
+                         bool fresh) {
   const int n = p->n, C = p->chunks, base = p->i_base;
   const int L = p->dims == 3 ? p->nplanes : n;
   // bytes of one unit of the outermost dimension
@@ -162,6 +168,7 @@ static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
   for (int c = 0; c < C; c++) {
     const int a = bound(c), b = bound(c + 1);
     for (size_t k = 0; k < na; k++) {
+      if (!up[k]) continue;
       if (cudaMemcpyAsync((char*)p->dev[k] + a * plane, (const char*)arrays[k] + a * plane,
                           (b - a) * plane, cudaMemcpyHostToDevice, p->s_h2d) != cudaSuccess) {
         sgb::set_error("sgb_plan_run_adjoint_host: H2D copy failed");
@@ -181,16 +188,20 @@ static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
       if (p->dims == 3 && p->dtype == 4) {
         float** d = reinterpret_cast<float**>(p->dev.data());
         if (p->family == "wave3d_r4")
-          rc = wave3d_r4_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L, a, b,
-                                    p->s_cmp);
+          rc = fresh ? wave3d_r4_b_fresh_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4],
+                                                  base, L, a, b, p->s_cmp)
+                     : wave3d_r4_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L,
+                                            a, b, p->s_cmp);
         else if (p->family == "wave3d_c")
           rc = wave3d_c_b_slab_f32(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], base, L,
                                    a, b, p->s_cmp);
       } else if (p->dims == 3) {
         double** d = reinterpret_cast<double**>(p->dev.data());
         if (p->family == "wave3d_r4")
-          rc = wave3d_r4_b_slab_f64(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L, a, b,
-                                    p->s_cmp);
+          rc = fresh ? wave3d_r4_b_fresh_slab_f64(n, scalars[0], d[0], d[1], d[2], d[3], d[4],
+                                                  base, L, a, b, p->s_cmp)
+                     : wave3d_r4_b_slab_f64(n, scalars[0], d[0], d[1], d[2], d[3], d[4], base, L,
+                                            a, b, p->s_cmp);
         else if (p->family == "wave3d_c")
           rc = wave3d_c_b_slab_f64(n, scalars[0], d[0], d[1], d[2], d[3], d[4], d[5], base, L,
                                    a, b, p->s_cmp);
@@ -216,7 +227,7 @@ static int run_pipelined(sgb_plan* p, const double* scalars, void** arrays) {
     if (a >= b) continue;
     const size_t off = (size_t)(a - base) * plane, len = (size_t)(b - a) * plane;
     for (size_t k = 0; k < na; k++) {
-      if (!p->rmw[k]) continue;
+      if (!down[k]) continue;
       if (cudaMemcpyAsync((char*)arrays[k] + off, (const char*)p->dev[k] + off, len,
                           cudaMemcpyDeviceToHost, p->s_d2h) != cudaSuccess) {
         sgb::set_error("sgb_plan_run_adjoint_host: D2H copy failed");
@@ -249,7 +260,8 @@ int sgb_plan_run_adjoint_host(sgb_plan* p, const double* scalars, void** arrays,
     cudaEventRecord(start, sgb::as_stream(stream));
     cudaStreamWaitEvent(p->s_h2d, start, 0);
     cudaEventDestroy(start);
-    return run_pipelined(p, scalars, arrays);
+    return run_pipelined(p, scalars, arrays, std::vector<bool>(p->dev.size(), true), p->rmw,
+                         false);
   }
   cudaStream_t s = sgb::as_stream(stream);
   const size_t na = p->dev.size();
@@ -296,6 +308,83 @@ int sgb_plan_run_adjoint_host(sgb_plan* p, const double* scalars, void** arrays,
     return -1;
   }
   return 0;
+}
+
+// ---- reverse sweep over host-held states (BASELINE cfg 5 with the forward
+// states checkpointed in host memory) ----------------------------------------
+// c is the same at every step and c_b accumulates over the sweep, so both stay
+// resident between sweep_begin and sweep_end; a step moves only u_1 and u_b in
+// and the step's own adjoint u_1_b out (8 + 4 bytes per point in fp32 against
+// the 20 + 8 of the accumulating call).  Arrays in the prototype order of
+// wave3d_r4_b: c, c_b, u_1, u_1_b, u_b.
+static int sweep_check(sgb_plan* p, void** arrays, const char* who) {
+  if (!p || !arrays) {
+    sgb::set_error(std::string(who) + ": null argument");
+    return SGB_EINVAL;
+  }
+  if (p->family != "wave3d_r4" || !p->s_cmp) {
+    sgb::set_error(std::string(who) + ": sweeps need a pipelined wave3d_r4 plan");
+    return SGB_EINVAL;
+  }
+  return 0;
+}
+
+static int sweep_copy(sgb_plan* p, void* host, int k, cudaMemcpyKind kind, sgb_stream_t stream,
+                      const char* who) {
+  if (!host) {
+    sgb::set_error(std::string(who) + ": null host array");
+    return SGB_EINVAL;
+  }
+  cudaStream_t s = sgb::as_stream(stream);
+  cudaError_t e = kind == cudaMemcpyHostToDevice
+                      ? cudaMemcpyAsync(p->dev[k], host, p->bytes, kind, s)
+                      : cudaMemcpyAsync(host, p->dev[k], p->bytes, kind, s);
+  if (e != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) {
+    sgb::set_error(std::string(who) + ": copy failed");
+    return -1;
+  }
+  return 0;
+}
+
+int sgb_plan_sweep_begin(sgb_plan* p, void** arrays, sgb_stream_t stream) {
+  if (int rc = sweep_check(p, arrays, "sgb_plan_sweep_begin")) return rc;
+  for (int k = 0; k < 2; k++)
+    if (int rc = sweep_copy(p, arrays[k], k, cudaMemcpyHostToDevice, stream,
+                            "sgb_plan_sweep_begin"))
+      return rc;
+  p->in_sweep = true;
+  return 0;
+}
+
+int sgb_plan_sweep_step_host(sgb_plan* p, const double* scalars, void** arrays,
+                             sgb_stream_t stream) {
+  if (int rc = sweep_check(p, arrays, "sgb_plan_sweep_step_host")) return rc;
+  if (!scalars || !p->in_sweep) {
+    sgb::set_error("sgb_plan_sweep_step_host: no sweep begun on this plan");
+    return SGB_EINVAL;
+  }
+  for (int k = 2; k < 5; k++)
+    if (!arrays[k]) {
+      sgb::set_error("sgb_plan_sweep_step_host: null host array");
+      return SGB_EINVAL;
+    }
+  cudaEvent_t start;
+  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  cudaEventRecord(start, sgb::as_stream(stream));
+  cudaStreamWaitEvent(p->s_h2d, start, 0);
+  cudaEventDestroy(start);
+  return run_pipelined(p, scalars, arrays, {false, false, true, false, true},
+                       {false, false, false, true, false}, true);
+}
+
+int sgb_plan_sweep_end(sgb_plan* p, void** arrays, sgb_stream_t stream) {
+  if (int rc = sweep_check(p, arrays, "sgb_plan_sweep_end")) return rc;
+  if (!p->in_sweep) {
+    sgb::set_error("sgb_plan_sweep_end: no sweep begun on this plan");
+    return SGB_EINVAL;
+  }
+  p->in_sweep = false;
+  return sweep_copy(p, arrays[1], 1, cudaMemcpyDeviceToHost, stream, "sgb_plan_sweep_end");
 }
 
 }  // extern "C"

@@ -35,6 +35,11 @@ def test_bench_line_contract(config, n):
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    if config == "5":  # the host-state sweep, the per-step accumulating ABI beside it
+        assert e["mode"] == "sweep" and e["accumulating_abi"]["value"] > 0
+        assert e["h2d_bytes_per_step"] < e["accumulating_abi"]["h2d_bytes_per_step"]
+    else:
+        assert e["mode"] == "abi"
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("reference", "port")
     assert d["clocks"]["samples"] >= 0

@@ -440,6 +440,70 @@ def test_slab_plans_reassemble_full_plan(api, name, n, nslabs):
                 assert np.array_equal(loc[k][a:b], full[k][sl.own0:sl.own1]), (rank, k)
 
 
+@pytest.mark.parametrize("n,dtype,nslabs", [(136, "f32", 1), (160, "f32", 1), (136, "f64", 1),
+                                             (40, "f32", 1), (272, "f32", 2)])
+def test_host_sweep_equals_per_step_calls(api, n, dtype, nslabs):
+    """sgb_plan_sweep_* (c, c_b resident on the device for the whole reverse
+    sweep; a step moves u_1, u_b in and its own adjoint u_1_b out) gives, bit
+    for bit, what the caller of the reference ABI gets from zeroing u_1_b and
+    calling the accumulating host entry once per step; the first step also
+    against the oracle.  nslabs = 2: one rank's slab plan (halos in the host
+    arrays) returns the owned planes of the full-grid sweep."""
+    from paper_1907_02818_b200 import slab
+    name, T = "wave3d_r4", 3
+    np_dt = np.float32 if dtype == "f32" else np.float64
+    names = api.array_params(name, "adjoint")
+    scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 31, accumulate=True)
+    c = np.ascontiguousarray(grids["c"].astype(np_dt))
+    c_b0 = np.ascontiguousarray(adjs["c_b"].astype(np_dt))
+    steps = []
+    for t in range(T):
+        _, g, a = gen.family_inputs(name, n, seed=1000 + 7 * t + n, accumulate=True)
+        steps.append((np.ascontiguousarray(g["u_1"].astype(np_dt)),
+                      np.ascontiguousarray(a["u_b"].astype(np_dt))))
+    # per-step calls of the accumulating entry, u_1_b zeroed by the caller
+    ref = {"c": c.copy(), "c_b": c_b0.copy()}
+    want_u1b = []
+    plan = api.Plan(name, n, dtype)
+    for u_1, u_b in steps:
+        ref.update(u_1=u_1.copy(), u_b=u_b.copy(), u_1_b=np.zeros_like(u_1))
+        plan.run_adjoint_host(scalars, ref)
+        want_u1b.append(ref["u_1_b"].copy())
+    plan.close()
+    ranks = [slab.decompose(n, 4, nslabs, r) for r in range(nslabs)] if nslabs > 1 else [None]
+    for sl in ranks:
+        loc = (lambda x: x) if sl is None else \
+            (lambda x: np.ascontiguousarray(x[sl.base:sl.base + sl.nplanes]))
+        own = slice(None) if sl is None else slice(sl.own0 - sl.base, sl.own1 - sl.base)
+        gown = slice(None) if sl is None else slice(sl.own0, sl.own1)
+        host = {"c": loc(c), "c_b": loc(c_b0).copy()}
+        plan = api.Plan(name, n, dtype, slab=sl)
+        with pytest.raises(api._lib.StencilError):
+            plan.sweep_step_host(scalars, {"u_1": loc(steps[0][0]), "u_b": loc(steps[0][1]),
+                                           "u_1_b": loc(steps[0][0]).copy()})
+        plan.sweep_begin(host)
+        for t, (u_1, u_b) in enumerate(steps):
+            out = np.full_like(loc(u_1), np.nan)
+            plan.sweep_step_host(scalars, {"u_1": loc(u_1), "u_b": loc(u_b), "u_1_b": out})
+            assert np.array_equal(out[own], want_u1b[t][gown]), ("u_1_b", t)
+        plan.sweep_end(host)
+        plan.close()
+        assert np.array_equal(host["c_b"][own], ref["c_b"][gown])
+    # the first step against the oracle
+    g0 = {"c": c.astype(np.float64), "u_1": steps[0][0].astype(np.float64)}
+    a0 = {"c_b": c_b0.astype(np.float64), "u_1_b": np.zeros((n, n, n)),
+          "u_b": steps[0][1].astype(np.float64)}
+    want = oracle_gather(name, n, scalars, g0, a0)
+    check_close(want_u1b[0].astype(np.float64), want["u_1_b"], dtype, "sweep step 0 u_1_b")
+
+
+def test_host_sweep_refuses_other_families(api):
+    plan = api.Plan("wave3d_c", 128, "f32")
+    with pytest.raises(api._lib.StencilError):
+        plan.sweep_begin({})
+    plan.close()
+
+
 @pytest.mark.parametrize("n", [24, 40, 68, 97])
 def test_plane_kernels_tma_equals_plain_fp64(api, n, sgbopt):
     """fp64 radius-4 plane kernels (the general-shape path behind the
