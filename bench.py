@@ -19,9 +19,14 @@ other_configs; the other configs run with ``--config 4|2|1|3``.
 value  = grid-point updates / s over all ranks (GPts/s), device time with CUDA
          events, max over ranks; inputs resident in HBM (>= 3.7 GB touched per
          rank and step >> 126 MB L2, so no flush is needed).
-e2e    = the same metric through the host-facing entry: pinned host arrays
-         in, H2D (+ the halo exchange at N > 1) + the gather + D2H of the
-         accumulated adjoints inside the timed region.
+e2e    = the same metric through the host-facing C ABI with pinned HOST
+         arrays, every copy inside the timed region.  cfg 5: the reverse
+         sweep over host-held states (sgb_plan_sweep_*: c, c_b resident on
+         the device for the sweep; per step u_1, u_b in, the fresh gather,
+         u_1_b out), with the per-step accumulating ABI call
+         (sgb_plan_run_adjoint_host: every array in, adjoints out) beside it
+         in e2e.accumulating_abi; the other configs: that per-step call.
+         N > 1: owned planes per rank + the halo exchange.
 roofline: algorithmic bytes of the step (24 B/pt gather with fresh u_1_b + 8
          B/pt regenerated inputs) / step time vs MEASURED_PEAKS.json hbm_gbs.
 fp64   = the same workload at the reference's precision, device and e2e.

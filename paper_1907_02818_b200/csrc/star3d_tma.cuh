@@ -142,28 +142,26 @@ __device__ __forceinline__ void ld4(const double* p, A* out) {
   const double2 b = *reinterpret_cast<const double2*>(p + 2);
   out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
 }
-// Row reads of the stencils: thread tx reads 4 elements at 4 tx + const.  For
-// doubles that is two 16-byte loads 32 bytes apart per lane, and the 8 lanes
-// of each 128-bit load phase then hit every other 16-byte bank group twice
-// (a 2-way conflict: 45 % of the PREC kernel's shared wavefronts, ncu).
-// Lanes with tx & 4 load their upper half first, so each phase covers all 32
-// banks once; the values land in the same registers (512^3 U2SET call 875 ->
-// 821 us, conflicts 82 M -> 53 M).  The same swap on the q-pass stores and
-// the g queue removed most of the rest (22 M) but cost more selects and
-// registers than it saved (939 us), and a 2-element-per-lane q pass (one
-// conflict-free double2 store per lane) cost more iterations than it saved
-// (accumulating call 855 -> 906 us), so those stay plain.
-template <typename A>
-__device__ __forceinline__ void ld4r(const float* p, int tx, A* out) {
-  ld4(p, out);
+// Row reads of the stencils: thread tx reads 4 elements at 4 tx + const.  With
+// doubles stored contiguously that is two 16-byte accesses 32 bytes apart per
+// lane, and the 8 lanes of each 128-bit phase hit every other 16-byte bank
+// group twice (a 2-way conflict: 45 % of the PREC kernel's shared wavefronts,
+// ncu).  The double fields of the PREC form (the q box, the g queue) are
+// therefore stored SPLIT: elements 0, 1 of every 4-element group in one half
+// (16 bytes per group, so consecutive lanes touch consecutive 16 bytes), 2, 3
+// in the other half, HALF doubles further -- every load and store phase covers
+// the 32 banks once, with no lane-dependent selects.  (Round 2 first swapped
+// the halves by lane on the loads only: 875 -> 821 us at 512^3, conflicts
+// 82 M -> 53 M wavefronts; the split layout removes the rest.)
+template <int HALF, typename A>
+__device__ __forceinline__ void ld4r(const float* p, int off, A* out) {
+  ld4(p + off, out);
 }
-template <typename A>
-__device__ __forceinline__ void ld4r(const double* p, int tx, A* out) {
-  const bool sw = (tx >> 2) & 1;
-  const double2 f = *reinterpret_cast<const double2*>(p + (sw ? 2 : 0));
-  const double2 g = *reinterpret_cast<const double2*>(p + (sw ? 0 : 2));
-  out[0] = sw ? g.x : f.x; out[1] = sw ? g.y : f.y;
-  out[2] = sw ? f.x : g.x; out[3] = sw ? f.y : g.y;
+template <int HALF, typename A>
+__device__ __forceinline__ void ld4r(const double* p, int off, A* out) {  // off % 4 == 0
+  const double2 f = *reinterpret_cast<const double2*>(p + (off >> 1));
+  const double2 g = *reinterpret_cast<const double2*>(p + HALF + (off >> 1));
+  out[0] = f.x; out[1] = f.y; out[2] = g.x; out[3] = g.y;
 }
 
 // One field's contribution from one plane: in-plane (k from a 12-element
@@ -172,15 +170,15 @@ __device__ __forceinline__ void ld4r(const double* p, int tx, A* out) {
 // accumulators (i direction).  ph is a compile-time constant after unrolling.
 // A = the accumulation type, E = the field's element type in shared memory
 // (fp32 values are widened exactly for double).
-template <int R, int RING, typename A = float, typename E = float>
+template <int R, int RING, typename A = float, typename E = float, int HALF = 0>
 __device__ __forceinline__ void star_field_plane(const E* F, int crow, int tx, A w0,
                                                  const A (&wr)[R + 1],
                                                  typename Vec4<A>::type (&acc)[RING], int ph) {
   constexpr int HK = 4, BW = 72;
   A win[12];
-  ld4r(F + crow + 4 * tx, tx, win);
-  ld4r(F + crow + 4 * tx + 4, tx, win + 4);
-  ld4r(F + crow + 4 * tx + 8, tx, win + 8);
+  ld4r<HALF>(F, crow + 4 * tx, win);
+  ld4r<HALF>(F, crow + 4 * tx + 4, win + 4);
+  ld4r<HALF>(F, crow + 4 * tx + 8, win + 8);
   A inp[4];
 #pragma unroll
   for (int m = 0; m < 4; m++) {
@@ -192,8 +190,8 @@ __device__ __forceinline__ void star_field_plane(const E* F, int crow, int tx, A
 #pragma unroll
   for (int r = 1; r <= R; r++) {
     A up[4], dn[4];
-    ld4r(F + crow - r * BW + HK + 4 * tx, tx, up);
-    ld4r(F + crow + r * BW + HK + 4 * tx, tx, dn);
+    ld4r<HALF>(F, crow - r * BW + HK + 4 * tx, up);
+    ld4r<HALF>(F, crow + r * BW + HK + 4 * tx, dn);
     inp[0] += wr[r] * (up[0] + dn[0]);
     inp[1] += wr[r] * (up[1] + dn[1]);
     inp[2] += wr[r] * (up[2] + dn[2]);
@@ -248,6 +246,8 @@ __global__ void __launch_bounds__(256, 2)
   using A4 = typename Vec4<A>::type;
   constexpr int R = Tl::R, HJ = Tl::HJ, HK = Tl::HK, BW = Tl::BW, BJ = Tl::BJ;
   constexpr int RING = Tl::RING, NS = Tl::STAGES, FW = Tl::FIELD_FLOATS, QD = Tl::QUEUE;
+  constexpr int QHALF = BW * BJ / 2;  // PREC: doubles per half of the split q box
+  static_assert((QHALF * 8) % 16 == 0 && 2 * QHALF <= FW, "split q box");
   const A D = (A)Dd;  // fp32 path: the float the host used to pass
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -354,9 +354,10 @@ __global__ void __launch_bounds__(256, 2)
           for (int m = 0; m < 4; m++)
             qv[m] = (rm && kg + m >= lo && kg + m <= hi)
                         ? D * (S3::kC2 ? cw[m] * cw[m] : cw[m]) * uw[m] : A(0);
-          if constexpr (PREC) {
-            *reinterpret_cast<double2*>(Q + row * BW + 4 * c4) = make_double2(qv[0], qv[1]);
-            *reinterpret_cast<double2*>(Q + row * BW + 4 * c4 + 2) = make_double2(qv[2], qv[3]);
+          if constexpr (PREC) {  // split halves (see ld4r): group e = row * (BW / 4) + c4
+            double2* Q2 = reinterpret_cast<double2*>(Q);
+            Q2[e] = make_double2(qv[0], qv[1]);
+            Q2[QHALF / 2 + e] = make_double2(qv[2], qv[3]);
           } else {
             *reinterpret_cast<float4*>(Q + row * BW + 4 * c4) =
                 make_float4(qv[0], qv[1], qv[2], qv[3]);
@@ -381,7 +382,13 @@ __global__ void __launch_bounds__(256, 2)
             g = Vec4<A>::make(D * ubm.x, D * ubm.y, D * ubm.z, D * ubm.w);
           }
           const int slot = (it % QD) * Tl::THREADS + tid;
-          gq[slot] = g;
+          if constexpr (PREC) {  // the queue's double4s split the same way
+            double2* g2 = reinterpret_cast<double2*>(gq);
+            g2[slot] = make_double2(g.x, g.y);
+            g2[QD * Tl::THREADS + slot] = make_double2(g.z, g.w);
+          } else {
+            gq[slot] = g;
+          }
           if (S3::kU2) uq[slot] = ubm;
         }
         __syncthreads();
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(256, 2)
 
         // ---- in-plane stencils (k window in registers, j rows from smem)
         star_field_plane<R, RING, A>(U1s, (ty + HJ) * BW, tx, w0, wr, accL, ph);
-        star_field_plane<R, RING, A, A>(Q, (ty + HJ) * BW, tx, w0, wr, accQ, ph);
+        star_field_plane<R, RING, A, A, QHALF>(Q, (ty + HJ) * BW, tx, w0, wr, accQ, ph);
         accQ[ph].x += A(2) * ubm.x;
         accQ[ph].y += A(2) * ubm.y;
         accQ[ph].z += A(2) * ubm.z;
@@ -417,7 +424,14 @@ __global__ void __launch_bounds__(256, 2)
             *reinterpret_cast<float4*>(u_1_b + gidx) = nv;
             if (oin && jin) {
               const int qs = ((it - R) % QD) * Tl::THREADS + tid;
-              const A4 g = gq[qs];
+              A4 g;
+              if constexpr (PREC) {
+                const double2* g2 = reinterpret_cast<const double2*>(gq);
+                const double2 ga = g2[qs], gb = g2[QD * Tl::THREADS + qs];
+                g = Vec4<A>::make(ga.x, ga.y, gb.x, gb.y);
+              } else {
+                g = gq[qs];
+              }
               const A4 L = accL[es];
               float4 cb = cb_old;
               if (kin[0]) cb.x = (float)((A)cb.x + g.x * L.x);
