@@ -4,6 +4,10 @@
 //   Env run_nest(const StencilLoopNest&, const Env&)           interp.hpp:56
 //   Env run_program(const AdjointProgram&, const Env&)         interp.hpp:59
 //   Env run_scatter_adjoint(const Problem&, const Env&)        interp.hpp:63
+//   Env make_env(const Problem&, sizes, seed)                  interp.hpp:45
+//   GridCompare compare_grids(a, b, rel_tol)                   interp.hpp:71
+//   DotReport dot_product_test(p, program, env, trials)        interp.hpp:83
+//   VerifyReport verify_problem(p, sizes, seed, trials, fd)    interp.hpp:102
 // with the same argument meaning and error behaviour: the input Env is taken
 // by const& and left untouched, an updated copy is returned; adjoint grids
 // are accumulated (+=); a minimum-extent guard violation, a missing grid or a
@@ -19,6 +23,7 @@
 #pragma once
 
 #include <cstddef>
+#include <cstdint>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -57,6 +62,7 @@ struct Env {
   std::map<std::string, long long> sizes;
   std::map<std::string, double> scalars;
   std::map<std::string, DenseGrid> grids;
+  std::uint64_t seed = 0;  // make_env's seed (dot_product_test derives its draws from it)
 };
 
 enum class Precision { f64, f32 };
@@ -86,6 +92,61 @@ Env run_program(const std::string& family, const Env& env, Precision p = Precisi
 // Atomic-scatter adjoint (run_scatter_adjoint semantics, ablation).
 Env run_scatter_adjoint(const std::string& family, const Env& env,
                         Precision p = Precision::f64);
+
+// make_env (interp.hpp:42-45, interp.cpp:266-288): the reference's reproducible
+// environment for `family`, value for value -- one mt19937_64 seeded with
+// `seed` feeds a normal(0,1) stream: the scalars in spec order, the primal
+// grids in declaration order, then the output's adjoint seed; input adjoints
+// start at zero (inactive arrays get no adjoint).  Host-side input
+// generation; pinned to the reference's own make_env by tests/golden/
+// ref_make_env.json.
+Env make_env(const std::string& family, const std::map<std::string, long long>& sizes,
+             std::uint64_t seed);
+
+// compare_grids (interp.hpp:66-71): max over elements of |a - b| / (1 + |b|)
+// (NaN terms never raise the maximum, as with the reference's std::max), pass
+// iff <= rel_tol; a shape mismatch throws.  Reduced on the device
+// (sgb_compare_f64).
+struct GridCompare {
+  double max_rel_err = 0.0;
+  bool pass = false;
+};
+GridCompare compare_grids(const DenseGrid& a, const DenseGrid& b, double rel_tol);
+
+// dot_product_test (interp.hpp:73-84, interp.cpp:300-389): <J v, w> = <v, J^T w>
+// with Gaussian probes, a central finite difference of the PRIMAL KERNEL on the
+// left and the GATHER ADJOINT KERNEL on the right (fp64 on the device); the
+// same draws as the reference (mix_seed(env.seed, trial, attempt)), the same
+// step h = 1e-5 (1 + max |input|), the same redraw when a min/max argument is
+// within 1e-3 of a tie (burgers2d), threshold 1e-4 (every family is nonlinear
+// in its active inputs).
+struct DotReport {
+  double max_rel_err = 0.0;
+  double threshold = 0.0;
+  int trials = 0;
+  bool pass = false;
+};
+DotReport dot_product_test(const std::string& family, const Env& env, int trials);
+
+// verify_problem (interp.hpp:86-103, interp.cpp:413-435): "oracle-equivalence"
+// = the gather adjoint kernel against the atomic-scatter adjoint kernel on
+// make_env(family, sizes, seed) at 1e-12, plus (fd) "dot-product".  text() and
+// json_text() print the reference's report layout.
+struct CheckLine {
+  std::string name;
+  double metric = 0.0;
+  double threshold = 0.0;
+  bool pass = false;
+};
+struct VerifyReport {
+  std::vector<CheckLine> checks;
+  bool pass() const;
+  std::string text() const;
+  std::string json_text() const;
+};
+VerifyReport verify_problem(const std::string& family,
+                            const std::map<std::string, long long>& sizes, std::uint64_t seed,
+                            int trials, bool fd);
 
 // Array names a call reads / writes, in the C ABI (reference emitter) order.
 std::vector<std::string> array_params(const std::string& family, const std::string& kind);

@@ -11,6 +11,8 @@
 //                                             run_scatter_adjoint (interp.cpp:183-228)
 //                                             on raw fp64 grids read from in_dir
 //   verify <spec> <n> <seed> <trials>         verify_problem (interp.cpp:413-435)
+//   makeenv <spec> <n> <seed>                 make_env (interp.cpp:266-288): scalars
+//                                             and per-grid digests as JSON
 //   b200   <spec> <n> <in_dir> S=v            run_program vs run_program_b200 (the
 //                                             INTEGRATION.md binding, b200_binding.cpp)
 //                                             on the same Env; prints the max
@@ -352,6 +354,44 @@ static int cmd_verify(const sg::Problem& p, long long n, unsigned long long seed
   return rep.pass() ? 0 : 1;
 }
 
+// Digest of a grid: element count, sum, sum of squares, first / middle / last
+// value, all at full precision (the same function sits in tests/cpp/
+// test_host_api.cpp for sgb::make_env).
+static void env_digest(std::ostream& os, const std::map<std::string, double>& scalars,
+                       const std::map<std::string, std::vector<double>>& grids) {
+  char buf[64];
+  auto num = [&](double v) {
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return std::string(buf);
+  };
+  os << "{\"scalars\":{";
+  bool first = true;
+  for (const auto& kv : scalars) {
+    os << (first ? "" : ",") << "\"" << kv.first << "\":" << num(kv.second);
+    first = false;
+  }
+  os << "},\"grids\":{";
+  first = true;
+  for (const auto& kv : grids) {
+    const std::vector<double>& d = kv.second;
+    double s = 0, q = 0;
+    for (double x : d) s += x, q += x * x;
+    os << (first ? "" : ",") << "\"" << kv.first << "\":[" << d.size() << "," << num(s) << ","
+       << num(q) << "," << num(d.empty() ? 0 : d.front()) << ","
+       << num(d.empty() ? 0 : d[d.size() / 2]) << "," << num(d.empty() ? 0 : d.back()) << "]";
+    first = false;
+  }
+  os << "}}\n";
+}
+
+static int cmd_makeenv(const sg::Problem& p, long long n, unsigned long long seed) {
+  const sg::Env env = sg::make_env(p, {{"n", n}}, seed);
+  std::map<std::string, std::vector<double>> grids;
+  for (const auto& kv : env.grids) grids[kv.first] = kv.second.data();
+  env_digest(std::cout, env.scalars, grids);
+  return 0;
+}
+
 static int cmd_emit(const sg::Problem& p, const std::string& out_dir) {
   sg::EmitOptions opts;
   opts.restrict_pointers = true;  // as cmd_bench (tools/stencilgrad.cpp:286)
@@ -383,6 +423,8 @@ int main(int argc, char** argv) {
     if (cmd == "verify" && argc >= 6)
       return cmd_verify(p, std::atoll(argv[3]), std::strtoull(argv[4], nullptr, 10),
                         std::atoi(argv[5]));
+    if (cmd == "makeenv" && argc >= 5)
+      return cmd_makeenv(p, std::atoll(argv[3]), std::strtoull(argv[4], nullptr, 10));
     if (cmd == "emit" && argc >= 4) return cmd_emit(p, argv[3]);
     if (cmd == "spec") {
       std::cout << sg::serialize_spec(p);

@@ -6,6 +6,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <random>
+#include <sstream>
 #include <type_traits>
 
 #include "stencilgrad_b200.h"
@@ -211,6 +216,229 @@ std::string Program::family() const {
 
 Env run_program(const Program& program, const Env& env, Precision p) {
   return dispatch(program.family(), env, p, 1);
+}
+
+// ---------------------------------------------------------------- verification
+// The reference's verification entry points (interp.cpp:232-435) over the
+// B200 kernels.  The draws, steps and thresholds follow the reference so a
+// report can be read beside its own; every stencil evaluation (primal, gather
+// adjoint, scatter adjoint) is a kernel launch through the C ABI.
+namespace {
+
+bool has_adjoint(const Family& f, const std::string& array) {
+  return std::find(f.adjoint.begin(), f.adjoint.end(), array + "_b") != f.adjoint.end();
+}
+
+// active inputs (declaration order), i.e. active arrays other than the output
+std::vector<std::string> active_inputs(const Family& f) {
+  std::vector<std::string> in;
+  for (const auto& a : f.primal)
+    if (a != f.out && has_adjoint(f, a)) in.push_back(a);
+  return in;
+}
+
+void fill_normal(DenseGrid& g, std::mt19937_64& rng) {  // interp.cpp:242-245
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (double& x : g.data()) x = nd(rng);
+}
+
+std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t a, std::uint64_t b) {  // :232-240
+  std::uint64_t x = seed + 0x9E3779B97F4A7C15ull * (a + 1) + 0xBF58476D1CE4E5B9ull * (b + 1);
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+
+// tie_gap_of (interp.cpp:255-263): the smallest |a - b| over the min/max nodes
+// of the primal body on its iteration space.  Only burgers2d has such nodes
+// (max(u_1, 0), min(u_1, 0) at the centre point): min |u_1| over [1, n-2]^2.
+double tie_gap_of(const Family& f, const Env& env) {
+  double gap = std::numeric_limits<double>::infinity();
+  if (std::string(f.name) != "burgers2d") return gap;
+  const long long n = env.sizes.at("n");
+  const std::vector<double>& u = env.grids.at("u_1").data();
+  for (long long i = 1; i <= n - 2; i++)
+    for (long long j = 1; j <= n - 2; j++) gap = std::min(gap, std::fabs(u[i * n + j]));
+  return gap;
+}
+
+std::string shortest(double v) {  // shortest decimal that round-trips (JSON numbers)
+  char buf[40];
+  for (int p = 1; p <= 17; p++) {
+    std::snprintf(buf, sizeof(buf), "%.*g", p, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  return buf;
+}
+
+}  // namespace
+
+Env make_env(const std::string& family, const std::map<std::string, long long>& sizes,
+             std::uint64_t seed) {
+  const Family& f = find_family(family);
+  const auto nit = sizes.find("n");
+  if (nit == sizes.end()) throw Error("size symbol 'n' missing");
+  const std::vector<long long> shape(f.d, nit->second);
+  Env env;
+  env.sizes = sizes;
+  env.seed = seed;
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (const auto& s : f.scalars) env.scalars[s] = nd(rng);
+  for (const auto& a : f.primal) {
+    DenseGrid g(shape);
+    fill_normal(g, rng);
+    env.grids[a] = std::move(g);
+  }
+  for (const auto& a : f.primal) {
+    if (!has_adjoint(f, a)) continue;
+    DenseGrid g(shape);
+    if (a == f.out) fill_normal(g, rng);
+    env.grids[a + "_b"] = std::move(g);
+  }
+  return env;
+}
+
+GridCompare compare_grids(const DenseGrid& a, const DenseGrid& b, double rel_tol) {
+  if (a.shape() != b.shape()) throw Error("grid shape mismatch");
+  const std::size_t count = a.data().size();
+  if (count == 0) return {0.0, 0.0 <= rel_tol};
+  DeviceGrids<double> dev;
+  for (const DenseGrid* g : {&a, &b}) {
+    double* d = nullptr;
+    cuda_check(cudaMalloc(&d, count * sizeof(double)), "cudaMalloc");
+    dev.p.push_back(d);
+    cuda_check(cudaMemcpy(d, g->data().data(), count * sizeof(double), cudaMemcpyHostToDevice),
+               "H2D");
+  }
+  double out4[4] = {0, 0, 0, 0};
+  if (sgb_compare_f64(dev.p[0], dev.p[1], (long long)count, out4, nullptr) != 0)
+    throw Error(std::string("compare_grids: ") + sgb_last_error());
+  return {out4[0], out4[0] <= rel_tol};
+}
+
+DotReport dot_product_test(const std::string& family, const Env& env, int trials) {
+  if (trials < 1) throw Error("dot-product test needs at least one trial");
+  const Family& f = find_family(family);
+  const double threshold = 1e-4;  // every family is nonlinear in its active inputs
+  const std::vector<std::string> inputs = active_inputs(f);
+  const bool piecewise = std::string(f.name) == "burgers2d";
+  double max_err = 0.0;
+  for (int t = 0; t < trials; t++) {
+    for (std::uint64_t attempt = 0;; attempt++) {
+      if (attempt > 200) throw Error("no tie-free base point found after 200 redraws");
+      std::mt19937_64 rng(mix_seed(env.seed, static_cast<std::uint64_t>(t), attempt));
+      Env base = env;
+      if (attempt > 0)
+        for (const auto& a : inputs) fill_normal(base.grids.at(a), rng);
+      if (piecewise && tie_gap_of(f, base) < 1e-3) continue;
+
+      std::map<std::string, DenseGrid> v;
+      for (const auto& a : inputs) {
+        DenseGrid g(base.grids.at(a).shape());
+        fill_normal(g, rng);
+        v[a] = std::move(g);
+      }
+      DenseGrid w(base.grids.at(f.out).shape());
+      fill_normal(w, rng);
+
+      double umax = 0.0;
+      for (const auto& a : inputs)
+        for (double x : base.grids.at(a).data()) umax = std::max(umax, std::fabs(x));
+      const double h = 1e-5 * (1.0 + umax);
+
+      Env plus = base, minus = base;
+      for (const auto& a : inputs) {
+        auto& gp = plus.grids.at(a).data();
+        auto& gm = minus.grids.at(a).data();
+        const auto& gv = v.at(a).data();
+        for (std::size_t i = 0; i < gv.size(); i++) {
+          gp[i] += h * gv[i];
+          gm[i] -= h * gv[i];
+        }
+      }
+      const Env rp = run_nest(family, plus);   // primal kernel
+      const Env rm = run_nest(family, minus);
+      double lhs = 0.0;
+      {
+        const auto& dp = rp.grids.at(f.out).data();
+        const auto& dm = rm.grids.at(f.out).data();
+        for (std::size_t i = 0; i < dp.size(); i++)
+          lhs += w.data()[i] * (dp[i] - dm[i]) / (2.0 * h);
+      }
+
+      Env aenv = base;
+      aenv.grids.at(f.seed) = w;
+      for (const auto& a : inputs) {
+        auto& g = aenv.grids.at(a + "_b");
+        std::fill(g.data().begin(), g.data().end(), 0.0);
+      }
+      const Env res = run_program(family, aenv);  // gather adjoint kernel
+      double rhs = 0.0;
+      for (const auto& a : inputs) {
+        const auto& gu = res.grids.at(a + "_b").data();
+        const auto& gv = v.at(a).data();
+        for (std::size_t i = 0; i < gu.size(); i++) rhs += gv[i] * gu[i];
+      }
+      max_err = std::max(max_err, std::fabs(lhs - rhs) / (1.0 + std::fabs(rhs)));
+      break;
+    }
+  }
+  return {max_err, threshold, trials, max_err <= threshold};
+}
+
+bool VerifyReport::pass() const {
+  return std::all_of(checks.begin(), checks.end(), [](const CheckLine& c) { return c.pass; });
+}
+
+std::string VerifyReport::text() const {
+  std::ostringstream os;
+  for (const auto& c : checks) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "%-20s max_rel_err=%.6e threshold=%.1e %s", c.name.c_str(),
+                  c.metric, c.threshold, c.pass ? "PASS" : "FAIL");
+    os << buf << "\n";
+  }
+  return os.str();
+}
+
+std::string VerifyReport::json_text() const {
+  std::ostringstream os;
+  os << "{\n  \"checks\": [";
+  for (std::size_t i = 0; i < checks.size(); i++) {
+    const CheckLine& c = checks[i];
+    os << (i ? "," : "") << "\n    {\n      \"name\": \"" << c.name << "\",\n      \"metric\": "
+       << shortest(c.metric) << ",\n      \"threshold\": " << shortest(c.threshold)
+       << ",\n      \"pass\": " << (c.pass ? "true" : "false") << "\n    }";
+  }
+  os << (checks.empty() ? "]" : "\n  ]") << ",\n  \"pass\": " << (pass() ? "true" : "false")
+     << "\n}\n";
+  return os.str();
+}
+
+VerifyReport verify_problem(const std::string& family,
+                            const std::map<std::string, long long>& sizes, std::uint64_t seed,
+                            int trials, bool fd) {
+  const Family& f = find_family(family);
+  VerifyReport report;
+  const Env env = make_env(family, sizes, seed);
+  const Env gather = run_program(family, env);
+  const Env scatter = run_scatter_adjoint(family, env);
+  double metric = 0.0;
+  for (const auto& a : active_inputs(f)) {
+    const GridCompare c = compare_grids(gather.grids.at(a + "_b"), scatter.grids.at(a + "_b"),
+                                        1e-12);
+    metric = std::max(metric, c.max_rel_err);
+  }
+  report.checks.push_back({"oracle-equivalence", metric, 1e-12, metric <= 1e-12});
+  if (fd) {
+    const DotReport d = dot_product_test(family, env, trials);
+    report.checks.push_back({"dot-product", d.max_rel_err, d.threshold, d.pass});
+  }
+  return report;
 }
 
 std::vector<std::string> array_params(const std::string& family, const std::string& kind) {

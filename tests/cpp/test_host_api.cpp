@@ -7,6 +7,7 @@
 // tests/test_host_api.py.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 #include <string>
 
@@ -123,7 +124,47 @@ static bool throws(F&& f) {
   return false;
 }
 
-int main() {
+// `makeenv <family> <n> <seed>`: the digest oracle/ref/ref_harness.cpp prints
+// for the reference's make_env, here for sgb::make_env (host only, no GPU).
+static int cmd_makeenv(const char* family, long long n, unsigned long long seed) {
+  const sgb::Env env = sgb::make_env(family, {{"n", n}}, seed);
+  char buf[64];
+  auto num = [&](double v) {
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return std::string(buf);
+  };
+  std::string os = "{\"scalars\":{";
+  bool first = true;
+  for (const auto& kv : env.scalars) {
+    os += std::string(first ? "" : ",") + "\"" + kv.first + "\":" + num(kv.second);
+    first = false;
+  }
+  os += "},\"grids\":{";
+  first = true;
+  for (const auto& kv : env.grids) {
+    const std::vector<double>& d = kv.second.data();
+    double sum = 0, sq = 0;
+    for (double x : d) sum += x, sq += x * x;
+    os += std::string(first ? "" : ",") + "\"" + kv.first + "\":[" + std::to_string(d.size()) +
+          "," + num(sum) + "," + num(sq) + "," + num(d.empty() ? 0 : d.front()) + "," +
+          num(d.empty() ? 0 : d[d.size() / 2]) + "," + num(d.empty() ? 0 : d.back()) + "]";
+    first = false;
+  }
+  std::printf("%s}}\n", os.c_str());
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc >= 5 && std::string(argv[1]) == "makeenv")
+    return cmd_makeenv(argv[2], std::atoll(argv[3]), std::strtoull(argv[4], nullptr, 10));
+  if (argc >= 6 && std::string(argv[1]) == "verify") {  // verify <family> <n> <seed> <trials>
+    const sgb::VerifyReport rep = sgb::verify_problem(
+        argv[2], {{"n", std::atoll(argv[3])}}, std::strtoull(argv[4], nullptr, 10),
+        std::atoi(argv[5]), true);
+    std::fputs(rep.json_text().c_str(), stdout);
+    std::fputs(rep.text().c_str(), stderr);
+    return rep.pass() ? 0 : 1;
+  }
   test_family("wave1d", 257);
   test_family("wave3d_c", 20);
   test_family("wave3d_c2", 17);
@@ -163,6 +204,26 @@ int main() {
     bounds.text.replace(g, 11, "guard n - 8");
     CHECK(throws([&] { (void)bounds.family(); }));
     CHECK(throws([&] { (void)sgb::Program::of("lap1d"); }));
+  }
+
+  // compare_grids: the reference's metric, NaN terms ignored, shapes checked
+  {
+    sgb::DenseGrid a({3, 4}), b({3, 4});
+    for (std::size_t i = 0; i < 12; i++) a.data()[i] = b.data()[i] = 0.5 * (double)i - 2.0;
+    a.data()[5] += 3e-3;  // b[5] = 0.5: err = 3e-3 / 1.5
+    const sgb::GridCompare c = sgb::compare_grids(a, b, 1e-2);
+    CHECK(std::fabs(c.max_rel_err - 3e-3 / 1.5) < 1e-15 && c.pass);
+    CHECK(!sgb::compare_grids(a, b, 1e-3).pass);
+    a.data()[7] = std::nan("");
+    CHECK(std::fabs(sgb::compare_grids(a, b, 1e-2).max_rel_err - 3e-3 / 1.5) < 1e-15);
+    CHECK(throws([&] { sgb::compare_grids(a, sgb::DenseGrid({4, 3}), 1.0); }));
+  }
+  // dot_product_test on a caller's Env, and its argument check
+  {
+    const sgb::Env env = sgb::make_env("wave3d_c2", {{"n", 14}}, 5);
+    const sgb::DotReport d = sgb::dot_product_test("wave3d_c2", env, 2);
+    CHECK(d.pass && d.trials == 2 && d.threshold == 1e-4 && d.max_rel_err < 1e-6);
+    CHECK(throws([&] { sgb::dot_product_test("wave3d_c2", env, 0); }));
   }
 
   std::printf("host_api: %d checks, %d failures\n", g_checks, g_failures);

@@ -48,6 +48,10 @@ INFO_SIZES = {"wave1d": 64, "wave3d_c": 12, "wave3d_c2": 12, "burgers2d": 24, "w
               "lap1d": 16, "wave3d": 10, "burgers1d": 64}
 
 
+MAKE_ENV_CASES = [("wave1d", 256, 7), ("wave3d_c", 16, 7), ("wave3d_c2", 12, 3),
+                  ("burgers2d", 64, 7), ("wave3d_r4", 24, 7), ("wave3d_r4", 20, 0)]
+
+
 def harness(*args) -> str:
     r = subprocess.run([oracle.ref_harness_path(), *map(str, args)], check=True,
                        capture_output=True, text=True)
@@ -99,6 +103,13 @@ def main() -> None:
         verify[f"{name}_n{n}_s{seed}"] = {"exit": r.returncode, "report": json.loads(r.stdout)}
     with open(os.path.join(HERE, "ref_verify.json"), "w") as fh:
         json.dump(verify, fh, indent=1)
+    # make_env digests (scalars, per-grid sums and samples): pins sgb::make_env
+    envs = {}
+    for name, n, seed in MAKE_ENV_CASES:
+        envs[f"{name}_n{n}_s{seed}"] = json.loads(
+            harness("makeenv", oracle.spec_path(name), n, seed))
+    with open(os.path.join(HERE, "ref_make_env.json"), "w") as fh:
+        json.dump(envs, fh, indent=1)
     # the reference emitter's prototypes (emit_primal/_adjoint/_scatter_adjoint
     # with restrict, as cmd_bench; codegen.cpp:213-230) -- the C-ABI parameter order
     protos = {}

@@ -1,6 +1,7 @@
 """The C++ host API (include/stencilgrad_b200.hpp) -- the reference's
 interp.hpp entry points over the C ABI -- built with g++ against the in-tree
 library and run (tests/cpp/test_host_api.cpp)."""
+import json
 import os
 import subprocess
 
@@ -39,3 +40,62 @@ def test_host_api_matches_oracle(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def test_make_env_equals_the_references(tmp_path):
+    """CPU: sgb::make_env reproduces the reference's make_env (interp.cpp:266-288)
+    value for value -- scalars, per-grid sums / sums of squares / samples as
+    printed by `ref_harness makeenv` (tests/golden/ref_make_env.json)."""
+    from oracle import oracle
+    oracle.build()
+    exe = _build(str(tmp_path / "test_host_api"))
+    with open(os.path.join(GOLDEN, "ref_make_env.json")) as fh:
+        golden = json.load(fh)
+    assert len(golden) >= 5
+    for key, want in golden.items():
+        name, n, seed = key.rsplit("_", 2)
+        r = subprocess.run([exe, "makeenv", name, n[1:], seed[1:]], capture_output=True,
+                           text=True, timeout=120)
+        assert r.returncode == 0, r.stderr
+        assert json.loads(r.stdout) == want, key
+
+
+@pytest.mark.gpu
+def test_verify_problem_report_beside_the_references(tmp_path):
+    """sgb::verify_problem (gather kernel vs scatter kernel at 1e-12 + the
+    dot-product test on the primal and gather kernels) on the cases the
+    reference's own verify_problem was run on (tests/golden/ref_verify.json):
+    same checks, thresholds and verdicts; where the finite-difference
+    truncation dominates the dot-product metric (the cubic c^2 u families) the
+    metric itself agrees with the reference's -- the environments are equal."""
+    from oracle import oracle
+    oracle.build()
+    exe = _build(str(tmp_path / "test_host_api"))
+    with open(os.path.join(GOLDEN, "ref_verify.json")) as fh:
+        golden = json.load(fh)
+    ran = 0
+    for key, ref in golden.items():
+        name, n, seed = key.rsplit("_", 2)
+        if name not in ("wave1d", "wave3d_c", "burgers2d", "wave3d_r4"):
+            continue
+        r = subprocess.run([exe, "verify", name, n[1:], seed[1:], "2"], capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == ref["exit"] == 0, r.stdout + r.stderr
+        got, want = json.loads(r.stdout), ref["report"]
+        assert got["pass"] is True and want["pass"] is True
+        assert [c["name"] for c in got["checks"]] == [c["name"] for c in want["checks"]]
+        for g, w in zip(got["checks"], want["checks"]):
+            assert g["threshold"] == w["threshold"] and g["pass"] == w["pass"], (key, g, w)
+        eq, dot = got["checks"]
+        assert eq["metric"] <= 1e-12
+        wdot = want["checks"][1]["metric"]
+        if wdot > 1e-10:  # truncation-dominated: reproducible
+            assert abs(dot["metric"] - wdot) <= 0.02 * wdot, (key, dot["metric"], wdot)
+        else:             # rounding-dominated
+            assert dot["metric"] <= 1e-9, (key, dot["metric"])
+        assert "PASS" in r.stderr and "max_rel_err=" in r.stderr
+        ran += 1
+    assert ran == 4
