@@ -40,6 +40,8 @@ RPT = 1                 # rows per thread (2: rows shared in registers, but 224 
                         # and 8 warps per SM; 1: ~128 registers, 16 warps per SM)
 
 
+NSTG = 4                # planes of a staged field in shared memory (cp.async ring)
+PD = 2                  # planes requested ahead of the one being consumed
 UNROLL = False          # plane loop unrolled by the ring size (static modular slots, no
                         # shift-register moves; a RING-times larger body)
 
@@ -155,14 +157,40 @@ def stream_layout(ep):
                     {"kind": "raw", "array": f[2:]}
     BJ = TJ + 2 * HJ
     esz = 8 if ep.T == "double" else 4
+    seed_read = ("read", ep.seed, [(c, 0) for c in ep.lhs])
     off = 0
     for f in fields.values():
         f["off"] = off
-        off += 2 * BJ * BWQ * 4  # double-buffered plane
-    return {"rings": rings, "points": points, "roles": roles, "targets": targets,
-            "fields": fields, "HJ": HJ, "R": Rm, "RING": 2 * Rm + 1, "BJ": BJ,
-            "rpt": RPT, "unroll": UNROLL, "threads": _role(RPT) * len(roles),
-            "smem": off * esz}
+        if f["kind"] == "q":
+            # the formed Q plane, double-buffered, + an NSTG-plane cp.async ring
+            # per array F_g and the seed read (consumed by the copying thread)
+            off += 2 * BJ * BWQ * 4
+            rd = []
+            for r in _reads(ep.groups[f["g"]][0], [seed_read]):
+                if r[1] not in rd:
+                    rd.append(r[1])
+            f["reads"], f["st_off"] = rd, off
+            off += len(rd) * NSTG * BJ * BWQ * 4
+        else:
+            off += NSTG * BJ * BWQ * 4  # the raw planes themselves, read by the taps
+    lay = {"rings": rings, "points": points, "roles": roles, "targets": targets,
+           "fields": fields, "HJ": HJ, "R": Rm, "RING": 2 * Rm + 1, "BJ": BJ,
+           "rpt": RPT, "unroll": UNROLL, "threads": _role(RPT) * len(roles)}
+    # the emit's own reads (old adjoint values, pointwise arrays at the output
+    # point) go through per-thread cp.async slots too: [slot][row][thread of the
+    # role][4], requested with the plane that completes them
+    lay["emit"] = {}
+    for ri, T in enumerate(roles):
+        mine = [(T, True)] + ([(T2, False) for T2 in targets if T2 not in rings]
+                              if ri == 0 else [])
+        for Tt, rg in mine:
+            for a in _target_reads(ep, lay, Tt, rg):
+                lay["emit"][(Tt, a)] = off
+                off += NSTG * RPT * _role(RPT) * 4
+    lay["smem"] = off * esz
+    if lay["smem"] > 227 * 1024:  # does not fit one CTA's shared memory
+        return None
+    return lay
 
 
 def stream_source(ep, index="int"):
@@ -191,6 +219,20 @@ def stream_source(ep, index="int"):
                   "  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; }",
                   "__device__ __forceinline__ void st4(T* p, const T* v) {",
                   "  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]); }"]
+    # 4 consecutive elements global -> shared without registers (zero-filled
+    # when `ok` is false); groups are committed once per plane
+    lines += ["__device__ __forceinline__ void cpa4(T* dst, const T* src, bool ok) {",
+              "  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);",
+              "  const int nb = ok ? 16 : 0;"]
+    for half in range(2 if dbl else 1):
+        lines += [f'  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: '
+                  f'"r"(d + {16 * half}), "l"(reinterpret_cast<const char*>(src) + '
+                  f'{16 * half}), "r"(nb) : "memory");']
+    lines += ["}",
+              "__device__ __forceinline__ void cpa_commit() {",
+              '  asm volatile("cp.async.commit_group;" ::: "memory"); }',
+              "template <int N> __device__ __forceinline__ void cpa_wait() {",
+              '  asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }']
     for T in lay["roles"]:
         if lay["rings"][T]["kind"] == "fac":
             lines += _reach_fn(ep, lay, T, index)
@@ -209,6 +251,8 @@ def stream_source(ep, index="int"):
     L.append("  T* smem = reinterpret_cast<T*>(smem_raw);")
     for name, f in fields.items():
         L.append(f"  T* sh_{name} = smem + {f['off']};")
+        if f["kind"] == "q":
+            L.append(f"  T* st_{name} = smem + {f['st_off']};")
     ext = ep._write_box(szv)
     for i in range(3):
         L.append(f"  const I W{i} = {ext[i]};")
@@ -223,53 +267,73 @@ def stream_source(ep, index="int"):
     L.append("  const I yz1 = yz0 + zc < W0 ? yz0 + zc : W0;")
     L.append(f"  const I kc = k0 + 4 * tx, jr = j0 + {rpt} * ty;")
     L.append(f"  const I pstart = yz0 - ({Rm}), pend = yz1 + ({Rm});")
-    # ---- staging: prefetch (global -> registers) and store (registers -> smem)
+    # ---- staging: `pre` requests plane pp into ring slot ps with cp.async (no
+    # registers held across the planes in flight); `store` forms the Q planes
+    # from the copying thread's own staged elements (registers -> smem)
     NE = BJ * BWQ
     M = -(-NE // NTH)
     pre, store, decl = [], [], []
     for name, f in fields.items():
         if f["kind"] == "q":
             F = ep.groups[f["g"]][0]
-            rd = []
-            for r in _reads(F, [seed_read]):
-                if r[1] not in [x[1] for x in rd]:
-                    rd.append(r)
+            rd = f["reads"]
         for m in range(M):
             tag = f"{name}_{m}"
-            pre.append("    {")
+            guard = f"if (tid + {m * NTH} < {NE}) " if (m + 1) * NTH > NE else ""
+            pre.append(f"    {guard}{{")
             pre.append(f"      const int e = tid + {m * NTH};")
             pre.append(f"      const int row = e / {BWQ}, c4 = e - row * {BWQ};")
             pre.append(f"      const I x0 = pp, x1 = j0 - {HJ} + row, x2 = k0 - {HK} + 4 * c4;")
-            pre.append(f"      const bool ok = e < {NE} && x0 >= 0 && x0 < W0 && x1 >= 0 && "
-                       "x1 < W1 && x2 >= 0 && x2 < W2;")
-            pre.append("      const I fx = (x0 * W1 + x1) * W2 + x2;")
+            pre.append("      bool ok = x0 >= 0 && x0 < W0 && x1 >= 0 && x1 < W1 && x2 >= 0 && "
+                       "x2 < W2;")
             if f["kind"] == "q":
-                decl.append(f"  unsigned pm_{tag} = 0u;")
-                pre.append(f"      pm_{tag} = 0u;")
-                pre.append("      if (ok && x0 >= Blo0 && x0 <= Bhi0 && x1 >= Blo1 && x1 <= Bhi1)")
-                pre.append("        for (int l = 0; l < 4; l++)")
-                pre.append(f"          if (x2 + l >= Blo2 && x2 + l <= Bhi2) pm_{tag} |= 1u << l;")
-                for ri, r in enumerate(rd):
-                    reg = f"pf_{tag}_{ri}"
-                    decl.append(f"  T {reg}[4] = {{T(0), T(0), T(0), T(0)}};")
-                    pre.append(f"      if (pm_{tag}) ld4(a_{r[1]} + fx, {reg});")
-                vals = []
-                for lane in range(4):
-                    regs = {repr(r): f"pf_{tag}_{ri}[{lane}]" for ri, r in enumerate(rd)}
-                    for r in _reads(F, [seed_read]):
-                        regs[repr(r)] = f"pf_{tag}_{[x[1] for x in rd].index(r[1])}[{lane}]"
-                    rcg = _RegCGen(ep, {}, at, regs)
-                    vals.append(f"((pm_{tag} >> {lane}) & 1u) ? ({rcg.e(F)}) * "
-                                f"{rcg.e(seed_read)} : T(0)")
+                # off the box in the outer two counters, or all four points off
+                # it in the innermost: Q = 0 whatever was read -- nothing is
+                pre.append("      ok = ok && x0 >= Blo0 && x0 <= Bhi0 && x1 >= Blo1 && x1 <= Bhi1 "
+                           "&& x2 + 3 >= Blo2 && x2 <= Bhi2;")
+            pre.append("      const I fx = ok ? (x0 * W1 + x1) * W2 + x2 : (I)0;")
+            if f["kind"] == "q":
+                for ri, arr in enumerate(rd):
+                    pre.append(f"      cpa4(st_{name} + ({ri * NSTG} + ps) * {NE * 4} + e * 4, "
+                               f"a_{arr} + fx, ok);")
             else:
-                decl.append(f"  T pf_{tag}[4] = {{T(0), T(0), T(0), T(0)}};")
-                pre.append(f"      if (ok) ld4(a_{f['array']} + fx, pf_{tag}); else "
-                           f"pf_{tag}[0] = pf_{tag}[1] = pf_{tag}[2] = pf_{tag}[3] = T(0);")
-                vals = [f"pf_{tag}[{lane}]" for lane in range(4)]
+                pre.append(f"      cpa4(sh_{name} + ps * {NE * 4} + e * 4, a_{f['array']} + fx, ok);")
             pre.append("    }")
-            guard = f"if (tid + {m * NTH} < {NE}) " if (m + 1) * NTH > NE else ""
-            store.append(f"      {guard}{{ const T v_[4] = {{{', '.join(vals)}}}; "
-                         f"st4(sh_{name} + bsel * {NE * 4} + (tid + {m * NTH}) * 4, v_); }}")
+            if f["kind"] != "q":
+                continue
+            store.append(f"      {guard}{{")
+            store.append(f"        const int e = tid + {m * NTH};")
+            store.append(f"        const int row = e / {BWQ}, c4 = e - row * {BWQ};")
+            store.append(f"        const I x0 = p, x1 = j0 - {HJ} + row, x2 = k0 - {HK} + 4 * c4;")
+            store.append("        unsigned pm = 0u;")
+            store.append("        if (x0 >= 0 && x0 < W0 && x1 >= 0 && x1 < W1 && x2 >= 0 && x2 < W2 "
+                         "&& x0 >= Blo0 && x0 <= Bhi0 && x1 >= Blo1 && x1 <= Bhi1)")
+            store.append("          for (int l = 0; l < 4; l++)")
+            store.append("            if (x2 + l >= Blo2 && x2 + l <= Bhi2) pm |= 1u << l;")
+            for ri, arr in enumerate(rd):
+                store.append(f"        T pf_{ri}[4]; ld4(st_{name} + ({ri * NSTG} + rs) * {NE * 4} "
+                             f"+ e * 4, pf_{ri});")
+            vals = []
+            for lane in range(4):
+                regs = {}
+                for r in _reads(F, [seed_read]):
+                    regs[repr(r)] = f"pf_{rd.index(r[1])}[{lane}]"
+                rcg = _RegCGen(ep, {}, at, regs)
+                vals.append(f"((pm >> {lane}) & 1u) ? ({rcg.e(F)}) * {rcg.e(seed_read)} : T(0)")
+            store.append(f"        const T v_[4] = {{{', '.join(vals)}}};")
+            store.append(f"        st4(sh_{name} + bsel * {NE * 4} + e * 4, v_);")
+            store.append("      }")
+    # the emit's reads for output plane pp - R ride in plane pp's group
+    pre.append(f"    {{ const I yq = pp - ({Rm}); const bool eq_ok = yq >= yz0 && yq < yz1 && "
+               "kc < W2;")
+    for ri, T in enumerate(roles):
+        pre.append(f"      {'if' if ri == 0 else 'else if'} (role == {ri}) {{")
+        mine_q = [(T, True)] + ([(T2, False) for T2 in lay["targets"] if T2 not in rings]
+                                if ri == 0 else [])
+        for Tt, rg in mine_q:
+            pre += _emit_target(ep, lay, Tt, at, seed_read, ring=rg, part="request", rpt=rpt)
+        pre.append("      }")
+    pre.append("    }")
     L += decl
     # acc[s] holds output plane p - R + s (a shift register: plane p's taps
     # with outer offset di go to s = R - di; after the emit of acc[0] the
@@ -281,10 +345,14 @@ def stream_source(ep, index="int"):
     L.append(f"    for (int h = 0; h < {rpt}; h++)")
     L.append("#pragma unroll")
     L.append("      for (int l = 0; l < 4; l++) acc[q][h][l] = T(0);")
-    L.append("  { const I pp = pstart;")
-    L += pre
-    L.append("  }")
-    L.append("  int bsel = 0;")
+    for d_ in range(PD):  # planes pstart .. pstart + PD - 1 requested up front
+        L.append(f"  {{ const I pp = pstart + {d_}; const int ps = {d_ % NSTG};")
+        L.append("    if (pp < pend) {")
+        L += pre
+        L.append("    }")
+        L.append("    cpa_commit();")
+        L.append("  }")
+    L.append("  int bsel = 0, rs = 0;  // rs: ring slot of plane p")
     unroll = lay["unroll"]
     if unroll:
         L.append(f"  for (I base = pstart; base < pend; base += {RING}) {{")
@@ -296,11 +364,18 @@ def stream_source(ep, index="int"):
         L.append("#pragma unroll 1")
         L.append("  for (I p = pstart; p < pend; p++) {")
         L.append("    {")
+    # plane p has landed (this thread's copies; the others' by the barrier);
+    # plane p + PD goes to a slot last read PD + 1 < NSTG + 1 planes ago -- a
+    # thread still in plane p - 1's taps reads slot rs - 1, never this one
+    L.append(f"      cpa_wait<{PD - 1}>();")
+    L.append(f"      {{ const I pp = p + {PD}; const int ps = (rs + {PD}) % {NSTG};")
+    L.append("        if (pp < pend) {")
+    L += ["    " + x for x in pre]
+    L.append("        }")
+    L.append("        cpa_commit();")
+    L.append("      }")
     L += store
     L.append("      __syncthreads();")
-    L.append("      if (p + 1 < pend) { const I pp = p + 1;")
-    L += ["  " + x for x in pre]
-    L.append("      }")
     cg0 = _CGen(ep, {}, at)
 
     def ring_code(T):
@@ -317,7 +392,8 @@ def stream_source(ep, index="int"):
                 w = f"w_{fname}_{tap[1] + 8}_{h}"
                 if (key, h) not in loaded:
                     loaded.add((key, h))
-                    base_ = (f"sh_{fname} + bsel * {NE * 4} + ({rpt} * ty + {h} + "
+                    sel = "bsel" if fields[fname]["kind"] == "q" else "rs"
+                    base_ = (f"sh_{fname} + {sel} * {NE * 4} + ({rpt} * ty + {h} + "
                              f"{tap[1] + HJ}) * {BWQ * 4} + 4 * tx")
                     if wins[key]:
                         out.append(f"      T {w}[12]; ld4({base_}, {w}); ld4({base_} + 4, {w} + 4);"
@@ -370,6 +446,7 @@ def stream_source(ep, index="int"):
         L.append("#pragma unroll")
         L.append(f"        for (int l = 0; l < 4; l++) acc[{RING - 1}][h][l] = T(0);")
     L.append("      bsel ^= 1;")
+    L.append(f"      rs = (rs + 1) % {NSTG};")
     L.append("    }")
     L.append("  }")
     if unroll:
@@ -392,6 +469,22 @@ def _reach_fn(ep, lay, T, index):
             "      return true;",
             "  return false;",
             "}"]
+
+
+def _target_reads(ep, lay, T, ring):
+    """Arrays the emit of target T reads at the output point (the pointwise
+    partials, the seed, a linear ring's pointwise factors), then T itself."""
+    seed_read = ("read", ep.seed, [(c, 0) for c in ep.lhs])
+    r = lay["rings"].get(T) if ring else None
+    nodes = [ep.partials[ti] for ti in lay["points"][T]] + [seed_read]
+    if r and r["kind"] == "lin":
+        nodes += [f for i, f in enumerate(r["chain"]) if i != r["li"]]
+    reads = []
+    for nd in nodes:
+        for rd in _reads(nd, []):
+            if rd[1] not in reads:
+                reads.append(rd[1])
+    return reads + [T]
 
 
 def _emit_target(ep, lay, T, at, seed_read, ring, part, rpt):
@@ -419,15 +512,21 @@ def _emit_target(ep, lay, T, at, seed_read, ring, part, rpt):
         omin = min(ep.terms[ti].offset[i] for ti in mine)
         lo_, hi_ = ("y0", "y0") if i == 0 else (("y1", "y1") if i == 1 else ("kc", "kc + 3"))
         core.append(f"{lo_} >= Blo{i} + ({omax}) && {hi_} <= Bhi{i} + ({omin})")
+    ROLE = _role(rpt)
+    if part == "request":  # plane pp's group: the values output plane pp - R needs
+        for h in range(rpt):
+            out.append(f"        {{ const bool ok = eq_ok && jr + {h} < W1;")
+            out.append(f"          const I fy = ok ? (yq * W1 + jr + {h}) * W2 + kc : (I)0;")
+            for a in reads + [T]:
+                out.append(f"          cpa4(smem + {lay['emit'][(T, a)]} + ((ps * {rpt} + {h}) * "
+                           f"{ROLE} + rt) * 4, a_{a} + fy, ok);")
+            out.append("        }")
+        return out
     if part == "load":
         for h in range(rpt):
             for a in reads + [T]:
-                out.append(f"      T e_{T}_{a}_{h}[4];")
-            out.append(f"      if (emit_ok && jr + {h} < W1) {{")
-            out.append(f"        const I fy = (y0 * W1 + jr + {h}) * W2 + kc;")
-            for a in reads + [T]:
-                out.append(f"        ld4(a_{a} + fy, e_{T}_{a}_{h});")
-            out.append("      }")
+                out.append(f"      T e_{T}_{a}_{h}[4]; ld4(smem + {lay['emit'][(T, a)]} + "
+                           f"((rs * {rpt} + {h}) * {ROLE} + rt) * 4, e_{T}_{a}_{h});")
         return out
     for h in range(rpt):
         out.append(f"        {{ const I y1 = jr + {h};")
