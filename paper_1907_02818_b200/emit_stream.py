@@ -11,13 +11,23 @@ counter over a chunk of planes.  The program's terms are sorted into
   Laplacian of u_1;
 * pointwise terms: partials that read only at the output point.
 
-Per plane p the CTA stages every field a ring reads -- Q_g(x) = [x in B]
-F_g(x) seed(x), or the raw array A -- into shared memory (double buffer; the
-next plane's 16-byte global loads are in flight in registers), and one role
-of threads per target-with-a-ring forms, for RPT rows x 4 consecutive
-points each, the taps of its ring with outer offset di from k windows held
-in registers and adds them into the register-ring slot of output plane
-p - di.  Plane p - R is complete: its owner writes old value + ring (or
+Per plane the CTA stages every field a ring reads in shared memory with
+cp.async (16-byte copies, zero-filled off the grid; nothing is held in
+registers while in flight): the raw arrays of the taps straight into 4-plane
+rings, the arrays Q_g = [x in B] F_g(x) seed(x) is formed from into per-thread
+staging slots; planes p + 1 and p + 2 are in flight while plane p is
+consumed, one commit group per plane and one barrier per plane.  The
+copying thread forms Q_g for its own elements (double-buffered plane), then
+one role of threads per target-with-a-ring forms, for RPT rows x 4
+consecutive points each, the taps of its ring with outer offset di from k
+windows held in registers and adds them into the register-ring slot of
+output plane p - di.  The emit's own reads (the old adjoint values, the
+pointwise arrays at the output point) ride in the same cp.async groups,
+requested with the plane that completes their output plane (fp32; when the
+slots would leave one CTA per SM they are loaded at the start of the taps).
+Tiles whose staged box lies inside the primal box take a copy of the staging
+code with CTA-uniform predicates only.
+Plane p - R is complete: its owner writes old value + ring (or
 pointwise factors x ring x seed) + the pointwise terms, predicated per point
 off the core box (untouched cells are never written).  The sums run in a
 different order than the flat form's per-cell term order, so the results
@@ -40,6 +50,7 @@ RPT = 1                 # rows per thread (2: rows shared in registers, but 224 
                         # and 8 warps per SM; 1: ~128 registers, 16 warps per SM)
 
 
+ZCHUNK = 128            # planes of the outer counter per CTA (launcher)
 NSTG = 4                # planes of a staged field in shared memory (cp.async ring)
 PD = 2                  # planes requested ahead of the one being consumed
 UNROLL = False          # plane loop unrolled by the ring size (static modular slots, no
@@ -180,13 +191,21 @@ def stream_layout(ep):
     # point) go through per-thread cp.async slots too: [slot][row][thread of the
     # role][4], requested with the plane that completes them
     lay["emit"] = {}
+    eoff = off
     for ri, T in enumerate(roles):
         mine = [(T, True)] + ([(T2, False) for T2 in targets if T2 not in rings]
                               if ri == 0 else [])
         for Tt, rg in mine:
             for a in _target_reads(ep, lay, Tt, rg):
-                lay["emit"][(Tt, a)] = off
-                off += NSTG * RPT * _role(RPT) * 4
+                lay["emit"][(Tt, a)] = eoff
+                eoff += NSTG * RPT * _role(RPT) * 4
+    # ... when two CTAs per SM still fit (fp32 at cfg 4: 101 KB per CTA; in fp64
+    # the slots would leave one CTA per SM -- 16.4 -> 19 ms -- so the emit then
+    # loads its values from global memory at the start of the plane's taps)
+    per_sm = max(1, 512 // lay["threads"])  # CTAs per SM the launch bounds ask for
+    lay["emit_async"] = eoff * esz <= (227 // per_sm - 1) * 1024
+    if lay["emit_async"]:
+        off = eoff
     lay["smem"] = off * esz
     if lay["smem"] > 227 * 1024:  # does not fit one CTA's shared memory
         return None
@@ -221,8 +240,7 @@ def stream_source(ep, index="int"):
                   "  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]); }"]
     # 4 consecutive elements global -> shared without registers (zero-filled
     # when `ok` is false); groups are committed once per plane
-    lines += ["__device__ __forceinline__ void cpa4(T* dst, const T* src, bool ok) {",
-              "  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);",
+    lines += ["__device__ __forceinline__ void cpa4(unsigned d, const T* src, bool ok) {",
               "  const int nb = ok ? 16 : 0;"]
     for half in range(2 if dbl else 1):
         lines += [f'  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: '
@@ -272,68 +290,98 @@ def stream_source(ep, index="int"):
     # from the copying thread's own staged elements (registers -> smem)
     NE = BJ * BWQ
     M = -(-NE // NTH)
+    EB = 8 if dbl else 4  # element bytes
     pre, store, decl = [], [], []
-    for name, f in fields.items():
-        if f["kind"] == "q":
-            F = ep.groups[f["g"]][0]
-            rd = f["reads"]
-        for m in range(M):
-            tag = f"{name}_{m}"
-            guard = f"if (tid + {m * NTH} < {NE}) " if (m + 1) * NTH > NE else ""
-            pre.append(f"    {guard}{{")
-            pre.append(f"      const int e = tid + {m * NTH};")
-            pre.append(f"      const int row = e / {BWQ}, c4 = e - row * {BWQ};")
-            pre.append(f"      const I x0 = pp, x1 = j0 - {HJ} + row, x2 = k0 - {HK} + 4 * c4;")
-            pre.append("      bool ok = x0 >= 0 && x0 < W0 && x1 >= 0 && x1 < W1 && x2 >= 0 && "
-                       "x2 < W2;")
+    decl.append("  const unsigned smem_u = (unsigned)__cvta_generic_to_shared(smem);")
+    decl.append("  const I sdp = W1 * W2;")
+    # per thread and staged element group: everything that does not depend on
+    # the plane (row / column, in-grid and in-box tests, the in-plane offset)
+    for m in range(M):
+        decl.append(f"  const int se{m} = tid + {m * NTH};")
+        decl.append(f"  const int srow{m} = se{m} / {BWQ}, sc4{m} = se{m} - srow{m} * {BWQ};")
+        decl.append(f"  const I sx1{m} = j0 - {HJ} + srow{m}, sx2{m} = k0 - {HK} + 4 * sc4{m};")
+        decl.append(f"  const bool sin{m} = se{m} < {NE} && sx1{m} >= 0 && sx1{m} < W1 && "
+                    f"sx2{m} >= 0 && sx2{m} < W2;")
+        decl.append(f"  const I soff{m} = sin{m} ? sx1{m} * W2 + sx2{m} : (I)0;")
+        decl.append(f"  unsigned spm{m} = 0u;  // lanes of the group inside the box (rows too)")
+        decl.append(f"  if (sin{m} && sx1{m} >= Blo1 && sx1{m} <= Bhi1)")
+        decl.append("    for (int l = 0; l < 4; l++)")
+        decl.append(f"      if (sx2{m} + l >= Blo2 && sx2{m} + l <= Bhi2) spm{m} |= 1u << l;")
+    # A tile whose staged box lies inside the primal box in the inner two
+    # counters (the interior of the grid) needs none of the per-thread tests:
+    # `tin` picks a second copy of the staging code with CTA-uniform predicates
+    # only (the plane tests).  Same values either way.
+    decl.append(f"  const bool tin = j0 - {HJ} >= Blo1 && j0 + {TJ + HJ - 1} <= Bhi1 && "
+                f"k0 - {HK} >= Blo2 && k0 + {TK + HK - 1} <= Bhi2 && Blo1 >= 0 && Bhi1 < W1 && "
+                "Blo2 >= 0 && Bhi2 < W2;")
+
+    def staging(fast):
+        pre, store = [], []
+        pre.append("    const bool pokr = pp >= 0 && pp < W0, pokq = pokr && pp >= Blo0 && "
+                   "pp <= Bhi0;")
+        store.append("      const bool pin = p >= Blo0 && p <= Bhi0 && p >= 0 && p < W0;")
+        for name, f in fields.items():
             if f["kind"] == "q":
-                # off the box in the outer two counters, or all four points off
-                # it in the innermost: Q = 0 whatever was read -- nothing is
-                pre.append("      ok = ok && x0 >= Blo0 && x0 <= Bhi0 && x1 >= Blo1 && x1 <= Bhi1 "
-                           "&& x2 + 3 >= Blo2 && x2 <= Bhi2;")
-            pre.append("      const I fx = ok ? (x0 * W1 + x1) * W2 + x2 : (I)0;")
-            if f["kind"] == "q":
+                F = ep.groups[f["g"]][0]
+                rd = f["reads"]
+            for m in range(M):
+                guard = f"if (se{m} < {NE}) " if (m + 1) * NTH > NE else ""
+                pre.append(f"    {guard}{{")
+                if f["kind"] == "q":
+                    # off the box in the outer counter, or the whole group off it
+                    # in the inner two: Q = 0 whatever is read -- nothing is
+                    pre.append("      const bool ok = pokq" + ("" if fast else f" && spm{m} != 0u")
+                               + ";")
+                else:
+                    pre.append("      const bool ok = pokr" + ("" if fast else f" && sin{m}") + ";")
+                pre.append(f"      const I fx = ok ? pp * sdp + soff{m} : (I)0;")
+                if f["kind"] == "q":
+                    for ri, arr in enumerate(rd):
+                        pre.append(f"      cpa4(smem_u + ({f['st_off']} + ({ri * NSTG} + ps) * "
+                                   f"{NE * 4} + se{m} * 4) * {EB}, a_{arr} + fx, ok);")
+                else:
+                    pre.append(f"      cpa4(smem_u + ({f['off']} + ps * {NE * 4} + se{m} * 4) * "
+                               f"{EB}, a_{f['array']} + fx, ok);")
+                pre.append("    }")
+                if f["kind"] != "q":
+                    continue
+                store.append(f"      {guard}{{")
+                store.append("        const unsigned pm = pin ? " + ("15u" if fast else f"spm{m}")
+                             + " : 0u;")
                 for ri, arr in enumerate(rd):
-                    pre.append(f"      cpa4(st_{name} + ({ri * NSTG} + ps) * {NE * 4} + e * 4, "
-                               f"a_{arr} + fx, ok);")
-            else:
-                pre.append(f"      cpa4(sh_{name} + ps * {NE * 4} + e * 4, a_{f['array']} + fx, ok);")
-            pre.append("    }")
-            if f["kind"] != "q":
-                continue
-            store.append(f"      {guard}{{")
-            store.append(f"        const int e = tid + {m * NTH};")
-            store.append(f"        const int row = e / {BWQ}, c4 = e - row * {BWQ};")
-            store.append(f"        const I x0 = p, x1 = j0 - {HJ} + row, x2 = k0 - {HK} + 4 * c4;")
-            store.append("        unsigned pm = 0u;")
-            store.append("        if (x0 >= 0 && x0 < W0 && x1 >= 0 && x1 < W1 && x2 >= 0 && x2 < W2 "
-                         "&& x0 >= Blo0 && x0 <= Bhi0 && x1 >= Blo1 && x1 <= Bhi1)")
-            store.append("          for (int l = 0; l < 4; l++)")
-            store.append("            if (x2 + l >= Blo2 && x2 + l <= Bhi2) pm |= 1u << l;")
-            for ri, arr in enumerate(rd):
-                store.append(f"        T pf_{ri}[4]; ld4(st_{name} + ({ri * NSTG} + rs) * {NE * 4} "
-                             f"+ e * 4, pf_{ri});")
-            vals = []
-            for lane in range(4):
-                regs = {}
-                for r in _reads(F, [seed_read]):
-                    regs[repr(r)] = f"pf_{rd.index(r[1])}[{lane}]"
-                rcg = _RegCGen(ep, {}, at, regs)
-                vals.append(f"((pm >> {lane}) & 1u) ? ({rcg.e(F)}) * {rcg.e(seed_read)} : T(0)")
-            store.append(f"        const T v_[4] = {{{', '.join(vals)}}};")
-            store.append(f"        st4(sh_{name} + bsel * {NE * 4} + e * 4, v_);")
-            store.append("      }")
-    # the emit's reads for output plane pp - R ride in plane pp's group
-    pre.append(f"    {{ const I yq = pp - ({Rm}); const bool eq_ok = yq >= yz0 && yq < yz1 && "
-               "kc < W2;")
-    for ri, T in enumerate(roles):
-        pre.append(f"      {'if' if ri == 0 else 'else if'} (role == {ri}) {{")
-        mine_q = [(T, True)] + ([(T2, False) for T2 in lay["targets"] if T2 not in rings]
-                                if ri == 0 else [])
-        for Tt, rg in mine_q:
-            pre += _emit_target(ep, lay, Tt, at, seed_read, ring=rg, part="request", rpt=rpt)
-        pre.append("      }")
-    pre.append("    }")
+                    store.append(f"        T pf_{ri}[4]; ld4(st_{name} + ({ri * NSTG} + rs) * "
+                                 f"{NE * 4} + se{m} * 4, pf_{ri});")
+                vals = []
+                for lane in range(4):
+                    regs = {}
+                    for r in _reads(F, [seed_read]):
+                        regs[repr(r)] = f"pf_{rd.index(r[1])}[{lane}]"
+                    rcg = _RegCGen(ep, {}, at, regs)
+                    vals.append(f"((pm >> {lane}) & 1u) ? ({rcg.e(F)}) * {rcg.e(seed_read)} : "
+                                "T(0)")
+                store.append(f"        const T v_[4] = {{{', '.join(vals)}}};")
+                store.append(f"        st4(sh_{name} + bsel * {NE * 4} + se{m} * 4, v_);")
+                store.append("      }")
+        # the emit's reads for output plane pp - R ride in plane pp's group
+        pre.append(f"    {{ const I yq = pp - ({Rm}); const bool eq_ok = yq >= yz0 && yq < yz1"
+                   + ("" if fast else " && kc < W2") + ";")
+        for ri, T in enumerate(roles):
+            pre.append(f"      {'if' if ri == 0 else 'else if'} (role == {ri}) {{")
+            mine_q = [(T, True)] + ([(T2, False) for T2 in lay["targets"] if T2 not in rings]
+                                    if ri == 0 else [])
+            for Tt, rg in mine_q:
+                pre += _emit_target(ep, lay, Tt, at, seed_read, ring=rg,
+                                    part="request_fast" if fast else "request", rpt=rpt)
+            pre.append("      }")
+        pre.append("    }")
+        return pre, store
+
+    pre_g, store_g = staging(False)
+    pre_f, store_f = staging(True)
+    pre = ["    if (tin) {"] + ["  " + x for x in pre_f] + ["    } else {"] + \
+        ["  " + x for x in pre_g] + ["    }"]
+    store = ["      if (tin) {"] + ["  " + x for x in store_f] + ["      } else {"] + \
+        ["  " + x for x in store_g] + ["      }"]
     L += decl
     # acc[s] holds output plane p - R + s (a shift register: plane p's taps
     # with outer offset di go to s = R - di; after the emit of acc[0] the
@@ -513,20 +561,34 @@ def _emit_target(ep, lay, T, at, seed_read, ring, part, rpt):
         lo_, hi_ = ("y0", "y0") if i == 0 else (("y1", "y1") if i == 1 else ("kc", "kc + 3"))
         core.append(f"{lo_} >= Blo{i} + ({omax}) && {hi_} <= Bhi{i} + ({omin})")
     ROLE = _role(rpt)
-    if part == "request":  # plane pp's group: the values output plane pp - R needs
+    if part in ("request", "request_fast"):  # plane pp's group: what output plane pp - R needs
+        if not lay["emit_async"]:
+            return out
+        EB = 8 if ep.T == "double" else 4
         for h in range(rpt):
-            out.append(f"        {{ const bool ok = eq_ok && jr + {h} < W1;")
-            out.append(f"          const I fy = ok ? (yq * W1 + jr + {h}) * W2 + kc : (I)0;")
+            out.append("        { const bool ok = eq_ok" +
+                       ("" if part == "request_fast" else f" && jr + {h} < W1") + ";")
+            out.append(f"          const I fy = ok ? yq * sdp + (jr + {h}) * W2 + kc : (I)0;")
             for a in reads + [T]:
-                out.append(f"          cpa4(smem + {lay['emit'][(T, a)]} + ((ps * {rpt} + {h}) * "
-                           f"{ROLE} + rt) * 4, a_{a} + fy, ok);")
+                out.append(f"          cpa4(smem_u + ({lay['emit'][(T, a)]} + ((ps * {rpt} + {h}) * "
+                           f"{ROLE} + rt) * 4) * {EB}, a_{a} + fy, ok);")
             out.append("        }")
         return out
-    if part == "load":
+    if part == "load" and lay["emit_async"]:
         for h in range(rpt):
             for a in reads + [T]:
                 out.append(f"      T e_{T}_{a}_{h}[4]; ld4(smem + {lay['emit'][(T, a)]} + "
                            f"((rs * {rpt} + {h}) * {ROLE} + rt) * 4, e_{T}_{a}_{h});")
+        return out
+    if part == "load":
+        for h in range(rpt):
+            for a in reads + [T]:
+                out.append(f"      T e_{T}_{a}_{h}[4];")
+            out.append(f"      if (emit_ok && jr + {h} < W1) {{")
+            out.append(f"        const I fy = (y0 * W1 + jr + {h}) * W2 + kc;")
+            for a in reads + [T]:
+                out.append(f"        ld4(a_{a} + fy, e_{T}_{a}_{h});")
+            out.append("      }")
         return out
     for h in range(rpt):
         out.append(f"        {{ const I y1 = jr + {h};")

@@ -1111,8 +1111,8 @@ class EmittedProblem:
         if form not in ("auto", "flat", "tiled", "stream"):
             raise _lib.StencilError(f"unknown emitted form {form!r}")
         if form == "auto":
-            # the stream form where it applies in fp32 (cfg 4 768^3: 6.0 vs
-            # 8.3 ms flat); in fp64 the flat form is faster (14.8 vs 18.7 ms)
+            # the stream form where it applies in fp32 (cfg 4 768^3: 4.9 vs
+            # 8.3 ms flat); in fp64 the flat form is faster (14.7 vs 16.3 ms)
             from . import emit_stream
             form = "flat"
             if self.T == "float" and W[2] % 4 == 0 and \
@@ -1129,7 +1129,12 @@ class EmittedProblem:
                                         "extent a multiple of 4 and 16-byte aligned arrays")
             gx = (W[2] + emit_stream.TK - 1) // emit_stream.TK
             gy = (W[1] + emit_stream.TJ - 1) // emit_stream.TJ
-            nz = max(1, -(-W[0] // 256))
+            # outer-counter chunks of ~ZCHUNK planes (2R warm-up planes each): short
+            # chunks keep the resident CTAs on nearly the same planes, so the halo
+            # rows neighbouring tiles share are still in L2 -- one chunk per column
+            # (the wave model's choice) measured 20 % slower at 768^3; 48 ... 256
+            # planes: 4.86 / 4.77 / 4.71 / 4.71 / 4.81 / 4.92 ms at 48 / 64 / 96 / 128 / 192 / 256
+            nz = max(1, -(-W[0] // emit_stream.ZCHUNK))
             while nz < W[0] and gx * gy * nz < 2 * 148:
                 nz *= 2
             zc = -(-W[0] // nz)
