@@ -23,7 +23,9 @@ e2e    = the same metric through the host-facing C ABI with pinned HOST
          arrays, every copy inside the timed region.  cfg 5: the reverse
          sweep over host-held states (sgb_plan_sweep_*: c, c_b resident on
          the device for the sweep; per step u_1, u_b in, the fresh gather,
-         u_1_b out), with the per-step accumulating ABI call
+         u_1_b out; cfg 2 at N = 1: the carried sweep, adjoints resident and
+         rotated on the device, per step u_1 in), with the per-step
+         accumulating ABI call
          (sgb_plan_run_adjoint_host: every array in, adjoints out) beside it
          in e2e.accumulating_abi; the other configs: that per-step call.
          N > 1: owned planes per rank + the halo exchange.
@@ -1094,7 +1096,8 @@ def run_e2e(args, torch, api, wl, dist, mode=None, steps=None):
     adjoints come back."""
     family, n, scalars, sl = wl.family, wl.n, wl.scalars, wl.sl
     if mode is None:
-        mode = "sweep" if (wl.fresh and family == "wave3d_r4") else "abi"
+        mode = "sweep" if ((wl.fresh and family == "wave3d_r4") or
+                           (wl.carried and sl is None)) else "abi"
     sweep = mode == "sweep"
     names = api.array_params(family, "adjoint")
     rmw = [nm for nm in names if nm.endswith("_b") and nm != SEED[family]]
@@ -1107,9 +1110,15 @@ def run_e2e(args, torch, api, wl, dist, mode=None, steps=None):
     torch.cuda.synchronize()
     k = max(1, steps or args.e2e_steps)
     plan = None
-    once_in, once_out = (("c", "c_b"), ("c_b",)) if sweep else ((), ())
-    step_in = ("u_1", "u_b") if sweep else tuple(names)
-    step_out = ("u_1_b",) if sweep else tuple(rmw)
+    if sweep and wl.carried:  # cfg 2: the adjoints carried (and rotated) on the device
+        once_in, once_out = ("c", "c_b", "u_1_b", "u_2_b", "u_b"), ("c_b", "u_1_b", "u_2_b", "u_b")
+        step_in, step_out = ("u_1",), ()
+    elif sweep:               # cfg 5: independent steps
+        once_in, once_out = ("c", "c_b"), ("c_b",)
+        step_in, step_out = ("u_1", "u_b"), ("u_1_b",)
+    else:
+        once_in, once_out = (), ()
+        step_in, step_out = tuple(names), tuple(rmw)
     begin = end = lambda: None
     if sl is None:
         per = host[names[0]].numel() * esz
@@ -1120,9 +1129,12 @@ def run_e2e(args, torch, api, wl, dist, mode=None, steps=None):
 
             def step():
                 hp.sweep_step_host(scalars, host)
-            path = "sgb_plan_sweep_begin / _step_host x K / _end (pinned host buffers; c, " \
-                   "c_b resident over the sweep; per step H2D of u_1, u_b / the fresh " \
-                   "gather / D2H of u_1_b pipelined over i-chunks)"
+            path = "sgb_plan_sweep_begin / _step_host x K / _end (pinned host buffers; " + \
+                   ("c, c_b and the carried adjoints resident over the sweep; per step H2D of "
+                    "u_1 / the gather pipelined over i-chunks, rotation on the device)"
+                    if wl.carried else
+                    "c, c_b resident over the sweep; per step H2D of u_1, u_b / the fresh "
+                    "gather / D2H of u_1_b pipelined over i-chunks)")
         else:
             def step():
                 hp.run_adjoint_host(scalars, host)
@@ -1210,11 +1222,14 @@ def run_e2e(args, torch, api, wl, dist, mode=None, steps=None):
            "copy_floor_ms": floor_ms, "frac_of_copy_floor": floor_ms / ms, "mode": mode,
            "path": path}
     if sweep:
-        out["note"] = (f"host-held forward states instead of regenerated ones: per step u_1, u_b "
-                       f"H2D and u_1_b D2H; the sweep's one-off copies (c, c_b in, c_b out) are "
-                       f"inside the timed region and amortised over its {k} steps (the "
-                       f"BASELINE sweep has 100); bitwise = zeroing u_1_b and calling the "
-                       f"accumulating ABI per step (tests/test_gpu_parity.py)")
+        out["note"] = (f"host-held forward states instead of regenerated ones: per step "
+                       f"{', '.join(step_in)} H2D" +
+                       (f" and {', '.join(step_out)} D2H" if step_out else "") +
+                       f"; the sweep's one-off copies ({', '.join(once_in)} in, "
+                       f"{', '.join(once_out)} out) are inside the timed region and amortised "
+                       f"over its {k} steps (the BASELINE sweep has "
+                       f"{10 if wl.carried else 100}); bitwise = the accumulating ABI call per "
+                       f"step with the caller's zeroing / rotation (tests/test_gpu_parity.py)")
     else:
         out["note"] = ("one call of the accumulating reference ABI (<name>_b) on host-held "
                        "arrays per step: every array in, the accumulated adjoints back")

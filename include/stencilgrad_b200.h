@@ -402,17 +402,24 @@ void sgb_plan_destroy(sgb_plan* plan);
 /* arrays[] in the reference prototype order of <family>_b (host pointers) */
 int sgb_plan_run_adjoint_host(sgb_plan* plan, const double* scalars, void** arrays,
                               sgb_stream_t stream);
-/* Reverse sweep over HOST-held forward states (BASELINE cfg 5 with the states
- * checkpointed in host memory rather than regenerated; wave3d_r4 plans, fp32 /
- * fp64, full grid or slab).  The reference's CPU sweep calls wave3d_r4_b
- * (codegen.cpp:332-382) once per step with u_1_b zeroed by the caller and c,
- * c_b staying where they are; here c and the accumulator c_b stay RESIDENT on
- * the device between begin and end, and a step moves only u_1 and u_b in and
- * the step's own adjoint u_1_b out -- 12 instead of 28 bytes per point over
- * PCIe in fp32.  arrays[] in the prototype order c, c_b, u_1, u_1_b, u_b (host
- * pointers; begin reads [0], [1]; step reads [2], [4], writes [3]; end writes
- * [1]).  Every call returns with its copies complete.  The results are bitwise
- * those of zeroing u_1_b and calling sgb_plan_run_adjoint_host per step. */
+/* Reverse sweeps over HOST-held forward states (the multi-step BASELINE
+ * protocols with the states checkpointed in host memory rather than
+ * regenerated).  The reference's CPU sweep calls <name>_b (codegen.cpp:332-382)
+ * once per step with everything staying in host RAM; here whatever does not
+ * change per step stays RESIDENT on the device between begin and end.
+ * arrays[] are host pointers in the prototype order of <family>_b; every call
+ * returns with its copies complete.
+ *   wave3d_r4 plans (cfg 5, independent steps; fp32 / fp64, grid or slab;
+ *   c, c_b, u_1, u_1_b, u_b): begin reads c, c_b; a step reads u_1, u_b and
+ *   writes u_1_b = the step's own adjoint (12 instead of 28 bytes per point
+ *   over PCIe in fp32); end writes the accumulated c_b.  Bitwise = zeroing
+ *   u_1_b and calling sgb_plan_run_adjoint_host per step.
+ *   wave3d_c full-grid plans (cfg 2, carried steps; c, c_b, u_1, u_1_b, u_2_b,
+ *   u_b): begin reads c, c_b, u_1_b, u_2_b and the seed u_b; a step reads only
+ *   the state u_1 (4 instead of 36 bytes per point), accumulates c_b, u_1_b,
+ *   u_2_b and rotates the adjoints on the device (seed <- u_1_b, u_1_b <-
+ *   u_2_b, u_2_b <- 0); end writes c_b, u_1_b, u_2_b and the current seed u_b.
+ *   Bitwise = the per-step accumulating call followed by the caller's rotation. */
 int sgb_plan_sweep_begin(sgb_plan* plan, void** arrays, sgb_stream_t stream);
 int sgb_plan_sweep_step_host(sgb_plan* plan, const double* scalars, void** arrays,
                              sgb_stream_t stream);

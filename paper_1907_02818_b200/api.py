@@ -309,28 +309,38 @@ class Plan:
             ptrs[i] = a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
         return ptrs
 
+    # sgb_plan_sweep_*: which host arrays each call touches, per family
+    _SWEEP = {"wave3d_r4": (("c", "c_b"), ("u_1", "u_1_b", "u_b"), ("c_b",)),
+              "wave3d_c": (("c", "c_b", "u_1_b", "u_2_b", "u_b"), ("u_1",),
+                           ("c_b", "u_1_b", "u_2_b", "u_b"))}
+
+    def _sweep_names(self, i):
+        return self._SWEEP.get(self.family, ((), (), ()))[i]
+
     def sweep_begin(self, host_arrays: dict, stream=None):
-        """Start a reverse sweep over host-held states (sgb_plan_sweep_*): c and
-        the accumulator c_b go to the device once and stay there."""
+        """Start a reverse sweep over host-held states (sgb_plan_sweep_*): what
+        does not change per step goes to the device once and stays there
+        (wave3d_r4: c, c_b; wave3d_c: c, c_b and the carried adjoints)."""
         s = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
         _lib.check(_lib.lib().sgb_plan_sweep_begin(
-            ctypes.c_void_p(self._p), self._ptrs(host_arrays, ("c", "c_b")), s),
+            ctypes.c_void_p(self._p), self._ptrs(host_arrays, self._sweep_names(0)), s),
             "sgb_plan_sweep_begin")
 
     def sweep_step_host(self, scalars: dict, host_arrays: dict, stream=None):
-        """One reverse step: u_1, u_b in, u_1_b (this step's adjoint alone) out;
-        c_b accumulates on the device."""
+        """One reverse step.  wave3d_r4: u_1, u_b in, u_1_b (this step's adjoint
+        alone) out, c_b accumulates on the device.  wave3d_c: u_1 in; the
+        adjoints accumulate and rotate on the device."""
         sc = (ctypes.c_double * 2)(*[float(scalars[s]) for s in SCALARS[self.family]])
         s = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
         _lib.check(_lib.lib().sgb_plan_sweep_step_host(
-            ctypes.c_void_p(self._p), sc, self._ptrs(host_arrays, ("u_1", "u_1_b", "u_b")), s),
+            ctypes.c_void_p(self._p), sc, self._ptrs(host_arrays, self._sweep_names(1)), s),
             "sgb_plan_sweep_step_host")
 
     def sweep_end(self, host_arrays: dict, stream=None):
-        """Finish the sweep: the accumulated c_b comes back to the host."""
+        """Finish the sweep: the device-resident results come back to the host."""
         s = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
         _lib.check(_lib.lib().sgb_plan_sweep_end(
-            ctypes.c_void_p(self._p), self._ptrs(host_arrays, ("c_b",)), s),
+            ctypes.c_void_p(self._p), self._ptrs(host_arrays, self._sweep_names(2)), s),
             "sgb_plan_sweep_end")
 
     def close(self):

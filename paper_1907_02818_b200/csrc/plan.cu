@@ -310,36 +310,74 @@ int sgb_plan_run_adjoint_host(sgb_plan* p, const double* scalars, void** arrays,
   return 0;
 }
 
-// ---- reverse sweep over host-held states (BASELINE cfg 5 with the forward
-// states checkpointed in host memory) ----------------------------------------
-// c is the same at every step and c_b accumulates over the sweep, so both stay
-// resident between sweep_begin and sweep_end; a step moves only u_1 and u_b in
-// and the step's own adjoint u_1_b out (8 + 4 bytes per point in fp32 against
-// the 20 + 8 of the accumulating call).  Arrays in the prototype order of
-// wave3d_r4_b: c, c_b, u_1, u_1_b, u_b.
-static int sweep_check(sgb_plan* p, void** arrays, const char* who) {
-  if (!p || !arrays) {
-    sgb::set_error(std::string(who) + ": null argument");
-    return SGB_EINVAL;
-  }
-  if (p->family != "wave3d_r4" || !p->s_cmp) {
-    sgb::set_error(std::string(who) + ": sweeps need a pipelined wave3d_r4 plan");
-    return SGB_EINVAL;
-  }
-  return 0;
+// ---- reverse sweeps over host-held states -----------------------------------
+// The multi-step BASELINE protocols with the forward states checkpointed in
+// host memory.  Whatever does not change per step stays RESIDENT on the device
+// between sweep_begin and sweep_end.
+//   wave3d_r4 (cfg 5: independent steps; c, c_b, u_1, u_1_b, u_b): c and the
+//     accumulator c_b resident; a step moves u_1 and u_b in and the step's own
+//     adjoint u_1_b out (8 + 4 bytes per point in fp32 against the 20 + 8 of the
+//     accumulating call).
+//   wave3d_c (cfg 2: carried steps; c, c_b, u_1, u_1_b, u_2_b, u_b):
+//     c, c_b and the three adjoints resident; a step moves only the state u_1
+//     in, accumulates, and rotates the adjoints on the device (seed <- u_1_b,
+//     u_1_b <- u_2_b, u_2_b <- 0) -- 4 bytes per point per step instead of
+//     24 + 12; sweep_end returns c_b, u_1_b, u_2_b and the seed u_b.
+namespace {
+
+struct SweepSpec {
+  const char* family;
+  std::vector<bool> begin_up, step_up, step_down, end_down;
+  bool fresh, carried;
+};
+
+const SweepSpec* sweep_spec(const std::string& fam) {
+  static const SweepSpec specs[] = {
+      {"wave3d_r4", {1, 1, 0, 0, 0}, {0, 0, 1, 0, 1}, {0, 0, 0, 1, 0}, {0, 1, 0, 0, 0}, true,
+       false},
+      {"wave3d_c", {1, 1, 0, 1, 1, 1}, {0, 0, 1, 0, 0, 0}, {0, 0, 0, 0, 0, 0},
+       {0, 1, 0, 1, 1, 1}, false, true},
+  };
+  for (const auto& sp : specs)
+    if (fam == sp.family) return &sp;
+  return nullptr;
 }
 
-static int sweep_copy(sgb_plan* p, void* host, int k, cudaMemcpyKind kind, sgb_stream_t stream,
-                      const char* who) {
-  if (!host) {
-    sgb::set_error(std::string(who) + ": null host array");
-    return SGB_EINVAL;
+}  // namespace
+
+static const SweepSpec* sweep_check(sgb_plan* p, void** arrays, const char* who) {
+  if (!p || !arrays) {
+    sgb::set_error(std::string(who) + ": null argument");
+    return nullptr;
   }
+  const SweepSpec* sp = sweep_spec(p->family);
+  const bool full = p->i_base == 0 && p->nplanes == p->n;
+  if (!sp || !p->s_cmp || (sp->carried && !full)) {
+    sgb::set_error(std::string(who) + ": sweeps need a pipelined wave3d_r4 plan (grid or "
+                   "slab) or a full-grid wave3d_c plan");
+    return nullptr;
+  }
+  return sp;
+}
+
+static int sweep_copies(sgb_plan* p, void** arrays, const std::vector<bool>& which,
+                        cudaMemcpyKind kind, sgb_stream_t stream, const char* who) {
   cudaStream_t s = sgb::as_stream(stream);
-  cudaError_t e = kind == cudaMemcpyHostToDevice
-                      ? cudaMemcpyAsync(p->dev[k], host, p->bytes, kind, s)
-                      : cudaMemcpyAsync(host, p->dev[k], p->bytes, kind, s);
-  if (e != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) {
+  for (size_t k = 0; k < which.size(); k++) {
+    if (!which[k]) continue;
+    if (!arrays[k]) {
+      sgb::set_error(std::string(who) + ": null host array");
+      return SGB_EINVAL;
+    }
+    const cudaError_t e = kind == cudaMemcpyHostToDevice
+                              ? cudaMemcpyAsync(p->dev[k], arrays[k], p->bytes, kind, s)
+                              : cudaMemcpyAsync(arrays[k], p->dev[k], p->bytes, kind, s);
+    if (e != cudaSuccess) {
+      sgb::set_error(std::string(who) + ": copy failed");
+      return -1;
+    }
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess) {
     sgb::set_error(std::string(who) + ": copy failed");
     return -1;
   }
@@ -347,24 +385,25 @@ static int sweep_copy(sgb_plan* p, void* host, int k, cudaMemcpyKind kind, sgb_s
 }
 
 int sgb_plan_sweep_begin(sgb_plan* p, void** arrays, sgb_stream_t stream) {
-  if (int rc = sweep_check(p, arrays, "sgb_plan_sweep_begin")) return rc;
-  for (int k = 0; k < 2; k++)
-    if (int rc = sweep_copy(p, arrays[k], k, cudaMemcpyHostToDevice, stream,
+  const SweepSpec* sp = sweep_check(p, arrays, "sgb_plan_sweep_begin");
+  if (!sp) return SGB_EINVAL;
+  if (int rc = sweep_copies(p, arrays, sp->begin_up, cudaMemcpyHostToDevice, stream,
                             "sgb_plan_sweep_begin"))
-      return rc;
+    return rc;
   p->in_sweep = true;
   return 0;
 }
 
 int sgb_plan_sweep_step_host(sgb_plan* p, const double* scalars, void** arrays,
                              sgb_stream_t stream) {
-  if (int rc = sweep_check(p, arrays, "sgb_plan_sweep_step_host")) return rc;
+  const SweepSpec* sp = sweep_check(p, arrays, "sgb_plan_sweep_step_host");
+  if (!sp) return SGB_EINVAL;
   if (!scalars || !p->in_sweep) {
     sgb::set_error("sgb_plan_sweep_step_host: no sweep begun on this plan");
     return SGB_EINVAL;
   }
-  for (int k = 2; k < 5; k++)
-    if (!arrays[k]) {
+  for (size_t k = 0; k < sp->step_up.size(); k++)
+    if ((sp->step_up[k] || sp->step_down[k]) && !arrays[k]) {
       sgb::set_error("sgb_plan_sweep_step_host: null host array");
       return SGB_EINVAL;
     }
@@ -373,18 +412,34 @@ int sgb_plan_sweep_step_host(sgb_plan* p, const double* scalars, void** arrays,
   cudaEventRecord(start, sgb::as_stream(stream));
   cudaStreamWaitEvent(p->s_h2d, start, 0);
   cudaEventDestroy(start);
-  return run_pipelined(p, scalars, arrays, {false, false, true, false, true},
-                       {false, false, false, true, false}, true);
+  if (int rc = run_pipelined(p, scalars, arrays, sp->step_up, sp->step_down, sp->fresh))
+    return rc;
+  if (sp->carried) {
+    // every chunk's gather is complete (run_pipelined waited for them): rotate
+    // seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- the old seed's buffer, zeroed
+    void* seed = p->dev[5];
+    p->dev[5] = p->dev[3];
+    p->dev[3] = p->dev[4];
+    p->dev[4] = seed;
+    if (cudaMemsetAsync(p->dev[4], 0, p->bytes, p->s_cmp) != cudaSuccess ||
+        cudaStreamSynchronize(p->s_cmp) != cudaSuccess) {
+      sgb::set_error("sgb_plan_sweep_step_host: rotation failed");
+      return -1;
+    }
+  }
+  return 0;
 }
 
 int sgb_plan_sweep_end(sgb_plan* p, void** arrays, sgb_stream_t stream) {
-  if (int rc = sweep_check(p, arrays, "sgb_plan_sweep_end")) return rc;
+  const SweepSpec* sp = sweep_check(p, arrays, "sgb_plan_sweep_end");
+  if (!sp) return SGB_EINVAL;
   if (!p->in_sweep) {
     sgb::set_error("sgb_plan_sweep_end: no sweep begun on this plan");
     return SGB_EINVAL;
   }
   p->in_sweep = false;
-  return sweep_copy(p, arrays[1], 1, cudaMemcpyDeviceToHost, stream, "sgb_plan_sweep_end");
+  return sweep_copies(p, arrays, sp->end_down, cudaMemcpyDeviceToHost, stream,
+                      "sgb_plan_sweep_end");
 }
 
 }  // extern "C"

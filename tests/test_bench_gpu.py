@@ -35,9 +35,10 @@ def test_bench_line_contract(config, n):
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    if config == "5":  # the host-state sweep, the per-step accumulating ABI beside it
+    if config in ("5", "2"):  # the host-state sweep, the per-step accumulating ABI beside it
         assert e["mode"] == "sweep" and e["accumulating_abi"]["value"] > 0
-        assert e["h2d_bytes_per_step"] < e["accumulating_abi"]["h2d_bytes_per_step"]
+        # (--e2e-steps 1: the sweep's one-off copies are not amortised at all)
+        assert e["h2d_bytes_per_step"] <= e["accumulating_abi"]["h2d_bytes_per_step"]
     else:
         assert e["mode"] == "abi"
     cb = d["cpu_baseline"]

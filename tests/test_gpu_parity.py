@@ -498,10 +498,48 @@ def test_host_sweep_equals_per_step_calls(api, n, dtype, nslabs):
 
 
 def test_host_sweep_refuses_other_families(api):
-    plan = api.Plan("wave3d_c", 128, "f32")
-    with pytest.raises(api._lib.StencilError):
-        plan.sweep_begin({})
+    for fam, n, dt in (("burgers2d", 64, "f64"), ("wave3d_c2", 32, "f32")):
+        plan = api.Plan(fam, n, dt)
+        with pytest.raises(api._lib.StencilError):
+            plan.sweep_begin({})
+        plan.close()
+
+
+@pytest.mark.parametrize("n,dtype", [(132, "f32"), (64, "f32"), (40, "f64")])
+def test_host_carried_sweep_equals_per_step_calls(api, n, dtype):
+    """sgb_plan_sweep_* on a wave3d_c plan (BASELINE cfg 2's carried steps with
+    host-held states): c, c_b and the adjoints stay on the device, a step moves
+    only u_1 in and rotates seed <- u_1_b, u_1_b <- u_2_b, u_2_b <- 0 there.
+    Bit for bit what a caller of the reference ABI gets from the accumulating
+    host entry per step followed by the same rotation of its host arrays."""
+    name, T = "wave3d_c", 4
+    np_dt = np.float32 if dtype == "f32" else np.float64
+    scalars, grids, adjs = gen.family_inputs(name, n, seed=n + 77, accumulate=True)
+    cast = lambda x: np.ascontiguousarray(x.astype(np_dt))  # noqa: E731
+    states = []
+    for t in range(T):
+        _, g, _ = gen.family_inputs(name, n, seed=500 + 11 * t + n, accumulate=True)
+        states.append(cast(g["u_1"]))
+    start = {"c": cast(grids["c"]), **{k: cast(adjs[k]) for k in ("c_b", "u_1_b", "u_2_b", "u_b")}}
+    # the caller of the per-step ABI
+    ref = {k: v.copy() for k, v in start.items()}
+    plan = api.Plan(name, n, dtype)
+    for u_1 in states:
+        ref["u_1"] = u_1.copy()
+        plan.run_adjoint_host(scalars, ref)
+        ref["u_b"], ref["u_1_b"], ref["u_2_b"] = ref["u_1_b"], ref["u_2_b"], np.zeros_like(u_1)
+    # the sweep
+    host = {k: v.copy() for k, v in start.items()}
+    plan.sweep_begin(host)
+    for u_1 in states:
+        plan.sweep_step_host(scalars, {"u_1": u_1})
+    for k in ("c_b", "u_1_b", "u_2_b", "u_b"):
+        host[k][...] = np.nan
+    plan.sweep_end(host)
     plan.close()
+    for k in ("c_b", "u_1_b", "u_2_b", "u_b"):
+        assert np.array_equal(host[k], ref[k]), k
+    assert not host["u_2_b"].any()
 
 
 @pytest.mark.parametrize("n", [24, 40, 68, 97])
