@@ -300,6 +300,42 @@ def test_stream_form_matches_reference(name):
             assert oracle.max_rel_err(dev[t].cpu().numpy(), want) <= 1e-12, (name, t)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt,n", [("f32", 200), ("f32", 132), ("f64", 68)])
+def test_stream_form_is_deterministic(dt, n):
+    """The stream form's shared-memory rings (cp.async planes two ahead, one
+    barrier per plane; the sanitizer's racecheck is not available on this pool):
+    a slot reused too early would show as run-to-run differences -- 12 runs on
+    the same inputs, several waves of CTAs, partial tiles and several
+    outer-counter chunks, give bitwise identical results, equal to a run with
+    the planes requested one at a time (PD = 1)."""
+    import hashlib
+    import torch
+    from paper_1907_02818_b200 import emit_stream, emitter
+    ep = emitter.load_program("wave3d_r4", dt)
+    td_ = torch.float64 if dt == "f64" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(n)
+    base = {k: torch.randn((n, n, n), generator=g, device="cuda", dtype=td_)
+            for k in ep.param_arrays()}
+
+    def run(problem):
+        a = {k: v.clone() for k, v in base.items()}
+        problem.adjoint({"n": n}, {"D": 0.01}, a, form="stream")
+        torch.cuda.synchronize()
+        h = hashlib.sha1()
+        for k in ("c_b", "u_1_b"):
+            h.update(a[k].cpu().numpy().tobytes())
+        return h.hexdigest()
+    digests = {run(ep) for _ in range(12)}
+    assert len(digests) == 1
+    pd = emit_stream.PD
+    try:
+        emit_stream.PD = 1
+        assert run(emitter.load_program("wave3d_r4", dt)) in digests
+    finally:
+        emit_stream.PD = pd
+
+
 def test_stream_form_layouts():
     """Which programs the stream form takes (CPU): the 3D config families
     (two rings: the c_b term's Laplacian of u_1 and the shared q = D c^2 u_b
