@@ -248,6 +248,10 @@ int sgb_plan_run_adjoint_host(sgb_plan* p, const double* scalars, void** arrays,
     sgb::set_error("sgb_plan_run_adjoint_host: null argument");
     return SGB_EINVAL;
   }
+  if (p->in_sweep) {  // the call would overwrite the sweep's resident arrays
+    sgb::set_error("sgb_plan_run_adjoint_host: a sweep is open on this plan (sgb_plan_sweep_end)");
+    return SGB_EINVAL;
+  }
   if (p->s_cmp) {
     for (size_t a = 0; a < p->dev.size(); a++)
       if (!arrays[a]) {

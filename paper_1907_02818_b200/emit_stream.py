@@ -51,6 +51,7 @@ RPT = 1                 # rows per thread (2: rows shared in registers, but 224 
 
 
 ZCHUNK = 128            # planes of the outer counter per CTA (launcher)
+L2HINT = ""             # cp.async L2 prefetch qualifier ("", ".L2::128B", ".L2::256B")
 NSTG = 4                # planes of a staged field in shared memory (cp.async ring)
 PD = 2                  # planes requested ahead of the one being consumed
 UNROLL = False          # plane loop unrolled by the ring size (static modular slots, no
@@ -243,7 +244,7 @@ def stream_source(ep, index="int"):
     lines += ["__device__ __forceinline__ void cpa4(unsigned d, const T* src, bool ok) {",
               "  const int nb = ok ? 16 : 0;"]
     for half in range(2 if dbl else 1):
-        lines += [f'  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: '
+        lines += [f'  asm volatile("cp.async.cg.shared.global{L2HINT} [%0], [%1], 16, %2;" :: '
                   f'"r"(d + {16 * half}), "l"(reinterpret_cast<const char*>(src) + '
                   f'{16 * half}), "r"(nb) : "memory");']
     lines += ["}",

@@ -61,6 +61,11 @@ static void independent_steps(int n, int T) {
   void* a[5] = {cc.data(), cb.data(), nullptr, nullptr, nullptr};
   CHECK(sgb_plan_sweep_step_host(plan, &D, a, nullptr) != 0);  // no sweep begun
   CHECK(sgb_plan_sweep_begin(plan, a, nullptr) == 0);
+  {  // the per-step entry would overwrite the resident arrays: refused while a sweep is open
+    Grid x = u_1[0], s = u_b[0];
+    void* b[5] = {cc.data(), cb.data(), x.data(), out.data(), s.data()};
+    CHECK(sgb_plan_run_adjoint_host(plan, &D, b, nullptr) != 0);
+  }
   for (int t = 0; t < T; t++) {
     a[2] = u_1[t].data();
     a[3] = out.data();
