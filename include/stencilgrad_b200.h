@@ -419,7 +419,9 @@ int sgb_plan_run_adjoint_host(sgb_plan* plan, const double* scalars, void** arra
  *   the state u_1 (4 instead of 36 bytes per point), accumulates c_b, u_1_b,
  *   u_2_b and rotates the adjoints on the device (seed <- u_1_b, u_1_b <-
  *   u_2_b, u_2_b <- 0); end writes c_b, u_1_b, u_2_b and the current seed u_b.
- *   Bitwise = the per-step accumulating call followed by the caller's rotation. */
+ *   Bitwise = the per-step accumulating call followed by the caller's rotation.
+ * While a sweep is open sgb_plan_run_adjoint_host on the same plan is refused
+ * (it would overwrite the resident arrays). */
 int sgb_plan_sweep_begin(sgb_plan* plan, void** arrays, sgb_stream_t stream);
 int sgb_plan_sweep_step_host(sgb_plan* plan, const double* scalars, void** arrays,
                              sgb_stream_t stream);
