@@ -50,7 +50,7 @@ struct StarTileD {
   static constexpr int SF = 3 * BP + NT * TILE;
   static constexpr int QPAIRS = BOX / 2;
   static constexpr int EPT = (QPAIRS + THREADS - 1) / THREADS;
-  static constexpr size_t SMEM = (size_t)(NS * SF + BP + QD * TILE) * 8 + NS * 8;
+  static constexpr size_t SMEM = (size_t)(NS * SF + BP + QD * TILE) * 8 + 2 * NS * 8;
   static_assert(RING % NS == 0, "static stage index");
   static_assert((TILE * 8) % 128 == 0, "TMA destinations 128-B aligned");
   static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -163,13 +163,20 @@ __global__ void __launch_bounds__(StarTileD<MODE>::THREADS, 1)
 #pragma unroll
   for (int r = 1; r <= R; r++) wr[r] = S3::template w<double>(r);
 
+  // Fresh form (MODE 4): split stage barriers as in the fp32 v8 kernel -- the
+  // c / u_b boxes (A half; read only by the q pass, before the plane's first
+  // barrier) complete on their own mbarrier and are requested a plane earlier
+  // than the u_1 box and the c_b tile (B half).  The accumulating forms keep
+  // one barrier per stage (the split loses there, as it does in fp32).
+  constexpr bool SPLIT = S3::kU1bFresh && !S3::kU2;
+  uint64_t* barsB = bars + NS;
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < NS; s++) tma::mbar_init(&bars[s], 1);
+    for (int s = 0; s < (SPLIT ? 2 * NS : NS); s++) tma::mbar_init(&bars[s], 1);
     tma::fence_barrier_init();
   }
   __syncthreads();
-  auto issue = [&](int it) {
+  auto issueA = [&](int it) {  // c, u_b boxes (the whole stage when !SPLIT)
     const int s = it % NS;
     double* dst = stage + s * SF;
     const int pl = pstart + it - i_base;
@@ -179,10 +186,12 @@ __global__ void __launch_bounds__(StarTileD<MODE>::THREADS, 1)
     // fresh u_1_b (MODE 4): its old tile is not needed
     tma::mbar_arrive_expect_tx(
         &bars[s],
-        (3 * BOX + ((emit ? (S3::kU1bFresh ? 1 : 2) : 0) + (u2 ? 1 : 0)) * TILE) * 8);
+        SPLIT ? 2 * BOX * 8
+              : (3 * BOX + ((emit ? (S3::kU1bFresh ? 1 : 2) : 0) + (u2 ? 1 : 0)) * TILE) * 8);
     tma::load_3d(dst, &tm_c, &bars[s], k0 - HK, j0 - HJ, pl);
     tma::load_3d(dst + BP, &tm_ub, &bars[s], k0 - HK - (UBW ? lo : 0), j0 - HJ - (UBW ? lo : 0),
                  pl);
+    if (SPLIT) return;
     tma::load_3d(dst + 2 * BP, &tm_u1, &bars[s], k0 - HK, j0 - HJ, pl);
     if (emit) {
       tma::load_3d(dst + 3 * BP, &tm_cb, &bars[s], k0, j0, pl - R);
@@ -190,8 +199,20 @@ __global__ void __launch_bounds__(StarTileD<MODE>::THREADS, 1)
     }
     if (u2) tma::load_3d(dst + 3 * BP + 2 * TILE, &tm_u2b, &bars[s], k0, j0, pl);
   };
+  auto issueB = [&](int it) {  // SPLIT only: u_1 box and the c_b tile of the output plane
+    const int s = it % NS;
+    double* dst = stage + s * SF;
+    const int pl = pstart + it - i_base;
+    const bool emit = it >= 2 * R;
+    tma::mbar_arrive_expect_tx(&barsB[s], (BOX + (emit ? TILE : 0)) * 8);
+    tma::load_3d(dst + 2 * BP, &tm_u1, &barsB[s], k0 - HK, j0 - HJ, pl);
+    if (emit) tma::load_3d(dst + 3 * BP, &tm_cb, &barsB[s], k0, j0, pl - R);
+  };
   if (tid == 0)
-    for (int it = 0; it < NS && it < P; it++) issue(it);
+    for (int it = 0; it < NS && it < P; it++) {
+      issueA(it);
+      if (SPLIT) issueB(it);
+    }
 
   const int jr0 = j0 + 2 * ty, kc = k0 + 2 * tx;
   const int r0 = 2 * ty + HJ, col = HK + 2 * tx;
@@ -303,7 +324,15 @@ __global__ void __launch_bounds__(StarTileD<MODE>::THREADS, 1)
           }
         }
         __syncthreads();  // Q / G of plane p complete; stage of plane p-1 free
-        if (tid == 0 && it >= 1 && it - 1 + NS < P) issue(it - 1 + NS);
+        if (tid == 0) {
+          if (SPLIT) {  // B of plane it-1+NS first (needed first), then A of plane it+NS
+            if (it >= 1 && it - 1 + NS < P) issueB(it - 1 + NS);
+            if (it + NS < P) issueA(it + NS);
+          } else if (it >= 1 && it - 1 + NS < P) {
+            issueA(it - 1 + NS);
+          }
+        }
+        if (SPLIT) tma::mbar_wait(&barsB[s], (par0 + ph / NS) & 1);
 
         field2x2_d<MODE>(q_role ? Q : U1s, r0, col, w0, wr, acc, ph);
 
