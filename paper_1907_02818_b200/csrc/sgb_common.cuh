@@ -90,6 +90,7 @@ __device__ __forceinline__ bool star_reached(long long i, long long j, long long
   X(V8_INTERIOR)      /* radius 4: the 4-row-per-thread interior kernel (0 | 1) */     \
   X(F64_V8)           /* fp64 radius 4: the 4-row-per-thread streaming kernel (0 | 1) */ \
   X(V8_FRAME)         /* radius 4, v8 on: the frame tiles in v8 as well */              \
+  X(V8_BALANCE)       /* radius 4, v8 interior: balanced last wave (0 off, 1 on) */      \
   X(R1_FP64ACC)       /* radius-1 fp32 gathers accumulate in fp64 (default 1) */
 
 #define SGB_OPT_ENUM(n) OPT_##n,

@@ -688,7 +688,10 @@ __device__ __forceinline__ void star3_v8_body(
     const CUtensorMap& tm_c, const CUtensorMap& tm_ub, const CUtensorMap& tm_u1,
     const CUtensorMap& tm_cb, const CUtensorMap& tm_u1b, float* __restrict__ c_b,
     float* __restrict__ u_1_b, int n, int i_base, int lo, int hi, int out_i0, int out_i1,
-    int chunk, int tk, int tj, float D) {
+    int chunk, int tk, int tj, float D, int ob = -1, int oe = -1, bool again = false) {
+  // ob / oe: an explicit output plane range (else chunk blockIdx.y of
+  // [out_i0, out_i1)); again: the CTA ran a range before -- its mbarriers are
+  // invalidated and set up anew (every load it issued was consumed)
   using Tl = StarTile8<MODE>;
   using S3 = Star3<MODE>;
   static_assert(!S3::kU2 && !S3::kU2Set, "v8: radius-4 specs without u_2 partials");
@@ -707,8 +710,8 @@ __device__ __forceinline__ void star3_v8_body(
   const int rt = q_role ? tid - ROLE : tid;
   const int tx = rt & 15, ty = rt >> 4;  // 4 k-points x rows 4ty .. 4ty+3
   const int k0 = tk * TK, j0 = tj * Tl::TJ;
-  const int o_begin = out_i0 + blockIdx.y * chunk;
-  const int o_end = min(o_begin + chunk, out_i1);
+  const int o_begin = ob >= 0 ? ob : out_i0 + blockIdx.y * chunk;
+  const int o_end = ob >= 0 ? oe : min(o_begin + chunk, out_i1);
   if (o_begin >= o_end) return;
   const int pstart = o_begin - R;
   const int P = (o_end - o_begin) + 2 * R;
@@ -720,9 +723,13 @@ __device__ __forceinline__ void star3_v8_body(
   for (int r = 1; r <= R; r++) wr[r] = S3::template w<float>(r);
 
   uint64_t* barsB = bars + NS;
+  if (again) __syncthreads();  // every thread is done with the previous range
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < 2 * NS; s++) tma::mbar_init(&bars[s], 1);
+    for (int s = 0; s < 2 * NS; s++) {
+      if (again) tma::mbar_inval(&bars[s]);
+      tma::mbar_init(&bars[s], 1);
+    }
     tma::fence_barrier_init();
   }
   __syncthreads();
@@ -943,6 +950,44 @@ __global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
                                hi, out_i0, out_i1, chunk, tk, tj, D);
 }
 
+// Interior launch with a balanced last wave (v8, one chunk per column).  With
+// T interior tiles on S SMs the last of ceil(T / S) waves runs T % S CTAs and
+// leaves the other SMs idle for a whole column (1024^3: 420 tiles, 2.84
+// waves).  Here the first `full` tiles run whole columns; of the remaining
+// `rem` tiles the planes [out_i0, split) go to one CTA each and the planes
+// [split, out_i1) of ALL of them to the gridDim.x - full - rem filler CTAs,
+// filler f taking tiles full + f, full + f + nfill, ... -- so the fillers move
+// through adjacent tiles in lock-step (halo rows shared in L2) and every SM
+// finishes at about the same time.  Same arithmetic per point: bitwise equal.
+template <int MODE>
+__global__ void __launch_bounds__(StarTile8<MODE>::THREADS, 1)
+    star3_v8_balanced(const __grid_constant__ CUtensorMap tm_c,
+                      const __grid_constant__ CUtensorMap tm_ub,
+                      const __grid_constant__ CUtensorMap tm_u1,
+                      const __grid_constant__ CUtensorMap tm_cb,
+                      const __grid_constant__ CUtensorMap tm_u1b, float* __restrict__ c_b,
+                      float* __restrict__ u_1_b, int n, int i_base, int lo, int hi, int out_i0,
+                      int out_i1, TileMap tmap, float D, int full, int rem, int split) {
+  // one call site for the body (two inlined copies of its ~5 K instructions
+  // thrash the instruction cache: 15 % slower)
+  const int b = blockIdx.x;
+  const bool filler = b >= full + rem;
+  const int nfill = (int)gridDim.x - full - rem;
+  const int t0 = filler ? full + (b - full - rem) : b;
+  const int tend = filler ? full + rem : b + 1;
+  const int step = filler ? nfill : 1;
+  const int ob = filler ? split : out_i0;
+  const int oe = (filler || b < full) ? out_i1 : split;
+  bool again = false;
+  for (int t = t0; t < tend; t += step) {
+    int tk, tj;
+    tmap.interior(t, tk, tj);
+    star3_v8_body<MODE, true>(tm_c, tm_ub, tm_u1, tm_cb, tm_u1b, c_b, u_1_b, n, i_base, lo, hi,
+                              out_i0, out_i1, 0, tk, tj, D, ob, oe, again);
+    again = true;
+  }
+}
+
 #define SGB_V7_PARAMS                                                                   \
   const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_ub,     \
       const __grid_constant__ CUtensorMap tm_u1, const __grid_constant__ CUtensorMap tm_cb, \
@@ -1135,6 +1180,29 @@ inline int star3_v7_gather(const Slab3& g, long long lo, long long hi, long long
                   (int)g.n, (int)g.i_base, (int)lo, (int)hi, (int)out_i0, (int)out_i1,
                   cf.first, tm, D, pf);
           if (int st = launch_status(name)) return st;
+        }
+      }
+      // balanced last wave (star3_v8_balanced): one chunk per column, more
+      // tiles than SMs and a partly filled last wave that the model prices
+      // >= 2 % above the balanced schedule
+      const long long T = tm.n_interior();
+      const long long rem = T % sms, nfill = sms - rem;
+      if (ci.second == 1 && T > sms && rem > 0 && opt(OPT_V8_BALANCE, 1) != 0) {
+        const long long ppf = (rem + nfill - 1) / nfill;  // pieces per filler CTA
+        // rem CTAs run m + 2R planes, fillers ppf * (nout - m + 2R): equal at
+        long long m = (ppf * (nout + 2 * Tl::R) - 2 * Tl::R) / (ppf + 1);
+        if (opt(OPT_V8_BALANCE, 1) > 1) m = opt(OPT_V8_BALANCE, 1);  // forced split (sweeps)
+        m = std::max<long long>(1, std::min<long long>(m, nout - 1));
+        const long long bal = (T / sms) * (nout + 2 * Tl::R) +
+                              std::max(m + 2 * Tl::R, ppf * (nout - m + 2 * Tl::R));
+        const long long plain = ((T + sms - 1) / sms) * (nout + 2 * Tl::R);
+        if (bal * 100 <= plain * 98) {
+          if (int r = ensure_smem((const void*)star3_v8_balanced<MODE>, T8::SMEM, name)) return r;
+          star3_v8_balanced<MODE><<<dim3((unsigned)(T + nfill)), T8::THREADS, T8::SMEM, s>>>(
+              maps[0], maps[1], maps[2], maps[3], maps[4], c_b, u_1_b, (int)g.n, (int)g.i_base,
+              (int)lo, (int)hi, (int)out_i0, (int)out_i1, tm, D, (int)(T - rem), (int)rem,
+              (int)(out_i0 + m));
+          return launch_status(name);
         }
       }
       return launch8(0, (unsigned)tm.n_interior(), ci);

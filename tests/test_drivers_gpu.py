@@ -495,6 +495,40 @@ def test_v8_interior_bitwise_equals_v7(mods, n, fresh, sgbopt):
 
 
 @pytest.mark.parametrize("fresh", [False, True])
+def test_v8_balanced_last_wave_bitwise_equal(mods, fresh, sgbopt):
+    """star3_v8_balanced (the interior launch when one chunk per column leaves
+    a partly filled last wave: the remaining tiles' columns split between one
+    CTA each and filler CTAs that walk several tiles, re-arming their
+    mbarriers) computes the plain launch's bits -- automatic and forced split
+    points, against the plain v8 launch and v7.  n = 704: 180 interior tiles on
+    148 SMs with SGB_ICHUNKS=1 (cfg 5's 1024^3 takes this path by itself)."""
+    torch, api, drivers = mods
+    n, fam, sc = 704, "wave3d_r4", {"D": 0.01}
+    g = torch.Generator(device="cuda").manual_seed(n)
+    base = {k: torch.randn((n, n, n), generator=g, device="cuda")
+            for k in ("c", "c_b", "u_1", "u_1_b", "u_b")}
+    out = {}
+    for name, env in (("v7", {"SGB_V8_INTERIOR": "0"}),
+                      ("plain", {"SGB_V8_INTERIOR": "1", "SGB_V8_BALANCE": "0"}),
+                      ("auto", {"SGB_V8_INTERIOR": "1", "SGB_V8_BALANCE": "1"}),
+                      ("m100", {"SGB_V8_INTERIOR": "1", "SGB_V8_BALANCE": "100"}),
+                      ("m500", {"SGB_V8_INTERIOR": "1", "SGB_V8_BALANCE": "500"})):
+        with sgbopt.context() as m:
+            m.setenv("SGB_ICHUNKS", "1")
+            for k, v in env.items():
+                m.setenv(k, v)
+            a = {k: t.clone() for k, t in base.items() if k in ("c_b", "u_1_b")}
+            a.update({k: base[k] for k in ("c", "u_1", "u_b")})
+            (api.adjoint_fresh if fresh else api.adjoint)(fam, n, sc, a)
+            torch.cuda.synchronize()
+        out[name] = {k: a[k] for k in ("c_b", "u_1_b")}
+    for name in ("plain", "auto", "m100", "m500"):
+        for k in ("c_b", "u_1_b"):
+            assert torch.equal(out["v7"][k].view(torch.int32),
+                               out[name][k].view(torch.int32)), (name, k)
+
+
+@pytest.mark.parametrize("fresh", [False, True])
 def test_f64_v8_bitwise_equals_two_row_form(mods, fresh, sgbopt):
     """The opt-in 4-rows-per-thread fp64 radius-4 kernel (SGB_F64_V8=1) forms
     every term in the 2-row kernel's order: bitwise the same result."""
